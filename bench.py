@@ -1,0 +1,322 @@
+"""Benchmark of the memoized ADMM-FFT hot path (BASELINE.json configs[1]:
+256^3 phantom, 256 angles, 1 B200, memo off and on).
+
+A step is one ADMM outer iteration (LSP with 4 inner CG steps, RSP, the
+multiplier/penalty update, memo flush, objective) of the device solver,
+called through the C-ABI (mlrg_solver_step). Inputs are resident in HBM;
+every array of an iteration (V = 256^3 complex64 = 134 MB) is larger than L2,
+so no L2 flush is inserted between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0). Under torchrun every rank runs an independent
+replica (the z-slab sharded path is not built yet): scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max clock (no measured figure)
+METRIC = "ADMM-FFT iterations/sec at N^3 volume"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--n-theta", type=int, default=None)
+    ap.add_argument("--no-memo-run", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def config_text(n, nt, memo):
+    return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer=1000000\n"
+            f"memoization={memo}\nnudft_path=gridding\n")
+
+
+def algorithmic(n, nt, kernel, launches_per_step):
+    """Per-launch algorithmic work of the profiled kernels."""
+    T = nt * n
+    if kernel == "k_fu2d_gather":  # 16 detector rows per launch, 576 taps + 24 outer + 12 epilogue flops
+        return {"flops": T * 16 * (24 * 24 * 4 + 24 * 4 + 12), "bytes": 8 * (2 * n) ** 2 * 16 + 8 * T * 16}
+    if kernel == "k_fu2d_adj_spread":
+        return {"flops": T * 16 * (24 * 24 * 4 + 24 * 4 + 12), "bytes": 8 * (2 * n) ** 2 * 16 + 8 * T * 16}
+    if kernel in ("k_fu1d", "k_fu1d_adj"):
+        return {"flops": None, "bytes": 8 * 2 * n ** 3}
+    return {"flops": None, "bytes": None}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n
+    nt = args.n_theta or n
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank, n, nt)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_01893_b200 as m
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m.lib()
+    stream = torch.cuda.current_stream()
+
+    # synthetic data of the configured shape: the "blocks" phantom (seed 1) projected on the device
+    ph_host = m.make_phantom("blocks", n, n, n, 1).numpy().astype(np.complex64)
+    phantom = torch.from_numpy(ph_host).cuda()
+    ctx = m.Context(n, n, n, nt, n, n, stream=stream.cuda_stream)
+    d = torch.empty((nt, n, n), dtype=torch.complex64, device="cuda")
+    ctx.forward_L(phantom, d)
+    ctx.sync()
+    del ctx
+
+    def timed_run(memo: str, profile: bool):
+        solver = m.Solver(config_text(n, nt, memo), d, reference=phantom, stream=stream.cuda_stream)
+        for _ in range(args.warmup):
+            solver.step()
+        m.lib().mlrg_prof_reset()
+        m.lib().mlrg_prof_enable(1 if profile else 0)
+        c0 = solver.counters()
+        launches0 = m.lib().mlrg_launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clocks:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            done = 0
+            for _ in range(args.steps):
+                if not solver.step():
+                    break
+                done += 1
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        m.lib().mlrg_prof_enable(0)
+        ms = ev0.elapsed_time(ev1)
+        launches = m.lib().mlrg_launch_count() - launches0
+        c1 = solver.counters()
+        prof = {}
+        if profile:
+            for k in ("k_fu2d_gather", "k_fu2d_adj_spread", "k_fu2d_rows", "k_fu2d_cols", "k_fu2d_adj_cols",
+                      "k_fu2d_adj_rows", "k_fu2d_adj_prep", "k_fu1d", "k_fu1d_adj"):
+                tot, cnt = m.prof_query(k)
+                if cnt:
+                    prof[k] = {"ms_total": tot, "launches": cnt}
+        csv = solver.csv
+        del solver
+        return dict(ms=ms, steps_done=done, launches=launches, clocks=clocks.summary(), prof=prof,
+                    counters={k: c1[k] - c0[k] for k in c1}, csv=csv)
+
+    off = timed_run("off", profile=True)
+    ms_step = off["ms"] / max(off["steps_done"], 1)
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * 1000.0 / ms_step
+
+    memo_on = None
+    if not args.no_memo_run:
+        on = timed_run("local", profile=False)
+        c = on["counters"]
+        hits = c["remote_hits"] + c["cache_hits"]
+        memo_on = {"value": 1000.0 * on["steps_done"] / on["ms"] if on["steps_done"] else None,
+                   "steps_done": on["steps_done"], "lookups": c["lookups"], "misses": c["misses"],
+                   "remote_hits": c["remote_hits"], "cache_hits": c["cache_hits"],
+                   "hit_rate": hits / c["lookups"] if c["lookups"] else None,
+                   "aborted": on["steps_done"] < args.steps}
+
+    # dominant kernel roofline from the live CUDA-event timers
+    P, src = peaks()
+    roof = None
+    if off["prof"]:
+        name, rec = max(off["prof"].items(), key=lambda kv: kv[1]["ms_total"])
+        avg_ms = rec["ms_total"] / rec["launches"]
+        work = algorithmic(n, nt, name, rec["launches"] / max(off["steps_done"], 1))
+        total_ms = sum(v["ms_total"] for v in off["prof"].values())
+        if work["flops"]:
+            ach = work["flops"] / (avg_ms * 1e-3) / 1e12
+            roof = {"kernel": name, "bound": "fp32", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP32_PEAK_TFLOPS,
+                    "peak_source": "computed 148 SM x 128 FFMA lanes x 2 x 1.965 GHz (MEASURED_PEAKS has no FP32 figure)",
+                    "algorithmic_per_launch": work["flops"], "avg_launch_ms": avg_ms, "traffic": None}
+        else:
+            ach = work["bytes"] / (avg_ms * 1e-3) / 1e9
+            roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / P["hbm_gbs"], "peak_source": src, "algorithmic_per_launch": work["bytes"],
+                    "avg_launch_ms": avg_ms, "traffic": None}
+        roof["share_of_step"] = rec["ms_total"] / off["ms"]
+        roof["kernels_ms_per_step"] = {k: v["ms_total"] / max(off["steps_done"], 1) for k, v in off["prof"].items()}
+    # whole-iteration HBM view against SURVEY §8(d)'s fused-minimum bytes
+    V, M, Pp = n ** 3, n ** 3, nt * n * n
+    b_iter = 8 * (131 * V + 26 * M + 22 * Pp)
+    iter_hbm = {"bytes_per_iter": b_iter, "achieved_gbs": b_iter / (ms_step * 1e-3) / 1e9,
+                "frac": b_iter / (ms_step * 1e-3) / 1e9 / P["hbm_gbs"], "peak_source": src}
+
+    e2e = None
+    if not args.no_e2e:
+        cfg = m.Config(n1=n, n0=n, n2=n, n_theta=nt, h=n, w=n, n_outer=args.steps, memoization="off",
+                       nudft_path="gridding")
+        ph = m.make_phantom("blocks", n, n, n, 1)
+        data = m.project(cfg, ph)
+        t0 = time.perf_counter()
+        res = m.reconstruct(cfg, data, ph)
+        vol = res.volume.numpy()
+        wall = time.perf_counter() - t0
+        k = len(m.parse_csv(res.csv))
+        e2e = {"value": k / wall, "unit": "it/s", "h2d_bytes_per_step": (2 * 16 * V) / max(k, 1),
+               "d2h_bytes_per_step": 16 * V / max(k, 1), "steps": k, "wall_s": wall,
+               "path": "mlr_reconstruct (drop-in mlr.h) on host complex128 arrays, incl. setup and copies",
+               "checksum": float(np.abs(vol).sum())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(n, nt, n_inner=1)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64 (fp32)", "data": "synthetic (blocks phantom seed 1, d = forward_L on GPU)",
+        "config": {"workload": f"configs[1]: {n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)",
+                   "n": n, "n_theta": nt, "n_inner": 4, "memo": "off", "nudft": "gridding, 24-tap Gaussian",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "no flush: every per-iteration array (134 MB) exceeds the 126 MB L2"},
+        "memo_on": memo_on, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": off["launches"], "clocks": off["clocks"],
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_ref(n, nt, n_inner, timeout=900):
+    cmd = [sys.executable, os.path.join(ROOT, "oracle", "ref_runner.py"), "--n", str(n), "--n-theta", str(nt),
+           "--n-inner", str(n_inner)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    if p.returncode != 0:
+        raise RuntimeError(p.stderr[-400:])
+    return json.loads(p.stdout)
+
+
+def cpu_baseline(n, nt, n_inner):
+    try:
+        r = run_ref(n, nt, n_inner)
+    except Exception as e:  # report, do not fail the bench
+        return {"value": None, "unit": "it/s", "kind": "reference", "error": str(e)[:300]}
+    return {"value": r["it_per_s"], "unit": "it/s", "cores": r["workers"], "kind": "reference",
+            "host_cores": r["cores"], "cpu": r["cpu"],
+            "sample": (f"unmodified reference mlr_reconstruct (oracle/_ref), {n}^3, {nt} angles, memo off, gridding, "
+                       f"1 outer iteration with n_inner={n_inner}; per-iteration time = its own phase timers "
+                       f"(ms_lsp x {4 // n_inner} + ms_rsp + ms_update)"),
+            "per_iter_ms": r["per_iter_ms"], "wall_s": r["wall_s"]}
+
+
+def reference_arm(args, world, rank, n, nt):
+    if rank != 0:
+        return 0
+    try:
+        r = run_ref(n, nt, 4, timeout=1500)
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {str(e)[:200]}"}))
+        return 0
+    v = r["it_per_s"]
+    sample = (f"unmodified reference mlr_reconstruct (oracle/_ref, built from /root/reference by oracle/Makefile), "
+              f"{n}^3, {nt} angles, memo off, gridding, workers={r['workers']}: one full outer iteration "
+              f"(n_inner=4); time = its own phase timers ms_lsp + ms_rsp + ms_update")
+    out = {"metric": METRIC, "value": v, "unit": "it/s", "n_gpus": world, "steps": 1, "warmup": 0,
+           "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "c128 (fp64)", "data": "synthetic (random complex data of the configured shape)",
+           "config": {"workload": f"configs[1]: {n}^3 volume, {nt} angles, memo off", "n": n, "n_theta": nt},
+           "impl": "reference",
+           "cpu_baseline": {"value": v, "unit": "it/s", "cores": r["workers"], "kind": "reference",
+                            "host_cores": r["cores"], "cpu": r["cpu"], "sample": sample},
+           "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": r["wall_s"]}
+    print(json.dumps(out))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

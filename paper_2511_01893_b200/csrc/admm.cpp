@@ -1,0 +1,242 @@
+#include "admm.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <iomanip>
+#include <sstream>
+#include <utility>
+
+#include "kernels.hpp"
+
+namespace mlrg {
+
+void AdmmConfig::validate() const {  // admm.cpp:11-17
+  if (!(alpha >= 0.0)) throw std::invalid_argument("admm: alpha must be >= 0");
+  if (!(rho0 > 0.0)) throw std::invalid_argument("admm: rho0 must be positive");
+  if (n_inner < 1) throw std::invalid_argument("admm: n_inner must be >= 1");
+  if (n_outer < 1) throw std::invalid_argument("admm: n_outer must be >= 1");
+  if (!(tau > 0.0f && tau <= 1.0f)) throw std::invalid_argument("admm: tau must be in (0, 1]");
+}
+
+std::string ReconReport::csv() const {
+  std::ostringstream out;
+  out << "iteration,loss,E,accuracy,miss,remote_hit,cache_hit,ms_lsp,ms_rsp,ms_update\n";
+  out << std::setprecision(12);
+  for (const IterationRow& r : rows)
+    out << r.iteration << ',' << r.loss << ',' << r.e << ',' << r.accuracy << ',' << r.miss << ',' << r.remote_hit
+        << ',' << r.cache_hit << ',' << r.ms_lsp << ',' << r.ms_rsp << ',' << r.ms_update << '\n';
+  return out.str();
+}
+
+namespace {
+
+/// Device ADMM state (admm.hpp:38-49). lambda is stored scaled: the true
+/// multiplier is lam * lam_scale, with lam_scale a power of two, so the
+/// residual-balancing rescale (admm.cpp:173-180) is exact and costs no pass.
+struct State {
+  std::int64_t V, M, P;
+  DeviceBuffer<float2> u, G, G_prev, p, p_prev, mid, mid2, rhat, dhat, dpred, fu2d_out;
+  DeviceBuffer<float2> psi[3], psi_prev[3], lam[3], g[3];
+  double rho = 1.0, lam_scale = 1.0;
+  bool have_direction = false;
+  std::vector<double> inner_losses;
+
+  State(const Geometry& geo, bool baseline, cudaStream_t s)
+      : V(geo.volume_shape().count()), M(geo.mid_shape().count()), P(geo.projection_shape().count()) {
+    auto vz = [&](DeviceBuffer<float2>& b, std::int64_t n) {
+      b.resize(static_cast<std::size_t>(n));
+      b.zero(s);
+    };
+    for (auto* b : {&u, &G, &G_prev, &p, &p_prev}) vz(*b, V);
+    for (int c = 0; c < 3; ++c) {
+      vz(psi[c], V);
+      vz(psi_prev[c], V);
+      vz(lam[c], V);
+      vz(g[c], V);
+    }
+    vz(mid, M);
+    vz(mid2, M);
+    vz(rhat, P);
+    vz(dhat, P);
+    if (baseline) {
+      vz(dpred, P);
+      vz(fu2d_out, P);
+    }
+  }
+  Field3 f(DeviceBuffer<float2> (&a)[3]) { return Field3{{a[0].get(), a[1].get(), a[2].get()}}; }
+};
+
+std::int64_t geo_count(const Engine& e) { return e.geometry().volume_shape().count(); }
+
+double ms_between(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+  return std::chrono::duration<double, std::milli>(b - a).count();
+}
+
+}  // namespace
+
+struct SolverState : State {
+  const float2* d;
+  const float2* reference;
+  AdmmConfig cfg;
+  Engine& eng;
+  ReconReport rep;
+  MemoCounters prev;
+  int outer = 0;
+  SolverState(const float2* d_, const AdmmConfig& c, Engine& e, const float2* ref)
+      : State(e.geometry(), c.pipeline == Pipeline::baseline, e.stream()), d(d_), reference(ref), cfg(c), eng(e) {}
+};
+
+Solver::Solver(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2* reference) {
+  cfg.validate();
+  st_ = new SolverState(d, cfg, eng, reference);
+  st_->rho = cfg.rho0;
+  eng.f2d(d, st_->dhat.get(), false);  // admm.cpp:220
+  st_->prev = eng.memo() ? eng.memo()->counters() : MemoCounters{};
+}
+
+Solver::~Solver() { delete st_; }
+int Solver::iteration() const { return st_->outer; }
+const ReconReport& Solver::report() const { return st_->rep; }
+const float2* Solver::u() const { return st_->u.get(); }
+
+bool Solver::step() {
+  SolverState& st = *st_;
+  if (st.rep.aborted) return false;
+  const AdmmConfig& cfg = st.cfg;
+  Engine& eng = st.eng;
+  const Geometry& geo = eng.geometry();
+  cudaStream_t s = eng.stream();
+  Partials& part = eng.usfft().partials();
+  const Dims dims{geo.n1, geo.n0, geo.n2};
+  const bool baseline = cfg.pipeline == Pipeline::baseline;
+  const float2* d = st.d;
+  using clock = std::chrono::steady_clock;
+  auto sum = [&](int slots, int nv) { return part.sum(slots, nv, s); };
+  const int outer = st.outer++;
+  {
+    eng.set_iteration(outer);
+    IterationRow row;
+    row.iteration = outer;
+    try {
+      const auto t0 = clock::now();
+      // ---- LSP (admm.cpp:59-118, 122-152) ----
+      ops::g_init(CField3(st.f(st.psi)), CField3(st.f(st.lam)), st.f(st.g), st.V,
+                  static_cast<float>(st.lam_scale / st.rho), s);
+      st.have_direction = false;
+      const std::size_t phase_start = st.inner_losses.size();
+      for (int inner = 0; inner < cfg.n_inner; ++inner) {
+        // gradient(u): r_hat, loss terms, G
+        double rr = 0.0;
+        eng.fu1d(st.u.get(), st.mid.get());
+        if (baseline) {
+          eng.fu2d(st.mid.get(), st.fu2d_out.get());
+          eng.f2d_adj(st.fu2d_out.get(), st.dpred.get());
+          rr = sum(ops::sub_norm(st.dpred.get(), d, st.P, part.dev(), s), 1)[0];
+          eng.f2d(st.dpred.get(), st.rhat.get());
+        } else {
+          eng.fu2d_fused(st.mid.get(), st.dhat.get(), st.rhat.get());
+          rr = sum(ops::norm2_diff(st.rhat.get(), nullptr, st.P, part.dev(), s), 2)[1];
+        }
+        eng.fu2d_adj(st.rhat.get(), st.mid2.get());
+        eng.fu1d_adj(st.mid2.get(), st.G.get());
+        const bool hd = st.have_direction;
+        const std::vector<double> gu = sum(
+            ops::grad_update(st.u.get(), CField3(st.f(st.g)), st.G.get(), hd ? st.p_prev.get() : nullptr,
+                             hd ? st.G_prev.get() : nullptr, dims, static_cast<float>(st.rho), part.dev(), s),
+            3);
+        const double loss = 0.5 * rr + 0.5 * st.rho * gu[0];
+        st.inner_losses.push_back(loss);
+        const std::size_t n = st.inner_losses.size();
+        if (n >= phase_start + 4 && st.inner_losses[n - 1] > 10.0 * st.inner_losses[n - 4]) {
+          std::ostringstream msg;
+          msg << "inner loss diverged: " << st.inner_losses[n - 4] << " -> " << st.inner_losses[n - 1]
+              << " within 3 iterations";
+          throw AdmmAbort(msg.str());
+        }
+        const double normG2 = gu[1];
+        double beta = 0.0;
+        if (hd && gu[2] > 0.0) beta = normG2 / gu[2];
+        auto step_terms = [&](double bt, double& a, double& b) {
+          const std::vector<double> dr = sum(ops::direction(st.G.get(), st.p_prev.get(), static_cast<float>(bt),
+                                                            st.u.get(), CField3(st.f(st.g)), st.p.get(), dims,
+                                                            part.dev(), s),
+                                             2);
+          eng.fu1d(st.p.get(), st.mid.get(), false);
+          const std::array<double, 2> q = eng.fu2d_reduce(st.mid.get(), nullptr, st.rhat.get());
+          a = q[0] + st.rho * dr[0];
+          b = q[1] + st.rho * dr[1];
+        };
+        double a = 0.0, b = 0.0;
+        step_terms(beta, a, b);
+        if (b > 0.0) step_terms(0.0, a, b);  // uphill: steepest descent (admm.cpp:103-106)
+        if (a > 0.0 && b < 0.0) ops::axpy(st.u.get(), st.p.get(), static_cast<float>(-b / a), st.V, s);
+        std::swap(st.G_prev, st.G);
+        std::swap(st.p_prev, st.p);
+        st.have_direction = true;
+      }
+      MLRG_CUDA(cudaStreamSynchronize(s));
+      const auto t1 = clock::now();
+      // ---- RSP + multiplier/penalty, one fused pass (admm.cpp:154-181) ----
+      const std::vector<double> rs =
+          sum(ops::rsp_multiplier(st.u.get(), st.f(st.lam), CField3(st.f(st.psi)), st.f(st.psi_prev), dims,
+                                  static_cast<float>(st.lam_scale / st.rho), static_cast<float>(cfg.alpha / st.rho),
+                                  static_cast<float>(st.rho / st.lam_scale), part.dev(), s),
+              2);
+      for (int c = 0; c < 3; ++c) std::swap(st.psi[c], st.psi_prev[c]);  // psi_prev <- old psi
+      const auto t2 = clock::now();
+      const double r = std::sqrt(rs[0]);
+      const double sres = st.rho * std::sqrt(rs[1]);
+      if (!cfg.freeze_rho) {
+        if (r > 10.0 * sres) {
+          st.rho *= 2.0;
+          st.lam_scale *= 0.5;
+        } else if (sres > 10.0 * r) {
+          st.rho *= 0.5;
+          st.lam_scale *= 2.0;
+        }
+      }
+      const auto t3 = clock::now();
+      row.ms_lsp = ms_between(t0, t1);
+      row.ms_rsp = ms_between(t1, t2);
+      row.ms_update = ms_between(t2, t3);
+    } catch (const AdmmAbort& ex) {
+      st.rep.aborted = true;
+      st.rep.abort_reason = ex.what();
+      return false;
+    }
+    eng.flush_inserts();  // admm.cpp:251-254
+    // objective (admm.cpp:190-195), not memoized
+    eng.fu1d(st.u.get(), st.mid.get(), false);
+    const std::array<double, 2> data = eng.fu2d_reduce(st.mid.get(), st.dhat.get(), nullptr);
+    const double tv = sum(ops::tv_norm(st.u.get(), dims, part.dev(), s), 1)[0];
+    row.loss = 0.5 * data[0] + cfg.alpha * tv;
+    if (st.reference) {  // accuracy(reference, u), admm.cpp:183-188
+      const std::vector<double> nd = sum(ops::norm2_diff(st.reference, st.u.get(), st.V, part.dev(), s), 2);
+      if (nd[1] == 0.0) throw std::invalid_argument("accuracy: reference volume has zero norm");
+      row.e = std::sqrt(nd[0]) / std::sqrt(nd[1]);
+      row.accuracy = 1.0 - row.e;
+    }
+    if (eng.memo()) {
+      const MemoCounters now = eng.memo()->counters();
+      row.miss = now.misses - st.prev.misses;
+      row.remote_hit = now.remote_hits - st.prev.remote_hits;
+      row.cache_hit = now.cache_hits - st.prev.cache_hits;
+      st.prev = now;
+    }
+    st.rep.rows.push_back(row);
+  }
+  return true;
+}
+
+ReconReport reconstruct(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2* reference, float2* u_out) {
+  Solver solver(d, cfg, eng, reference);
+  for (int outer = 0; outer < cfg.n_outer; ++outer)
+    if (!solver.step()) break;
+  cudaStream_t s = eng.stream();
+  MLRG_CUDA(cudaMemcpyAsync(u_out, solver.u(), static_cast<std::size_t>(geo_count(eng)) * sizeof(float2),
+                            cudaMemcpyDeviceToDevice, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));
+  return solver.report();
+}
+
+}  // namespace mlrg

@@ -1,0 +1,775 @@
+// C-ABI of the B200 build: the drop-in mlr.h surface (capi.cpp of the
+// reference, re-implemented over the device engine) and the device mlrg.h
+// surface. All exceptions stop here and become a thread-local message plus
+// an MLR_* code (capi.cpp:37-47 error model).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "admm.hpp"
+#include "config.hpp"
+#include "encoder.hpp"
+#include "engine.hpp"
+#include "host_io.hpp"
+#include "kernels.hpp"
+#include "memo.hpp"
+#include "mlr.h"
+#include "mlrg.h"
+#include "usfft.hpp"
+
+struct mlr_config {
+  mlrg::RunConfig rc;
+};
+struct mlr_array {
+  mlrg::HostArray a;
+};
+struct mlr_result {
+  mlr_array u;
+  mlrg::ReconReport report;
+  std::vector<mlrg::ChunkAudit> audit;
+};
+struct mlr_server {};
+
+struct mlrg_ctx {
+  mlrg::Geometry g;
+  cudaStream_t s = nullptr;
+  bool own_stream = false;
+  std::unique_ptr<mlrg::Usfft> usfft;
+  mlrg::DeviceBuffer<float2> scratch_mid, scratch_proj;
+  ~mlrg_ctx() {
+    usfft.reset();
+    if (own_stream && s) cudaStreamDestroy(s);
+  }
+};
+struct mlrg_recon {
+  mlrg::ReconReport report;
+  std::vector<mlrg::ChunkAudit> audit;
+  mlrg::MemoCounters counters;
+};
+struct mlrg_solver {
+  cudaStream_t own = nullptr;
+  std::unique_ptr<mlrg::Engine> eng;
+  std::unique_ptr<mlrg::Solver> solver;
+  ~mlrg_solver() {
+    solver.reset();
+    eng.reset();
+    if (own) cudaStreamDestroy(own);
+  }
+};
+struct mlrg_memo {
+  std::shared_ptr<mlrg::MemoStore> store;
+  std::unique_ptr<mlrg::MemoClient> client;
+};
+
+namespace {
+
+thread_local std::string t_error;
+
+int code_for(const std::exception& e) {
+  return dynamic_cast<const std::invalid_argument*>(&e) != nullptr ? MLR_ERR_CONFIG : MLR_ERR_RUNTIME;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MLR_OK;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return code_for(e);
+  }
+}
+
+template <class T, class F>
+T* guarded_ptr(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return nullptr;
+  }
+}
+
+char* dup_text(const std::string& s) {
+  char* out = static_cast<char*>(std::malloc(s.size() + 1));
+  if (out) std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
+/// Engine assembly per reconstruction (capi.cpp:70-86). Both memo modes use
+/// the device-resident store: "distributed" keeps the reference's decision
+/// semantics (its transport only adds timeouts) without a TCP memory node.
+std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg::Geometry& g, cudaStream_t s) {
+  mlrg::EngineConfig ec = rc.engine;
+  ec.memo_enabled = rc.admm.memoization != mlrg::MemoMode::off;
+  if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s);
+  if (rc.encoder.variant != mlrg::EncoderConfig::Variant::projection)
+    throw std::invalid_argument("encoder_variant=cnn is not provided by the B200 build (projection only)");
+  auto client = std::make_shared<mlrg::MemoClient>(rc.memo, std::make_shared<mlrg::MemoStore>());
+  auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
+  return std::make_unique<mlrg::Engine>(g, ec, s, enc, client);
+}
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  StreamGuard() { MLRG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~StreamGuard() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+/// Uploads a host complex128 array as device complex64.
+void upload_c64(const mlrg::HostArray& a, mlrg::DeviceBuffer<float2>& dst, cudaStream_t s) {
+  const std::size_t n = a.data.size();
+  mlrg::DeviceBuffer<double2> tmp(n);
+  MLRG_CUDA(cudaMemcpyAsync(tmp.get(), a.data.data(), n * sizeof(double2), cudaMemcpyHostToDevice, s));
+  dst.resize(n);
+  mlrg::ops::c128_to_c64(tmp.get(), dst.get(), static_cast<std::int64_t>(n), s);
+  MLRG_CUDA(cudaStreamSynchronize(s));
+}
+
+void download_c128(const float2* src, mlrg::HostArray& a, cudaStream_t s) {
+  const std::size_t n = a.data.size();
+  mlrg::DeviceBuffer<double2> tmp(n);
+  mlrg::ops::c64_to_c128(src, tmp.get(), static_cast<std::int64_t>(n), s);
+  MLRG_CUDA(cudaMemcpyAsync(a.data.data(), tmp.get(), n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));
+}
+
+/// forward_L = f2d_adj(fu2d(fu1d(u))) on full device arrays (operators.cpp:301-304).
+void forward_L(mlrg::Usfft& op, const float2* u, float2* out, mlrg::DeviceBuffer<float2>& mid,
+               mlrg::DeviceBuffer<float2>& proj) {
+  const mlrg::Geometry& g = op.geometry();
+  mid.resize(static_cast<std::size_t>(g.mid_shape().count()));
+  proj.resize(static_cast<std::size_t>(g.projection_shape().count()));
+  op.fu1d(u, mid.get(), g.n1);
+  mlrg::Fu2dEpilogue e;
+  e.out = proj.get();
+  e.ld_out = g.h;
+  op.fu2d(mid.get(), g.h, 0, g.h, e);
+  op.f2d(proj.get(), out, g.n_theta, true);
+}
+
+void adjoint_L(mlrg::Usfft& op, const float2* d, float2* out, mlrg::DeviceBuffer<float2>& mid,
+               mlrg::DeviceBuffer<float2>& proj) {  // operators.cpp:306-309
+  const mlrg::Geometry& g = op.geometry();
+  mid.resize(static_cast<std::size_t>(g.mid_shape().count()));
+  proj.resize(static_cast<std::size_t>(g.projection_shape().count()));
+  op.f2d(d, proj.get(), g.n_theta, false);
+  op.fu2d_adj(proj.get(), g.h, 0, g.h, mid.get(), g.h, 0);
+  op.fu1d_adj(mid.get(), out, g.n1);
+}
+
+void fill_counters(const mlrg::MemoCounters& c, uint64_t out[11]) {
+  const uint64_t v[11] = {c.lookups,      c.cache_hits,   c.remote_hits, c.misses,
+                          c.cache_comparisons, c.cache_probes, c.timeouts,    c.batches_sent,
+                          c.inserts_enqueued,  c.inserts_sent, c.inserts_dropped};
+  std::memcpy(out, v, sizeof(v));
+}
+
+int64_t copy_audit(const std::vector<mlrg::ChunkAudit>& a, int32_t* meta4, float* cs, int64_t cap) {
+  const int64_t n = static_cast<int64_t>(a.size());
+  for (int64_t i = 0; i < n && i < cap; ++i) {
+    const mlrg::ChunkAudit& e = a[static_cast<std::size_t>(i)];
+    if (meta4) {
+      meta4[4 * i + 0] = e.iteration;
+      meta4[4 * i + 1] = static_cast<int32_t>(e.op);
+      meta4[4 * i + 2] = static_cast<int32_t>(e.index);
+      meta4[4 * i + 3] = static_cast<int32_t>(e.outcome);
+    }
+    if (cs) cs[i] = e.cs;
+  }
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ============================== mlr.h ==============================
+
+const char* mlr_last_error(void) { return t_error.c_str(); }
+void mlr_free(char* text) { std::free(text); }
+
+mlr_config* mlr_config_new(void) {
+  return guarded_ptr<mlr_config>([] { return new mlr_config{}; });
+}
+
+mlr_config* mlr_config_from_file(const char* path) {
+  return guarded_ptr<mlr_config>([&] {
+    need(path != nullptr, "config path is null");
+    return new mlr_config{mlrg::RunConfig::from_file(path)};
+  });
+}
+
+int mlr_config_set(mlr_config* cfg, const char* key, const char* value) {
+  return guarded([&] {
+    need(cfg && key && value, "null argument");
+    cfg->rc.set(key, value);
+  });
+}
+
+char* mlr_config_dump(const mlr_config* cfg) {
+  return guarded_ptr<char>([&] {
+    need(cfg != nullptr, "null config");
+    return dup_text(cfg->rc.str());
+  });
+}
+
+void mlr_config_free(mlr_config* cfg) { delete cfg; }
+
+mlr_array* mlr_array_load(const char* path) {
+  return guarded_ptr<mlr_array>([&] {
+    need(path != nullptr, "array path is null");
+    return new mlr_array{mlrg::load_lvol(path)};
+  });
+}
+
+int mlr_array_save(const mlr_array* a, const char* path) {
+  try {
+    need(a && path, "null argument");
+    mlrg::save_lvol(path, a->a);
+    return MLR_OK;
+  } catch (const std::invalid_argument& e) {
+    t_error = e.what();
+    return MLR_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return MLR_ERR_IO;
+  }
+}
+
+int mlr_array_shape(const mlr_array* a, int64_t shape[3]) {
+  return guarded([&] {
+    need(a && shape, "null argument");
+    shape[0] = a->a.shape.d0;
+    shape[1] = a->a.shape.d1;
+    shape[2] = a->a.shape.d2;
+  });
+}
+
+const double* mlr_array_data(const mlr_array* a) {
+  if (a == nullptr) {
+    t_error = "null array";
+    return nullptr;
+  }
+  return reinterpret_cast<const double*>(a->a.data.data());
+}
+
+void mlr_array_free(mlr_array* a) { delete a; }
+
+mlr_array* mlr_make_phantom(const char* kind, int64_t d0, int64_t d1, int64_t d2, uint64_t seed) {
+  return guarded_ptr<mlr_array>([&] {
+    need(kind != nullptr, "phantom kind is null");
+    return new mlr_array{mlrg::make_phantom({d0, d1, d2}, kind, seed)};
+  });
+}
+
+mlr_array* mlr_project(const mlr_config* cfg, const mlr_array* volume) {
+  return guarded_ptr<mlr_array>([&] {
+    need(cfg && volume, "null argument");
+    cfg->rc.validate();
+    const mlrg::Geometry g = cfg->rc.make_geometry();
+    if (!(volume->a.shape == g.volume_shape()))
+      throw std::invalid_argument("volume shape " + volume->a.shape.str() +
+                                  " does not match the configured geometry " + g.volume_shape().str());
+    StreamGuard sg;
+    mlrg::Usfft op(g, sg.s);
+    mlrg::DeviceBuffer<float2> u, out, mid, proj;
+    upload_c64(volume->a, u, sg.s);
+    out.resize(static_cast<std::size_t>(g.projection_shape().count()));
+    forward_L(op, u.get(), out.get(), mid, proj);
+    auto* res = new mlr_array{mlrg::HostArray(g.projection_shape(), 0)};
+    download_c128(out.get(), res->a, sg.s);
+    return res;
+  });
+}
+
+mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const mlr_array* reference) {
+  return guarded_ptr<mlr_result>([&] {
+    need(cfg && data, "null argument");
+    cfg->rc.validate();
+    const mlrg::Geometry g = cfg->rc.make_geometry();
+    if (!(data->a.shape == g.projection_shape()))
+      throw std::invalid_argument("data shape " + data->a.shape.str() + " does not match the configured geometry " +
+                                  g.projection_shape().str());
+    if (reference && !(reference->a.shape == g.volume_shape()))
+      throw std::invalid_argument("reference shape " + reference->a.shape.str() +
+                                  " does not match the configured geometry " + g.volume_shape().str());
+    StreamGuard sg;
+    std::unique_ptr<mlrg::Engine> eng = build_engine(cfg->rc, g, sg.s);
+    mlrg::DeviceBuffer<float2> d, ref, u;
+    upload_c64(data->a, d, sg.s);
+    if (reference) upload_c64(reference->a, ref, sg.s);
+    u.resize(static_cast<std::size_t>(g.volume_shape().count()));
+    auto res = std::make_unique<mlr_result>();
+    res->report = mlrg::reconstruct(d.get(), cfg->rc.admm, *eng, reference ? ref.get() : nullptr, u.get());
+    res->audit = eng->audit_log();
+    res->u.a = mlrg::HostArray(g.volume_shape(), 0);
+    download_c128(u.get(), res->u.a, sg.s);
+    return res.release();
+  });
+}
+
+const mlr_array* mlr_result_volume(const mlr_result* r) {
+  if (r == nullptr) {
+    t_error = "null result";
+    return nullptr;
+  }
+  return &r->u;
+}
+
+char* mlr_result_csv(const mlr_result* r) {
+  return guarded_ptr<char>([&] {
+    need(r != nullptr, "null result");
+    return dup_text(r->report.csv());
+  });
+}
+
+int mlr_result_aborted(const mlr_result* r) { return (r != nullptr && r->report.aborted) ? 1 : 0; }
+
+char* mlr_result_abort_reason(const mlr_result* r) {
+  return guarded_ptr<char>([&] {
+    need(r != nullptr, "null result");
+    return dup_text(r->report.abort_reason);
+  });
+}
+
+void mlr_result_free(mlr_result* r) { delete r; }
+
+mlr_server* mlr_server_start(const char*, int, int, int, int) {
+  t_error = "mlr_server_start: the B200 build keeps the memo store in HBM; no TCP memo node is provided";
+  return nullptr;
+}
+int mlr_server_port(const mlr_server*) {
+  t_error = "mlr_server_port: no memo server in the B200 build";
+  return -1;
+}
+void mlr_server_stop(mlr_server* s) { delete s; }
+
+char* mlr_plan_offload(const char*, double, const char*) {
+  t_error = "mlr_plan_offload: the ADMM-Offload planner is outside the B200 build's scope";
+  return nullptr;
+}
+char* mlr_lru_baseline(const char*, double, uint64_t) {
+  t_error = "mlr_lru_baseline: the ADMM-Offload planner is outside the B200 build's scope";
+  return nullptr;
+}
+char* mlr_train_encoder(const mlr_config*, const char*, uint64_t, const char*) {
+  t_error = "mlr_train_encoder: the CNN encoder is outside the B200 build's scope (projection encoder only)";
+  return nullptr;
+}
+
+char* mlr_bench(const mlr_config* cfg) {  // capi.cpp:437-499 on the device engine
+  return guarded_ptr<char>([&] {
+    need(cfg != nullptr, "null config");
+    cfg->rc.validate();
+    const mlrg::RunConfig& rc = cfg->rc;
+    const mlrg::Geometry g = rc.make_geometry();
+    StreamGuard sg;
+    mlrg::DeviceBuffer<float2> u, out;
+    upload_c64(mlrg::make_phantom(g.volume_shape(), "blocks", 42), u, sg.s);
+    out.resize(static_cast<std::size_t>(g.mid_shape().count()));
+    using clock = std::chrono::steady_clock;
+    auto timed = [&](auto&& fn) {
+      const auto t0 = clock::now();
+      fn();
+      MLRG_CUDA(cudaStreamSynchronize(sg.s));
+      return std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+    };
+    mlrg::EngineConfig off = rc.engine;
+    off.memo_enabled = false;
+    mlrg::Engine plain(g, off, sg.s);
+    const double ms_compute = timed([&] { plain.fu1d(u.get(), out.get()); });
+    mlrg::EngineConfig on = rc.engine;
+    on.memo_enabled = true;
+    auto store = std::make_shared<mlrg::MemoStore>();
+    auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
+    auto c_miss = std::make_shared<mlrg::MemoClient>(rc.memo, store);
+    mlrg::Engine e_miss(g, on, sg.s, enc, c_miss);
+    const double ms_miss = timed([&] { e_miss.fu1d(u.get(), out.get()); });
+    e_miss.flush_inserts();
+    const mlrg::MemoCounters s_miss = c_miss->counters();
+    auto c_hit = std::make_shared<mlrg::MemoClient>(rc.memo, store);
+    mlrg::Engine e_hit(g, on, sg.s, enc, c_hit);
+    const double ms_remote = timed([&] { e_hit.fu1d(u.get(), out.get()); });
+    const mlrg::MemoCounters s_remote = c_hit->counters();
+    const double ms_cache = timed([&] { e_hit.fu1d(u.get(), out.get()); });
+    const mlrg::MemoCounters s_cache = c_hit->counters();
+    std::ostringstream o;
+    o << "case,lookups,misses,remote_hits,cache_hits,ms\n"
+      << "compute,0,0,0,0," << ms_compute << '\n'
+      << "miss," << s_miss.lookups << ',' << s_miss.misses << ',' << s_miss.remote_hits << ',' << s_miss.cache_hits
+      << ',' << ms_miss << '\n'
+      << "service_hit," << s_remote.lookups << ',' << s_remote.misses << ',' << s_remote.remote_hits << ','
+      << s_remote.cache_hits << ',' << ms_remote << '\n'
+      << "cache_hit," << (s_cache.lookups - s_remote.lookups) << ',' << (s_cache.misses - s_remote.misses) << ','
+      << (s_cache.remote_hits - s_remote.remote_hits) << ',' << (s_cache.cache_hits - s_remote.cache_hits) << ','
+      << ms_cache << '\n';
+    return dup_text(o.str());
+  });
+}
+
+// ============================== mlrg.h ==============================
+
+const char* mlrg_last_error(void) { return t_error.c_str(); }
+void mlrg_free(char* text) { std::free(text); }
+int mlrg_version(void) { return 1; }
+
+mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w, double phi,
+                          void* stream) {
+  return guarded_ptr<mlrg_ctx>([&] {
+    auto c = std::make_unique<mlrg_ctx>();
+    c->g = mlrg::Geometry::make(n1, n0, n2, n_theta, h, w, phi);
+    if (stream) {
+      c->s = static_cast<cudaStream_t>(stream);
+    } else {
+      MLRG_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    c->usfft = std::make_unique<mlrg::Usfft>(c->g, c->s);
+    return c.release();
+  });
+}
+
+void mlrg_ctx_destroy(mlrg_ctx* ctx) { delete ctx; }
+
+int mlrg_sync(mlrg_ctx* ctx) {
+  return guarded([&] {
+    need(ctx != nullptr, "null context");
+    MLRG_CUDA(cudaStreamSynchronize(ctx->s));
+  });
+}
+
+int mlrg_fu1d(mlrg_ctx* ctx, const void* u, void* out, int64_t d0) {
+  return guarded([&] {
+    need(ctx && u && out && d0 >= 1, "mlrg_fu1d: bad argument");
+    ctx->usfft->fu1d(static_cast<const float2*>(u), static_cast<float2*>(out), d0);
+  });
+}
+
+int mlrg_fu1d_adj(mlrg_ctx* ctx, const void* v, void* out, int64_t d0) {
+  return guarded([&] {
+    need(ctx && v && out && d0 >= 1, "mlrg_fu1d_adj: bad argument");
+    ctx->usfft->fu1d_adj(static_cast<const float2*>(v), static_cast<float2*>(out), d0);
+  });
+}
+
+int mlrg_fu2d(mlrg_ctx* ctx, const void* v, const void* d_hat, void* out, int64_t d1) {
+  return guarded([&] {
+    need(ctx && v && out && d1 >= 1, "mlrg_fu2d: bad argument");
+    mlrg::Fu2dEpilogue e;
+    e.out = static_cast<float2*>(out);
+    e.ld_out = d1;
+    e.sub = static_cast<const float2*>(d_hat);
+    e.ld_sub = d1;
+    ctx->usfft->fu2d(static_cast<const float2*>(v), d1, 0, d1, e);
+  });
+}
+
+int mlrg_fu2d_adj(mlrg_ctx* ctx, const void* p, void* out, int64_t d1) {
+  return guarded([&] {
+    need(ctx && p && out && d1 >= 1, "mlrg_fu2d_adj: bad argument");
+    ctx->usfft->fu2d_adj(static_cast<const float2*>(p), d1, 0, d1, static_cast<float2*>(out), d1, 0);
+  });
+}
+
+int mlrg_f2d(mlrg_ctx* ctx, const void* p, void* out, int64_t d0, int adjoint) {
+  return guarded([&] {
+    need(ctx && p && out && d0 >= 1, "mlrg_f2d: bad argument");
+    ctx->usfft->f2d(static_cast<const float2*>(p), static_cast<float2*>(out), d0, adjoint != 0);
+  });
+}
+
+int mlrg_forward_L(mlrg_ctx* ctx, const void* u, void* out) {
+  return guarded([&] {
+    need(ctx && u && out, "mlrg_forward_L: bad argument");
+    forward_L(*ctx->usfft, static_cast<const float2*>(u), static_cast<float2*>(out), ctx->scratch_mid,
+              ctx->scratch_proj);
+  });
+}
+
+int mlrg_adjoint_L(mlrg_ctx* ctx, const void* d, void* out) {
+  return guarded([&] {
+    need(ctx && d && out, "mlrg_adjoint_L: bad argument");
+    adjoint_L(*ctx->usfft, static_cast<const float2*>(d), static_cast<float2*>(out), ctx->scratch_mid,
+              ctx->scratch_proj);
+  });
+}
+
+int mlrg_grad(mlrg_ctx* ctx, const void* u, void* g0, void* g1, void* g2) {
+  return guarded([&] {
+    need(ctx && u && g0 && g1 && g2, "mlrg_grad: bad argument");
+    mlrg::Field3 f{{static_cast<float2*>(g0), static_cast<float2*>(g1), static_cast<float2*>(g2)}};
+    mlrg::ops::grad(static_cast<const float2*>(u), f, {ctx->g.n1, ctx->g.n0, ctx->g.n2}, ctx->s);
+  });
+}
+
+int mlrg_div(mlrg_ctx* ctx, const void* g0, const void* g1, const void* g2, void* out) {
+  return guarded([&] {
+    need(ctx && g0 && g1 && g2 && out, "mlrg_div: bad argument");
+    mlrg::CField3 f;
+    f.c[0] = static_cast<const float2*>(g0);
+    f.c[1] = static_cast<const float2*>(g1);
+    f.c[2] = static_cast<const float2*>(g2);
+    mlrg::ops::div(f, static_cast<float2*>(out), {ctx->g.n1, ctx->g.n0, ctx->g.n2}, ctx->s);
+  });
+}
+
+int mlrg_encode(mlrg_ctx* ctx, int op, const void* x, int64_t chunk_extent, int key_dim, uint64_t seed,
+                float* keys, double* norms, int64_t n_slabs) {
+  return guarded([&] {
+    need(ctx && x && keys && norms && op >= 0 && op <= 5 && chunk_extent >= 1, "mlrg_encode: bad argument");
+    const mlrg::OpId oid = static_cast<mlrg::OpId>(op);
+    const mlrg::Geometry& g = ctx->g;
+    const mlrg::Shape3 in = oid == mlrg::OpId::fu1d ? g.volume_shape()
+                            : (oid == mlrg::OpId::fu1d_adj || oid == mlrg::OpId::fu2d) ? g.mid_shape()
+                                                                                         : g.projection_shape();
+    const int axis = mlrg::chunk_axis_of(oid);
+    const int64_t len = in.extent(axis);
+    const int64_t ns = (len + chunk_extent - 1) / chunk_extent;
+    need(n_slabs == ns, "mlrg_encode: n_slabs does not match the slab count");
+    mlrg::Encoder enc(key_dim, seed);
+    mlrg::DeviceBuffer<float> dkeys(static_cast<std::size_t>(ns * key_dim));
+    mlrg::DeviceBuffer<double> dnorm(static_cast<std::size_t>(ns));
+    for (int64_t c0 = 0; c0 < ns;) {
+      const int64_t e = std::min(chunk_extent, len - c0 * chunk_extent);
+      int64_t c1 = c0;
+      while (c1 < ns && std::min(chunk_extent, len - c1 * chunk_extent) == e) ++c1;
+      mlrg::Shape3 sh = in;
+      (axis == 0 ? sh.d0 : sh.d1) = e;
+      enc.register_shape(sh, ctx->s);
+      std::vector<int64_t> starts;
+      for (int64_t c = c0; c < c1; ++c) starts.push_back(c * chunk_extent);
+      mlrg::DeviceBuffer<double> work(mlrg::ops::encode_work_doubles(static_cast<int>(c1 - c0), key_dim));
+      mlrg::ops::encode(static_cast<const float2*>(x), {in.d0, in.d1, in.d2, axis, 0, e}, starts.data(),
+                        static_cast<int>(c1 - c0), enc.device_matrix(sh), key_dim, work.get(),
+                        dkeys.get() + c0 * key_dim, dnorm.get() + c0, ctx->s);
+      MLRG_CUDA(cudaStreamSynchronize(ctx->s));
+      c0 = c1;
+    }
+    MLRG_CUDA(cudaMemcpy(keys, dkeys.get(), sizeof(float) * ns * key_dim, cudaMemcpyDeviceToHost));
+    MLRG_CUDA(cudaMemcpy(norms, dnorm.get(), sizeof(double) * ns, cudaMemcpyDeviceToHost));
+    for (int64_t c = 0; c < ns; ++c) {
+      mlrg::slot_mix(keys + c * key_dim, key_dim, seed, c, oid);
+      norms[c] = std::sqrt(norms[c]);
+    }
+  });
+}
+
+mlrg_recon* mlrg_reconstruct(const char* config_text, const void* d, const void* reference, void* u_out,
+                             void* stream) {
+  return guarded_ptr<mlrg_recon>([&] {
+    need(config_text && d && u_out, "mlrg_reconstruct: bad argument");
+    const mlrg::RunConfig rc = mlrg::RunConfig::from_text(config_text);
+    rc.validate();
+    const mlrg::Geometry g = rc.make_geometry();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::unique_ptr<StreamGuard> own;
+    if (!s) {
+      own = std::make_unique<StreamGuard>();
+      s = own->s;
+    }
+    std::unique_ptr<mlrg::Engine> eng = build_engine(rc, g, s);
+    auto r = std::make_unique<mlrg_recon>();
+    r->report = mlrg::reconstruct(static_cast<const float2*>(d), rc.admm, *eng,
+                                  static_cast<const float2*>(reference), static_cast<float2*>(u_out));
+    r->audit = eng->audit_log();
+    if (eng->memo()) r->counters = eng->memo()->counters();
+    return r.release();
+  });
+}
+
+char* mlrg_recon_csv(const mlrg_recon* r) {
+  return guarded_ptr<char>([&] {
+    need(r != nullptr, "null result");
+    return dup_text(r->report.csv());
+  });
+}
+int mlrg_recon_aborted(const mlrg_recon* r) { return (r && r->report.aborted) ? 1 : 0; }
+char* mlrg_recon_abort_reason(const mlrg_recon* r) {
+  return guarded_ptr<char>([&] {
+    need(r != nullptr, "null result");
+    return dup_text(r->report.abort_reason);
+  });
+}
+int64_t mlrg_recon_audit(const mlrg_recon* r, int32_t* meta4, float* cs, int64_t cap) {
+  if (!r) return -1;
+  return copy_audit(r->audit, meta4, cs, cap);
+}
+int mlrg_recon_counters(const mlrg_recon* r, uint64_t out[11]) {
+  return guarded([&] {
+    need(r && out, "null argument");
+    fill_counters(r->counters, out);
+  });
+}
+void mlrg_recon_free(mlrg_recon* r) { delete r; }
+
+mlrg_solver* mlrg_solver_new(const char* config_text, const void* d, const void* reference, void* stream) {
+  return guarded_ptr<mlrg_solver>([&] {
+    need(config_text && d, "mlrg_solver_new: bad argument");
+    const mlrg::RunConfig rc = mlrg::RunConfig::from_text(config_text);
+    rc.validate();
+    const mlrg::Geometry g = rc.make_geometry();
+    auto sv = std::make_unique<mlrg_solver>();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) {
+      MLRG_CUDA(cudaStreamCreateWithFlags(&sv->own, cudaStreamNonBlocking));
+      s = sv->own;
+    }
+    sv->eng = build_engine(rc, g, s);
+    sv->solver = std::make_unique<mlrg::Solver>(static_cast<const float2*>(d), rc.admm, *sv->eng,
+                                                static_cast<const float2*>(reference));
+    MLRG_CUDA(cudaStreamSynchronize(s));
+    return sv.release();
+  });
+}
+
+int mlrg_solver_step(mlrg_solver* s, int* aborted) {
+  return guarded([&] {
+    need(s != nullptr, "null solver");
+    const bool ok = s->solver->step();
+    MLRG_CUDA(cudaStreamSynchronize(s->eng->stream()));
+    if (aborted) *aborted = ok ? 0 : 1;
+  });
+}
+
+int mlrg_solver_volume(mlrg_solver* s, void* u_out) {
+  return guarded([&] {
+    need(s && u_out, "null argument");
+    const std::size_t n = static_cast<std::size_t>(s->eng->geometry().volume_shape().count());
+    MLRG_CUDA(cudaMemcpyAsync(u_out, s->solver->u(), n * sizeof(float2), cudaMemcpyDeviceToDevice, s->eng->stream()));
+    MLRG_CUDA(cudaStreamSynchronize(s->eng->stream()));
+  });
+}
+
+char* mlrg_solver_csv(const mlrg_solver* s) {
+  return guarded_ptr<char>([&] {
+    need(s != nullptr, "null solver");
+    return dup_text(s->solver->report().csv());
+  });
+}
+
+int mlrg_solver_counters(const mlrg_solver* s, uint64_t out[11]) {
+  return guarded([&] {
+    need(s && out, "null argument");
+    fill_counters(s->eng->memo() ? s->eng->memo()->counters() : mlrg::MemoCounters{}, out);
+  });
+}
+
+int64_t mlrg_solver_audit(const mlrg_solver* s, int32_t* meta4, float* cs, int64_t cap) {
+  if (!s) return -1;
+  return copy_audit(s->eng->audit_log(), meta4, cs, cap);
+}
+
+void mlrg_solver_free(mlrg_solver* s) { delete s; }
+
+int64_t mlrg_result_audit(const struct mlr_result* r, int32_t* meta4, float* cs, int64_t cap) {
+  if (!r) return -1;
+  return copy_audit(r->audit, meta4, cs, cap);
+}
+
+mlrg_memo* mlrg_memo_new(float tau, int nprobe, uint64_t insert_cap, uint64_t coalesce_bytes, int global_cache,
+                         int nlist, int train_size) {
+  return guarded_ptr<mlrg_memo>([&] {
+    mlrg::IvfConfig ic;
+    ic.nlist = nlist;
+    ic.train_size = train_size;
+    ic.nprobe = nprobe;
+    mlrg::MemoClientConfig mc;
+    mc.tau = tau;
+    mc.nprobe = nprobe;
+    mc.insert_queue_cap = insert_cap;
+    mc.coalesce_bytes = coalesce_bytes;
+    mc.global_cache = global_cache != 0;
+    auto m = std::make_unique<mlrg_memo>();
+    m->store = std::make_shared<mlrg::MemoStore>(ic);
+    m->client = std::make_unique<mlrg::MemoClient>(mc, m->store);
+    return m.release();
+  });
+}
+
+void mlrg_memo_free(mlrg_memo* m) { delete m; }
+
+int mlrg_memo_lookup(mlrg_memo* m, int64_t n, int key_dim, const float* keys, const int64_t* locations,
+                     const int32_t* ops, const uint64_t* value_bytes, int32_t* outcome, float* cs,
+                     uint64_t* value_id) {
+  return guarded([&] {
+    need(m && keys && locations && ops && value_bytes && outcome && cs && value_id, "null argument");
+    std::vector<mlrg::MemoKey> ks(static_cast<std::size_t>(n));
+    std::vector<std::size_t> vb(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      ks[static_cast<std::size_t>(i)].values.assign(keys + i * key_dim, keys + (i + 1) * key_dim);
+      ks[static_cast<std::size_t>(i)].location = locations[i];
+      ks[static_cast<std::size_t>(i)].op = static_cast<mlrg::OpId>(ops[i]);
+      vb[static_cast<std::size_t>(i)] = value_bytes[i];
+    }
+    const std::vector<mlrg::MemoDecision> d = m->client->lookup_batch(ks, vb);
+    for (int64_t i = 0; i < n; ++i) {
+      outcome[i] = static_cast<int32_t>(d[static_cast<std::size_t>(i)].outcome);
+      cs[i] = d[static_cast<std::size_t>(i)].cs;
+      value_id[i] = d[static_cast<std::size_t>(i)].value_id;
+    }
+  });
+}
+
+int mlrg_memo_insert(mlrg_memo* m, int key_dim, const float* key, uint64_t value_bytes) {
+  try {
+    need(m && key, "null argument");
+    mlrg::MemoKey k;
+    k.values.assign(key, key + key_dim);
+    const bool staged = m->client->insert_async(k, [&] {
+      mlrg::ValueRef v;
+      v.bytes = value_bytes;
+      return v;
+    });
+    return staged ? 1 : 0;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return -code_for(e);
+  }
+}
+
+int mlrg_memo_flush(mlrg_memo* m) {
+  return guarded([&] {
+    need(m != nullptr, "null memo");
+    m->client->flush_inserts();
+  });
+}
+
+int mlrg_memo_counters(const mlrg_memo* m, uint64_t out[11]) {
+  return guarded([&] {
+    need(m && out, "null argument");
+    fill_counters(m->client->counters(), out);
+  });
+}
+
+int mlrg_projection_matrix(int64_t d0, int64_t d1, int64_t d2, int key_dim, uint64_t seed, float* out,
+                           int64_t count) {
+  return guarded([&] {
+    need(out != nullptr && count >= 0, "null argument");
+    const std::vector<float> m = mlrg::projection_matrix({d0, d1, d2}, key_dim, seed);
+    need(count <= static_cast<int64_t>(m.size()), "count exceeds the matrix size");
+    std::memcpy(out, m.data(), static_cast<std::size_t>(count) * sizeof(float));
+  });
+}
+
+int mlrg_slot_mix(float* key, int key_dim, uint64_t seed, int64_t location, int op) {
+  return guarded([&] {
+    need(key != nullptr, "null key");
+    mlrg::slot_mix(key, key_dim, seed, location, static_cast<mlrg::OpId>(op));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Device plumbing for the host side: CUDA error mapping to exceptions, owning
+// device/pinned buffers, and the deterministic two-level reduction buffer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace mlrg {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+/// Launch accounting and opt-in per-kernel CUDA-event timing (bench.py reads
+/// both through mlrg_prof_* / mlrg_launch_count).
+namespace prof {
+void count_launch();
+bool enabled();
+/// Brackets one launch of `name` on `s` with events when profiling is on.
+void begin(const char* name, cudaStream_t s);
+void end(const char* name, cudaStream_t s);
+}  // namespace prof
+
+#define MLRG_CUDA(call) ::mlrg::cuda_check((call), #call)
+#define MLRG_LAUNCH_CHECK(name) (::mlrg::prof::count_launch(), ::mlrg::cuda_check(cudaGetLastError(), name))
+
+/// Owning device allocation (cudaMalloc), movable, zero-length allowed.
+template <class T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t n) { resize(n); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = std::exchange(o.p_, nullptr);
+      n_ = std::exchange(o.n_, 0);
+    }
+    return *this;
+  }
+  void resize(std::size_t n) {
+    if (n == n_) return;
+    release();
+    if (n > 0) MLRG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    n_ = n;
+  }
+  void upload(const T* host, std::size_t n, cudaStream_t s) {
+    resize(n);
+    if (n) MLRG_CUDA(cudaMemcpyAsync(p_, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  void zero(cudaStream_t s) {
+    if (n_) MLRG_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+  }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+/// Owning page-locked host allocation for D2H of small results.
+template <class T>
+class PinnedBuffer {
+ public:
+  PinnedBuffer() = default;
+  ~PinnedBuffer() {
+    if (p_) cudaFreeHost(p_);
+  }
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  void reserve(std::size_t n) {
+    if (n <= n_) return;
+    if (p_) cudaFreeHost(p_);
+    p_ = nullptr;
+    MLRG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    n_ = n;
+  }
+  T* get() const { return p_; }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+/// Per-CTA partial sums written by the fused kernels; the host adds them in
+/// CTA order, so every reduction is deterministic (no float atomics).
+class Partials {
+ public:
+  static constexpr int kMaxSlots = 1 << 16;
+  Partials() {
+    dev_.resize(static_cast<std::size_t>(kMaxSlots));
+    host_.reserve(static_cast<std::size_t>(kMaxSlots));
+  }
+  double* dev() const { return dev_.get(); }
+  /// Copies `count` doubles back (synchronising `s`) and returns the column sums
+  /// of a [count / nv][nv] table.
+  std::vector<double> sum(int count, int nv, cudaStream_t s) {
+    if (count > kMaxSlots) throw std::logic_error("Partials: too many slots");
+    MLRG_CUDA(cudaMemcpyAsync(host_.get(), dev_.get(), static_cast<std::size_t>(count) * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> out(static_cast<std::size_t>(nv), 0.0);
+    for (int i = 0; i < count; ++i) out[static_cast<std::size_t>(i % nv)] += host_.get()[i];
+    return out;
+  }
+
+ private:
+  DeviceBuffer<double> dev_;
+  PinnedBuffer<double> host_;
+};
+
+/// Number of SMs of the current device (grids are sized in multiples of it).
+int sm_count();
+
+}  // namespace mlrg

@@ -1,0 +1,94 @@
+// Device operator engine: the B200 replacement of the reference's
+// OperatorEngine (scalerun.hpp:61-116, scalerun.cpp:168-287). Arrays are full
+// device arrays; slabs are views (no split/merge copies). With memoisation on,
+// every memoizable application encodes all slabs in one device GEMM, makes
+// the reference's decisions on the host, computes the misses in as few
+// launches as possible (contiguous miss runs batched), materialises hits from
+// the HBM value arena and stages the miss values for the next flush.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "encoder.hpp"
+#include "geometry.hpp"
+#include "memo.hpp"
+#include "usfft.hpp"
+
+namespace mlrg {
+
+struct EngineConfig {  // scalerun.hpp:27-42
+  int workers = 1;                  // accepted for drop-in configs; the device path ignores it
+  std::int64_t chunk_extent = 16;
+  bool memo_enabled = false;
+  bool flush_after_apply = false;
+};
+
+struct ChunkAudit {  // scalerun.hpp:45-54
+  OpId op = OpId::fu1d;
+  int axis = 0;
+  std::int64_t index = 0, extent = 0;
+  MemoOutcome outcome = MemoOutcome::miss;
+  float cs = 0.0f;
+  int iteration = 0;
+  float rel_err = -1.0f;
+};
+
+/// Partition axis of each operator's input (scalerun.cpp:29-42).
+int chunk_axis_of(OpId op);
+
+class Engine {
+ public:
+  Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_ptr<Encoder> enc = nullptr,
+         std::shared_ptr<MemoClient> memo = nullptr);
+
+  const Geometry& geometry() const { return g_; }
+  Usfft& usfft() { return usfft_; }
+  cudaStream_t stream() const { return s_; }
+  MemoClient* memo() const { return memo_.get(); }
+
+  void set_iteration(int it) { iteration_ = it; }
+  void flush_inserts();
+  const std::vector<ChunkAudit>& audit_log() const { return audit_; }
+
+  // Full-array applications (scalerun.hpp:77-92).
+  void fu1d(const float2* u, float2* out, bool memoize = true);
+  void fu1d_adj(const float2* v, float2* out, bool memoize = true);
+  void fu2d(const float2* v, float2* out, bool memoize = true);
+  void fu2d_fused(const float2* v, const float2* d_hat, float2* out, bool memoize = true);
+  void fu2d_adj(const float2* p, float2* out, bool memoize = true);
+  void f2d(const float2* p, float2* out, bool memoize = true);
+  void f2d_adj(const float2* p, float2* out, bool memoize = true);
+
+  /// Non-memoized fu2d whose output is only reduced: {sum |fu2d(v) - sub|^2,
+  /// Re<dot, fu2d(v) - sub>} (line search terms admm.cpp:95-102 and the data
+  /// term of objective(), admm.cpp:190-195).
+  std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot);
+
+ private:
+  void apply(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, bool memoize);
+  void compute(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, std::int64_t start,
+               std::int64_t extent);
+  Shape3 in_shape(OpId op) const;
+  Shape3 out_shape(OpId op) const;
+  void register_shapes();
+
+  Geometry g_;
+  EngineConfig cfg_;
+  cudaStream_t s_;
+  Usfft usfft_;
+  std::shared_ptr<Encoder> enc_;
+  std::shared_ptr<MemoClient> memo_;
+  int iteration_ = 0;
+  std::vector<ChunkAudit> audit_;
+  DeviceBuffer<double> enc_work_, enc_norms_;
+  DeviceBuffer<float> enc_keys_;
+  PinnedBuffer<float> keys_host_;
+  PinnedBuffer<double> norms_host_;
+};
+
+}  // namespace mlrg

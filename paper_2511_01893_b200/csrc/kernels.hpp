@@ -1,0 +1,108 @@
+// Host launchers for the fused ADMM kernels (vecops.cu) and the memo-layer
+// kernels (memo_kernels.cu). Every reduction writes nv doubles per CTA into
+// `partials`; the launcher returns the number of doubles written so the host
+// sums them in CTA order (deterministic, no float atomics).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define MLRG_HD __host__ __device__
+#else
+#define MLRG_HD
+#endif
+
+namespace mlrg {
+
+/// Volume extents for the stencil kernels (row-major (n1, n0, n2)).
+struct Dims {
+  std::int64_t n1 = 0, n0 = 0, n2 = 0;
+  std::int64_t count() const { return n1 * n0 * n2; }
+};
+
+/// Three-component field (GradField, operators.hpp:17-30), one plane per axis.
+struct Field3 {
+  float2* c[3] = {nullptr, nullptr, nullptr};
+};
+struct CField3 {
+  const float2* c[3] = {nullptr, nullptr, nullptr};
+  CField3() = default;
+  CField3(const Field3& f) : c{f.c[0], f.c[1], f.c[2]} {}
+};
+
+namespace ops {
+
+/// g = psi - lambda * lc (admm.cpp:64 with the lazy lambda scale folded in lc).
+void g_init(CField3 psi, CField3 lam, Field3 g, std::int64_t n, float lc, cudaStream_t s);
+
+/// G -= rho * div(grad(u) - g) (admm.cpp:144-147) with partials
+/// [|grad u - g|^2, |G|^2, Re<p_prev, G - G_prev>] (the last one only when
+/// p_prev/G_prev are non-null).
+int grad_update(const float2* u, CField3 g, float2* G, const float2* p_prev, const float2* G_prev, Dims d,
+                float rho, double* partials, cudaStream_t s);
+
+/// p = -G + beta * p_prev (admm.cpp:86-93) with partials
+/// [|grad p|^2, Re<grad u - g, grad p>] (admm.cpp:95-102).
+int direction(const float2* G, const float2* p_prev, float beta, const float2* u, CField3 g, float2* p, Dims d,
+              double* partials, cudaStream_t s);
+
+/// y += a * x (admm.cpp:108-110).
+void axpy(float2* y, const float2* x, float a, std::int64_t n, cudaStream_t s);
+
+/// Fused rsp_update + multiplier update (admm.cpp:154-181):
+/// psi_new = shrink(grad u + lam*lc, thr); lam += rho_over_lam_scale * (grad u - psi_new).
+/// Partials [|grad u - psi_new|^2, |psi_new - psi_old|^2].
+int rsp_multiplier(const float2* u, Field3 lam, CField3 psi_old, Field3 psi_new, Dims d, float lc, float thr,
+                   float rho_over_scale, double* partials, cudaStream_t s);
+
+/// Isotropic TV: partials [sum sqrt(sum_c |grad_c u|^2)] (admm.cpp:39-46).
+int tv_norm(const float2* u, Dims d, double* partials, cudaStream_t s);
+
+/// Partials [|a - b|^2, |a|^2] (b may be null).
+int norm2_diff(const float2* a, const float2* b, std::int64_t n, double* partials, cudaStream_t s);
+
+/// a -= b with partials [|a - b|^2] (resid = d_pred - d, admm.cpp:126-128).
+int sub_norm(float2* a, const float2* b, std::int64_t n, double* partials, cudaStream_t s);
+
+/// Forward differences (operators.cpp:311-328) and the negative-adjoint
+/// divergence (operators.cpp:330-352), materialised (tests and the C-ABI).
+void grad(const float2* u, Field3 out, Dims d, cudaStream_t s);
+void div(CField3 g, float2* out, Dims d, cudaStream_t s);
+
+/// complex128 <-> complex64 conversion of host-interleaved arrays on the device.
+void c128_to_c64(const double2* in, float2* out, std::int64_t n, cudaStream_t s);
+void c64_to_c128(const float2* in, double2* out, std::int64_t n, cudaStream_t s);
+
+/// Elementwise scale / copy helpers.
+void scale(float2* y, const float2* x, float a, std::int64_t n, cudaStream_t s);
+
+// ---- memo layer ----
+
+/// A chunk of a full row-major array (split_chunks, array.cpp:30-63): slab
+/// `start..start+extent` along axis 0 or 1.
+struct SlabGeom {
+  std::int64_t d0 = 0, d1 = 0, d2 = 0;
+  int axis = 0;
+  std::int64_t start = 0, extent = 0;
+  MLRG_HD std::int64_t count() const { return axis == 0 ? extent * d1 * d2 : d0 * extent * d2; }
+};
+
+/// keys[s][r] = sum_i P[r][i] Re x_s[i] + P[r][n+i] Im x_s[i] for `ns` slabs of
+/// one shape (encoder.cpp:405-422), float keys; norms2[s] = sum |x_s|^2 (double).
+/// `starts` lists each slab's start along the split axis; `work` needs
+/// encode_work_doubles(ns, kd) doubles.
+void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+            double* work, float* keys, double* norms2, cudaStream_t s);
+std::size_t encode_work_doubles(int ns, int kd);
+
+/// out[slab] = value * scale - sub[slab] (sub may be null) (scalerun.cpp:250-255).
+void slab_materialize(float2* out, SlabGeom g, const float2* value, float scale, const float2* sub, cudaStream_t s);
+/// value = out[slab] (contiguous chunk order).
+void slab_store(const float2* out, SlabGeom g, float2* value, cudaStream_t s);
+/// out[slab] -= sub[slab].
+void slab_sub(float2* out, SlabGeom g, const float2* sub, cudaStream_t s);
+
+}  // namespace ops
+}  // namespace mlrg

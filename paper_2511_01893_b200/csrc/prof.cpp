@@ -1,0 +1,94 @@
+// Kernel launch counter and opt-in CUDA-event timers per hot kernel. Events
+// are recorded on the launching stream, so a timer measures exactly the
+// kernel's device time span even when the host runs ahead.
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "device.hpp"
+#include "mlr.h"
+#include "mlrg.h"
+
+namespace mlrg::prof {
+
+namespace {
+std::atomic<std::uint64_t> g_launches{0};
+std::atomic<bool> g_enabled{false};
+std::mutex g_mx;
+struct Span {
+  cudaEvent_t a, b;
+};
+std::map<std::string, std::vector<Span>>& spans() {
+  static std::map<std::string, std::vector<Span>> m;
+  return m;
+}
+std::map<std::string, cudaEvent_t>& open_events() {
+  static std::map<std::string, cudaEvent_t> m;
+  return m;
+}
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool enabled() { return g_enabled.load(std::memory_order_relaxed); }
+
+void begin(const char* name, cudaStream_t s) {
+  if (!enabled()) return;
+  cudaEvent_t e;
+  MLRG_CUDA(cudaEventCreate(&e));
+  MLRG_CUDA(cudaEventRecord(e, s));
+  std::lock_guard<std::mutex> lk(g_mx);
+  open_events()[name] = e;
+}
+
+void end(const char* name, cudaStream_t s) {
+  if (!enabled()) return;
+  cudaEvent_t e;
+  MLRG_CUDA(cudaEventCreate(&e));
+  MLRG_CUDA(cudaEventRecord(e, s));
+  std::lock_guard<std::mutex> lk(g_mx);
+  auto it = open_events().find(name);
+  if (it == open_events().end()) return;
+  spans()[name].push_back({it->second, e});
+  open_events().erase(it);
+}
+
+}  // namespace mlrg::prof
+
+extern "C" {
+
+uint64_t mlrg_launch_count(void) { return mlrg::prof::g_launches.load(); }
+
+void mlrg_prof_enable(int on) { mlrg::prof::g_enabled.store(on != 0); }
+
+void mlrg_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(mlrg::prof::g_mx);
+  for (auto& [k, v] : mlrg::prof::spans())
+    for (auto& s : v) {
+      cudaEventDestroy(s.a);
+      cudaEventDestroy(s.b);
+    }
+  mlrg::prof::spans().clear();
+}
+
+int mlrg_prof_query(const char* name, double* total_ms, int64_t* count) {
+  std::lock_guard<std::mutex> lk(mlrg::prof::g_mx);
+  double tot = 0.0;
+  int64_t n = 0;
+  auto it = mlrg::prof::spans().find(name ? name : "");
+  if (it != mlrg::prof::spans().end())
+    for (auto& s : it->second) {
+      if (cudaEventSynchronize(s.b) != cudaSuccess) return MLR_ERR_RUNTIME;
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, s.a, s.b) != cudaSuccess) return MLR_ERR_RUNTIME;
+      tot += ms;
+      ++n;
+    }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = n;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// The laminography USFFT operators on one B200: fu1d / fu1d_adj (1D gridding
+// along axis 1 of the volume), fu2d / fu2d_adj (2D gridding per detector
+// row), and the centred unitary 2D DFT f2d / f2d_adj. All arrays are device
+// complex64 (float2) in the reference's row-major layouts (array.hpp:38-73).
+//
+// Reference operators replaced (numerically, to fp32 rounding):
+//   nufft::fu1d_gridding      nufft.cpp:107-134
+//   nufft::fu1d_adj_gridding  nufft.cpp:136-162
+//   nufft::fu2d_gridding      nufft.cpp:183-225  (+ fused_sub_fu2d, operators.cpp:285-299)
+//   nufft::fu2d_adj_gridding  nufft.cpp:227-267
+//   f2d / f2d_adj             operators.cpp:39-74, 249-259
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.hpp"
+#include "geometry.hpp"
+
+namespace mlrg {
+
+/// Output stage of fu2d: val = fac * acc - sub; stores val to `out` when set
+/// and, when `reduce` is set, accumulates sum |val|^2 and Re<dot, val> into
+/// the per-CTA partials (2 doubles per CTA, summed across row batches).
+struct Fu2dEpilogue {
+  float2* out = nullptr;
+  std::int64_t ld_out = 0, k0_out = 0;
+  const float2* sub = nullptr;
+  std::int64_t ld_sub = 0, k0_sub = 0;
+  const float2* dot = nullptr;
+  std::int64_t ld_dot = 0, k0_dot = 0;
+  bool reduce = false;
+};
+
+class Usfft {
+ public:
+  static constexpr int kRowBatch = 16;  // detector rows per fu2d grid batch
+
+  Usfft(const Geometry& g, cudaStream_t stream);
+  ~Usfft();
+  Usfft(const Usfft&) = delete;
+  Usfft& operator=(const Usfft&) = delete;
+
+  const Geometry& geometry() const { return g_; }
+  cudaStream_t stream() const { return stream_; }
+
+  /// u: contiguous (d0, n0, n2) -> out (d0, h, n2).
+  void fu1d(const float2* u, float2* out, std::int64_t d0);
+  /// v: contiguous (d0, h, n2) -> out (d0, n0, n2).
+  void fu1d_adj(const float2* v, float2* out, std::int64_t d0);
+
+  /// Rows [k0, k0+nk) of an (n1, ld, n2) array -> rows of an (n_theta, ., w)
+  /// array via the epilogue. Returns the number of partial doubles written
+  /// (2 per gather CTA) when epi.reduce is set, else 0.
+  int fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t nk, const Fu2dEpilogue& epi);
+  /// Rows [k0, k0+nk) of an (n_theta, ld, w) array -> rows [k0_out, k0_out+nk)
+  /// of an (n1, ld_out, n2) array.
+  void fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
+                std::int64_t ld_out, std::int64_t k0_out);
+
+  /// Centred unitary 2D DFT of `count` contiguous (h, w) planes.
+  void f2d(const float2* p, float2* out, std::int64_t count, bool adjoint);
+
+  Partials& partials() { return partials_; }
+  int reduce_grid() const;  // CTAs of an elementwise reduction kernel
+
+ private:
+  struct Tables;
+  Geometry g_;
+  cudaStream_t stream_;
+  Tables* t_;
+  Partials partials_;
+};
+
+}  // namespace mlrg

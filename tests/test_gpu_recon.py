@@ -1,0 +1,78 @@
+"""End-to-end reconstructions on the device against the reference's own runs
+(tests/golden/recon_*.npz): the same memo hit/miss sequence, the same abort
+behaviour, per-iteration losses, and rel-L2(u) <= 1e-4 (BASELINE.json
+north_star tolerance, fp32)."""
+import numpy as np
+import pytest
+
+from conftest import golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_rows(z):
+    lines = str(z["txt_report_csv"]).strip().splitlines()
+    return [[float(v) for v in l.split(",")] for l in lines[1:]]
+
+
+def config_text(n, nt, n_outer, memo):
+    return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
+            f"memoization={memo}\nnudft_path=gridding\n")
+
+
+@pytest.mark.parametrize("case,memo", [("recon_c16_memo_grid", "local"), ("recon_c32_memo_grid", "local"),
+                                       ("recon_c32_off_grid", "off"), ("recon_c64_off_grid", "off"),
+                                       ("recon_cfg1_memo_direct", "local")])
+def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo):
+    torch = torch_cuda
+    z = golden(case)
+    n = z["phantom"].shape[0]
+    nt = z["data"].shape[0]
+    d = torch.from_numpy(z["data"]).cuda()
+    ref = torch.from_numpy(z["phantom"]).cuda()
+    u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+    r = mlrg.reconstruct_device(config_text(n, nt, 10, memo), d, u, reference=ref)
+    aborted = bool(int(str(z["txt_aborted_txt"]).split()[0]))
+    assert r.aborted == aborted
+    if memo != "off":
+        meta, _ = r.audit()
+        assert np.array_equal(meta, z["audit_int"]), "memo hit/miss sequence differs from the reference"
+    rows = mlrg.parse_csv(r.csv)
+    want = ref_rows(z)
+    assert len(rows) == len(want)
+    for got, w in zip(rows, want):
+        assert abs(got["loss"] - w[1]) <= 1e-4 * abs(w[1])
+        assert abs(got["E"] - w[2]) <= 1e-4 * max(abs(w[2]), 1e-3)
+        assert (got["miss"], got["remote_hit"], got["cache_hit"]) == (w[4], w[5], w[6])
+    assert rel(u.cpu().numpy(), z["u"]) <= 1e-4
+
+
+def test_dropin_c_api_end_to_end(mlrg, torch_cuda):
+    """mlr_make_phantom -> mlr_project -> mlr_reconstruct through the drop-in ABI
+    on host arrays, with the reference's d fed through an LVOL file."""
+    z = golden("recon_c32_memo_grid")
+    n = 32
+    cfg = mlrg.Config(n1=n, n0=n, n2=n, n_theta=n, h=n, w=n, n_outer=10, memoization="local",
+                      nudft_path="gridding")
+    ph = mlrg.make_phantom("blocks", n, n, n, 1)
+    proj = mlrg.project(cfg, ph).numpy()
+    assert rel(proj, z["data"]) < 2e-5  # GPU forward_L vs the reference's
+    data = mlrg.array_from_numpy(z["data"].astype(np.complex128))
+    res = mlrg.reconstruct(cfg, data, ph)
+    meta, _ = res.audit()
+    assert np.array_equal(meta, z["audit_int"])
+    assert res.aborted == bool(int(str(z["txt_aborted_txt"]).split()[0]))
+    assert rel(res.volume.numpy(), z["u"]) <= 1e-4
+    assert res.csv.startswith("iteration,loss,E,accuracy,miss,remote_hit,cache_hit,ms_lsp,ms_rsp,ms_update")
+
+
+def test_bench_entry_point(mlrg, torch_cuda):
+    cfg = mlrg.Config(n1=32, n0=32, n2=32, n_theta=32, h=32, w=32)
+    import ctypes as C
+    p = mlrg.lib().mlr_bench(cfg._h)
+    text = C.cast(p, C.c_char_p).value.decode()
+    mlrg.lib().mlr_free(p)
+    lines = text.strip().splitlines()
+    assert lines[0] == "case,lookups,misses,remote_hits,cache_hits,ms"
+    assert lines[2].startswith("miss,2,2,0,0") and lines[3].startswith("service_hit,2,0,2,0")
+    assert lines[4].startswith("cache_hit,2,0,0,2")
