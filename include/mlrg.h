@@ -29,7 +29,8 @@ void mlrg_free(char* text);
 int mlrg_version(void);
 
 /* ---- operator context (scalerun.hpp:61-116 OperatorEngine, per geometry) ---- */
-/* stream: a cudaStream_t or NULL for a private stream. */
+/* stream: a cudaStream_t; NULL selects the legacy default stream (stream 0), which
+ * orders the calls with work a host framework issued on its default stream. */
 mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w,
                           double phi, void* stream);
 void mlrg_ctx_destroy(mlrg_ctx* ctx);
@@ -80,7 +81,7 @@ void mlrg_recon_free(mlrg_recon* r);
 /* ---- steppable device solver (the outer loop of admm.cpp:208-272) ----
  * mlrg_solver_new runs the setup (engine, encoder matrices, d_hat = f2d(d));
  * each mlrg_solver_step runs exactly one ADMM outer iteration on `stream`
- * (NULL = private stream) and synchronises it. */
+ * (NULL = the legacy default stream) and synchronises it. */
 typedef struct mlrg_solver mlrg_solver;
 mlrg_solver* mlrg_solver_new(const char* config_text, const void* d, const void* reference, void* stream);
 int mlrg_solver_step(mlrg_solver* s, int* aborted);

@@ -223,6 +223,68 @@ int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_out
   return 0;
 }
 
+// Runs the reference outer loop by hand (admm.cpp:226-244 without memo) and
+// prints rho, r, s and the inner losses per outer iteration.
+int cmd_trace(std::int64_t n, int n_outer) {
+  mlr::RunConfig rc;
+  for (const char* k : {"n1", "n0", "n2", "n_theta", "h", "w"}) rc.set(k, std::to_string(n));
+  rc.set("nudft_path", "gridding");
+  rc.set("workers", "8");
+  const mlr::Geometry geom = rc.make_geometry();
+  const mlr::Volume phantom = round_c64(mlr::make_phantom(geom.volume_shape(), mlr::PhantomKind::blocks, 1));
+  const mlr::ProjectionSet d = round_c64(mlr::forward_L(phantom, geom, rc.engine.path));
+  mlr::OperatorEngine eng(geom, rc.engine);
+  mlr::AdmmState st = mlr::AdmmState::init(geom, rc.admm.rho0);
+  const mlr::ProjectionSet d_hat = eng.f2d(d, false);
+  for (int outer = 0; outer < n_outer; ++outer) {
+    const std::size_t before = st.inner_losses.size();
+    mlr::lsp_optimized(st, d_hat, rc.admm, eng);
+    mlr::rsp_update(st, rc.admm);
+    mlr::multiplier_penalty_update(st, rc.admm);
+    std::printf("outer %d rho %.17g r %.17g s %.17g losses", outer, st.rho, st.r, st.s);
+    for (std::size_t i = before; i < st.inner_losses.size(); ++i) std::printf(" %.17g", st.inner_losses[i]);
+    std::printf("\n");
+  }
+  return 0;
+}
+
+// Sensitivity of the reference itself: reconstruct from d and from d with
+// relative Gaussian noise eps, print rel-L2 of the two u per outer iteration.
+int cmd_sens(std::int64_t n, int n_outer, double eps, const std::string& memo) {
+  mlr::RunConfig rc;
+  for (const char* k : {"n1", "n0", "n2", "n_theta", "h", "w"}) rc.set(k, std::to_string(n));
+  rc.set("nudft_path", "gridding");
+  rc.set("workers", "8");
+  rc.set("memoization", memo);
+  const mlr::Geometry geom = rc.make_geometry();
+  const mlr::Volume phantom = round_c64(mlr::make_phantom(geom.volume_shape(), mlr::PhantomKind::blocks, 1));
+  const mlr::ProjectionSet d = round_c64(mlr::forward_L(phantom, geom, rc.engine.path));
+  mlr::ProjectionSet dp = d;
+  std::mt19937_64 rng(77);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  const double rms = mlr::norm2(d) / std::sqrt(static_cast<double>(d.size()));
+  for (cplx& v : dp.flat()) v += cplx(nd(rng), nd(rng)) * (eps * rms / std::sqrt(2.0));
+  for (int k = 1; k <= n_outer; ++k) {
+    rc.set("n_outer", std::to_string(k));
+    auto run = [&](const mlr::ProjectionSet& dd) {
+      mlr::EngineConfig ecfg = rc.engine;
+      ecfg.memo_enabled = rc.admm.memoization != mlr::MemoMode::off;
+      std::shared_ptr<mlr::Encoder> enc;
+      std::shared_ptr<mlr::MemoClient> client;
+      if (ecfg.memo_enabled) {
+        client = std::make_shared<mlr::MemoClient>(rc.memo);
+        enc = std::make_shared<mlr::Encoder>(rc.encoder);
+      }
+      mlr::OperatorEngine eng(geom, ecfg, enc, client);
+      return mlr::reconstruct(dd, geom, rc.admm, eng, &phantom).u;
+    };
+    const mlr::Volume u0 = run(d), u1 = run(dp);
+    std::printf("eps %.1e outer %d rel_u %.3e\n", eps, k, mlr::norm2(mlr::sub(u1, u0)) / mlr::norm2(u0));
+    std::fflush(stdout);
+  }
+  return 0;
+}
+
 int cmd_encoder(const std::string& dir) {
   mlr::EncoderConfig ec;  // projection, key_dim 60, seed 1337
   mlr::Encoder enc(ec);
@@ -321,6 +383,8 @@ int main(int argc, char** argv) {
       return cmd_recon(dir, I(3), I(4), static_cast<int>(I(5)), argv[6], argv[7],
                        argc > 8 ? static_cast<int>(I(8)) : 1);
     if (cmd == "encoder") return cmd_encoder(dir);
+    if (cmd == "trace" && argc == 5) return cmd_trace(I(3), static_cast<int>(I(4)));
+    if (cmd == "sens" && argc == 7) return cmd_sens(I(3), static_cast<int>(I(4)), std::stod(argv[5]), argv[6]);
     if (cmd == "store") return cmd_store(dir);
     std::fprintf(stderr, "bad arguments\n");
     return 2;

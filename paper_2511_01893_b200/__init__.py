@@ -290,12 +290,25 @@ def _gcheck(code: int):
         raise MlrError(code, (lib().mlrg_last_error() or b"").decode())
 
 
+def _default_stream(stream):
+    """None -> torch's current CUDA stream when torch is in use, so device
+    calls are ordered with the torch work that produced their inputs."""
+    if stream is not None:
+        return stream
+    import sys as _sys
+
+    torch = _sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available():
+        return torch.cuda.current_stream().cuda_stream
+    return None
+
+
 class Context:
     """mlrg_ctx: device operator tables for one geometry, bound to a CUDA stream."""
 
     def __init__(self, n1, n0, n2, n_theta, h, w, phi=0.5235987755982988, stream=None):
         self.geom = (n1, n0, n2, n_theta, h, w)
-        self._h = lib().mlrg_ctx_create(n1, n0, n2, n_theta, h, w, phi, stream)
+        self._h = lib().mlrg_ctx_create(n1, n0, n2, n_theta, h, w, phi, _default_stream(stream))
         if not self._h:
             raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
 
@@ -393,7 +406,7 @@ class DeviceRecon:
 
 
 def reconstruct_device(config_text: str, d, u_out, reference=None, stream=None) -> DeviceRecon:
-    h = lib().mlrg_reconstruct(config_text.encode(), _dp(d), _dp(reference), _dp(u_out), stream)
+    h = lib().mlrg_reconstruct(config_text.encode(), _dp(d), _dp(reference), _dp(u_out), _default_stream(stream))
     if not h:
         raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
     return DeviceRecon(h)
@@ -403,7 +416,7 @@ class Solver:
     """mlrg_solver: the ADMM outer loop on the device, one outer iteration per step()."""
 
     def __init__(self, config_text: str, d, reference=None, stream=None):
-        self._h = lib().mlrg_solver_new(config_text.encode(), _dp(d), _dp(reference), stream)
+        self._h = lib().mlrg_solver_new(config_text.encode(), _dp(d), _dp(reference), _default_stream(stream))
         if not self._h:
             raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
 

@@ -13,10 +13,10 @@
 #include <string>
 #include <vector>
 
-#include "admm.hpp"
+#include "solver.hpp"
 #include "config.hpp"
 #include "encoder.hpp"
-#include "engine.hpp"
+#include "engine_api.hpp"
 #include "host_io.hpp"
 #include "kernels.hpp"
 #include "memo.hpp"
@@ -309,15 +309,22 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
                                   " does not match the configured geometry " + g.volume_shape().str());
     StreamGuard sg;
     std::unique_ptr<mlrg::Engine> eng = build_engine(cfg->rc, g, sg.s);
-    mlrg::DeviceBuffer<float2> d, ref, u;
+    mlrg::DeviceBuffer<float2> d, ref;
     upload_c64(data->a, d, sg.s);
     if (reference) upload_c64(reference->a, ref, sg.s);
-    u.resize(static_cast<std::size_t>(g.volume_shape().count()));
     auto res = std::make_unique<mlr_result>();
-    res->report = mlrg::reconstruct(d.get(), cfg->rc.admm, *eng, reference ? ref.get() : nullptr, u.get());
+    {
+      mlrg::Solver solver(d.get(), cfg->rc.admm, *eng, reference ? ref.get() : nullptr);
+      for (int it = 0; it < cfg->rc.admm.n_outer; ++it)
+        if (!solver.step()) break;
+      res->report = solver.report();
+      res->u.a = mlrg::HostArray(g.volume_shape(), 0);
+      // the iterate is complex128 on the device: no rounding on the way out
+      MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver.u(), res->u.a.data.size() * sizeof(double2),
+                                cudaMemcpyDeviceToHost, sg.s));
+      MLRG_CUDA(cudaStreamSynchronize(sg.s));
+    }
     res->audit = eng->audit_log();
-    res->u.a = mlrg::HostArray(g.volume_shape(), 0);
-    download_c128(u.get(), res->u.a, sg.s);
     return res.release();
   });
 }
@@ -432,12 +439,7 @@ mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, i
   return guarded_ptr<mlrg_ctx>([&] {
     auto c = std::make_unique<mlrg_ctx>();
     c->g = mlrg::Geometry::make(n1, n0, n2, n_theta, h, w, phi);
-    if (stream) {
-      c->s = static_cast<cudaStream_t>(stream);
-    } else {
-      MLRG_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
-      c->own_stream = true;
-    }
+    c->s = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
     c->usfft = std::make_unique<mlrg::Usfft>(c->g, c->s);
     return c.release();
   });
@@ -575,12 +577,7 @@ mlrg_recon* mlrg_reconstruct(const char* config_text, const void* d, const void*
     const mlrg::RunConfig rc = mlrg::RunConfig::from_text(config_text);
     rc.validate();
     const mlrg::Geometry g = rc.make_geometry();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    std::unique_ptr<StreamGuard> own;
-    if (!s) {
-      own = std::make_unique<StreamGuard>();
-      s = own->s;
-    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
     std::unique_ptr<mlrg::Engine> eng = build_engine(rc, g, s);
     auto r = std::make_unique<mlrg_recon>();
     r->report = mlrg::reconstruct(static_cast<const float2*>(d), rc.admm, *eng,
@@ -623,11 +620,7 @@ mlrg_solver* mlrg_solver_new(const char* config_text, const void* d, const void*
     rc.validate();
     const mlrg::Geometry g = rc.make_geometry();
     auto sv = std::make_unique<mlrg_solver>();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!s) {
-      MLRG_CUDA(cudaStreamCreateWithFlags(&sv->own, cudaStreamNonBlocking));
-      s = sv->own;
-    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
     sv->eng = build_engine(rc, g, s);
     sv->solver = std::make_unique<mlrg::Solver>(static_cast<const float2*>(d), rc.admm, *sv->eng,
                                                 static_cast<const float2*>(reference));
@@ -648,8 +641,8 @@ int mlrg_solver_step(mlrg_solver* s, int* aborted) {
 int mlrg_solver_volume(mlrg_solver* s, void* u_out) {
   return guarded([&] {
     need(s && u_out, "null argument");
-    const std::size_t n = static_cast<std::size_t>(s->eng->geometry().volume_shape().count());
-    MLRG_CUDA(cudaMemcpyAsync(u_out, s->solver->u(), n * sizeof(float2), cudaMemcpyDeviceToDevice, s->eng->stream()));
+    const std::int64_t n = s->eng->geometry().volume_shape().count();
+    mlrg::ops::c128_to_c64(s->solver->u(), static_cast<float2*>(u_out), n, s->eng->stream());
     MLRG_CUDA(cudaStreamSynchronize(s->eng->stream()));
   });
 }

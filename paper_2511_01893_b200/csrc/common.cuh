@@ -1,8 +1,18 @@
-// Shared device helpers for the sm_100a kernels: complex64 arithmetic on
-// float2, bit reversal for the in-place DIF FFTs, and block reductions.
+// Shared device helpers for the sm_100a kernels: complex arithmetic on
+// float2/double2, bit reversal for the in-place FFTs, block reductions and the
+// shared-memory FFT cores.
+//
+// Precision: the transforms store their big intermediates (oversampled
+// grids) in complex64 but compute every FFT butterfly, twiddle and long
+// accumulation in double. The reference solve is sensitive to operator
+// noise (a 1e-6 relative perturbation of every operator output moves the
+// 64^3 iterate by 2.7e-4 after ten iterations), so the operators must stay
+// within a few complex64 ulps of the reference, which fp32 butterflies and
+// fp32 accumulations over thousands of terms do not.
 #pragma once
 
 #include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace mlrg {
@@ -12,13 +22,32 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-// multiply by +i (sign>0) or -i (sign<0)
-template <int SIGN>
-__device__ __forceinline__ float2 cmul_i(float2 a) {
-  return SIGN > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// multiply by +i (SIGN>0) or -i (SIGN<0)
+template <int SIGN, class T>
+__device__ __forceinline__ T cmul_i(T a) {
+  T r;
+  if (SIGN > 0) {
+    r.x = -a.y;
+    r.y = a.x;
+  } else {
+    r.x = a.y;
+    r.y = -a.x;
+  }
+  return r;
+}
+
+__device__ __forceinline__ double2 to_d(float2 a) { return make_double2(a.x, a.y); }
+__device__ __forceinline__ double2 to_d(double2 a) { return a; }
+__device__ __forceinline__ float2 to_f(double2 a) { return make_float2(static_cast<float>(a.x), static_cast<float>(a.y)); }
 
 // Position of frequency k inside a length-2^logm DIF output (bit-reversed order).
 __device__ __forceinline__ int brev(int k, int logm) {
@@ -54,26 +83,29 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
 // is replaced by its unnormalised transform X[k] = sum_m x[m] e^{SIGN 2 pi i mk/M}
 // stored at position brev(k). `tw` holds e^{+2 pi i k/M} for k < M/2.
 // Lanes run along c first, so rows stay contiguous across a warp.
-template <int SIGN>
-__device__ void fft_dif(float2* s, int logm, int ncols, int sm, const float2* __restrict__ tw) {
+template <int SIGN, class T>
+__device__ void fft_dif(T* s, int logm, int ncols, int sm, const T* __restrict__ tw) {
   const int m = 1 << logm;
   int span = m;  // current sub-transform size
   while (span >= 4) {
     const int l = span >> 2;
-    const int tws1 = m / span;        // w_{4L}^j -> tw[j * m/(4L)]
+    const int tws1 = m / span;         // w_{4L}^j -> tw[j * m/(4L)]
     const int tws2 = (m << 1) / span;  // w_{2L}^j -> tw[j * m/(2L)]
     const int nbf = (m >> 2) * ncols;
     for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
       const int c = idx % ncols, bf = idx / ncols;
       const int j = bf % l, base = (bf / l) * span + j;
-      float2* p = s + base * sm + c;
-      const float2 a0 = p[0], a1 = p[l * sm], a2 = p[2 * l * sm], a3 = p[3 * l * sm];
-      float2 w4 = __ldg(tw + j * tws1);
-      float2 w2 = __ldg(tw + j * tws2);
-      if (SIGN < 0) { w4.y = -w4.y; w2.y = -w2.y; }
-      const float2 y0 = cadd(a0, a2), y1 = cadd(a1, a3);
-      const float2 y2 = cmul(csub(a0, a2), w4);
-      const float2 y3 = cmul(cmul_i<SIGN>(csub(a1, a3)), w4);  // w_{4L}^{j+L} = w_{4L}^j * (SIGN i)
+      T* p = s + base * sm + c;
+      const T a0 = p[0], a1 = p[l * sm], a2 = p[2 * l * sm], a3 = p[3 * l * sm];
+      T w4 = tw[j * tws1];
+      T w2 = tw[j * tws2];
+      if (SIGN < 0) {
+        w4.y = -w4.y;
+        w2.y = -w2.y;
+      }
+      const T y0 = cadd(a0, a2), y1 = cadd(a1, a3);
+      const T y2 = cmul(csub(a0, a2), w4);
+      const T y3 = cmul(cmul_i<SIGN>(csub(a1, a3)), w4);  // w_{4L}^{j+L} = w_{4L}^j * (SIGN i)
       p[0] = cadd(y0, y1);
       p[l * sm] = cmul(csub(y0, y1), w2);
       p[2 * l * sm] = cadd(y2, y3);
@@ -86,8 +118,8 @@ __device__ void fft_dif(float2* s, int logm, int ncols, int sm, const float2* __
     const int nbf = (m >> 1) * ncols;
     for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
       const int c = idx % ncols, bf = idx / ncols;
-      float2* p = s + (bf * 2) * sm + c;
-      const float2 a0 = p[0], a1 = p[sm];
+      T* p = s + (bf * 2) * sm + c;
+      const T a0 = p[0], a1 = p[sm];
       p[0] = cadd(a0, a1);
       p[sm] = csub(a0, a1);
     }
@@ -98,16 +130,16 @@ __device__ void fft_dif(float2* s, int logm, int ncols, int sm, const float2* __
 // In-place radix-2/radix-4 decimation-in-time FFT over shared memory: the
 // input sits at bit-reversed positions (x[m] at brev(m)), the output X[k] is
 // left in natural order. Same layout and twiddle table as fft_dif.
-template <int SIGN>
-__device__ void fft_dit(float2* s, int logm, int ncols, int sm, const float2* __restrict__ tw) {
+template <int SIGN, class T>
+__device__ void fft_dit(T* s, int logm, int ncols, int sm, const T* __restrict__ tw) {
   const int m = 1 << logm;
   int l = 1;  // size of the sub-transforms being combined
   if (logm & 1) {
     const int nbf = (m >> 1) * ncols;
     for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
       const int c = idx % ncols, bf = idx / ncols;
-      float2* p = s + (bf * 2) * sm + c;
-      const float2 a0 = p[0], a1 = p[sm];
+      T* p = s + (bf * 2) * sm + c;
+      const T a0 = p[0], a1 = p[sm];
       p[0] = cadd(a0, a1);
       p[sm] = csub(a0, a1);
     }
@@ -122,13 +154,16 @@ __device__ void fft_dit(float2* s, int logm, int ncols, int sm, const float2* __
     for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
       const int c = idx % ncols, bf = idx / ncols;
       const int j = bf % l, base = (bf / l) * span + j;
-      float2* p = s + base * sm + c;
-      float2 t = __ldg(tw + j * tws2);
-      float2 u = __ldg(tw + j * tws4);
-      if (SIGN < 0) { t.y = -t.y; u.y = -u.y; }
-      const float2 a0 = p[0], a1 = cmul(p[l * sm], t), a2 = p[2 * l * sm], a3 = cmul(p[3 * l * sm], t);
-      const float2 y0 = cadd(a0, a1), y1 = csub(a0, a1), y2 = cadd(a2, a3), y3 = csub(a2, a3);
-      const float2 uy2 = cmul(y2, u), uy3 = cmul_i<SIGN>(cmul(y3, u));
+      T* p = s + base * sm + c;
+      T t = tw[j * tws2];
+      T u = tw[j * tws4];
+      if (SIGN < 0) {
+        t.y = -t.y;
+        u.y = -u.y;
+      }
+      const T a0 = p[0], a1 = cmul(p[l * sm], t), a2 = p[2 * l * sm], a3 = cmul(p[3 * l * sm], t);
+      const T y0 = cadd(a0, a1), y1 = csub(a0, a1), y2 = cadd(a2, a3), y3 = csub(a2, a3);
+      const T uy2 = cmul(y2, u), uy3 = cmul_i<SIGN>(cmul(y3, u));
       p[0] = cadd(y0, uy2);
       p[2 * l * sm] = csub(y0, uy2);
       p[l * sm] = cadd(y1, uy3);

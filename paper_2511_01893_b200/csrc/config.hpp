@@ -7,8 +7,8 @@
 #include <string>
 #include <utility>
 
-#include "admm.hpp"
-#include "engine.hpp"
+#include "solver.hpp"
+#include "engine_api.hpp"
 #include "geometry.hpp"
 #include "memo.hpp"
 

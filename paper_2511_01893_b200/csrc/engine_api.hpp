@@ -56,7 +56,11 @@ class Engine {
   const std::vector<ChunkAudit>& audit_log() const { return audit_; }
 
   // Full-array applications (scalerun.hpp:77-92).
+  // The volume side (fu1d input, fu1d_adj output) is the solver's complex128
+  // iterate; complex64 overloads serve the C-ABI and the memo benchmark.
+  void fu1d(const double2* u, float2* out, bool memoize = true);
   void fu1d(const float2* u, float2* out, bool memoize = true);
+  void fu1d_adj(const float2* v, double2* out, bool memoize = true);
   void fu1d_adj(const float2* v, float2* out, bool memoize = true);
   void fu2d(const float2* v, float2* out, bool memoize = true);
   void fu2d_fused(const float2* v, const float2* d_hat, float2* out, bool memoize = true);
@@ -70,9 +74,10 @@ class Engine {
   std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot);
 
  private:
-  void apply(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, bool memoize);
-  void compute(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, std::int64_t start,
-               std::int64_t extent);
+  void apply(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
+             bool memoize);
+  void compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
+               std::int64_t start, std::int64_t extent);
   Shape3 in_shape(OpId op) const;
   Shape3 out_shape(OpId op) const;
   void register_shapes();

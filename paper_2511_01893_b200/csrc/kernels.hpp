@@ -2,6 +2,12 @@
 // kernels (memo_kernels.cu). Every reduction writes nv doubles per CTA into
 // `partials`; the launcher returns the number of doubles written so the host
 // sums them in CTA order (deterministic, no float atomics).
+//
+// Precision split: the USFFT operators compute in complex64, but the ADMM
+// iterate and its multipliers (u, G, p, psi, lambda, g; the volume side) are
+// complex128. Differences such as grad(u) and grad(u) - psi + lambda/rho
+// cancel leading digits; in complex64 storage that cancellation alone moved
+// the 64^3 reference trajectory by 1e-3 after ten iterations.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,45 +29,52 @@ struct Dims {
 };
 
 /// Three-component field (GradField, operators.hpp:17-30), one plane per axis.
-struct Field3 {
-  float2* c[3] = {nullptr, nullptr, nullptr};
+template <class T>
+struct Field3T {
+  T* c[3] = {nullptr, nullptr, nullptr};
 };
-struct CField3 {
-  const float2* c[3] = {nullptr, nullptr, nullptr};
-  CField3() = default;
-  CField3(const Field3& f) : c{f.c[0], f.c[1], f.c[2]} {}
+template <class T>
+struct CField3T {
+  const T* c[3] = {nullptr, nullptr, nullptr};
+  CField3T() = default;
+  CField3T(const Field3T<T>& f) : c{f.c[0], f.c[1], f.c[2]} {}
 };
+using Field3 = Field3T<float2>;
+using CField3 = CField3T<float2>;
+using DField3 = Field3T<double2>;
+using CDField3 = CField3T<double2>;
 
 namespace ops {
 
 /// g = psi - lambda * lc (admm.cpp:64 with the lazy lambda scale folded in lc).
-void g_init(CField3 psi, CField3 lam, Field3 g, std::int64_t n, float lc, cudaStream_t s);
+void g_init(CDField3 psi, CDField3 lam, DField3 g, std::int64_t n, double lc, cudaStream_t s);
 
 /// G -= rho * div(grad(u) - g) (admm.cpp:144-147) with partials
 /// [|grad u - g|^2, |G|^2, Re<p_prev, G - G_prev>] (the last one only when
 /// p_prev/G_prev are non-null).
-int grad_update(const float2* u, CField3 g, float2* G, const float2* p_prev, const float2* G_prev, Dims d,
-                float rho, double* partials, cudaStream_t s);
+int grad_update(const double2* u, CDField3 g, double2* G, const double2* p_prev, const double2* G_prev, Dims d,
+                double rho, double* partials, cudaStream_t s);
 
 /// p = -G + beta * p_prev (admm.cpp:86-93) with partials
 /// [|grad p|^2, Re<grad u - g, grad p>] (admm.cpp:95-102).
-int direction(const float2* G, const float2* p_prev, float beta, const float2* u, CField3 g, float2* p, Dims d,
-              double* partials, cudaStream_t s);
+int direction(const double2* G, const double2* p_prev, double beta, const double2* u, CDField3 g, double2* p,
+              Dims d, double* partials, cudaStream_t s);
 
 /// y += a * x (admm.cpp:108-110).
-void axpy(float2* y, const float2* x, float a, std::int64_t n, cudaStream_t s);
+void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s);
 
 /// Fused rsp_update + multiplier update (admm.cpp:154-181):
 /// psi_new = shrink(grad u + lam*lc, thr); lam += rho_over_lam_scale * (grad u - psi_new).
 /// Partials [|grad u - psi_new|^2, |psi_new - psi_old|^2].
-int rsp_multiplier(const float2* u, Field3 lam, CField3 psi_old, Field3 psi_new, Dims d, float lc, float thr,
-                   float rho_over_scale, double* partials, cudaStream_t s);
+int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
+                   double rho_over_scale, double* partials, cudaStream_t s);
 
 /// Isotropic TV: partials [sum sqrt(sum_c |grad_c u|^2)] (admm.cpp:39-46).
-int tv_norm(const float2* u, Dims d, double* partials, cudaStream_t s);
+int tv_norm(const double2* u, Dims d, double* partials, cudaStream_t s);
 
 /// Partials [|a - b|^2, |a|^2] (b may be null).
 int norm2_diff(const float2* a, const float2* b, std::int64_t n, double* partials, cudaStream_t s);
+int norm2_diff(const double2* a, const double2* b, std::int64_t n, double* partials, cudaStream_t s);
 
 /// a -= b with partials [|a - b|^2] (resid = d_pred - d, admm.cpp:126-128).
 int sub_norm(float2* a, const float2* b, std::int64_t n, double* partials, cudaStream_t s);
@@ -71,12 +84,9 @@ int sub_norm(float2* a, const float2* b, std::int64_t n, double* partials, cudaS
 void grad(const float2* u, Field3 out, Dims d, cudaStream_t s);
 void div(CField3 g, float2* out, Dims d, cudaStream_t s);
 
-/// complex128 <-> complex64 conversion of host-interleaved arrays on the device.
+/// complex128 <-> complex64 conversion on the device.
 void c128_to_c64(const double2* in, float2* out, std::int64_t n, cudaStream_t s);
 void c64_to_c128(const float2* in, double2* out, std::int64_t n, cudaStream_t s);
-
-/// Elementwise scale / copy helpers.
-void scale(float2* y, const float2* x, float a, std::int64_t n, cudaStream_t s);
 
 // ---- memo layer ----
 
@@ -95,12 +105,16 @@ struct SlabGeom {
 /// encode_work_doubles(ns, kd) doubles.
 void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
             double* work, float* keys, double* norms2, cudaStream_t s);
+void encode(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+            double* work, float* keys, double* norms2, cudaStream_t s);
 std::size_t encode_work_doubles(int ns, int kd);
 
 /// out[slab] = value * scale - sub[slab] (sub may be null) (scalerun.cpp:250-255).
-void slab_materialize(float2* out, SlabGeom g, const float2* value, float scale, const float2* sub, cudaStream_t s);
-/// value = out[slab] (contiguous chunk order).
+void slab_materialize(float2* out, SlabGeom g, const float2* value, double scale, const float2* sub, cudaStream_t s);
+void slab_materialize(double2* out, SlabGeom g, const float2* value, double scale, cudaStream_t s);
+/// value = out[slab] (contiguous chunk order, complex64).
 void slab_store(const float2* out, SlabGeom g, float2* value, cudaStream_t s);
+void slab_store(const double2* out, SlabGeom g, float2* value, cudaStream_t s);
 /// out[slab] -= sub[slab].
 void slab_sub(float2* out, SlabGeom g, const float2* sub, cudaStream_t s);
 

@@ -32,11 +32,12 @@ __device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long st
 
 // Split-K GEMM keys[s][r] = sum_k P[r][k] X[s][k] over K = 2n, with P stored
 // interleaved on the device (column 2i weights Re x_i, 2i+1 weights Im x_i;
-// the reference's row layout is [re block | im block], encoder.cpp:414-419). Thread (ty, tx) owns slabs {ty + 16 q} x rows {tx + 16 p}
+// the reference's row layout is [re block | im block], encoder.cpp:414-419).
+// Thread (ty, tx) owns slabs {ty + 16 q} x rows {tx + 16 p}
 // (q < SG, p < 4); each CTA walks K chunks grid-stride and writes its double
 // partial tile. The first row slot past kd accumulates |x|^2.
-template <int SG>
-__global__ void __launch_bounds__(kEncThreads) k_encode(const float2* __restrict__ x, SlabGeom g, SlabList sl, int ns,
+template <int SG, class TX>
+__global__ void __launch_bounds__(kEncThreads) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
                                                         const float* __restrict__ P, long long n, int kd,
                                                         double* __restrict__ part) {
   __shared__ float xs[kChunk][16 * SG + 1];
@@ -57,10 +58,14 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const float2* __restrict
     for (int e = threadIdx.x; e < (kChunk / 2) * 16 * SG; e += blockDim.x) {
       const int s = e / (kChunk / 2), ee = e - s * (kChunk / 2);
       const long long ce = k0 / 2 + ee;
-      float2 xv = make_float2(0.f, 0.f);
-      if (s < ns && ce < n) xv = x[slab_offset(g, sl.start[s], ce)];
-      xs[2 * ee][s] = xv.x;
-      xs[2 * ee + 1][s] = xv.y;
+      float xr = 0.f, xi = 0.f;
+      if (s < ns && ce < n) {
+        const TX xv = x[slab_offset(g, sl.start[s], ce)];
+        xr = static_cast<float>(xv.x);
+        xi = static_cast<float>(xv.y);
+      }
+      xs[2 * ee][s] = xr;
+      xs[2 * ee + 1][s] = xi;
     }
     for (int e = threadIdx.x; e < kChunk * kRows; e += blockDim.x) {
       const int r = e / kChunk, kk = e - r * kChunk;
@@ -125,23 +130,32 @@ __global__ void k_encode_reduce(const double* __restrict__ part, int nblocks, in
   else norms2[slab] = s;
 }
 
-__global__ void k_slab_materialize(float2* __restrict__ out, SlabGeom g, const float2* __restrict__ value,
-                                   float scale, const float2* __restrict__ sub) {
+template <class TO>
+__global__ void k_slab_materialize(TO* __restrict__ out, SlabGeom g, const float2* __restrict__ value, double scale,
+                                   const float2* __restrict__ sub) {
   const long long n = g.count();
   for (long long ce = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ce < n;
        ce += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long o = slab_offset(g, g.start, ce);
-    float2 v = cscale(value[ce], scale);
-    if (sub) v = csub(v, sub[o]);
-    out[o] = v;
+    const float2 v = value[ce];
+    double re = v.x * scale, im = v.y * scale;
+    if (sub) {
+      re -= sub[o].x;
+      im -= sub[o].y;
+    }
+    out[o].x = static_cast<decltype(out[o].x)>(re);
+    out[o].y = static_cast<decltype(out[o].y)>(im);
   }
 }
 
-__global__ void k_slab_store(const float2* __restrict__ out, SlabGeom g, float2* __restrict__ value) {
+template <class TO>
+__global__ void k_slab_store(const TO* __restrict__ out, SlabGeom g, float2* __restrict__ value) {
   const long long n = g.count();
   for (long long ce = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ce < n;
-       ce += static_cast<long long>(gridDim.x) * blockDim.x)
-    value[ce] = out[slab_offset(g, g.start, ce)];
+       ce += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const TO v = out[slab_offset(g, g.start, ce)];
+    value[ce] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+  }
 }
 
 __global__ void k_slab_sub(float2* __restrict__ out, SlabGeom g, const float2* __restrict__ sub) {
@@ -162,8 +176,10 @@ std::size_t encode_work_doubles(int ns, int kd) {
          static_cast<std::size_t>(kd + 1);
 }
 
-void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
-            double* work, float* keys, double* norms2, cudaStream_t s) {
+namespace {
+template <class TX>
+void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+                 double* work, float* keys, double* norms2, cudaStream_t s) {
   if (kd > kRows - 1) throw std::invalid_argument("encode: key_dim must be < 64");
   const long long n = shape.count();
   for (int b = 0; b < ns; b += kMaxSlabs) {
@@ -171,23 +187,46 @@ void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns,
     SlabList sl{};
     for (int q = 0; q < nb; ++q) sl.start[q] = starts[b + q];
     const int blocks = enc_blocks();
-    if (nb <= 16) k_encode<1><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
-    else if (nb <= 32) k_encode<2><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
-    else k_encode<4><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
+    prof::begin("k_encode", s);
+    if (nb <= 16) k_encode<1, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
+    else if (nb <= 32) k_encode<2, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
+    else k_encode<4, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
     MLRG_LAUNCH_CHECK("k_encode");
+    prof::end("k_encode", s);
     const int per = nb * (kd + 1);
     k_encode_reduce<<<(per + 255) / 256, 256, 0, s>>>(work, blocks, nb, kd, keys + b * kd, norms2 + b);
     MLRG_LAUNCH_CHECK("k_encode_reduce");
   }
 }
+}  // namespace
 
-void slab_materialize(float2* out, SlabGeom g, const float2* value, float scale, const float2* sub, cudaStream_t s) {
-  k_slab_materialize<<<2 * sm_count(), 256, 0, s>>>(out, g, value, scale, sub);
+void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+            double* work, float* keys, double* norms2, cudaStream_t s) {
+  encode_impl(x, shape, starts, ns, P, kd, work, keys, norms2, s);
+}
+
+void encode(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+            double* work, float* keys, double* norms2, cudaStream_t s) {
+  encode_impl(x, shape, starts, ns, P, kd, work, keys, norms2, s);
+}
+
+void slab_materialize(float2* out, SlabGeom g, const float2* value, double scale, const float2* sub, cudaStream_t s) {
+  k_slab_materialize<float2><<<2 * sm_count(), 256, 0, s>>>(out, g, value, scale, sub);
+  MLRG_LAUNCH_CHECK("k_slab_materialize");
+}
+
+void slab_materialize(double2* out, SlabGeom g, const float2* value, double scale, cudaStream_t s) {
+  k_slab_materialize<double2><<<2 * sm_count(), 256, 0, s>>>(out, g, value, scale, nullptr);
   MLRG_LAUNCH_CHECK("k_slab_materialize");
 }
 
 void slab_store(const float2* out, SlabGeom g, float2* value, cudaStream_t s) {
-  k_slab_store<<<2 * sm_count(), 256, 0, s>>>(out, g, value);
+  k_slab_store<float2><<<2 * sm_count(), 256, 0, s>>>(out, g, value);
+  MLRG_LAUNCH_CHECK("k_slab_store");
+}
+
+void slab_store(const double2* out, SlabGeom g, float2* value, cudaStream_t s) {
+  k_slab_store<double2><<<2 * sm_count(), 256, 0, s>>>(out, g, value);
   MLRG_LAUNCH_CHECK("k_slab_store");
 }
 

@@ -1,4 +1,4 @@
-#include "engine.hpp"
+#include "engine_api.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -79,15 +79,21 @@ Shape3 Engine::out_shape(OpId op) const {
   throw std::invalid_argument("out_shape: unknown operator");
 }
 
-void Engine::compute(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, std::int64_t start,
-                     std::int64_t extent) {
+void Engine::compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
+                     std::int64_t start, std::int64_t extent) {
   const std::int64_t n0 = g_.n0, n2 = g_.n2, h = g_.h, w = g_.w;
   switch (op) {
-    case OpId::fu1d: usfft_.fu1d(in + start * n0 * n2, out + start * h * n2, extent); return;
-    case OpId::fu1d_adj: usfft_.fu1d_adj(in + start * h * n2, out + start * n0 * n2, extent); return;
+    case OpId::fu1d:
+      if (in_d) usfft_.fu1d(static_cast<const double2*>(in) + start * n0 * n2, static_cast<float2*>(out) + start * h * n2, extent);
+      else usfft_.fu1d(static_cast<const float2*>(in) + start * n0 * n2, static_cast<float2*>(out) + start * h * n2, extent);
+      return;
+    case OpId::fu1d_adj:
+      if (out_d) usfft_.fu1d_adj(static_cast<const float2*>(in) + start * h * n2, static_cast<double2*>(out) + start * n0 * n2, extent);
+      else usfft_.fu1d_adj(static_cast<const float2*>(in) + start * h * n2, static_cast<float2*>(out) + start * n0 * n2, extent);
+      return;
     case OpId::fu2d: {
       Fu2dEpilogue e;
-      e.out = out;
+      e.out = static_cast<float2*>(out);
       e.ld_out = h;
       e.k0_out = start;
       if (fused) {
@@ -95,22 +101,28 @@ void Engine::compute(OpId op, bool fused, const float2* in, const float2* d_hat,
         e.ld_sub = h;
         e.k0_sub = start;
       }
-      usfft_.fu2d(in, h, start, extent, e);
+      usfft_.fu2d(static_cast<const float2*>(in), h, start, extent, e);
       return;
     }
-    case OpId::fu2d_adj: usfft_.fu2d_adj(in, h, start, extent, out, h, start); return;
-    case OpId::f2d: usfft_.f2d(in + start * h * w, out + start * h * w, extent, false); return;
-    case OpId::f2d_adj: usfft_.f2d(in + start * h * w, out + start * h * w, extent, true); return;
+    case OpId::fu2d_adj:
+      usfft_.fu2d_adj(static_cast<const float2*>(in), h, start, extent, static_cast<float2*>(out), h, start);
+      return;
+    case OpId::f2d:
+    case OpId::f2d_adj:
+      usfft_.f2d(static_cast<const float2*>(in) + start * h * w, static_cast<float2*>(out) + start * h * w, extent,
+                 op == OpId::f2d_adj);
+      return;
   }
 }
 
-void Engine::apply(OpId op, bool fused, const float2* in, const float2* d_hat, float2* out, bool memoize) {
+void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
+                   bool memoize) {
   const int axis = chunk_axis_of(op);
   const Shape3 ishape = in_shape(op), oshape = out_shape(op);
   const std::int64_t len = ishape.extent(axis);
   const bool use_memo = memoize && cfg_.memo_enabled;
   if (!use_memo) {
-    compute(op, fused, in, d_hat, out, 0, len);
+    compute(op, fused, in, in_d, d_hat, out, out_d, 0, len);
     return;
   }
   // ---- encode every slab (one GEMM per distinct slab shape) ----
@@ -128,8 +140,14 @@ void Engine::apply(OpId op, bool fused, const float2* in, const float2* d_hat, f
     while (c1 < n && ext[static_cast<std::size_t>(c1)] == ext[static_cast<std::size_t>(c0)]) ++c1;
     ops::SlabGeom sg{ishape.d0, ishape.d1, ishape.d2, axis, 0, ext[static_cast<std::size_t>(c0)]};
     enc_work_.resize(ops::encode_work_doubles(c1 - c0, kd));
-    ops::encode(in, sg, starts.data() + c0, c1 - c0, enc_->device_matrix(with_axis(ishape, axis, sg.extent)), kd,
-                enc_work_.get(), enc_keys_.get() + static_cast<std::size_t>(c0) * kd, enc_norms_.get() + c0, s_);
+    const float* P = enc_->device_matrix(with_axis(ishape, axis, sg.extent));
+    float* kdst = enc_keys_.get() + static_cast<std::size_t>(c0) * kd;
+    if (in_d)
+      ops::encode(static_cast<const double2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
+                  enc_norms_.get() + c0, s_);
+    else
+      ops::encode(static_cast<const float2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
+                  enc_norms_.get() + c0, s_);
     c0 = c1;
   }
   MLRG_CUDA(cudaMemcpyAsync(keys_host_.get(), enc_keys_.get(), sizeof(float) * n * kd, cudaMemcpyDeviceToHost, s_));
@@ -142,7 +160,8 @@ void Engine::apply(OpId op, bool fused, const float2* in, const float2* d_hat, f
   std::vector<std::int64_t> out_counts(static_cast<std::size_t>(n));
   for (int c = 0; c < n; ++c) {
     MemoKey& k = keys[static_cast<std::size_t>(c)];
-    k.values.assign(keys_host_.get() + static_cast<std::size_t>(c) * kd, keys_host_.get() + static_cast<std::size_t>(c + 1) * kd);
+    k.values.assign(keys_host_.get() + static_cast<std::size_t>(c) * kd,
+                    keys_host_.get() + static_cast<std::size_t>(c + 1) * kd);
     k.location = c;
     k.op = op;
     slot_mix(k.values.data(), kd, enc_->seed(), c, op);
@@ -163,36 +182,40 @@ void Engine::apply(OpId op, bool fused, const float2* in, const float2* d_hat, f
     std::int64_t extent = 0;
     while (c1 < n && dec[static_cast<std::size_t>(c1)].outcome == MemoOutcome::miss)
       extent += ext[static_cast<std::size_t>(c1++)];
-    compute(op, false, in, nullptr, out, starts[static_cast<std::size_t>(c0)], extent);
+    compute(op, false, in, in_d, nullptr, out, out_d, starts[static_cast<std::size_t>(c0)], extent);
     c0 = c1;
   }
   // ---- hits: value * (live norm / stored norm), minus the live d_hat slab when fused ----
   for (int c = 0; c < n; ++c) {
     const MemoDecision& d = dec[static_cast<std::size_t>(c)];
-    ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)], ext[static_cast<std::size_t>(c)]};
+    const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)],
+                           ext[static_cast<std::size_t>(c)]};
     if (d.outcome != MemoOutcome::miss) {
       const ValueRef& v = memo_->store().value(d.value_id);
       const double live = in_norms[static_cast<std::size_t>(c)];
       const double scale = (v.norm > 0.0 && live > 0.0) ? live / v.norm : 1.0;
-      ops::slab_materialize(out, og, v.dev, static_cast<float>(scale), fused ? d_hat : nullptr, s_);
+      if (out_d) ops::slab_materialize(static_cast<double2*>(out), og, v.dev, scale, s_);
+      else ops::slab_materialize(static_cast<float2*>(out), og, v.dev, scale, fused ? d_hat : nullptr, s_);
     }
     audit_.push_back(ChunkAudit{op, axis, c, ext[static_cast<std::size_t>(c)], d.outcome, d.cs, iteration_, -1.0f});
   }
   // ---- stage the miss values (the linear part for fused), then apply d_hat ----
   for (int c = 0; c < n; ++c) {
     if (dec[static_cast<std::size_t>(c)].outcome != MemoOutcome::miss) continue;
-    ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)], ext[static_cast<std::size_t>(c)]};
+    const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)],
+                           ext[static_cast<std::size_t>(c)]};
     memo_->insert_async(keys[static_cast<std::size_t>(c)], [&]() {
       ValueRef v;
       v.count = out_counts[static_cast<std::size_t>(c)];
       float2* dst = memo_->store().arena().alloc(v.count);
-      ops::slab_store(out, og, dst, s_);
+      if (out_d) ops::slab_store(static_cast<const double2*>(out), og, dst, s_);
+      else ops::slab_store(static_cast<const float2*>(out), og, dst, s_);
       v.dev = dst;
       v.norm = in_norms[static_cast<std::size_t>(c)];
       v.bytes = value_bytes[static_cast<std::size_t>(c)];
       return v;
     });
-    if (fused) ops::slab_sub(out, og, d_hat, s_);
+    if (fused) ops::slab_sub(static_cast<float2*>(out), og, d_hat, s_);
   }
   if (cfg_.flush_after_apply) memo_->flush_inserts();
 }
@@ -201,20 +224,32 @@ void Engine::flush_inserts() {
   if (memo_) memo_->flush_inserts();
 }
 
-void Engine::fu1d(const float2* u, float2* out, bool memoize) { apply(OpId::fu1d, false, u, nullptr, out, memoize); }
-void Engine::fu1d_adj(const float2* v, float2* out, bool memoize) {
-  apply(OpId::fu1d_adj, false, v, nullptr, out, memoize);
+void Engine::fu1d(const double2* u, float2* out, bool memoize) {
+  apply(OpId::fu1d, false, u, true, nullptr, out, false, memoize);
 }
-void Engine::fu2d(const float2* v, float2* out, bool memoize) { apply(OpId::fu2d, false, v, nullptr, out, memoize); }
+void Engine::fu1d(const float2* u, float2* out, bool memoize) {
+  apply(OpId::fu1d, false, u, false, nullptr, out, false, memoize);
+}
+void Engine::fu1d_adj(const float2* v, double2* out, bool memoize) {
+  apply(OpId::fu1d_adj, false, v, false, nullptr, out, true, memoize);
+}
+void Engine::fu1d_adj(const float2* v, float2* out, bool memoize) {
+  apply(OpId::fu1d_adj, false, v, false, nullptr, out, false, memoize);
+}
+void Engine::fu2d(const float2* v, float2* out, bool memoize) {
+  apply(OpId::fu2d, false, v, false, nullptr, out, false, memoize);
+}
 void Engine::fu2d_fused(const float2* v, const float2* d_hat, float2* out, bool memoize) {
-  apply(OpId::fu2d, true, v, d_hat, out, memoize);
+  apply(OpId::fu2d, true, v, false, d_hat, out, false, memoize);
 }
 void Engine::fu2d_adj(const float2* p, float2* out, bool memoize) {
-  apply(OpId::fu2d_adj, false, p, nullptr, out, memoize);
+  apply(OpId::fu2d_adj, false, p, false, nullptr, out, false, memoize);
 }
-void Engine::f2d(const float2* p, float2* out, bool memoize) { apply(OpId::f2d, false, p, nullptr, out, memoize); }
+void Engine::f2d(const float2* p, float2* out, bool memoize) {
+  apply(OpId::f2d, false, p, false, nullptr, out, false, memoize);
+}
 void Engine::f2d_adj(const float2* p, float2* out, bool memoize) {
-  apply(OpId::f2d_adj, false, p, nullptr, out, memoize);
+  apply(OpId::f2d_adj, false, p, false, nullptr, out, false, memoize);
 }
 
 std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot) {

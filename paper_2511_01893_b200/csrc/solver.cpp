@@ -1,6 +1,8 @@
-#include "admm.hpp"
+#include "solver.hpp"
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <iomanip>
 #include <sstream>
@@ -35,15 +37,17 @@ namespace {
 /// residual-balancing rescale (admm.cpp:173-180) is exact and costs no pass.
 struct State {
   std::int64_t V, M, P;
-  DeviceBuffer<float2> u, G, G_prev, p, p_prev, mid, mid2, rhat, dhat, dpred, fu2d_out;
-  DeviceBuffer<float2> psi[3], psi_prev[3], lam[3], g[3];
+  DeviceBuffer<double2> u, G, G_prev, p, p_prev;       // volume side, complex128
+  DeviceBuffer<double2> psi[3], psi_prev[3], lam[3], g[3];
+  DeviceBuffer<double2> ref;                            // accuracy reference (optional)
+  DeviceBuffer<float2> mid, mid2, rhat, dhat, dpred, fu2d_out;  // operator side, complex64
   double rho = 1.0, lam_scale = 1.0;
   bool have_direction = false;
   std::vector<double> inner_losses;
 
   State(const Geometry& geo, bool baseline, cudaStream_t s)
       : V(geo.volume_shape().count()), M(geo.mid_shape().count()), P(geo.projection_shape().count()) {
-    auto vz = [&](DeviceBuffer<float2>& b, std::int64_t n) {
+    auto vz = [&](auto& b, std::int64_t n) {
       b.resize(static_cast<std::size_t>(n));
       b.zero(s);
     };
@@ -63,10 +67,18 @@ struct State {
       vz(fu2d_out, P);
     }
   }
-  Field3 f(DeviceBuffer<float2> (&a)[3]) { return Field3{{a[0].get(), a[1].get(), a[2].get()}}; }
+  DField3 f(DeviceBuffer<double2> (&a)[3]) { return DField3{{a[0].get(), a[1].get(), a[2].get()}}; }
 };
 
 std::int64_t geo_count(const Engine& e) { return e.geometry().volume_shape().count(); }
+
+bool trace_on() {  // MLRG_TRACE=1: per-step solver scalars on stderr (diagnostics)
+  static const bool on = [] {
+    const char* v = std::getenv("MLRG_TRACE");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
 
 double ms_between(std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
   return std::chrono::duration<double, std::milli>(b - a).count();
@@ -76,14 +88,23 @@ double ms_between(std::chrono::steady_clock::time_point a, std::chrono::steady_c
 
 struct SolverState : State {
   const float2* d;
-  const float2* reference;
+  bool has_reference;
   AdmmConfig cfg;
   Engine& eng;
   ReconReport rep;
   MemoCounters prev;
   int outer = 0;
   SolverState(const float2* d_, const AdmmConfig& c, Engine& e, const float2* ref)
-      : State(e.geometry(), c.pipeline == Pipeline::baseline, e.stream()), d(d_), reference(ref), cfg(c), eng(e) {}
+      : State(e.geometry(), c.pipeline == Pipeline::baseline, e.stream()),
+        d(d_),
+        has_reference(ref != nullptr),
+        cfg(c),
+        eng(e) {
+    if (ref) {
+      this->ref.resize(static_cast<std::size_t>(V));
+      ops::c64_to_c128(ref, this->ref.get(), V, e.stream());
+    }
+  }
 };
 
 Solver::Solver(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2* reference) {
@@ -97,7 +118,7 @@ Solver::Solver(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2
 Solver::~Solver() { delete st_; }
 int Solver::iteration() const { return st_->outer; }
 const ReconReport& Solver::report() const { return st_->rep; }
-const float2* Solver::u() const { return st_->u.get(); }
+const double2* Solver::u() const { return st_->u.get(); }
 
 bool Solver::step() {
   SolverState& st = *st_;
@@ -120,8 +141,7 @@ bool Solver::step() {
     try {
       const auto t0 = clock::now();
       // ---- LSP (admm.cpp:59-118, 122-152) ----
-      ops::g_init(CField3(st.f(st.psi)), CField3(st.f(st.lam)), st.f(st.g), st.V,
-                  static_cast<float>(st.lam_scale / st.rho), s);
+      ops::g_init(CDField3(st.f(st.psi)), CDField3(st.f(st.lam)), st.f(st.g), st.V, st.lam_scale / st.rho, s);
       st.have_direction = false;
       const std::size_t phase_start = st.inner_losses.size();
       for (int inner = 0; inner < cfg.n_inner; ++inner) {
@@ -141,8 +161,8 @@ bool Solver::step() {
         eng.fu1d_adj(st.mid2.get(), st.G.get());
         const bool hd = st.have_direction;
         const std::vector<double> gu = sum(
-            ops::grad_update(st.u.get(), CField3(st.f(st.g)), st.G.get(), hd ? st.p_prev.get() : nullptr,
-                             hd ? st.G_prev.get() : nullptr, dims, static_cast<float>(st.rho), part.dev(), s),
+            ops::grad_update(st.u.get(), CDField3(st.f(st.g)), st.G.get(), hd ? st.p_prev.get() : nullptr,
+                             hd ? st.G_prev.get() : nullptr, dims, st.rho, part.dev(), s),
             3);
         const double loss = 0.5 * rr + 0.5 * st.rho * gu[0];
         st.inner_losses.push_back(loss);
@@ -157,9 +177,8 @@ bool Solver::step() {
         double beta = 0.0;
         if (hd && gu[2] > 0.0) beta = normG2 / gu[2];
         auto step_terms = [&](double bt, double& a, double& b) {
-          const std::vector<double> dr = sum(ops::direction(st.G.get(), st.p_prev.get(), static_cast<float>(bt),
-                                                            st.u.get(), CField3(st.f(st.g)), st.p.get(), dims,
-                                                            part.dev(), s),
+          const std::vector<double> dr = sum(ops::direction(st.G.get(), st.p_prev.get(), bt, st.u.get(),
+                                                            CDField3(st.f(st.g)), st.p.get(), dims, part.dev(), s),
                                              2);
           eng.fu1d(st.p.get(), st.mid.get(), false);
           const std::array<double, 2> q = eng.fu2d_reduce(st.mid.get(), nullptr, st.rhat.get());
@@ -169,7 +188,10 @@ bool Solver::step() {
         double a = 0.0, b = 0.0;
         step_terms(beta, a, b);
         if (b > 0.0) step_terms(0.0, a, b);  // uphill: steepest descent (admm.cpp:103-106)
-        if (a > 0.0 && b < 0.0) ops::axpy(st.u.get(), st.p.get(), static_cast<float>(-b / a), st.V, s);
+        if (trace_on())
+          std::fprintf(stderr, "mlrg-trace outer %d inner %d loss %.9g normG2 %.9g dy %.9g beta %.9g a %.9g b %.9g\n",
+                       outer, inner, loss, normG2, gu[2], beta, a, b);
+        if (a > 0.0 && b < 0.0) ops::axpy(st.u.get(), st.p.get(), -b / a, st.V, s);
         std::swap(st.G_prev, st.G);
         std::swap(st.p_prev, st.p);
         st.have_direction = true;
@@ -178,9 +200,8 @@ bool Solver::step() {
       const auto t1 = clock::now();
       // ---- RSP + multiplier/penalty, one fused pass (admm.cpp:154-181) ----
       const std::vector<double> rs =
-          sum(ops::rsp_multiplier(st.u.get(), st.f(st.lam), CField3(st.f(st.psi)), st.f(st.psi_prev), dims,
-                                  static_cast<float>(st.lam_scale / st.rho), static_cast<float>(cfg.alpha / st.rho),
-                                  static_cast<float>(st.rho / st.lam_scale), part.dev(), s),
+          sum(ops::rsp_multiplier(st.u.get(), st.f(st.lam), CDField3(st.f(st.psi)), st.f(st.psi_prev), dims,
+                                  st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s),
               2);
       for (int c = 0; c < 3; ++c) std::swap(st.psi[c], st.psi_prev[c]);  // psi_prev <- old psi
       const auto t2 = clock::now();
@@ -195,6 +216,7 @@ bool Solver::step() {
           st.lam_scale *= 2.0;
         }
       }
+      if (trace_on()) std::fprintf(stderr, "mlrg-trace outer %d rho %.17g r %.17g s %.17g\n", outer, st.rho, r, sres);
       const auto t3 = clock::now();
       row.ms_lsp = ms_between(t0, t1);
       row.ms_rsp = ms_between(t1, t2);
@@ -210,8 +232,8 @@ bool Solver::step() {
     const std::array<double, 2> data = eng.fu2d_reduce(st.mid.get(), st.dhat.get(), nullptr);
     const double tv = sum(ops::tv_norm(st.u.get(), dims, part.dev(), s), 1)[0];
     row.loss = 0.5 * data[0] + cfg.alpha * tv;
-    if (st.reference) {  // accuracy(reference, u), admm.cpp:183-188
-      const std::vector<double> nd = sum(ops::norm2_diff(st.reference, st.u.get(), st.V, part.dev(), s), 2);
+    if (st.has_reference) {  // accuracy(reference, u), admm.cpp:183-188
+      const std::vector<double> nd = sum(ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev(), s), 2);
       if (nd[1] == 0.0) throw std::invalid_argument("accuracy: reference volume has zero norm");
       row.e = std::sqrt(nd[0]) / std::sqrt(nd[1]);
       row.accuracy = 1.0 - row.e;
@@ -233,8 +255,7 @@ ReconReport reconstruct(const float2* d, const AdmmConfig& cfg, Engine& eng, con
   for (int outer = 0; outer < cfg.n_outer; ++outer)
     if (!solver.step()) break;
   cudaStream_t s = eng.stream();
-  MLRG_CUDA(cudaMemcpyAsync(u_out, solver.u(), static_cast<std::size_t>(geo_count(eng)) * sizeof(float2),
-                            cudaMemcpyDeviceToDevice, s));
+  ops::c128_to_c64(solver.u(), u_out, geo_count(eng), s);
   MLRG_CUDA(cudaStreamSynchronize(s));
   return solver.report();
 }

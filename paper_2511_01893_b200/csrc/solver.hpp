@@ -12,7 +12,7 @@
 #include <vector>
 
 #include "device.hpp"
-#include "engine.hpp"
+#include "engine_api.hpp"
 
 namespace mlrg {
 
@@ -66,13 +66,13 @@ class Solver {
   bool step();
   int iteration() const;
   const ReconReport& report() const;
-  const float2* u() const;
+  const double2* u() const;  // the complex128 iterate (device)
 
  private:
   SolverState* st_;
 };
 
-/// Full solve: n_outer steps, result copied to `u_out` (device).
+/// Full solve: n_outer steps, result rounded to complex64 into `u_out` (device).
 ReconReport reconstruct(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2* reference, float2* u_out);
 
 }  // namespace mlrg

@@ -12,6 +12,8 @@
 //             per target with the weights amortised over the 16 rows.
 //   fu2d_adj  mirror: targets binned per 8x8 cell tile (host CSR) -> each cell
 //             gathers its targets (no atomics) -> column DIF(-1) -> row DIT(-1).
+// FFT butterflies, twiddles, deconvolution and accumulations run in double;
+// the oversampled grids between passes are stored in complex64 (common.cuh).
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -28,33 +30,32 @@ namespace {
 constexpr int KB = Usfft::kRowBatch;
 constexpr int kTile = 8;  // adjoint spread tile edge, in grid cells
 
-// k-columns per CTA of a 2D-grid FFT pass over length m: keeps smem <= ~150 KB.
-int pass_cols(std::int64_t m) { return m <= 1024 ? KB : (m <= 2048 ? 8 : 4); }
+// k-columns per CTA of a 2D-grid FFT pass over length m (double smem <= ~140 KB).
+int pass_cols(std::int64_t m) { return static_cast<int>(std::clamp<std::int64_t>(8192 / m, 2, KB)); }
 
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_fu1d(const float2* __restrict__ u, float2* __restrict__ out,
-                                              int n0, int n2, int h, int logm, int center, int ncol,
-                                              const float* __restrict__ deconv,
-                                              const int* __restrict__ start,
-                                              const float* __restrict__ wts,
-                                              const float2* __restrict__ fac,
-                                              const float2* __restrict__ tw) {
-  extern __shared__ float2 s[];
+template <class TIn>
+__global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
+                                              int h, int logm, int center, int ncol,
+                                              const double* __restrict__ deconv, const int* __restrict__ start,
+                                              const float* __restrict__ wts, const double2* __restrict__ fac,
+                                              const double2* __restrict__ tw) {
+  extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
   const int j0 = blockIdx.x * ncol;
-  const float2* ui = u + static_cast<long long>(blockIdx.y) * n0 * n2;
+  const TIn* ui = u + static_cast<long long>(blockIdx.y) * n0 * n2;
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int r = idx / ncol, c = idx - r * ncol;
     const int mode = (r + center) & mask;  // grid slot r holds mode (r + center) mod m
     const int j = j0 + c;
-    float2 v = make_float2(0.f, 0.f);
-    if (mode < n0 && j < n2) v = cscale(ui[static_cast<long long>(mode) * n2 + j], deconv[mode]);
-    s[idx] = v;
+    double2 v = make_double2(0.0, 0.0);
+    if (mode < n0 && j < n2) v = cscale(to_d(ui[static_cast<long long>(mode) * n2 + j]), deconv[mode]);
+    sd[idx] = v;
   }
   __syncthreads();
-  fft_dif<+1>(s, logm, ncol, ncol, tw);
+  fft_dif<+1>(sd, logm, ncol, ncol, tw);
   float2* oi = out + static_cast<long long>(blockIdx.y) * h * n2;
   for (int idx = threadIdx.x; idx < h * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
@@ -62,58 +63,61 @@ __global__ void __launch_bounds__(256) k_fu1d(const float2* __restrict__ u, floa
     if (j >= n2) continue;
     const int st = start[k];
     const float* wk = wts + k * kTaps;
-    float2 acc = make_float2(0.f, 0.f);
+    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
     for (int a = 0; a < kTaps; ++a) {
-      const float2 g = s[brev((st + a) & mask, logm) * ncol + c];
-      const float wa = __ldg(wk + a);
-      acc.x = fmaf(g.x, wa, acc.x);
-      acc.y = fmaf(g.y, wa, acc.y);
+      const double2 g = sd[brev((st + a) & mask, logm) * ncol + c];
+      const double wa = __ldg(wk + a);
+      acc.x = fma(g.x, wa, acc.x);
+      acc.y = fma(g.y, wa, acc.y);
     }
-    oi[static_cast<long long>(k) * n2 + j] = cmul(acc, fac[k]);
+    oi[static_cast<long long>(k) * n2 + j] = to_f(cmul(acc, fac[k]));
   }
 }
 
-__global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, float2* __restrict__ out,
-                                                  int n0, int n2, int h, int logm, int center, int ncol,
-                                                  const float2* __restrict__ cphase,
-                                                  const int* __restrict__ cell_ptr,
-                                                  const int* __restrict__ cell_k,
+template <class TOut>
+__global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, TOut* __restrict__ out, int n0,
+                                                  int n2, int h, int logm, int center, int ncol,
+                                                  const double2* __restrict__ cphase,
+                                                  const int* __restrict__ cell_ptr, const int* __restrict__ cell_k,
                                                   const float* __restrict__ cell_w,
-                                                  const float* __restrict__ pdeconv,
-                                                  const float2* __restrict__ tw) {
-  extern __shared__ float2 s[];
+                                                  const double* __restrict__ pdeconv,
+                                                  const double2* __restrict__ tw) {
+  extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
-  float2* vt = s + m * ncol;
+  double2* vt = sd + m * ncol;
   const int j0 = blockIdx.x * ncol;
   const float2* vi = v + static_cast<long long>(blockIdx.y) * h * n2;
   for (int idx = threadIdx.x; idx < h * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
     const int j = j0 + c;
-    vt[idx] = j < n2 ? cmul(vi[static_cast<long long>(k) * n2 + j], cphase[k]) : make_float2(0.f, 0.f);
+    vt[idx] = j < n2 ? cmul(to_d(vi[static_cast<long long>(k) * n2 + j]), cphase[k]) : make_double2(0.0, 0.0);
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int l = idx / ncol, c = idx - l * ncol;
-    float2 acc = make_float2(0.f, 0.f);
+    double2 acc = make_double2(0.0, 0.0);
     const int e1 = cell_ptr[l + 1];
     for (int e = cell_ptr[l]; e < e1; ++e) {
-      const float2 x = vt[cell_k[e] * ncol + c];
-      const float wv = __ldg(cell_w + e);
-      acc.x = fmaf(x.x, wv, acc.x);
-      acc.y = fmaf(x.y, wv, acc.y);
+      const double2 x = vt[cell_k[e] * ncol + c];
+      const double wv = __ldg(cell_w + e);
+      acc.x = fma(x.x, wv, acc.x);
+      acc.y = fma(x.y, wv, acc.y);
     }
-    s[idx] = acc;
+    sd[idx] = acc;
   }
   __syncthreads();
-  fft_dif<-1>(s, logm, ncol, ncol, tw);
-  float2* oi = out + static_cast<long long>(blockIdx.y) * n0 * n2;
+  fft_dif<-1>(sd, logm, ncol, ncol, tw);
+  TOut* oi = out + static_cast<long long>(blockIdx.y) * n0 * n2;
   for (int idx = threadIdx.x; idx < n0 * ncol; idx += blockDim.x) {
     const int mode = idx / ncol, c = idx - mode * ncol;
     const int j = j0 + c;
     if (j >= n2) continue;
     const int slot = (mode - center) & mask;
-    oi[static_cast<long long>(mode) * n2 + j] = cscale(s[brev(slot, logm) * ncol + c], pdeconv[mode]);
+    const double2 r = cscale(sd[brev(slot, logm) * ncol + c], pdeconv[mode]);
+    TOut& o = oi[static_cast<long long>(mode) * n2 + j];
+    o.x = static_cast<decltype(o.x)>(r.x);
+    o.y = static_cast<decltype(o.y)>(r.y);
   }
 }
 
@@ -121,51 +125,48 @@ __global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, 
 // fu2d forward: row pass, column pass, gather
 // ------------------------------------------------------------------------------------------
 // S[i][c'][KB]: row FFT of v[i, k0+kk, :] * dx[i] * dy[:] placed at wrapped slots.
-__global__ void __launch_bounds__(256) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0,
-                                                   int nk, int n2, int logm2, int center2, int ks_n,
-                                                   const float* __restrict__ dx,
-                                                   const float* __restrict__ dy,
-                                                   const float2* __restrict__ tw2,
-                                                   float2* __restrict__ S) {
-  extern __shared__ float2 s[];
+__global__ void __launch_bounds__(256) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
+                                                   int n2, int logm2, int center2, int ks_n,
+                                                   const double* __restrict__ dx, const double* __restrict__ dy,
+                                                   const double2* __restrict__ tw2, float2* __restrict__ S) {
+  extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
-  const float di = dx[i];
+  const double di = dx[i];
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
     const int kk = idx / m2, r = idx - kk * m2;
     const int j = (r + center2) & mask2;
-    float2 val = make_float2(0.f, 0.f);
+    double2 val = make_double2(0.0, 0.0);
     if (j < n2 && ks + kk < nk)
-      val = cscale(v[(static_cast<long long>(i) * ld + k0 + ks + kk) * n2 + j], di * dy[j]);
-    s[r * sm + kk] = val;
+      val = cscale(to_d(v[(static_cast<long long>(i) * ld + k0 + ks + kk) * n2 + j]), di * dy[j]);
+    sd[r * sm + kk] = val;
   }
   __syncthreads();
-  fft_dif<+1>(s, logm2, ks_n, sm, tw2);
+  fft_dif<+1>(sd, logm2, ks_n, sm, tw2);
   float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
-    Si[static_cast<long long>(r) * KB + kk] = s[r * sm + kk];
+    Si[static_cast<long long>(r) * KB + kk] = to_f(sd[r * sm + kk]);
   }
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
-__global__ void __launch_bounds__(256) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1,
-                                                   int center1, int logm2, int ks_n,
-                                                   const float2* __restrict__ tw1,
+__global__ void __launch_bounds__(256) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
+                                                   int logm2, int ks_n, const double2* __restrict__ tw1,
                                                    float2* __restrict__ G) {
-  extern __shared__ float2 s[];
+  extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
   for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
     const int i = (r + center1) & mask1;
-    s[idx] = i < n1 ? S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] : make_float2(0.f, 0.f);
+    sd[idx] = i < n1 ? to_d(S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk]) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_dif<+1>(s, logm1, ks_n, ks_n, tw1);
+  fft_dif<+1>(sd, logm1, ks_n, ks_n, tw1);
   for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
-    G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = s[idx];
+    G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(sd[idx]);
   }
 }
 
@@ -180,14 +181,18 @@ struct GatherOut {
 };
 
 constexpr int kGatherThreads = 128;
+constexpr int kHalf = KB / 2;  // rows per gather thread (two threads per target)
 
+// Two threads per target, each owning 8 of the 16 batch rows: a tap loads
+// 64 B per thread (one 128 B grid cell per thread pair) and the 24-tap inner
+// and outer sums accumulate in double.
 __global__ void __launch_bounds__(kGatherThreads) k_fu2d_gather(
-    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk,
-    const int* __restrict__ r0, const int* __restrict__ c0, const float* __restrict__ w1,
-    const float* __restrict__ w2, const float2* __restrict__ fac, GatherOut eo,
-    double* __restrict__ partials, int accumulate) {
+    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ r0,
+    const int* __restrict__ c0, const float* __restrict__ w1, const float* __restrict__ w2,
+    const double2* __restrict__ fac, GatherOut eo, double* __restrict__ partials, int accumulate) {
   __shared__ double red_scratch[(kGatherThreads / 32) * 2];
-  const int tq = blockIdx.x * kGatherThreads + threadIdx.x;
+  const int gt = blockIdx.x * kGatherThreads + threadIdx.x;
+  const int tq = gt >> 1, half = gt & 1;
   const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1, m2 = 1 << logm2;
   double red[2] = {0.0, 0.0};
   if (tq < T) {
@@ -195,45 +200,47 @@ __global__ void __launch_bounds__(kGatherThreads) k_fu2d_gather(
 #pragma unroll
     for (int b = 0; b < kTaps; ++b) wb[b] = __ldg(w2 + static_cast<long long>(tq) * kTaps + b);
     const int rs = r0[tq], cs = c0[tq];
-    float2 acc[KB];
+    double2 acc[kHalf];
 #pragma unroll
-    for (int kk = 0; kk < KB; ++kk) acc[kk] = make_float2(0.f, 0.f);
+    for (int kk = 0; kk < kHalf; ++kk) acc[kk] = make_double2(0.0, 0.0);
     for (int a = 0; a < kTaps; ++a) {
       const long long rbase = static_cast<long long>(brev((rs + a) & mask1, logm1)) * m2;
-      float2 inner[KB];
+      double2 inner[kHalf];
 #pragma unroll
-      for (int kk = 0; kk < KB; ++kk) inner[kk] = make_float2(0.f, 0.f);
+      for (int kk = 0; kk < kHalf; ++kk) inner[kk] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int b = 0; b < kTaps; ++b) {
         const float4* gp =
-            reinterpret_cast<const float4*>(G + (rbase + brev((cs + b) & mask2, logm2)) * KB);
-        const float wv = wb[b];
+            reinterpret_cast<const float4*>(G + (rbase + brev((cs + b) & mask2, logm2)) * KB + half * kHalf);
+        const double wv = wb[b];
 #pragma unroll
-        for (int q = 0; q < KB / 2; ++q) {
+        for (int q = 0; q < kHalf / 2; ++q) {
           const float4 g = __ldg(gp + q);
-          inner[2 * q].x = fmaf(wv, g.x, inner[2 * q].x);
-          inner[2 * q].y = fmaf(wv, g.y, inner[2 * q].y);
-          inner[2 * q + 1].x = fmaf(wv, g.z, inner[2 * q + 1].x);
-          inner[2 * q + 1].y = fmaf(wv, g.w, inner[2 * q + 1].y);
+          inner[2 * q].x = fma(wv, static_cast<double>(g.x), inner[2 * q].x);
+          inner[2 * q].y = fma(wv, static_cast<double>(g.y), inner[2 * q].y);
+          inner[2 * q + 1].x = fma(wv, static_cast<double>(g.z), inner[2 * q + 1].x);
+          inner[2 * q + 1].y = fma(wv, static_cast<double>(g.w), inner[2 * q + 1].y);
         }
       }
-      const float wa = __ldg(w1 + static_cast<long long>(tq) * kTaps + a);
+      const double wa = __ldg(w1 + static_cast<long long>(tq) * kTaps + a);
 #pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
-        acc[kk].x = fmaf(wa, inner[kk].x, acc[kk].x);
-        acc[kk].y = fmaf(wa, inner[kk].y, acc[kk].y);
+      for (int kk = 0; kk < kHalf; ++kk) {
+        acc[kk].x = fma(wa, inner[kk].x, acc[kk].x);
+        acc[kk].y = fma(wa, inner[kk].y, acc[kk].y);
       }
     }
     const int t = tq / w, q = tq - (tq / w) * w;
-    const float2 f = fac[tq];
+    const double2 f = fac[tq];
 #pragma unroll
-    for (int kk = 0; kk < KB; ++kk) {
+    for (int kq = 0; kq < kHalf; ++kq) {
+      const int kk = half * kHalf + kq;
       if (kk >= nk) break;
-      float2 val = cmul(acc[kk], f);
-      if (eo.sub) val = csub(val, eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]);
-      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = val;
+      double2 val = cmul(acc[kq], f);
+      if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
+      const float2 vf = to_f(val);
+      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = vf;
       if (eo.reduce) {
-        red[0] += static_cast<double>(val.x) * val.x + static_cast<double>(val.y) * val.y;
+        red[0] += val.x * val.x + val.y * val.y;
         if (eo.dot) {
           const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
           red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
@@ -261,8 +268,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_fu2d_gather(
 // ------------------------------------------------------------------------------------------
 // val[t][KB] = p[t_, k0+kk, q_] * conj(phase product), zero for kk >= nk.
 __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict__ p, long long ld, long long k0,
-                                                       int nk, int T, int w,
-                                                       const float2* __restrict__ cfac,
+                                                       int nk, int T, int w, const double2* __restrict__ cfac,
                                                        float2* __restrict__ val) {
   __shared__ float2 tile[32][KB + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
     float2 x = make_float2(0.f, 0.f);
     if (t < T && kk < nk) {
       const int ta = t / w, q = t - ta * w;
-      x = cmul(p[(ta * ld + k0 + kk) * w + q], cfac[t]);
+      x = to_f(cmul(to_d(p[(ta * ld + k0 + kk) * w + q]), cfac[t]));
     }
     tile[tx][kk] = x;
   }
@@ -291,80 +297,78 @@ __global__ void __launch_bounds__(kTile* kTile) k_fu2d_adj_spread(
   const int tx = threadIdx.x % kTile, ty = threadIdx.x / kTile;
   const int r = blockIdx.y * kTile + ty, c = blockIdx.x * kTile + tx;
   const int tile = blockIdx.y * (m2 / kTile) + blockIdx.x;
-  float2 acc[KB];
+  double2 acc[KB];  // cells near nu = 0 sum thousands of terms
 #pragma unroll
-  for (int kk = 0; kk < KB; ++kk) acc[kk] = make_float2(0.f, 0.f);
+  for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
   const int e1 = tile_ptr[tile + 1];
   for (int e = tile_ptr[tile]; e < e1; ++e) {
     const int t = tile_t[e];
     const int a = (r - r0[t]) & mask1, b = (c - c0[t]) & mask2;
     if (a < kTaps && b < kTaps) {
-      const float wgt = __ldg(w1 + static_cast<long long>(t) * kTaps + a) *
-                        __ldg(w2 + static_cast<long long>(t) * kTaps + b);
+      const double wgt = static_cast<double>(__ldg(w1 + static_cast<long long>(t) * kTaps + a)) *
+                         static_cast<double>(__ldg(w2 + static_cast<long long>(t) * kTaps + b));
       const float4* vp = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB);
 #pragma unroll
       for (int q = 0; q < KB / 2; ++q) {
         const float4 x = __ldg(vp + q);
-        acc[2 * q].x = fmaf(wgt, x.x, acc[2 * q].x);
-        acc[2 * q].y = fmaf(wgt, x.y, acc[2 * q].y);
-        acc[2 * q + 1].x = fmaf(wgt, x.z, acc[2 * q + 1].x);
-        acc[2 * q + 1].y = fmaf(wgt, x.w, acc[2 * q + 1].y);
+        acc[2 * q].x = fma(wgt, static_cast<double>(x.x), acc[2 * q].x);
+        acc[2 * q].y = fma(wgt, static_cast<double>(x.y), acc[2 * q].y);
+        acc[2 * q + 1].x = fma(wgt, static_cast<double>(x.z), acc[2 * q + 1].x);
+        acc[2 * q + 1].y = fma(wgt, static_cast<double>(x.w), acc[2 * q + 1].y);
       }
     }
   }
   float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB);
 #pragma unroll
-  for (int q = 0; q < KB / 2; ++q)
-    gp[q] = make_float4(acc[2 * q].x, acc[2 * q].y, acc[2 * q + 1].x, acc[2 * q + 1].y);
+  for (int q = 0; q < KB / 2; ++q) {
+    const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
+    gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
-__global__ void __launch_bounds__(256) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1,
-                                                       int center1, int logm2, int ks_n,
-                                                       const float2* __restrict__ tw1,
+__global__ void __launch_bounds__(256) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
+                                                       int logm2, int ks_n, const double2* __restrict__ tw1,
                                                        float2* __restrict__ S) {
-  extern __shared__ float2 s[];
+  extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
   for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
-    s[idx] = G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk];
+    sd[idx] = to_d(G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk]);
   }
   __syncthreads();
-  fft_dif<-1>(s, logm1, ks_n, ks_n, tw1);
+  fft_dif<-1>(sd, logm1, ks_n, ks_n, tw1);
   for (int idx = threadIdx.x; idx < n1 * ks_n; idx += blockDim.x) {
     const int i = idx / ks_n, kk = idx - i * ks_n;
     const int slot = (i - center1) & mask1;
-    S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = s[brev(slot, logm1) * ks_n + kk];
+    S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = to_f(sd[brev(slot, logm1) * ks_n + kk]);
   }
 }
 
 // Row FFT(-1) (DIT from bit-reversed placement, natural output) and the
 // final deconvolution into out[i, k0_out+kk, j].
-__global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2,
-                                                       int logm2, int center2, int ks_n,
-                                                       const float* __restrict__ pdx,
-                                                       const float* __restrict__ dy,
-                                                       const float2* __restrict__ tw2,
+__global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
+                                                       int center2, int ks_n, const double* __restrict__ pdx,
+                                                       const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
                                                        long long k0_out) {
-  extern __shared__ float2 s[];
+  extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
   const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
     const int c = idx / ks_n, kk = idx - c * ks_n;
-    s[brev(c, logm2) * sm + kk] = Si[static_cast<long long>(c) * KB + kk];
+    sd[brev(c, logm2) * sm + kk] = to_d(Si[static_cast<long long>(c) * KB + kk]);
   }
   __syncthreads();
-  fft_dit<-1>(s, logm2, ks_n, sm, tw2);
-  const float pi = pdx[i];
+  fft_dit<-1>(sd, logm2, ks_n, sm, tw2);
+  const double pi = pdx[i];
   for (int idx = threadIdx.x; idx < ks_n * n2; idx += blockDim.x) {
     const int kk = idx / n2, j = idx - kk * n2;
     if (ks + kk >= nk) continue;
     const int slot = (j - center2) & mask2;
-    out[(static_cast<long long>(i) * ld_out + k0_out + ks + kk) * n2 + j] =
-        cscale(s[slot * sm + kk], pi * dy[j]);
+    out[(static_cast<long long>(i) * ld_out + k0_out + ks + kk) * n2 + j] = to_f(cscale(sd[slot * sm + kk], pi * dy[j]));
   }
 }
 
@@ -375,65 +379,63 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict_
 // ------------------------------------------------------------------------------------------
 // FFT along the contiguous axis of `rows` rows of length m (one CTA per ncol rows).
 template <int SIGN>
-__global__ void __launch_bounds__(256) k_center_fft_rows(const float2* __restrict__ in,
-                                                         float2* __restrict__ out, long long rows,
-                                                         int logm, int ncol, float scale,
-                                                         const float2* __restrict__ tw) {
-  extern __shared__ float2 s[];
+__global__ void __launch_bounds__(256) k_center_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
+                                                         long long rows, int logm, int ncol, double scale,
+                                                         const double2* __restrict__ tw) {
+  extern __shared__ double2 sd[];
   const int m = 1 << logm, sm = ncol + 1;
   const long long r0 = static_cast<long long>(blockIdx.x) * ncol;
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int c = idx / m, n = idx - c * m;
-    float2 x = make_float2(0.f, 0.f);
+    double2 x = make_double2(0.0, 0.0);
     if (r0 + c < rows) {
-      x = in[(r0 + c) * m + n];
-      if (n & 1) x = make_float2(-x.x, -x.y);
+      x = to_d(in[(r0 + c) * m + n]);
+      if (n & 1) x = make_double2(-x.x, -x.y);
     }
-    s[n * sm + c] = x;
+    sd[n * sm + c] = x;
   }
   __syncthreads();
-  fft_dif<SIGN>(s, logm, ncol, sm, tw);
+  fft_dif<SIGN>(sd, logm, ncol, sm, tw);
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int c = idx / m, k = idx - c * m;
     if (r0 + c >= rows) continue;
-    const float sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    out[(r0 + c) * m + k] = cscale(s[brev(k, logm) * sm + c], sg);
+    const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
+    out[(r0 + c) * m + k] = to_f(cscale(sd[brev(k, logm) * sm + c], sg));
   }
 }
 
 // FFT along the middle axis of [outer][m][inner] (one CTA per outer x ncol inner).
 template <int SIGN>
-__global__ void __launch_bounds__(256) k_center_fft_cols(const float2* in, float2* out, int inner,
-                                                         int logm, int ncol, float scale,
-                                                         const float2* __restrict__ tw) {
-  extern __shared__ float2 s[];
+__global__ void __launch_bounds__(256) k_center_fft_cols(const float2* in, float2* out, int inner, int logm, int ncol,
+                                                         double scale, const double2* __restrict__ tw) {
+  extern __shared__ double2 sd[];
   const int m = 1 << logm;
   const long long o = blockIdx.y;
   const int c0 = blockIdx.x * ncol;
   const float2* io = in + o * m * inner;
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int n = idx / ncol, c = idx - n * ncol;
-    float2 x = make_float2(0.f, 0.f);
+    double2 x = make_double2(0.0, 0.0);
     if (c0 + c < inner) {
-      x = io[static_cast<long long>(n) * inner + c0 + c];
-      if (n & 1) x = make_float2(-x.x, -x.y);
+      x = to_d(io[static_cast<long long>(n) * inner + c0 + c]);
+      if (n & 1) x = make_double2(-x.x, -x.y);
     }
-    s[idx] = x;
+    sd[idx] = x;
   }
   __syncthreads();
-  fft_dif<SIGN>(s, logm, ncol, ncol, tw);
+  fft_dif<SIGN>(sd, logm, ncol, ncol, tw);
   float2* oo = out + o * m * inner;
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
     if (c0 + c >= inner) continue;
-    const float sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    oo[static_cast<long long>(k) * inner + c0 + c] = cscale(s[brev(k, logm) * ncol + c], sg);
+    const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
+    oo[static_cast<long long>(k) * inner + c0 + c] = to_f(cscale(sd[brev(k, logm) * ncol + c], sg));
   }
 }
 
 // out[o, k, in] = sum_m W[k, m] x[o, m, in] (dense centred DFT along the middle axis).
-__global__ void k_dense_dft(const float2* __restrict__ in, float2* __restrict__ out, long long outer,
-                            int m, int inner, const float2* __restrict__ W) {
+__global__ void k_dense_dft(const float2* __restrict__ in, float2* __restrict__ out, long long outer, int m,
+                            int inner, const double2* __restrict__ W) {
   const long long total = outer * m * inner;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -442,22 +444,17 @@ __global__ void k_dense_dft(const float2* __restrict__ in, float2* __restrict__ 
     const int k = static_cast<int>(rest % m);
     const long long o = rest / m;
     const float2* io = in + o * m * inner + c;
-    float ax = 0.f, ay = 0.f;
-    for (int n = 0; n < m; ++n) {
-      const float2 x = io[static_cast<long long>(n) * inner];
-      const float2 wv = W[k * m + n];
-      ax = fmaf(x.x, wv.x, fmaf(-x.y, wv.y, ax));
-      ay = fmaf(x.x, wv.y, fmaf(x.y, wv.x, ay));
-    }
-    out[e] = make_float2(ax, ay);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int n = 0; n < m; ++n) acc = cadd(acc, cmul(to_d(io[static_cast<long long>(n) * inner]), W[k * m + n]));
+    out[e] = to_f(acc);
   }
 }
 
-std::vector<float2> twiddles(std::int64_t m) {
-  std::vector<float2> t(static_cast<std::size_t>(std::max<std::int64_t>(m / 2, 1)));
+std::vector<double2> twiddles(std::int64_t m) {
+  std::vector<double2> t(static_cast<std::size_t>(std::max<std::int64_t>(m / 2, 1)));
   for (std::int64_t k = 0; k < m / 2; ++k) {
     const double a = 2.0 * std::numbers::pi * static_cast<double>(k) / static_cast<double>(m);
-    t[static_cast<std::size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    t[static_cast<std::size_t>(k)] = make_double2(std::cos(a), std::sin(a));
   }
   return t;
 }
@@ -470,6 +467,11 @@ int ilog2(std::int64_t n) {
 }
 
 std::vector<float> to_float(const std::vector<double>& v) { return {v.begin(), v.end()}; }
+
+template <class K>
+void allow_big_smem(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
 
 }  // namespace
 
@@ -487,18 +489,21 @@ struct Usfft::Tables {
   // fu1d
   DimPlan pz;
   int z_ncol = 0;
-  DeviceBuffer<float> z_deconv, z_pdeconv, z_w, z_cell_w;
+  DeviceBuffer<double> z_deconv, z_pdeconv;
+  DeviceBuffer<float> z_w, z_cell_w;
   DeviceBuffer<int> z_start, z_cell_ptr, z_cell_k;
-  DeviceBuffer<float2> z_fac, z_cphase, z_tw;
+  DeviceBuffer<double2> z_fac, z_cphase, z_tw;
   // fu2d
   DimPlan px, py;
-  DeviceBuffer<float> x_deconv, x_pdeconv, y_deconv, t_w1, t_w2;
+  DeviceBuffer<double> x_deconv, x_pdeconv, y_deconv;
+  DeviceBuffer<float> t_w1, t_w2;
   DeviceBuffer<int> t_r0, t_c0, tile_ptr, tile_t;
-  DeviceBuffer<float2> t_fac, t_cfac, x_tw, y_tw;
+  DeviceBuffer<double2> t_fac, t_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint values
   // f2d
   bool f2d_fft = false;
-  DeviceBuffer<float2> h_tw, w_tw, Wh, Ww, Whc, Wwc, f2d_tmp;
+  DeviceBuffer<double2> h_tw, w_tw, Wh, Ww, Whc, Wwc;
+  DeviceBuffer<float2> f2d_tmp;
 };
 
 Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t_(new Tables) {
@@ -507,18 +512,18 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   // ---- fu1d plan (nufft.cpp:109-110) ----
   t.pz = DimPlan::make(g_.n0, fg.nu_z);
   const DimPlan& pz = t.pz;
-  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(8192 / pz.m, 1, 64));
+  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(4096 / pz.m, 1, 64));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
-  t.z_deconv.upload(to_float(pz.deconv), stream_);
-  std::vector<float> pdec(pz.deconv.size());
-  for (std::size_t i = 0; i < pdec.size(); ++i) pdec[i] = static_cast<float>(pz.pref * pz.deconv[i]);
+  t.z_deconv.upload(pz.deconv, stream_);
+  std::vector<double> pdec(pz.deconv.size());
+  for (std::size_t i = 0; i < pdec.size(); ++i) pdec[i] = pz.pref * pz.deconv[i];
   t.z_pdeconv.upload(pdec, stream_);
   t.z_start.upload(std::vector<int>(pz.start.begin(), pz.start.end()), stream_);
   t.z_w.upload(to_float(pz.weights), stream_);
-  std::vector<float2> fac(static_cast<std::size_t>(g_.h)), cph(static_cast<std::size_t>(g_.h));
+  std::vector<double2> fac(static_cast<std::size_t>(g_.h)), cph(static_cast<std::size_t>(g_.h));
   for (std::size_t k = 0; k < fac.size(); ++k) {
-    fac[k] = make_float2(static_cast<float>(pz.pref * pz.phase_re[k]), static_cast<float>(pz.pref * pz.phase_im[k]));
-    cph[k] = make_float2(static_cast<float>(pz.phase_re[k]), static_cast<float>(-pz.phase_im[k]));
+    fac[k] = make_double2(pz.pref * pz.phase_re[k], pz.pref * pz.phase_im[k]);
+    cph[k] = make_double2(pz.phase_re[k], -pz.phase_im[k]);
   }
   t.z_fac.upload(fac, stream_);
   t.z_cphase.upload(cph, stream_);
@@ -546,22 +551,22 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   t.py = DimPlan::make(g_.n2, fg.nu_y);
   const DimPlan &px = t.px, &py = t.py;
   const std::size_t T = fg.nu_x.size();
-  t.x_deconv.upload(to_float(px.deconv), stream_);
-  t.y_deconv.upload(to_float(py.deconv), stream_);
-  std::vector<float> pdx(px.deconv.size());
-  for (std::size_t i = 0; i < pdx.size(); ++i) pdx[i] = static_cast<float>(px.pref * py.pref * px.deconv[i]);
+  t.x_deconv.upload(px.deconv, stream_);
+  t.y_deconv.upload(py.deconv, stream_);
+  std::vector<double> pdx(px.deconv.size());
+  for (std::size_t i = 0; i < pdx.size(); ++i) pdx[i] = px.pref * py.pref * px.deconv[i];
   t.x_pdeconv.upload(pdx, stream_);
   t.t_r0.upload(std::vector<int>(px.start.begin(), px.start.end()), stream_);
   t.t_c0.upload(std::vector<int>(py.start.begin(), py.start.end()), stream_);
   t.t_w1.upload(to_float(px.weights), stream_);
   t.t_w2.upload(to_float(py.weights), stream_);
-  std::vector<float2> tf(T), tcf(T);
+  std::vector<double2> tf(T), tcf(T);
   for (std::size_t q = 0; q < T; ++q) {
     const std::complex<double> ph = std::complex<double>(px.phase_re[q], px.phase_im[q]) *
                                     std::complex<double>(py.phase_re[q], py.phase_im[q]);
     const std::complex<double> f = (px.pref * py.pref) * ph;
-    tf[q] = make_float2(static_cast<float>(f.real()), static_cast<float>(f.imag()));
-    tcf[q] = make_float2(static_cast<float>(ph.real()), static_cast<float>(-ph.imag()));
+    tf[q] = make_double2(f.real(), f.imag());
+    tcf[q] = make_double2(ph.real(), -ph.imag());
   }
   t.t_fac.upload(tf, stream_);
   t.t_cfac.upload(tcf, stream_);
@@ -613,15 +618,14 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
     t.w_tw.upload(twiddles(g_.w), stream_);
   } else {
     auto mat = [](std::int64_t n, bool conj) {
-      std::vector<float2> W(static_cast<std::size_t>(n * n));
+      std::vector<double2> W(static_cast<std::size_t>(n * n));
       const double c = static_cast<double>(n) / 2.0, sc = 1.0 / std::sqrt(static_cast<double>(n));
       for (std::int64_t k = 0; k < n; ++k)
         for (std::int64_t m = 0; m < n; ++m) {
           const std::complex<double> z = std::polar(
               sc, -2.0 * std::numbers::pi * (static_cast<double>(k) - c) * (static_cast<double>(m) - c) /
                       static_cast<double>(n));
-          W[static_cast<std::size_t>(k * n + m)] =
-              make_float2(static_cast<float>(z.real()), static_cast<float>(conj ? -z.imag() : z.imag()));
+          W[static_cast<std::size_t>(k * n + m)] = make_double2(z.real(), conj ? -z.imag() : z.imag());
         }
       return W;
     };
@@ -632,17 +636,18 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   }
   MLRG_CUDA(cudaStreamSynchronize(stream_));
   static bool smem_set = [] {
-    const int big = 200 * 1024;
-    cudaFuncSetAttribute(k_fu1d, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fu1d_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fu2d_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fu2d_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fu2d_adj_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_fu2d_adj_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_center_fft_rows<+1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_center_fft_rows<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_center_fft_cols<+1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_center_fft_cols<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    allow_big_smem(k_fu1d<float2>);
+    allow_big_smem(k_fu1d<double2>);
+    allow_big_smem(k_fu1d_adj<float2>);
+    allow_big_smem(k_fu1d_adj<double2>);
+    allow_big_smem(k_fu2d_rows);
+    allow_big_smem(k_fu2d_cols);
+    allow_big_smem(k_fu2d_adj_cols);
+    allow_big_smem(k_fu2d_adj_rows);
+    allow_big_smem(k_center_fft_rows<+1>);
+    allow_big_smem(k_center_fft_rows<-1>);
+    allow_big_smem(k_center_fft_cols<+1>);
+    allow_big_smem(k_center_fft_cols<-1>);
     return true;
   }();
   (void)smem_set;
@@ -652,63 +657,71 @@ Usfft::~Usfft() { delete t_; }
 
 int Usfft::reduce_grid() const { return 4 * sm_count(); }
 
-void Usfft::fu1d(const float2* u, float2* out, std::int64_t d0) {
+template <class TIn>
+void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0) {
   if (d0 <= 0) return;
   const Tables& t = *t_;
   const int ncol = t.z_ncol;
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
-  const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(float2);
+  const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(double2);
   prof::begin("k_fu1d", stream_);
-  k_fu1d<<<grid, 256, smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
-                                       static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
-                                       t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(),
-                                       t.z_tw.get());
+  k_fu1d<TIn><<<grid, 256, smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
+                                            static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
+                                            t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(),
+                                            t.z_tw.get());
   MLRG_LAUNCH_CHECK("k_fu1d");
   prof::end("k_fu1d", stream_);
 }
 
-void Usfft::fu1d_adj(const float2* v, float2* out, std::int64_t d0) {
+template <class TOut>
+void Usfft::fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0) {
   if (d0 <= 0) return;
   const Tables& t = *t_;
   const int ncol = t.z_ncol;
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
-  const std::size_t smem = static_cast<std::size_t>((t.pz.m + g_.h) * ncol) * sizeof(float2);
+  const std::size_t smem = static_cast<std::size_t>((t.pz.m + g_.h) * ncol) * sizeof(double2);
   prof::begin("k_fu1d_adj", stream_);
-  k_fu1d_adj<<<grid, 256, smem, stream_>>>(v, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
-                                           static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center),
-                                           ncol, t.z_cphase.get(), t.z_cell_ptr.get(), t.z_cell_k.get(),
-                                           t.z_cell_w.get(), t.z_pdeconv.get(), t.z_tw.get());
+  k_fu1d_adj<TOut><<<grid, 256, smem, stream_>>>(v, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
+                                                 static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center),
+                                                 ncol, t.z_cphase.get(), t.z_cell_ptr.get(), t.z_cell_k.get(),
+                                                 t.z_cell_w.get(), t.z_pdeconv.get(), t.z_tw.get());
   MLRG_LAUNCH_CHECK("k_fu1d_adj");
   prof::end("k_fu1d_adj", stream_);
 }
+
+void Usfft::fu1d(const float2* u, float2* out, std::int64_t d0) { fu1d_t(u, out, d0); }
+void Usfft::fu1d(const double2* u, float2* out, std::int64_t d0) { fu1d_t(u, out, d0); }
+void Usfft::fu1d_adj(const float2* v, float2* out, std::int64_t d0) { fu1d_adj_t(v, out, d0); }
+void Usfft::fu1d_adj(const float2* v, double2* out, std::int64_t d0) { fu1d_adj_t(v, out, d0); }
 
 int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t nk, const Fu2dEpilogue& epi) {
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int ggrid = static_cast<int>((T + kGatherThreads - 1) / kGatherThreads);
+  const int ggrid = static_cast<int>((2 * T + kGatherThreads - 1) / kGatherThreads);
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
     prof::begin("k_fu2d_rows", stream_);
     k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), 256,
-                  static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(float2), stream_>>>(
-        v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2,
-        t.x_deconv.get(), t.y_deconv.get(), t.y_tw.get(), t.S.get());
+                  static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
+        v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
+        t.y_deconv.get(), t.y_tw.get(), t.S.get());
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", stream_);
     prof::begin("k_fu2d_cols", stream_);
     k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), 256,
-                  static_cast<std::size_t>(t.px.m * ks1) * sizeof(float2), stream_>>>(
-        t.S.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1,
-        t.x_tw.get(), t.Gd.get());
+                  static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
+        t.S.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(),
+        t.Gd.get());
     MLRG_LAUNCH_CHECK("k_fu2d_cols");
     prof::end("k_fu2d_cols", stream_);
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
     prof::begin("k_fu2d_gather", stream_);
-    k_fu2d_gather<<<ggrid, kGatherThreads, 0, stream_>>>(
-        t.Gd.get(), static_cast<int>(T), static_cast<int>(g_.w), t.px.logm, t.py.logm, nb, t.t_r0.get(),
-        t.t_c0.get(), t.t_w1.get(), t.t_w2.get(), t.t_fac.get(), eo, partials_.dev(), b > 0 ? 1 : 0);
+    k_fu2d_gather<<<ggrid, kGatherThreads, 0, stream_>>>(t.Gd.get(), static_cast<int>(T), static_cast<int>(g_.w),
+                                                         t.px.logm, t.py.logm, nb, t.t_r0.get(), t.t_c0.get(),
+                                                         t.t_w1.get(), t.t_w2.get(), t.t_fac.get(), eo,
+                                                         partials_.dev(), b > 0 ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", stream_);
   }
@@ -730,22 +743,22 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     prof::begin("k_fu2d_adj_spread", stream_);
     k_fu2d_adj_spread<<<dim3(static_cast<unsigned>(t.py.m / kTile), static_cast<unsigned>(t.px.m / kTile)),
                         kTile * kTile, 0, stream_>>>(t.val.get(), t.px.logm, t.py.logm, t.tile_ptr.get(),
-                                                     t.tile_t.get(), t.t_r0.get(), t.t_c0.get(),
-                                                     t.t_w1.get(), t.t_w2.get(), t.Gd.get());
+                                                     t.tile_t.get(), t.t_r0.get(), t.t_c0.get(), t.t_w1.get(),
+                                                     t.t_w2.get(), t.Gd.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     prof::end("k_fu2d_adj_spread", stream_);
     prof::begin("k_fu2d_adj_cols", stream_);
     k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), 256,
-                      static_cast<std::size_t>(t.px.m * ks1) * sizeof(float2), stream_>>>(
+                      static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
         t.Gd.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1,
         t.x_tw.get(), t.S.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     prof::end("k_fu2d_adj_cols", stream_);
     prof::begin("k_fu2d_adj_rows", stream_);
     k_fu2d_adj_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), 256,
-                      static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(float2), stream_>>>(
-        t.S.get(), nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2,
-        t.x_pdeconv.get(), t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b);
+                      static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
+        t.S.get(), nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
+        t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
     prof::end("k_fu2d_adj_rows", stream_);
   }
@@ -758,20 +771,21 @@ void Usfft::f2d(const float2* p, float2* out, std::int64_t count, bool adjoint) 
   if (t.f2d_fft) {
     // rows (along w) into out, then columns (along h) in place
     const int lw = ilog2(w), lh = ilog2(h);
-    const int ncr = static_cast<int>(std::clamp<std::int64_t>(8192 / w, 1, 64));
+    const int ncr = static_cast<int>(std::clamp<std::int64_t>(4096 / w, 1, 64));
     const std::int64_t rows = count * h;
-    const std::size_t smr = static_cast<std::size_t>(w * (ncr + 1)) * sizeof(float2);
-    const float sw = static_cast<float>(1.0 / std::sqrt(static_cast<double>(w)));
-    const float sh = static_cast<float>(1.0 / std::sqrt(static_cast<double>(h)));
+    const std::size_t smr = static_cast<std::size_t>(w * (ncr + 1)) * sizeof(double2);
+    const double sw = 1.0 / std::sqrt(static_cast<double>(w)), sh = 1.0 / std::sqrt(static_cast<double>(h));
     const unsigned gr = static_cast<unsigned>((rows + ncr - 1) / ncr);
     if (adjoint) k_center_fft_rows<+1><<<gr, 256, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
     else k_center_fft_rows<-1><<<gr, 256, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
     MLRG_LAUNCH_CHECK("k_center_fft_rows");
-    const int ncc = static_cast<int>(std::clamp<std::int64_t>(8192 / h, 1, std::min<std::int64_t>(64, w)));
+    const int ncc = static_cast<int>(std::clamp<std::int64_t>(4096 / h, 1, std::min<std::int64_t>(64, w)));
     const dim3 gc(static_cast<unsigned>((w + ncc - 1) / ncc), static_cast<unsigned>(count));
-    const std::size_t smc = static_cast<std::size_t>(h * ncc) * sizeof(float2);
-    if (adjoint) k_center_fft_cols<+1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
-    else k_center_fft_cols<-1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
+    const std::size_t smc = static_cast<std::size_t>(h * ncc) * sizeof(double2);
+    if (adjoint)
+      k_center_fft_cols<+1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
+    else
+      k_center_fft_cols<-1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
     MLRG_LAUNCH_CHECK("k_center_fft_cols");
     return;
   }

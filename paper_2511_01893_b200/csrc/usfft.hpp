@@ -45,10 +45,13 @@ class Usfft {
   const Geometry& geometry() const { return g_; }
   cudaStream_t stream() const { return stream_; }
 
-  /// u: contiguous (d0, n0, n2) -> out (d0, h, n2).
+  /// u: contiguous (d0, n0, n2) -> out (d0, h, n2). The volume side may be
+  /// complex128 (the solver's iterate); the transform runs in complex64.
   void fu1d(const float2* u, float2* out, std::int64_t d0);
+  void fu1d(const double2* u, float2* out, std::int64_t d0);
   /// v: contiguous (d0, h, n2) -> out (d0, n0, n2).
   void fu1d_adj(const float2* v, float2* out, std::int64_t d0);
+  void fu1d_adj(const float2* v, double2* out, std::int64_t d0);
 
   /// Rows [k0, k0+nk) of an (n1, ld, n2) array -> rows of an (n_theta, ., w)
   /// array via the epilogue. Returns the number of partial doubles written
@@ -66,6 +69,10 @@ class Usfft {
   int reduce_grid() const;  // CTAs of an elementwise reduction kernel
 
  private:
+  template <class TIn>
+  void fu1d_t(const TIn* u, float2* out, std::int64_t d0);
+  template <class TOut>
+  void fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0);
   struct Tables;
   Geometry g_;
   cudaStream_t stream_;
