@@ -8,9 +8,9 @@
 //             host-built cell->target CSR (no atomics) -> DIF FFT(-1) -> read.
 //   fu2d      per batch of 16 detector rows, grid layout [M1][M2][16] (row
 //             batch innermost, 128 B per grid cell): row FFT pass, column FFT
-//             pass (both DIF, indices stay bit-reversed), then a 576-tap gather
-//             per target with the weights amortised over the 16 rows.
-//   fu2d_adj  mirror: targets binned per 8x8 cell tile (host CSR) -> each cell
+//             pass (both DIF, indices stay bit-reversed), then a warp-cooperative
+//             576-tap gather per target with weights amortised over the 16 rows.
+//   fu2d_adj  mirror: targets listed per 8x4 cell patch (host CSR) -> each cell
 //             gathers its targets (no atomics) -> column DIF(-1) -> row DIT(-1).
 // FFT butterflies, twiddles, deconvolution and accumulations run in double;
 // the oversampled grids between passes are stored in complex64 (common.cuh).
@@ -28,7 +28,6 @@ namespace mlrg {
 namespace {
 
 constexpr int KB = Usfft::kRowBatch;
-constexpr int kTile = 8;  // adjoint spread tile edge, in grid cells
 
 // k-columns per CTA of a 2D-grid FFT pass over length m (double smem <= ~140 KB).
 int pass_cols(std::int64_t m) { return static_cast<int>(std::clamp<std::int64_t>(8192 / m, 2, KB)); }
@@ -180,70 +179,145 @@ struct GatherOut {
   int reduce;
 };
 
-constexpr int kGatherThreads = 128;
-constexpr int kHalf = KB / 2;  // rows per gather thread (two threads per target)
 
-// Two threads per target, each owning 8 of the 16 batch rows: a tap loads
-// 64 B per thread (one 128 B grid cell per thread pair) and the 24-tap inner
-// and outer sums accumulate in double.
-__global__ void __launch_bounds__(kGatherThreads) k_fu2d_gather(
-    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ r0,
-    const int* __restrict__ c0, const float* __restrict__ w1, const float* __restrict__ w2,
-    const double2* __restrict__ fac, GatherOut eo, double* __restrict__ partials, int accumulate) {
-  __shared__ double red_scratch[(kGatherThreads / 32) * 2];
-  const int gt = blockIdx.x * kGatherThreads + threadIdx.x;
-  const int tq = gt >> 1, half = gt & 1;
+// ---- warp-cooperative gather -------------------------------------------------------------
+// Targets are binned by window origin (kBox x kBox cells) and cut into groups
+// of <= 32 (host, once per geometry). One
+// warp owns one group and walks the union of the group's 24x24 windows row by
+// row: the warp stages the row's grid cells (128 B each: 16 detector rows)
+// into shared memory with cp.async, double-buffered one row ahead, then every
+// lane reads the SAME cell (a broadcast) and weights it for its own target
+// (zero outside its window). Per cell a warp issues 8 broadcast loads and 32
+// FMA per lane instead of 32 scattered 128 B loads.
+struct GatherGroup {
+  int first, count, r0, c0, nr, nc;  // sorted-target range, union window origin and extent
+};
+
+constexpr int kGroupWarps = 4;
+constexpr int kWStride = kTaps + 1;  // padded smem weight rows (odd stride: no bank conflicts)
+constexpr int kBox = 12;             // group bounding box (cells) -> union window <= 37 x 37
+constexpr int kUnionMax = kTaps + kBox + 1;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct GatherSmem {
+  float4 row[2][kUnionMax][KB / 2];  // two staged union rows (complex64), 128 B per cell
+  double2 rowd[kUnionMax][KB];       // the row being consumed, widened once per warp
+  float w1[32][kWStride];
+  float w2[32][kWStride];
+};
+
+__device__ __forceinline__ void stage_row(GatherSmem& sm, int buf, const float2* __restrict__ G, long long rbase,
+                                          int c0, int c_lo, int c_hi, int mask2, int logm2, int lane) {
+  for (int idx = c_lo * (KB / 2) + lane; idx < c_hi * (KB / 2); idx += 32) {
+    const int cell = idx / (KB / 2), part = idx - cell * (KB / 2);
+    const float2* src = G + (rbase + brev((c0 + cell) & mask2, logm2)) * KB + 2 * part;
+    cp_async16(&sm.row[buf][cell][part], src);
+  }
+  cp_async_commit();
+}
+
+// Columns [c_lo, c_hi) that some lane needs in union row rr (empty: c_lo >= c_hi).
+__device__ __forceinline__ int2 row_span(int rr, int dr, int dc) {
+  const bool on = rr - dr >= 0 && rr - dr < kTaps;
+  return make_int2(__reduce_min_sync(0xffffffffu, on ? dc : 1 << 20),
+                   __reduce_max_sync(0xffffffffu, on ? dc + kTaps : -1));
+}
+
+__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_gather_warp(
+    const float2* __restrict__ G, int ngroups, const GatherGroup* __restrict__ groups, int w, int logm1, int logm2,
+    int nk, const int* __restrict__ g_tidx, const int* __restrict__ g_dr, const int* __restrict__ g_dc,
+    const float* __restrict__ g_w1, const float* __restrict__ g_w2, const double2* __restrict__ g_fac,
+    GatherOut eo, double* __restrict__ partials, int accumulate) {
+  extern __shared__ float4 dyn_smem[];
+  __shared__ double red_scratch[kGroupWarps * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  GatherSmem& sm = reinterpret_cast<GatherSmem*>(dyn_smem)[warp];
+  const int gi = blockIdx.x * kGroupWarps + warp;
   const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1, m2 = 1 << logm2;
   double red[2] = {0.0, 0.0};
-  if (tq < T) {
-    float wb[kTaps];
-#pragma unroll
-    for (int b = 0; b < kTaps; ++b) wb[b] = __ldg(w2 + static_cast<long long>(tq) * kTaps + b);
-    const int rs = r0[tq], cs = c0[tq];
-    double2 acc[kHalf];
-#pragma unroll
-    for (int kk = 0; kk < kHalf; ++kk) acc[kk] = make_double2(0.0, 0.0);
+  if (gi < ngroups) {
+    const GatherGroup gr = groups[gi];
+    const bool live = lane < gr.count;
+    const int st = gr.first + lane;
+    const int dr = live ? g_dr[st] : -1000, dc = live ? g_dc[st] : -1000;
+    int2 span = row_span(0, dr, dc);
+    stage_row(sm, 0, G, static_cast<long long>(brev(gr.r0 & mask1, logm1)) * m2, gr.c0, span.x, span.y, mask2,
+              logm2, lane);
     for (int a = 0; a < kTaps; ++a) {
-      const long long rbase = static_cast<long long>(brev((rs + a) & mask1, logm1)) * m2;
-      double2 inner[kHalf];
+      sm.w1[lane][a] = live ? g_w1[static_cast<long long>(st) * kTaps + a] : 0.f;
+      sm.w2[lane][a] = live ? g_w2[static_cast<long long>(st) * kTaps + a] : 0.f;
+    }
+    double2 acc[KB];
 #pragma unroll
-      for (int kk = 0; kk < kHalf; ++kk) inner[kk] = make_double2(0.0, 0.0);
+    for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
+    for (int rr = 0; rr < gr.nr; ++rr) {
+      const int2 cur = span;
+      if (rr + 1 < gr.nr) {
+        span = row_span(rr + 1, dr, dc);
+        stage_row(sm, (rr + 1) & 1, G, static_cast<long long>(brev((gr.r0 + rr + 1) & mask1, logm1)) * m2, gr.c0,
+                  span.x, span.y, mask2, logm2, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      // widen the staged row once per warp (not once per lane)
+      for (int idx = cur.x * (KB / 2) + lane; idx < cur.y * (KB / 2); idx += 32) {
+        const int cell = idx / (KB / 2), part = idx - cell * (KB / 2);
+        const float4 g = sm.row[rr & 1][cell][part];
+        sm.rowd[cell][2 * part] = make_double2(g.x, g.y);
+        sm.rowd[cell][2 * part + 1] = make_double2(g.z, g.w);
+      }
+      __syncwarp();
+      const int a = rr - dr;
+      const bool row_on = a >= 0 && a < kTaps;
+      double2 inner[KB];
 #pragma unroll
-      for (int b = 0; b < kTaps; ++b) {
-        const float4* gp =
-            reinterpret_cast<const float4*>(G + (rbase + brev((cs + b) & mask2, logm2)) * KB + half * kHalf);
-        const double wv = wb[b];
+      for (int kk = 0; kk < KB; ++kk) inner[kk] = make_double2(0.0, 0.0);
+      for (int cc = cur.x; cc < cur.y; ++cc) {
+        const int b = cc - dc;
+        const double wv = (row_on && b >= 0 && b < kTaps) ? static_cast<double>(sm.w2[lane][b]) : 0.0;
+        const double2* gp = sm.rowd[cc];
 #pragma unroll
-        for (int q = 0; q < kHalf / 2; ++q) {
-          const float4 g = __ldg(gp + q);
-          inner[2 * q].x = fma(wv, static_cast<double>(g.x), inner[2 * q].x);
-          inner[2 * q].y = fma(wv, static_cast<double>(g.y), inner[2 * q].y);
-          inner[2 * q + 1].x = fma(wv, static_cast<double>(g.z), inner[2 * q + 1].x);
-          inner[2 * q + 1].y = fma(wv, static_cast<double>(g.w), inner[2 * q + 1].y);
+        for (int kk = 0; kk < KB; ++kk) {
+          const double2 g = gp[kk];
+          inner[kk].x = fma(wv, g.x, inner[kk].x);
+          inner[kk].y = fma(wv, g.y, inner[kk].y);
         }
       }
-      const double wa = __ldg(w1 + static_cast<long long>(tq) * kTaps + a);
+      const double w1 = row_on ? static_cast<double>(sm.w1[lane][a]) : 0.0;
 #pragma unroll
-      for (int kk = 0; kk < kHalf; ++kk) {
-        acc[kk].x = fma(wa, inner[kk].x, acc[kk].x);
-        acc[kk].y = fma(wa, inner[kk].y, acc[kk].y);
+      for (int kk = 0; kk < KB; ++kk) {
+        acc[kk].x = fma(w1, inner[kk].x, acc[kk].x);
+        acc[kk].y = fma(w1, inner[kk].y, acc[kk].y);
       }
+      __syncwarp();  // row buffers are refilled by the next iterations
     }
-    const int t = tq / w, q = tq - (tq / w) * w;
-    const double2 f = fac[tq];
+    if (live) {
+      const int tq = g_tidx[st];
+      const int t = tq / w, q = tq - (tq / w) * w;
+      const double2 f = g_fac[st];
 #pragma unroll
-    for (int kq = 0; kq < kHalf; ++kq) {
-      const int kk = half * kHalf + kq;
-      if (kk >= nk) break;
-      double2 val = cmul(acc[kq], f);
-      if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
-      const float2 vf = to_f(val);
-      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = vf;
-      if (eo.reduce) {
-        red[0] += val.x * val.x + val.y * val.y;
-        if (eo.dot) {
-          const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
-          red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
+      for (int kk = 0; kk < KB; ++kk) {
+        if (kk >= nk) break;
+        double2 val = cmul(acc[kk], f);
+        if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
+        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
+        if (eo.reduce) {
+          red[0] += val.x * val.x + val.y * val.y;
+          if (eo.dot) {
+            const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
+            red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
+          }
         }
       }
     }
@@ -263,8 +337,143 @@ __global__ void __launch_bounds__(kGatherThreads) k_fu2d_gather(
   }
 }
 
+// ---- warp-cooperative spread (adjoint) -----------------------------------------------------
+// One warp owns an 8x4 patch of grid cells (lane = cell) and walks the host-built
+// list of targets whose window touches the patch, 32 targets per chunk: each
+// lane stages one target's window origin, weight rows and 16 values into
+// shared memory with cp.async (double-buffered one chunk ahead), the warp
+// widens the values to double once, then consumes the chunk target by target:
+// the values are a broadcast read and each lane adds its own weight. All sums
+// run in double (cells near nu = 0 receive thousands of terms). Patches are
+// processed heaviest first.
+constexpr int kPatchR = 8, kPatchC = 4;
+
+struct SpreadSmem {
+  float4 val[2][32][KB / 2];
+  double2 vald[32][KB];
+  float w1[2][32][kTaps];
+  float w2[2][32][kTaps];
+  int r0[2][32], c0[2][32];
+};
+
+__device__ __forceinline__ void stage_targets(SpreadSmem& sm, int buf, int e, int e1,
+                                              const int* __restrict__ patch_t, const int* __restrict__ r0,
+                                              const int* __restrict__ c0, const float* __restrict__ w1,
+                                              const float* __restrict__ w2, const float2* __restrict__ val,
+                                              int lane) {
+  if (e + lane < e1) {
+    const int t = patch_t[e + lane];
+    sm.r0[buf][lane] = r0[t];
+    sm.c0[buf][lane] = c0[t];
+    const float4* a = reinterpret_cast<const float4*>(w1 + static_cast<long long>(t) * kTaps);
+    const float4* b = reinterpret_cast<const float4*>(w2 + static_cast<long long>(t) * kTaps);
+    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB);
+#pragma unroll
+    for (int q = 0; q < kTaps / 4; ++q) {
+      cp_async16(&sm.w1[buf][lane][4 * q], a + q);
+      cp_async16(&sm.w2[buf][lane][4 * q], b + q);
+    }
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) cp_async16(&sm.val[buf][lane][q], v + q);
+  }
+  cp_async_commit();
+}
+
+// A work item is (patch, a sub-range of its target list): lists longer than
+// kSplit (the cells around nu = 0) are split over several warps whose double
+// partials are summed in item order by k_fu2d_adj_spread_reduce.
+struct SpreadItem {
+  int patch, e0, e1, slot;  // slot < 0: write the grid directly
+};
+constexpr int kSplit = 256;
+
+__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_adj_spread_warp(
+    const float2* __restrict__ val, int logm1, int logm2, int nitems, const SpreadItem* __restrict__ items,
+    const int* __restrict__ patch_t, const int* __restrict__ r0, const int* __restrict__ c0,
+    const float* __restrict__ w1, const float* __restrict__ w2, float2* __restrict__ G,
+    double2* __restrict__ partial) {
+  extern __shared__ float4 dyn_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SpreadSmem& sm = reinterpret_cast<SpreadSmem*>(dyn_smem)[warp];
+  const int pi = blockIdx.x * kGroupWarps + warp;
+  if (pi >= nitems) return;
+  const int m2 = 1 << logm2, mask1 = (1 << logm1) - 1, mask2 = m2 - 1;
+  const SpreadItem it = items[pi];
+  const int patch = it.patch;
+  const int npc = m2 / kPatchC;
+  const int r = (patch / npc) * kPatchR + lane / kPatchC, c = (patch % npc) * kPatchC + lane % kPatchC;
+  double2 acc[KB];
+#pragma unroll
+  for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
+  const int e0 = it.e0, e1 = it.e1;
+  if (e0 < e1) stage_targets(sm, 0, e0, e1, patch_t, r0, c0, w1, w2, val, lane);
+  for (int e = e0, chunk = 0; e < e1; e += 32, ++chunk) {
+    const int buf = chunk & 1;
+    if (e + 32 < e1) {
+      stage_targets(sm, buf ^ 1, e + 32, e1, patch_t, r0, c0, w1, w2, val, lane);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int n = min(32, e1 - e);
+    for (int idx = lane; idx < n * (KB / 2); idx += 32) {  // widen once per warp
+      const int j = idx / (KB / 2), part = idx - j * (KB / 2);
+      const float4 x = sm.val[buf][j][part];
+      sm.vald[j][2 * part] = make_double2(x.x, x.y);
+      sm.vald[j][2 * part + 1] = make_double2(x.z, x.w);
+    }
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {
+      const int a = (r - sm.r0[buf][j]) & mask1, b = (c - sm.c0[buf][j]) & mask2;
+      const double wgt = (a < kTaps && b < kTaps) ? static_cast<double>(sm.w1[buf][j][min(a, kTaps - 1)]) *
+                                                        static_cast<double>(sm.w2[buf][j][min(b, kTaps - 1)])
+                                                  : 0.0;
+      const double2* vp = sm.vald[j];
+#pragma unroll
+      for (int kk = 0; kk < KB; ++kk) {
+        const double2 x = vp[kk];
+        acc[kk].x = fma(wgt, x.x, acc[kk].x);
+        acc[kk].y = fma(wgt, x.y, acc[kk].y);
+      }
+    }
+    __syncwarp();  // this buffer is refilled by the prefetch two chunks ahead
+  }
+  if (it.slot >= 0) {
+    double2* pp = partial + (static_cast<long long>(it.slot) * 32 + lane) * KB;
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) pp[kk] = acc[kk];
+    return;
+  }
+  float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB);
+#pragma unroll
+  for (int q = 0; q < KB / 2; ++q) {
+    const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
+    gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
+}
+
+// Sums the split patches' partials in item order (deterministic) into the grid.
+__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_adj_spread_reduce(
+    int nsplit, const int4* __restrict__ split, int logm2, const double2* __restrict__ partial,
+    float2* __restrict__ G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int si = blockIdx.x * kGroupWarps + warp;
+  if (si >= nsplit) return;
+  const int4 sp = split[si];  // (patch, first slot, slot count, -)
+  const int m2 = 1 << logm2, npc = m2 / kPatchC;
+  const int r = (sp.x / npc) * kPatchR + lane / kPatchC, c = (sp.x % npc) * kPatchC + lane % kPatchC;
+  float2* gp = G + (static_cast<long long>(r) * m2 + c) * KB;
+#pragma unroll
+  for (int kk = 0; kk < KB; ++kk) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int q = 0; q < sp.z; ++q) a = cadd(a, partial[(static_cast<long long>(sp.y + q) * 32 + lane) * KB + kk]);
+    gp[kk] = to_f(a);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
-// fu2d adjoint: prep, tile spread, column pass, row pass
+// fu2d adjoint: prep, column pass, row pass (the spread is above)
 // ------------------------------------------------------------------------------------------
 // val[t][KB] = p[t_, k0+kk, q_] * conj(phase product), zero for kk >= nk.
 __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict__ p, long long ld, long long k0,
@@ -286,43 +495,6 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
     const int tt = e / KB, kk = e - tt * KB;
     const long long tg = static_cast<long long>(blockIdx.x) * 32 + tt;
     if (tg < T) val[tg * KB + kk] = tile[tt][kk];
-  }
-}
-
-__global__ void __launch_bounds__(kTile* kTile) k_fu2d_adj_spread(
-    const float2* __restrict__ val, int logm1, int logm2, const int* __restrict__ tile_ptr,
-    const int* __restrict__ tile_t, const int* __restrict__ r0, const int* __restrict__ c0,
-    const float* __restrict__ w1, const float* __restrict__ w2, float2* __restrict__ G) {
-  const int m2 = 1 << logm2, mask1 = (1 << logm1) - 1, mask2 = m2 - 1;
-  const int tx = threadIdx.x % kTile, ty = threadIdx.x / kTile;
-  const int r = blockIdx.y * kTile + ty, c = blockIdx.x * kTile + tx;
-  const int tile = blockIdx.y * (m2 / kTile) + blockIdx.x;
-  double2 acc[KB];  // cells near nu = 0 sum thousands of terms
-#pragma unroll
-  for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
-  const int e1 = tile_ptr[tile + 1];
-  for (int e = tile_ptr[tile]; e < e1; ++e) {
-    const int t = tile_t[e];
-    const int a = (r - r0[t]) & mask1, b = (c - c0[t]) & mask2;
-    if (a < kTaps && b < kTaps) {
-      const double wgt = static_cast<double>(__ldg(w1 + static_cast<long long>(t) * kTaps + a)) *
-                         static_cast<double>(__ldg(w2 + static_cast<long long>(t) * kTaps + b));
-      const float4* vp = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB);
-#pragma unroll
-      for (int q = 0; q < KB / 2; ++q) {
-        const float4 x = __ldg(vp + q);
-        acc[2 * q].x = fma(wgt, static_cast<double>(x.x), acc[2 * q].x);
-        acc[2 * q].y = fma(wgt, static_cast<double>(x.y), acc[2 * q].y);
-        acc[2 * q + 1].x = fma(wgt, static_cast<double>(x.z), acc[2 * q + 1].x);
-        acc[2 * q + 1].y = fma(wgt, static_cast<double>(x.w), acc[2 * q + 1].y);
-      }
-    }
-  }
-  float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB);
-#pragma unroll
-  for (int q = 0; q < KB / 2; ++q) {
-    const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
-    gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
   }
 }
 
@@ -497,9 +669,21 @@ struct Usfft::Tables {
   DimPlan px, py;
   DeviceBuffer<double> x_deconv, x_pdeconv, y_deconv;
   DeviceBuffer<float> t_w1, t_w2;
-  DeviceBuffer<int> t_r0, t_c0, tile_ptr, tile_t;
+  DeviceBuffer<int> t_r0, t_c0;
   DeviceBuffer<double2> t_fac, t_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint values
+  // warp-cooperative gather: Morton-sorted target groups
+  int ngroups = 0;
+  DeviceBuffer<GatherGroup> groups;
+  DeviceBuffer<int> g_tidx, g_dr, g_dc;
+  DeviceBuffer<float> g_w1, g_w2;
+  DeviceBuffer<double2> g_fac;
+  // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
+  int nitems = 0, nsplit = 0;
+  DeviceBuffer<int> patch_t;
+  DeviceBuffer<SpreadItem> items;
+  DeviceBuffer<int4> split;
+  DeviceBuffer<double2> partial;
   // f2d
   bool f2d_fft = false;
   DeviceBuffer<double2> h_tw, w_tw, Wh, Ww, Whc, Wwc;
@@ -558,8 +742,9 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   t.x_pdeconv.upload(pdx, stream_);
   t.t_r0.upload(std::vector<int>(px.start.begin(), px.start.end()), stream_);
   t.t_c0.upload(std::vector<int>(py.start.begin(), py.start.end()), stream_);
-  t.t_w1.upload(to_float(px.weights), stream_);
-  t.t_w2.upload(to_float(py.weights), stream_);
+  const std::vector<float> w1f = to_float(px.weights), w2f = to_float(py.weights);
+  t.t_w1.upload(w1f, stream_);
+  t.t_w2.upload(w2f, stream_);
   std::vector<double2> tf(T), tcf(T);
   for (std::size_t q = 0; q < T; ++q) {
     const std::complex<double> ph = std::complex<double>(px.phase_re[q], px.phase_im[q]) *
@@ -570,40 +755,114 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   }
   t.t_fac.upload(tf, stream_);
   t.t_cfac.upload(tcf, stream_);
-  {  // 8x8 cell tile -> targets whose 24x24 window touches it, targets ascending
-    const std::int64_t ntr = px.m / kTile, ntc = py.m / kTile;
-    auto tiles_of = [&](std::int32_t st, std::int64_t m, int* out) {
+  {  // gather groups: <= 32 targets from one kBox x kBox bin of window origins
+    std::vector<int> order(T);
+    for (std::size_t q = 0; q < T; ++q) order[q] = static_cast<int>(q);
+    // fixed kBox x kBox bins of the window origin (2.6M vs 3.3M union cells per
+    // 256^3 launch compared with Morton runs), row-major inside a bin
+    std::vector<std::uint64_t> key(T);
+    for (std::size_t q = 0; q < T; ++q) {
+      const std::uint64_t r = static_cast<std::uint64_t>(px.start[q]), c = static_cast<std::uint64_t>(py.start[q]);
+      key[q] = ((r / kBox) << 48) | ((c / kBox) << 32) | (r << 16) | c;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
+    std::vector<GatherGroup> grp;
+    std::vector<int> tidx(T), dr(T), dc(T);
+    std::vector<float> gw1(T * kTaps), gw2(T * kTaps);
+    std::vector<double2> gfac(T);
+    std::size_t i = 0;
+    while (i < T) {
+      const std::size_t first = i;
+      int rmin = px.start[static_cast<std::size_t>(order[i])], rmax = rmin;
+      int cmin = py.start[static_cast<std::size_t>(order[i])], cmax = cmin;
+      ++i;
+      while (i < T && i - first < 32) {
+        const int r = px.start[static_cast<std::size_t>(order[i])], c = py.start[static_cast<std::size_t>(order[i])];
+        if ((key[static_cast<std::size_t>(order[i])] >> 32) != (key[static_cast<std::size_t>(order[first])] >> 32)) break;
+        if (std::max(rmax, r) - std::min(rmin, r) > kBox || std::max(cmax, c) - std::min(cmin, c) > kBox) break;
+        rmin = std::min(rmin, r), rmax = std::max(rmax, r), cmin = std::min(cmin, c), cmax = std::max(cmax, c);
+        ++i;
+      }
+      grp.push_back(GatherGroup{static_cast<int>(first), static_cast<int>(i - first), rmin, cmin,
+                                rmax - rmin + kTaps, cmax - cmin + kTaps});
+      for (std::size_t s = first; s < i; ++s) {
+        const std::size_t q = static_cast<std::size_t>(order[s]);
+        tidx[s] = static_cast<int>(q);
+        dr[s] = px.start[q] - rmin;
+        dc[s] = py.start[q] - cmin;
+        std::copy_n(w1f.begin() + static_cast<std::ptrdiff_t>(q * kTaps), kTaps,
+                    gw1.begin() + static_cast<std::ptrdiff_t>(s * kTaps));
+        std::copy_n(w2f.begin() + static_cast<std::ptrdiff_t>(q * kTaps), kTaps,
+                    gw2.begin() + static_cast<std::ptrdiff_t>(s * kTaps));
+        gfac[s] = tf[q];
+      }
+    }
+    t.ngroups = static_cast<int>(grp.size());
+    t.groups.upload(grp, stream_);
+    t.g_tidx.upload(tidx, stream_);
+    t.g_dr.upload(dr, stream_);
+    t.g_dc.upload(dc, stream_);
+    t.g_w1.upload(gw1, stream_);
+    t.g_w2.upload(gw2, stream_);
+    t.g_fac.upload(gfac, stream_);
+  }
+  {  // spread patches: 8x4 cells -> targets whose 24x24 window touches them (targets ascending)
+    const std::int64_t npr = px.m / kPatchR, npc = py.m / kPatchC;
+    const int npatch = static_cast<int>(npr * npc);
+    auto cover = [&](std::int32_t st, std::int64_t m, int edge, int* out) {
       int n = 0;
       for (int a = 0; a < kTaps; ++a) {
-        const int tl = static_cast<int>(((st + a) % m) / kTile);
+        const int p = static_cast<int>(((st + a) % m) / edge);
         bool seen = false;
-        for (int e = 0; e < n; ++e) seen |= out[e] == tl;
-        if (!seen) out[n++] = tl;
+        for (int e = 0; e < n; ++e) seen |= out[e] == p;
+        if (!seen) out[n++] = p;
       }
       return n;
     };
-    std::vector<int> cnt(static_cast<std::size_t>(ntr * ntc + 1), 0);
-    int tr[kTaps], tc[kTaps];
+    std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0), lst;
+    int pr[kTaps], pc[kTaps];
     for (int pass = 0; pass < 2; ++pass) {
       std::vector<int> pos;
-      std::vector<int> lst;
       if (pass == 1) {
         for (std::size_t l = 1; l < cnt.size(); ++l) cnt[l] += cnt[l - 1];
         pos.assign(cnt.begin(), cnt.end() - 1);
         lst.resize(static_cast<std::size_t>(cnt.back()));
       }
       for (std::size_t q = 0; q < T; ++q) {
-        const int nr = tiles_of(px.start[q], px.m, tr), nc = tiles_of(py.start[q], py.m, tc);
+        const int nr = cover(px.start[q], px.m, kPatchR, pr), nc = cover(py.start[q], py.m, kPatchC, pc);
         for (int a = 0; a < nr; ++a)
           for (int b = 0; b < nc; ++b) {
-            const std::size_t tile = static_cast<std::size_t>(tr[a] * ntc + tc[b]);
-            if (pass == 0) cnt[tile + 1]++;
-            else lst[static_cast<std::size_t>(pos[tile]++)] = static_cast<int>(q);
+            const std::size_t p = static_cast<std::size_t>(pr[a] * npc + pc[b]);
+            if (pass == 0) cnt[p + 1]++;
+            else lst[static_cast<std::size_t>(pos[p]++)] = static_cast<int>(q);
           }
       }
-      if (pass == 1) t.tile_t.upload(lst, stream_);
     }
-    t.tile_ptr.upload(cnt, stream_);
+    std::vector<int> porder(static_cast<std::size_t>(npatch));
+    for (int p = 0; p < npatch; ++p) porder[static_cast<std::size_t>(p)] = p;
+    std::stable_sort(porder.begin(), porder.end(), [&](int a, int b) {
+      return cnt[static_cast<std::size_t>(a) + 1] - cnt[static_cast<std::size_t>(a)] >
+             cnt[static_cast<std::size_t>(b) + 1] - cnt[static_cast<std::size_t>(b)];
+    });
+    std::vector<SpreadItem> items;
+    std::vector<int4> split;
+    int slots = 0;
+    for (const int p : porder) {  // heaviest first
+      const int e0 = cnt[static_cast<std::size_t>(p)], e1 = cnt[static_cast<std::size_t>(p) + 1];
+      if (e1 - e0 <= kSplit) {
+        items.push_back(SpreadItem{p, e0, e1, -1});
+        continue;
+      }
+      const int first = slots;
+      for (int e = e0; e < e1; e += kSplit) items.push_back(SpreadItem{p, e, std::min(e1, e + kSplit), slots++});
+      split.push_back(make_int4(p, first, slots - first, 0));
+    }
+    t.nitems = static_cast<int>(items.size());
+    t.nsplit = static_cast<int>(split.size());
+    t.items.upload(items, stream_);
+    t.split.upload(split, stream_);
+    t.partial.resize(static_cast<std::size_t>(std::max(slots, 1)) * 32 * KB);
+    t.patch_t.upload(lst, stream_);
   }
   t.x_tw.upload(twiddles(px.m), stream_);
   t.y_tw.upload(twiddles(py.m), stream_);
@@ -641,6 +900,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
     allow_big_smem(k_fu1d_adj<float2>);
     allow_big_smem(k_fu1d_adj<double2>);
     allow_big_smem(k_fu2d_rows);
+    allow_big_smem(k_fu2d_gather_warp);
+    allow_big_smem(k_fu2d_adj_spread_warp);
     allow_big_smem(k_fu2d_cols);
     allow_big_smem(k_fu2d_adj_cols);
     allow_big_smem(k_fu2d_adj_rows);
@@ -698,7 +959,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int ggrid = static_cast<int>((2 * T + kGatherThreads - 1) / kGatherThreads);
+  const int ggrid = (t.ngroups + kGroupWarps - 1) / kGroupWarps;
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
     prof::begin("k_fu2d_rows", stream_);
@@ -718,10 +979,9 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
     prof::begin("k_fu2d_gather", stream_);
-    k_fu2d_gather<<<ggrid, kGatherThreads, 0, stream_>>>(t.Gd.get(), static_cast<int>(T), static_cast<int>(g_.w),
-                                                         t.px.logm, t.py.logm, nb, t.t_r0.get(), t.t_c0.get(),
-                                                         t.t_w1.get(), t.t_w2.get(), t.t_fac.get(), eo,
-                                                         partials_.dev(), b > 0 ? 1 : 0);
+    k_fu2d_gather_warp<<<ggrid, 32 * kGroupWarps, kGroupWarps * sizeof(GatherSmem), stream_>>>(
+        t.Gd.get(), t.ngroups, t.groups.get(), static_cast<int>(g_.w), t.px.logm, t.py.logm, nb, t.g_tidx.get(),
+        t.g_dr.get(), t.g_dc.get(), t.g_w1.get(), t.g_w2.get(), t.g_fac.get(), eo, partials_.dev(), b > 0 ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", stream_);
   }
@@ -741,11 +1001,16 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
     prof::end("k_fu2d_adj_prep", stream_);
     prof::begin("k_fu2d_adj_spread", stream_);
-    k_fu2d_adj_spread<<<dim3(static_cast<unsigned>(t.py.m / kTile), static_cast<unsigned>(t.px.m / kTile)),
-                        kTile * kTile, 0, stream_>>>(t.val.get(), t.px.logm, t.py.logm, t.tile_ptr.get(),
-                                                     t.tile_t.get(), t.t_r0.get(), t.t_c0.get(), t.t_w1.get(),
-                                                     t.t_w2.get(), t.Gd.get());
+    k_fu2d_adj_spread_warp<<<(t.nitems + kGroupWarps - 1) / kGroupWarps, 32 * kGroupWarps,
+                             kGroupWarps * sizeof(SpreadSmem), stream_>>>(
+        t.val.get(), t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
+        t.t_w1.get(), t.t_w2.get(), t.Gd.get(), t.partial.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
+    if (t.nsplit > 0) {
+      k_fu2d_adj_spread_reduce<<<(t.nsplit + kGroupWarps - 1) / kGroupWarps, 32 * kGroupWarps, 0, stream_>>>(
+          t.nsplit, t.split.get(), t.py.logm, t.partial.get(), t.Gd.get());
+      MLRG_LAUNCH_CHECK("k_fu2d_adj_spread_reduce");
+    }
     prof::end("k_fu2d_adj_spread", stream_);
     prof::begin("k_fu2d_adj_cols", stream_);
     k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), 256,
