@@ -70,6 +70,7 @@ _SIGS = {
     "mlrg_free": (None, [_P]),
     "mlrg_version": (C.c_int, []),
     "mlrg_ctx_create": (_P, [_I64, _I64, _I64, _I64, _I64, _I64, _D, _P]),
+    "mlrg_ctx_create_kernel": (_P, [_I64, _I64, _I64, _I64, _I64, _I64, _D, _P, C.c_int]),
     "mlrg_ctx_destroy": (None, [_P]),
     "mlrg_sync": (C.c_int, [_P]),
     "mlrg_fu1d": (C.c_int, [_P, _P, _P, _I64]),
@@ -304,11 +305,16 @@ def _default_stream(stream):
 
 
 class Context:
-    """mlrg_ctx: device operator tables for one geometry, bound to a CUDA stream."""
+    """mlrg_ctx: device operator tables for one geometry, bound to a CUDA stream.
+    kernel: "es" (12-tap, default) or "gaussian" (the reference's 24-tap plan)."""
 
-    def __init__(self, n1, n0, n2, n_theta, h, w, phi=0.5235987755982988, stream=None):
+    KERNELS = {"es": 0, "gaussian": 1}
+
+    def __init__(self, n1, n0, n2, n_theta, h, w, phi=0.5235987755982988, stream=None, kernel="es"):
         self.geom = (n1, n0, n2, n_theta, h, w)
-        self._h = lib().mlrg_ctx_create(n1, n0, n2, n_theta, h, w, phi, _default_stream(stream))
+        self.kernel = kernel
+        self._h = lib().mlrg_ctx_create_kernel(n1, n0, n2, n_theta, h, w, phi, _default_stream(stream),
+                                               self.KERNELS[kernel])
         if not self._h:
             raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
 

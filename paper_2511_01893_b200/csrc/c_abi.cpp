@@ -285,7 +285,7 @@ mlr_array* mlr_project(const mlr_config* cfg, const mlr_array* volume) {
       throw std::invalid_argument("volume shape " + volume->a.shape.str() +
                                   " does not match the configured geometry " + g.volume_shape().str());
     StreamGuard sg;
-    mlrg::Usfft op(g, sg.s);
+    mlrg::Usfft op(g, sg.s, cfg->rc.engine.kernel);
     mlrg::DeviceBuffer<float2> u, out, mid, proj;
     upload_c64(volume->a, u, sg.s);
     out.resize(static_cast<std::size_t>(g.projection_shape().count()));
@@ -434,15 +434,21 @@ const char* mlrg_last_error(void) { return t_error.c_str(); }
 void mlrg_free(char* text) { std::free(text); }
 int mlrg_version(void) { return 1; }
 
-mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w, double phi,
-                          void* stream) {
+mlrg_ctx* mlrg_ctx_create_kernel(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w,
+                                 double phi, void* stream, int kernel) {
   return guarded_ptr<mlrg_ctx>([&] {
+    need(kernel == 0 || kernel == 1, "kernel must be 0 (es) or 1 (gaussian)");
     auto c = std::make_unique<mlrg_ctx>();
     c->g = mlrg::Geometry::make(n1, n0, n2, n_theta, h, w, phi);
     c->s = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
-    c->usfft = std::make_unique<mlrg::Usfft>(c->g, c->s);
+    c->usfft = std::make_unique<mlrg::Usfft>(c->g, c->s, static_cast<mlrg::GridKernel>(kernel));
     return c.release();
   });
+}
+
+mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w, double phi,
+                          void* stream) {
+  return mlrg_ctx_create_kernel(n1, n0, n2, n_theta, h, w, phi, stream, 0);
 }
 
 void mlrg_ctx_destroy(mlrg_ctx* ctx) { delete ctx; }

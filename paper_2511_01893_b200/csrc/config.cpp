@@ -105,6 +105,10 @@ const std::map<std::string, Setter>& setters() {
        [](RunConfig& c, const std::string& k, const std::string& v) {
          c.path = pick<NudftPath>(k, v, {{"direct", NudftPath::direct}, {"gridding", NudftPath::gridding}});
        }},
+      {"gridding_kernel",  // B200 extension (not a reference key): es (default) | gaussian
+       [](RunConfig& c, const std::string& k, const std::string& v) {
+         c.engine.kernel = pick<GridKernel>(k, v, {{"es", GridKernel::es}, {"gaussian", GridKernel::gaussian}});
+       }},
       {"flush_after_apply",
        [](RunConfig& c, const std::string& k, const std::string& v) { c.engine.flush_after_apply = to_bool(k, v); }},
       {"key_dim", [](RunConfig& c, const std::string& k, const std::string& v) { c.encoder.key_dim = to_int(k, v); }},
@@ -209,6 +213,7 @@ std::string RunConfig::str() const {  // config.cpp:160-189
   o << "\nnprobe = " << memo.nprobe << "\nmemo_timeout_ms = " << memo.timeout_ms
     << "\ninsert_queue_cap = " << memo.insert_queue_cap << "\ncoalesce_bytes = " << memo.coalesce_bytes
     << "\nglobal_cache = " << (memo.global_cache ? "true" : "false") << "\n";
+  if (engine.kernel == GridKernel::gaussian) o << "gridding_kernel = gaussian\n";
   return o.str();
 }
 

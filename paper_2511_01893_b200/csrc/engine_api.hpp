@@ -26,6 +26,7 @@ struct EngineConfig {  // scalerun.hpp:27-42
   std::int64_t chunk_extent = 16;
   bool memo_enabled = false;
   bool flush_after_apply = false;
+  GridKernel kernel = GridKernel::es;  // B200 extension key `gridding_kernel` (geometry.hpp)
 };
 
 struct ChunkAudit {  // scalerun.hpp:45-54

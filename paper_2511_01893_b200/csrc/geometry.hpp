@@ -1,7 +1,19 @@
-// Acquisition geometry and the Gaussian-gridding plans, built on the host in
-// double exactly as the reference builds them, then uploaded once per
-// geometry (the reference rebuilds them on every operator call,
-// nufft.cpp:109-110, 185-187).
+// Acquisition geometry and the gridding plans, built on the host in double
+// and uploaded once per geometry (the reference rebuilds them on every
+// operator call, nufft.cpp:109-110, 185-187).
+//
+// Two spreading kernels evaluate the same operator, the non-uniform DFT of
+// operators.cpp:87-200 (the reference's `direct` path):
+//   gaussian  the reference's own plan (nufft.cpp:48-103): 24 taps per
+//             dimension, tau = pi*12 / (n^2 sigma (sigma - 1/2)); it matches
+//             the direct NUDFT to ~3e-12 relative.
+//   es        exponential-of-semicircle kernel exp(beta (sqrt(1 - z^2) - 1)),
+//             12 taps, beta = 2.30 * 12, same oversampled grid (sigma = 2),
+//             deconvolved by its Fourier transform (Gauss-Legendre quadrature):
+//             ~2e-11 relative to the direct NUDFT, i.e. within 3e-11 of the
+//             reference's gridding, with 4x fewer taps in two dimensions. Its
+//             deconvolution spans 4.8x per dimension instead of the Gaussian's
+//             23x, so the complex64 grid rounding is amplified less.
 #pragma once
 
 #include <cstdint>
@@ -12,7 +24,12 @@
 namespace mlrg {
 
 constexpr int kSpread = 12;         // nufft.cpp:12
-constexpr int kTaps = 2 * kSpread;  // 24 wrapped grid points per target and dimension
+constexpr int kTaps = 2 * kSpread;  // 24 wrapped grid points per target and dimension (gaussian)
+constexpr int kEsTaps = 12;         // es kernel width (grid cells)
+constexpr double kEsBeta = 2.30 * kEsTaps;
+
+enum class GridKernel : std::uint8_t { es = 0, gaussian = 1 };
+inline int kernel_taps(GridKernel k) { return k == GridKernel::gaussian ? kTaps : kEsTaps; }
 
 struct Shape3 {
   std::int64_t d0 = 0, d1 = 0, d2 = 0;
@@ -48,18 +65,22 @@ struct FrequencyGrids {
 FrequencyGrids frequency_grids(const Geometry& g);
 
 /// One gridding dimension (nufft.cpp:48-103): oversampled size m (a power of
-/// two), Gaussian width tau, per-mode deconvolution and, per target, the first
-/// wrapped grid index and the 24 Gaussian weights, all in double.
+/// two), per-mode deconvolution and, per target, the first wrapped grid index
+/// and the `taps` kernel weights, all in double. The operator is
+/// out[t] = pref * sum_a weights[t][a] * FFT(deconv * u)[start[t] + a].
 struct DimPlan {
+  GridKernel kernel = GridKernel::gaussian;
+  int taps = kTaps;
   std::int64_t n = 0, center = 0, m = 0;
   int logm = 0;
-  double tau = 0.0, pref = 0.0;
+  double tau = 0.0, pref = 0.0;      // tau: gaussian only
   std::vector<double> deconv;        // [n]
   std::vector<std::int32_t> start;   // [T] wrapped index of tap 0
-  std::vector<double> weights;       // [T * 24]
+  std::vector<double> weights;       // [T * taps]
   std::vector<double> phase_re, phase_im;  // e^{-2 pi i nu center} per target
 
-  static DimPlan make(std::int64_t n_modes, const std::vector<double>& freqs);
+  static DimPlan make(std::int64_t n_modes, const std::vector<double>& freqs,
+                      GridKernel kernel = GridKernel::gaussian);
   /// Wrapped grid slot of mode index i: (i - center) mod m.
   std::int64_t wrap(std::int64_t i) const {
     std::int64_t w = (i - center) % m;

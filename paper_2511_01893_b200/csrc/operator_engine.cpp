@@ -34,7 +34,7 @@ Shape3 with_axis(Shape3 s, int axis, std::int64_t e) {
 
 Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_ptr<Encoder> enc,
                std::shared_ptr<MemoClient> memo)
-    : g_(g), cfg_(cfg), s_(s), usfft_(g, s), enc_(std::move(enc)), memo_(std::move(memo)) {
+    : g_(g), cfg_(cfg), s_(s), usfft_(g, s, cfg.kernel), enc_(std::move(enc)), memo_(std::move(memo)) {
   if (cfg_.workers <= 0) throw std::invalid_argument("OperatorEngine: workers must be positive");
   if (cfg_.chunk_extent <= 0) throw std::invalid_argument("OperatorEngine: chunk_extent must be positive");
   if (cfg_.memo_enabled && (!enc_ || !memo_))

@@ -3,13 +3,14 @@
 // Data flow per operator (M = oversampled grid = next_pow2(2n)):
 //   fu1d      one CTA per (volume row i, tile of C columns j): wrapped +
 //             deconvolved placement -> in-smem DIF FFT (bit-reversed output)
-//             -> 24-tap gather read straight from the bit-reversed positions.
-//   fu1d_adj  mirror: conj-phase load -> 24-tap spread in gather form over a
+//             -> W-tap gather read straight from the bit-reversed positions.
+//   fu1d_adj  mirror: conj-phase load -> W-tap spread in gather form over a
 //             host-built cell->target CSR (no atomics) -> DIF FFT(-1) -> read.
 //   fu2d      per batch of 16 detector rows, grid layout [M1][M2][16] (row
 //             batch innermost, 128 B per grid cell): row FFT pass, column FFT
-//             pass (both DIF, indices stay bit-reversed), then a warp-cooperative
-//             576-tap gather per target with weights amortised over the 16 rows.
+//             pass (both DIF, indices stay bit-reversed), then a W x W-tap
+//             gather per target, one warp per target (lane = batch row).
+// W = 12 (es kernel) or 24 (the reference's Gaussian), geometry.hpp.
 //   fu2d_adj  mirror: targets listed per 8x4 cell patch (host CSR) -> each cell
 //             gathers its targets (no atomics) -> column DIF(-1) -> row DIT(-1).
 // FFT butterflies, twiddles, deconvolution and accumulations run in double;
@@ -35,11 +36,11 @@ int pass_cols(std::int64_t m) { return static_cast<int>(std::clamp<std::int64_t>
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
-template <class TIn>
+template <class TIn, int W>
 __global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
-                                              const float* __restrict__ wts, const double2* __restrict__ fac,
+                                              const double* __restrict__ wts, const double2* __restrict__ fac,
                                               const double2* __restrict__ tw) {
   extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
@@ -61,10 +62,10 @@ __global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2*
     const int j = j0 + c;
     if (j >= n2) continue;
     const int st = start[k];
-    const float* wk = wts + k * kTaps;
+    const double* wk = wts + k * W;
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int a = 0; a < kTaps; ++a) {
+    for (int a = 0; a < W; ++a) {
       const double2 g = sd[brev((st + a) & mask, logm) * ncol + c];
       const double wa = __ldg(wk + a);
       acc.x = fma(g.x, wa, acc.x);
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, 
                                                   int n2, int h, int logm, int center, int ncol,
                                                   const double2* __restrict__ cphase,
                                                   const int* __restrict__ cell_ptr, const int* __restrict__ cell_k,
-                                                  const float* __restrict__ cell_w,
+                                                  const double* __restrict__ cell_w,
                                                   const double* __restrict__ pdeconv,
                                                   const double2* __restrict__ tw) {
   extern __shared__ double2 sd[];
@@ -179,145 +180,74 @@ struct GatherOut {
   int reduce;
 };
 
+// ---- gather: one warp per target ---------------------------------------------------------
+// Lane l owns batch row l % 16 and the window columns of parity l / 16, so a
+// half warp reads one 128 B grid cell (16 rows x complex64) per tap: every
+// load is a full coalesced line, no tap is wasted and no lane idles. The
+// window columns' grid offsets and column weights stay in registers for the
+// whole target; per window row the warp reads W/2 cells per half warp, widens
+// them, sums them against the column weights (double) and adds the row
+// weight times that sum, which is the reference's order of summation
+// (inner over columns, outer over rows, nufft.cpp:205-216). Targets are
+// processed in a spatially sorted order, kGatherPerCta per CTA, so the warps
+// of a CTA share their windows' cells in L1.
+constexpr int kGatherWarps = 8;
+constexpr int kGatherPerCta = 64;
 
-// ---- warp-cooperative gather -------------------------------------------------------------
-// Targets are binned by window origin (kBox x kBox cells) and cut into groups
-// of <= 32 (host, once per geometry). One
-// warp owns one group and walks the union of the group's 24x24 windows row by
-// row: the warp stages the row's grid cells (128 B each: 16 detector rows)
-// into shared memory with cp.async, double-buffered one row ahead, then every
-// lane reads the SAME cell (a broadcast) and weights it for its own target
-// (zero outside its window). Per cell a warp issues 8 broadcast loads and 32
-// FMA per lane instead of 32 scattered 128 B loads.
-struct GatherGroup {
-  int first, count, r0, c0, nr, nc;  // sorted-target range, union window origin and extent
-};
-
-constexpr int kGroupWarps = 4;
-constexpr int kWStride = kTaps + 1;  // padded smem weight rows (odd stride: no bank conflicts)
-constexpr int kBox = 12;             // group bounding box (cells) -> union window <= 37 x 37
-constexpr int kUnionMax = kTaps + kBox + 1;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-struct GatherSmem {
-  float4 row[2][kUnionMax][KB / 2];  // two staged union rows (complex64), 128 B per cell
-  double2 rowd[kUnionMax][KB];       // the row being consumed, widened once per warp
-  float w1[32][kWStride];
-  float w2[32][kWStride];
-};
-
-__device__ __forceinline__ void stage_row(GatherSmem& sm, int buf, const float2* __restrict__ G, long long rbase,
-                                          int c0, int c_lo, int c_hi, int mask2, int logm2, int lane) {
-  for (int idx = c_lo * (KB / 2) + lane; idx < c_hi * (KB / 2); idx += 32) {
-    const int cell = idx / (KB / 2), part = idx - cell * (KB / 2);
-    const float2* src = G + (rbase + brev((c0 + cell) & mask2, logm2)) * KB + 2 * part;
-    cp_async16(&sm.row[buf][cell][part], src);
-  }
-  cp_async_commit();
-}
-
-// Columns [c_lo, c_hi) that some lane needs in union row rr (empty: c_lo >= c_hi).
-__device__ __forceinline__ int2 row_span(int rr, int dr, int dc) {
-  const bool on = rr - dr >= 0 && rr - dr < kTaps;
-  return make_int2(__reduce_min_sync(0xffffffffu, on ? dc : 1 << 20),
-                   __reduce_max_sync(0xffffffffu, on ? dc + kTaps : -1));
-}
-
-__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_gather_warp(
-    const float2* __restrict__ G, int ngroups, const GatherGroup* __restrict__ groups, int w, int logm1, int logm2,
-    int nk, const int* __restrict__ g_tidx, const int* __restrict__ g_dr, const int* __restrict__ g_dc,
-    const float* __restrict__ g_w1, const float* __restrict__ g_w2, const double2* __restrict__ g_fac,
-    GatherOut eo, double* __restrict__ partials, int accumulate) {
-  extern __shared__ float4 dyn_smem[];
-  __shared__ double red_scratch[kGroupWarps * 2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  GatherSmem& sm = reinterpret_cast<GatherSmem*>(dyn_smem)[warp];
-  const int gi = blockIdx.x * kGroupWarps + warp;
-  const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1, m2 = 1 << logm2;
+template <int W>
+__global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
+    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_tidx,
+    const int* __restrict__ s_r0, const int* __restrict__ s_c0, const double* __restrict__ s_w1,
+    const double* __restrict__ s_w2, const double2* __restrict__ s_fac, GatherOut eo, double* __restrict__ partials,
+    int accumulate) {
+  constexpr int WH = W / 2;
+  __shared__ double red_scratch[kGatherWarps * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, kk = lane & 15, ph = lane >> 4;
+  const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1;
+  const long long row_stride = static_cast<long long>(KB) << logm2;  // complex64 per grid row
   double red[2] = {0.0, 0.0};
-  if (gi < ngroups) {
-    const GatherGroup gr = groups[gi];
-    const bool live = lane < gr.count;
-    const int st = gr.first + lane;
-    const int dr = live ? g_dr[st] : -1000, dc = live ? g_dc[st] : -1000;
-    int2 span = row_span(0, dr, dc);
-    stage_row(sm, 0, G, static_cast<long long>(brev(gr.r0 & mask1, logm1)) * m2, gr.c0, span.x, span.y, mask2,
-              logm2, lane);
-    for (int a = 0; a < kTaps; ++a) {
-      sm.w1[lane][a] = live ? g_w1[static_cast<long long>(st) * kTaps + a] : 0.f;
-      sm.w2[lane][a] = live ? g_w2[static_cast<long long>(st) * kTaps + a] : 0.f;
+  const int s_end = min(T, static_cast<int>(blockIdx.x + 1) * kGatherPerCta);
+  for (int s = blockIdx.x * kGatherPerCta + warp; s < s_end; s += kGatherWarps) {
+    const int r0 = s_r0[s], c0 = s_c0[s];
+    int coff[WH];
+    double w2r[WH];
+#pragma unroll
+    for (int j = 0; j < WH; ++j) {
+      const int b = 2 * j + ph;
+      coff[j] = brev((c0 + b) & mask2, logm2) * KB + kk;
+      w2r[j] = s_w2[static_cast<long long>(s) * W + b];
     }
-    double2 acc[KB];
+    const double* w1p = s_w1 + static_cast<long long>(s) * W;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 2
+    for (int a = 0; a < W; ++a) {
+      const float2* gr = G + brev((r0 + a) & mask1, logm1) * row_stride;
+      float2 v[WH];
 #pragma unroll
-    for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
-    for (int rr = 0; rr < gr.nr; ++rr) {
-      const int2 cur = span;
-      if (rr + 1 < gr.nr) {
-        span = row_span(rr + 1, dr, dc);
-        stage_row(sm, (rr + 1) & 1, G, static_cast<long long>(brev((gr.r0 + rr + 1) & mask1, logm1)) * m2, gr.c0,
-                  span.x, span.y, mask2, logm2, lane);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      // widen the staged row once per warp (not once per lane)
-      for (int idx = cur.x * (KB / 2) + lane; idx < cur.y * (KB / 2); idx += 32) {
-        const int cell = idx / (KB / 2), part = idx - cell * (KB / 2);
-        const float4 g = sm.row[rr & 1][cell][part];
-        sm.rowd[cell][2 * part] = make_double2(g.x, g.y);
-        sm.rowd[cell][2 * part + 1] = make_double2(g.z, g.w);
-      }
-      __syncwarp();
-      const int a = rr - dr;
-      const bool row_on = a >= 0 && a < kTaps;
-      double2 inner[KB];
+      for (int j = 0; j < WH; ++j) v[j] = __ldg(gr + coff[j]);
+      double2 racc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int kk = 0; kk < KB; ++kk) inner[kk] = make_double2(0.0, 0.0);
-      for (int cc = cur.x; cc < cur.y; ++cc) {
-        const int b = cc - dc;
-        const double wv = (row_on && b >= 0 && b < kTaps) ? static_cast<double>(sm.w2[lane][b]) : 0.0;
-        const double2* gp = sm.rowd[cc];
-#pragma unroll
-        for (int kk = 0; kk < KB; ++kk) {
-          const double2 g = gp[kk];
-          inner[kk].x = fma(wv, g.x, inner[kk].x);
-          inner[kk].y = fma(wv, g.y, inner[kk].y);
-        }
+      for (int j = 0; j < WH; ++j) {
+        racc.x = fma(w2r[j], static_cast<double>(v[j].x), racc.x);
+        racc.y = fma(w2r[j], static_cast<double>(v[j].y), racc.y);
       }
-      const double w1 = row_on ? static_cast<double>(sm.w1[lane][a]) : 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
-        acc[kk].x = fma(w1, inner[kk].x, acc[kk].x);
-        acc[kk].y = fma(w1, inner[kk].y, acc[kk].y);
-      }
-      __syncwarp();  // row buffers are refilled by the next iterations
+      const double wa = w1p[a];
+      acc.x = fma(wa, racc.x, acc.x);
+      acc.y = fma(wa, racc.y, acc.y);
     }
-    if (live) {
-      const int tq = g_tidx[st];
-      const int t = tq / w, q = tq - (tq / w) * w;
-      const double2 f = g_fac[st];
-#pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
-        if (kk >= nk) break;
-        double2 val = cmul(acc[kk], f);
-        if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
-        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
-        if (eo.reduce) {
-          red[0] += val.x * val.x + val.y * val.y;
-          if (eo.dot) {
-            const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
-            red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
-          }
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    if (ph == 0 && kk < nk) {
+      const int tq = s_tidx[s];
+      const int t = tq / w, q = tq - t * w;
+      double2 val = cmul(acc, s_fac[s]);
+      if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
+      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
+      if (eo.reduce) {
+        red[0] += val.x * val.x + val.y * val.y;
+        if (eo.dot) {
+          const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
+          red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
         }
       }
     }
@@ -337,128 +267,159 @@ __global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_gather_warp(
   }
 }
 
-// ---- warp-cooperative spread (adjoint) -----------------------------------------------------
-// One warp owns an 8x4 patch of grid cells (lane = cell) and walks the host-built
-// list of targets whose window touches the patch, 32 targets per chunk: each
-// lane stages one target's window origin, weight rows and 16 values into
-// shared memory with cp.async (double-buffered one chunk ahead), the warp
-// widens the values to double once, then consumes the chunk target by target:
-// the values are a broadcast read and each lane adds its own weight. All sums
-// run in double (cells near nu = 0 receive thousands of terms). Patches are
-// processed heaviest first.
-constexpr int kPatchR = 8, kPatchC = 4;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
-struct SpreadSmem {
-  float4 val[2][32][KB / 2];
-  double2 vald[32][KB];
-  float w1[2][32][kTaps];
-  float w2[2][32][kTaps];
-  int r0[2][32], c0[2][32];
+// ---- warp-cooperative spread (adjoint) -----------------------------------------------------
+// One warp pair owns an 8x4 patch of grid cells (lane = cell), each warp 8 of
+// the 16 batch rows, and walks the host-built list of targets whose window
+// touches the patch, 32 targets per chunk, one chunk ahead: per target the
+// pair stages only the 8 row and 4 column weights this patch needs (zero
+// outside the window) and each warp cp.asyncs its half of the 16 values; the
+// warp widens them to double once, then every lane adds weight x value for its
+// cell. The 2D weight is the double product w1 * w2 as in nufft.cpp:250-256,
+// and all sums run in double (cells near nu = 0 receive thousands of terms).
+// Patches are processed heaviest first.
+constexpr int kPatchR = 8, kPatchC = 4;
+constexpr int KH = KB / 2;
+constexpr int kReduceWarps = 4;
+
+struct SpreadShared {
+  double wr[2][2][32][kPatchR];  // [pair][buf][target][patch row]
+  double wc[2][2][32][kPatchC];  // [pair][buf][target][patch column]
+  float4 vstage[4][2][32][KH / 2];  // per warp, double-buffered half values
+  double2 vald[4][32][KH];          // per warp, widened chunk values
 };
 
-__device__ __forceinline__ void stage_targets(SpreadSmem& sm, int buf, int e, int e1,
-                                              const int* __restrict__ patch_t, const int* __restrict__ r0,
-                                              const int* __restrict__ c0, const float* __restrict__ w1,
-                                              const float* __restrict__ w2, const float2* __restrict__ val,
-                                              int lane) {
-  if (e + lane < e1) {
-    const int t = patch_t[e + lane];
-    sm.r0[buf][lane] = r0[t];
-    sm.c0[buf][lane] = c0[t];
-    const float4* a = reinterpret_cast<const float4*>(w1 + static_cast<long long>(t) * kTaps);
-    const float4* b = reinterpret_cast<const float4*>(w2 + static_cast<long long>(t) * kTaps);
-    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB);
-#pragma unroll
-    for (int q = 0; q < kTaps / 4; ++q) {
-      cp_async16(&sm.w1[buf][lane][4 * q], a + q);
-      cp_async16(&sm.w2[buf][lane][4 * q], b + q);
-    }
-#pragma unroll
-    for (int q = 0; q < KB / 2; ++q) cp_async16(&sm.val[buf][lane][q], v + q);
-  }
-  cp_async_commit();
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;\n" ::"r"(pair + 1));
 }
 
 // A work item is (patch, a sub-range of its target list): lists longer than
-// kSplit (the cells around nu = 0) are split over several warps whose double
-// partials are summed in item order by k_fu2d_adj_spread_reduce.
+// kSplit (the cells around nu = 0) are split over several warp pairs whose
+// double partials are summed in item order by k_fu2d_adj_spread_reduce.
 struct SpreadItem {
   int patch, e0, e1, slot;  // slot < 0: write the grid directly
 };
 constexpr int kSplit = 256;
 
-__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_adj_spread_warp(
-    const float2* __restrict__ val, int logm1, int logm2, int nitems, const SpreadItem* __restrict__ items,
-    const int* __restrict__ patch_t, const int* __restrict__ r0, const int* __restrict__ c0,
-    const float* __restrict__ w1, const float* __restrict__ w2, float2* __restrict__ G,
-    double2* __restrict__ partial) {
+// Stages targets [e, min(e+32, e1)) into buffer `buf`: warp half 0 writes the
+// 8 row weights, half 1 the 4 column weights (both zero outside the window);
+// each warp cp.asyncs its half of the values.
+template <int W>
+__device__ __forceinline__ void stage_spread_chunk(SpreadShared& sh, int pair, int half, int warp, int buf, int e,
+                                                   int e1, int pr0, int pc0, int mask1, int mask2,
+                                                   const int* __restrict__ patch_t, const int* __restrict__ r0,
+                                                   const int* __restrict__ c0, const double* __restrict__ w1,
+                                                   const double* __restrict__ w2, const float2* __restrict__ val,
+                                                   int lane) {
+  if (e + lane < e1) {
+    const int t = patch_t[e + lane];
+    if (half == 0) {
+      const int a0 = pr0 - r0[t];
+      const double* wt = w1 + static_cast<long long>(t) * W;
+#pragma unroll
+      for (int i = 0; i < kPatchR; ++i) {
+        const int a = (a0 + i) & mask1;
+        sh.wr[pair][buf][lane][i] = a < W ? wt[a] : 0.0;
+      }
+    } else {
+      const int b0 = pc0 - c0[t];
+      const double* wt = w2 + static_cast<long long>(t) * W;
+#pragma unroll
+      for (int j = 0; j < kPatchC; ++j) {
+        const int b = (b0 + j) & mask2;
+        sh.wc[pair][buf][lane][j] = b < W ? wt[b] : 0.0;
+      }
+    }
+    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB + half * KH);
+#pragma unroll
+    for (int q = 0; q < KH / 2; ++q) cp_async16(&sh.vstage[warp][buf][lane][q], v + q);
+  }
+  cp_async_commit();
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restrict__ val, int logm1, int logm2,
+                                                         int nitems, const SpreadItem* __restrict__ items,
+                                                         const int* __restrict__ patch_t, const int* __restrict__ r0,
+                                                         const int* __restrict__ c0, const double* __restrict__ w1,
+                                                         const double* __restrict__ w2, float2* __restrict__ G,
+                                                         double2* __restrict__ partial) {
   extern __shared__ float4 dyn_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  SpreadSmem& sm = reinterpret_cast<SpreadSmem*>(dyn_smem)[warp];
-  const int pi = blockIdx.x * kGroupWarps + warp;
-  if (pi >= nitems) return;
+  SpreadShared& sh = *reinterpret_cast<SpreadShared*>(dyn_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, half = warp & 1;
+  const int pi = blockIdx.x * 2 + pair;
+  if (pi >= nitems) return;  // both warps of the pair leave together
   const int m2 = 1 << logm2, mask1 = (1 << logm1) - 1, mask2 = m2 - 1;
   const SpreadItem it = items[pi];
-  const int patch = it.patch;
   const int npc = m2 / kPatchC;
-  const int r = (patch / npc) * kPatchR + lane / kPatchC, c = (patch % npc) * kPatchC + lane % kPatchC;
-  double2 acc[KB];
+  const int pr0 = (it.patch / npc) * kPatchR, pc0 = (it.patch % npc) * kPatchC;
+  const int ri = lane / kPatchC, cj = lane % kPatchC;
+  double2 acc[KH];
 #pragma unroll
-  for (int kk = 0; kk < KB; ++kk) acc[kk] = make_double2(0.0, 0.0);
+  for (int kk = 0; kk < KH; ++kk) acc[kk] = make_double2(0.0, 0.0);
   const int e0 = it.e0, e1 = it.e1;
-  if (e0 < e1) stage_targets(sm, 0, e0, e1, patch_t, r0, c0, w1, w2, val, lane);
+  stage_spread_chunk<W>(sh, pair, half, warp, 0, e0, e1, pr0, pc0, mask1, mask2, patch_t, r0, c0, w1, w2, val, lane);
   for (int e = e0, chunk = 0; e < e1; e += 32, ++chunk) {
     const int buf = chunk & 1;
+    pair_sync(pair);  // weights of this chunk visible; the other buffer is free
     if (e + 32 < e1) {
-      stage_targets(sm, buf ^ 1, e + 32, e1, patch_t, r0, c0, w1, w2, val, lane);
+      stage_spread_chunk<W>(sh, pair, half, warp, buf ^ 1, e + 32, e1, pr0, pc0, mask1, mask2, patch_t, r0, c0, w1,
+                            w2, val, lane);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
     const int n = min(32, e1 - e);
-    for (int idx = lane; idx < n * (KB / 2); idx += 32) {  // widen once per warp
-      const int j = idx / (KB / 2), part = idx - j * (KB / 2);
-      const float4 x = sm.val[buf][j][part];
-      sm.vald[j][2 * part] = make_double2(x.x, x.y);
-      sm.vald[j][2 * part + 1] = make_double2(x.z, x.w);
+    for (int idx = lane; idx < n * (KH / 2); idx += 32) {  // widen once per warp
+      const int j = idx / (KH / 2), part = idx - j * (KH / 2);
+      const float4 x = sh.vstage[warp][buf][j][part];
+      sh.vald[warp][j][2 * part] = make_double2(x.x, x.y);
+      sh.vald[warp][j][2 * part + 1] = make_double2(x.z, x.w);
     }
     __syncwarp();
+#pragma unroll 2
     for (int j = 0; j < n; ++j) {
-      const int a = (r - sm.r0[buf][j]) & mask1, b = (c - sm.c0[buf][j]) & mask2;
-      const double wgt = (a < kTaps && b < kTaps) ? static_cast<double>(sm.w1[buf][j][min(a, kTaps - 1)]) *
-                                                        static_cast<double>(sm.w2[buf][j][min(b, kTaps - 1)])
-                                                  : 0.0;
-      const double2* vp = sm.vald[j];
+      const double wgt = sh.wr[pair][buf][j][ri] * sh.wc[pair][buf][j][cj];
+      const double2* vp = sh.vald[warp][j];
 #pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
+      for (int kk = 0; kk < KH; ++kk) {
         const double2 x = vp[kk];
         acc[kk].x = fma(wgt, x.x, acc[kk].x);
         acc[kk].y = fma(wgt, x.y, acc[kk].y);
       }
     }
-    __syncwarp();  // this buffer is refilled by the prefetch two chunks ahead
   }
+  const int r = pr0 + ri, c = pc0 + cj;
   if (it.slot >= 0) {
-    double2* pp = partial + (static_cast<long long>(it.slot) * 32 + lane) * KB;
+    double2* pp = partial + (static_cast<long long>(it.slot) * 32 + lane) * KB + half * KH;
 #pragma unroll
-    for (int kk = 0; kk < KB; ++kk) pp[kk] = acc[kk];
+    for (int kk = 0; kk < KH; ++kk) pp[kk] = acc[kk];
     return;
   }
-  float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB);
+  float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB + half * KH);
 #pragma unroll
-  for (int q = 0; q < KB / 2; ++q) {
+  for (int q = 0; q < KH / 2; ++q) {
     const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
     gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
   }
 }
 
 // Sums the split patches' partials in item order (deterministic) into the grid.
-__global__ void __launch_bounds__(32 * kGroupWarps) k_fu2d_adj_spread_reduce(
+__global__ void __launch_bounds__(32 * kReduceWarps) k_fu2d_adj_spread_reduce(
     int nsplit, const int4* __restrict__ split, int logm2, const double2* __restrict__ partial,
     float2* __restrict__ G) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int si = blockIdx.x * kGroupWarps + warp;
+  const int si = blockIdx.x * kReduceWarps + warp;
   if (si >= nsplit) return;
   const int4 sp = split[si];  // (patch, first slot, slot count, -)
   const int m2 = 1 << logm2, npc = m2 / kPatchC;
@@ -638,7 +599,6 @@ int ilog2(std::int64_t n) {
   return l;
 }
 
-std::vector<float> to_float(const std::vector<double>& v) { return {v.begin(), v.end()}; }
 
 template <class K>
 void allow_big_smem(K kernel) {
@@ -662,22 +622,20 @@ struct Usfft::Tables {
   DimPlan pz;
   int z_ncol = 0;
   DeviceBuffer<double> z_deconv, z_pdeconv;
-  DeviceBuffer<float> z_w, z_cell_w;
+  DeviceBuffer<double> z_w, z_cell_w;
   DeviceBuffer<int> z_start, z_cell_ptr, z_cell_k;
   DeviceBuffer<double2> z_fac, z_cphase, z_tw;
   // fu2d
   DimPlan px, py;
   DeviceBuffer<double> x_deconv, x_pdeconv, y_deconv;
-  DeviceBuffer<float> t_w1, t_w2;
+  DeviceBuffer<double> t_w1, t_w2;  // [T][W] in target order (spread)
   DeviceBuffer<int> t_r0, t_c0;
   DeviceBuffer<double2> t_fac, t_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint values
-  // warp-cooperative gather: Morton-sorted target groups
-  int ngroups = 0;
-  DeviceBuffer<GatherGroup> groups;
-  DeviceBuffer<int> g_tidx, g_dr, g_dc;
-  DeviceBuffer<float> g_w1, g_w2;
-  DeviceBuffer<double2> g_fac;
+  // gather: targets in spatially sorted order
+  DeviceBuffer<int> s_tidx, s_r0, s_c0;
+  DeviceBuffer<double> s_w1, s_w2;
+  DeviceBuffer<double2> s_fac;
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
   int nitems = 0, nsplit = 0;
   DeviceBuffer<int> patch_t;
@@ -690,11 +648,13 @@ struct Usfft::Tables {
   DeviceBuffer<float2> f2d_tmp;
 };
 
-Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t_(new Tables) {
+Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
+    : g_(g), stream_(stream), kernel_(kernel), t_(new Tables) {
   Tables& t = *t_;
   const FrequencyGrids fg = frequency_grids(g_);
   // ---- fu1d plan (nufft.cpp:109-110) ----
-  t.pz = DimPlan::make(g_.n0, fg.nu_z);
+  t.pz = DimPlan::make(g_.n0, fg.nu_z, kernel_);
+  const int W = t.pz.taps;
   const DimPlan& pz = t.pz;
   t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(4096 / pz.m, 1, 64));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
@@ -703,7 +663,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   for (std::size_t i = 0; i < pdec.size(); ++i) pdec[i] = pz.pref * pz.deconv[i];
   t.z_pdeconv.upload(pdec, stream_);
   t.z_start.upload(std::vector<int>(pz.start.begin(), pz.start.end()), stream_);
-  t.z_w.upload(to_float(pz.weights), stream_);
+  t.z_w.upload(pz.weights, stream_);
   std::vector<double2> fac(static_cast<std::size_t>(g_.h)), cph(static_cast<std::size_t>(g_.h));
   for (std::size_t k = 0; k < fac.size(); ++k) {
     fac[k] = make_double2(pz.pref * pz.phase_re[k], pz.pref * pz.phase_im[k]);
@@ -714,15 +674,15 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   {  // cell -> (target, weight) CSR for the scatter-free adjoint, targets ascending
     std::vector<int> cnt(static_cast<std::size_t>(pz.m + 1), 0);
     for (std::int64_t k = 0; k < g_.h; ++k)
-      for (int a = 0; a < kTaps; ++a) cnt[static_cast<std::size_t>((pz.start[k] + a) % pz.m) + 1]++;
+      for (int a = 0; a < W; ++a) cnt[static_cast<std::size_t>((pz.start[k] + a) % pz.m) + 1]++;
     for (std::size_t l = 1; l < cnt.size(); ++l) cnt[l] += cnt[l - 1];
     std::vector<int> ck(static_cast<std::size_t>(cnt.back())), pos(cnt.begin(), cnt.end() - 1);
-    std::vector<float> cw(ck.size());
+    std::vector<double> cw(ck.size());
     for (std::int64_t k = 0; k < g_.h; ++k)
-      for (int a = 0; a < kTaps; ++a) {
+      for (int a = 0; a < W; ++a) {
         const std::size_t l = static_cast<std::size_t>((pz.start[k] + a) % pz.m);
         ck[static_cast<std::size_t>(pos[l])] = static_cast<int>(k);
-        cw[static_cast<std::size_t>(pos[l]++)] = static_cast<float>(pz.weights[k * kTaps + a]);
+        cw[static_cast<std::size_t>(pos[l]++)] = pz.weights[static_cast<std::size_t>(k * W + a)];
       }
     t.z_cell_ptr.upload(cnt, stream_);
     t.z_cell_k.upload(ck, stream_);
@@ -731,8 +691,9 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   t.z_tw.upload(twiddles(pz.m), stream_);
 
   // ---- fu2d plans (nufft.cpp:185-187) ----
-  t.px = DimPlan::make(g_.n1, fg.nu_x);
-  t.py = DimPlan::make(g_.n2, fg.nu_y);
+  t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
+  t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
+  const std::size_t WS = static_cast<std::size_t>(W);
   const DimPlan &px = t.px, &py = t.py;
   const std::size_t T = fg.nu_x.size();
   t.x_deconv.upload(px.deconv, stream_);
@@ -742,9 +703,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   t.x_pdeconv.upload(pdx, stream_);
   t.t_r0.upload(std::vector<int>(px.start.begin(), px.start.end()), stream_);
   t.t_c0.upload(std::vector<int>(py.start.begin(), py.start.end()), stream_);
-  const std::vector<float> w1f = to_float(px.weights), w2f = to_float(py.weights);
-  t.t_w1.upload(w1f, stream_);
-  t.t_w2.upload(w2f, stream_);
+  t.t_w1.upload(px.weights, stream_);
+  t.t_w2.upload(py.weights, stream_);
   std::vector<double2> tf(T), tcf(T);
   for (std::size_t q = 0; q < T; ++q) {
     const std::complex<double> ph = std::complex<double>(px.phase_re[q], px.phase_im[q]) *
@@ -755,72 +715,53 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   }
   t.t_fac.upload(tf, stream_);
   t.t_cfac.upload(tcf, stream_);
-  {  // gather groups: <= 32 targets from one kBox x kBox bin of window origins
+  {  // gather order: 16 x 16 bins of the window origin, row-major inside a bin
     std::vector<int> order(T);
     for (std::size_t q = 0; q < T; ++q) order[q] = static_cast<int>(q);
-    // fixed kBox x kBox bins of the window origin (2.6M vs 3.3M union cells per
-    // 256^3 launch compared with Morton runs), row-major inside a bin
     std::vector<std::uint64_t> key(T);
     for (std::size_t q = 0; q < T; ++q) {
       const std::uint64_t r = static_cast<std::uint64_t>(px.start[q]), c = static_cast<std::uint64_t>(py.start[q]);
-      key[q] = ((r / kBox) << 48) | ((c / kBox) << 32) | (r << 16) | c;
+      key[q] = ((r / 16) << 48) | ((c / 16) << 32) | (r << 16) | c;
     }
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
-    std::vector<GatherGroup> grp;
-    std::vector<int> tidx(T), dr(T), dc(T);
-    std::vector<float> gw1(T * kTaps), gw2(T * kTaps);
-    std::vector<double2> gfac(T);
-    std::size_t i = 0;
-    while (i < T) {
-      const std::size_t first = i;
-      int rmin = px.start[static_cast<std::size_t>(order[i])], rmax = rmin;
-      int cmin = py.start[static_cast<std::size_t>(order[i])], cmax = cmin;
-      ++i;
-      while (i < T && i - first < 32) {
-        const int r = px.start[static_cast<std::size_t>(order[i])], c = py.start[static_cast<std::size_t>(order[i])];
-        if ((key[static_cast<std::size_t>(order[i])] >> 32) != (key[static_cast<std::size_t>(order[first])] >> 32)) break;
-        if (std::max(rmax, r) - std::min(rmin, r) > kBox || std::max(cmax, c) - std::min(cmin, c) > kBox) break;
-        rmin = std::min(rmin, r), rmax = std::max(rmax, r), cmin = std::min(cmin, c), cmax = std::max(cmax, c);
-        ++i;
-      }
-      grp.push_back(GatherGroup{static_cast<int>(first), static_cast<int>(i - first), rmin, cmin,
-                                rmax - rmin + kTaps, cmax - cmin + kTaps});
-      for (std::size_t s = first; s < i; ++s) {
-        const std::size_t q = static_cast<std::size_t>(order[s]);
-        tidx[s] = static_cast<int>(q);
-        dr[s] = px.start[q] - rmin;
-        dc[s] = py.start[q] - cmin;
-        std::copy_n(w1f.begin() + static_cast<std::ptrdiff_t>(q * kTaps), kTaps,
-                    gw1.begin() + static_cast<std::ptrdiff_t>(s * kTaps));
-        std::copy_n(w2f.begin() + static_cast<std::ptrdiff_t>(q * kTaps), kTaps,
-                    gw2.begin() + static_cast<std::ptrdiff_t>(s * kTaps));
-        gfac[s] = tf[q];
-      }
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
+    std::vector<int> tidx(T), r0(T), c0(T);
+    std::vector<double> sw1(T * WS), sw2(T * WS);
+    std::vector<double2> sfac(T);
+    for (std::size_t s = 0; s < T; ++s) {
+      const std::size_t q = static_cast<std::size_t>(order[s]);
+      tidx[s] = static_cast<int>(q);
+      r0[s] = px.start[q];
+      c0[s] = py.start[q];
+      std::copy_n(px.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
+                  sw1.begin() + static_cast<std::ptrdiff_t>(s * WS));
+      std::copy_n(py.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
+                  sw2.begin() + static_cast<std::ptrdiff_t>(s * WS));
+      sfac[s] = tf[q];
     }
-    t.ngroups = static_cast<int>(grp.size());
-    t.groups.upload(grp, stream_);
-    t.g_tidx.upload(tidx, stream_);
-    t.g_dr.upload(dr, stream_);
-    t.g_dc.upload(dc, stream_);
-    t.g_w1.upload(gw1, stream_);
-    t.g_w2.upload(gw2, stream_);
-    t.g_fac.upload(gfac, stream_);
+    t.s_tidx.upload(tidx, stream_);
+    t.s_r0.upload(r0, stream_);
+    t.s_c0.upload(c0, stream_);
+    t.s_w1.upload(sw1, stream_);
+    t.s_w2.upload(sw2, stream_);
+    t.s_fac.upload(sfac, stream_);
   }
-  {  // spread patches: 8x4 cells -> targets whose 24x24 window touches them (targets ascending)
+  {  // spread patches: 8x4 cells -> targets whose W x W window touches them (targets ascending)
     const std::int64_t npr = px.m / kPatchR, npc = py.m / kPatchC;
     const int npatch = static_cast<int>(npr * npc);
-    auto cover = [&](std::int32_t st, std::int64_t m, int edge, int* out) {
-      int n = 0;
-      for (int a = 0; a < kTaps; ++a) {
-        const int p = static_cast<int>(((st + a) % m) / edge);
-        bool seen = false;
-        for (int e = 0; e < n; ++e) seen |= out[e] == p;
-        if (!seen) out[n++] = p;
+    // patches touched by a target's W x W window (dedup within the target)
+    std::vector<int> touched;
+    auto patches_of = [&](std::size_t q) {
+      touched.clear();
+      for (int a = 0; a < W; ++a) {
+        const std::int64_t pr = ((px.start[q] + a) % px.m) / kPatchR;
+        for (int b = 0; b < W; ++b) {
+          const int p = static_cast<int>(pr * npc + ((py.start[q] + b) % py.m) / kPatchC);
+          if (std::find(touched.begin(), touched.end(), p) == touched.end()) touched.push_back(p);
+        }
       }
-      return n;
     };
     std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0), lst;
-    int pr[kTaps], pc[kTaps];
     for (int pass = 0; pass < 2; ++pass) {
       std::vector<int> pos;
       if (pass == 1) {
@@ -829,13 +770,11 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
         lst.resize(static_cast<std::size_t>(cnt.back()));
       }
       for (std::size_t q = 0; q < T; ++q) {
-        const int nr = cover(px.start[q], px.m, kPatchR, pr), nc = cover(py.start[q], py.m, kPatchC, pc);
-        for (int a = 0; a < nr; ++a)
-          for (int b = 0; b < nc; ++b) {
-            const std::size_t p = static_cast<std::size_t>(pr[a] * npc + pc[b]);
-            if (pass == 0) cnt[p + 1]++;
-            else lst[static_cast<std::size_t>(pos[p]++)] = static_cast<int>(q);
-          }
+        patches_of(q);
+        for (const int p : touched) {
+          if (pass == 0) cnt[static_cast<std::size_t>(p) + 1]++;
+          else lst[static_cast<std::size_t>(pos[static_cast<std::size_t>(p)]++)] = static_cast<int>(q);
+        }
       }
     }
     std::vector<int> porder(static_cast<std::size_t>(npatch));
@@ -895,13 +834,15 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream) : g_(g), stream_(stream), t
   }
   MLRG_CUDA(cudaStreamSynchronize(stream_));
   static bool smem_set = [] {
-    allow_big_smem(k_fu1d<float2>);
-    allow_big_smem(k_fu1d<double2>);
+    allow_big_smem(k_fu1d<float2, kEsTaps>);
+    allow_big_smem(k_fu1d<double2, kEsTaps>);
+    allow_big_smem(k_fu1d<float2, kTaps>);
+    allow_big_smem(k_fu1d<double2, kTaps>);
     allow_big_smem(k_fu1d_adj<float2>);
     allow_big_smem(k_fu1d_adj<double2>);
     allow_big_smem(k_fu2d_rows);
-    allow_big_smem(k_fu2d_gather_warp);
-    allow_big_smem(k_fu2d_adj_spread_warp);
+    allow_big_smem(k_fu2d_adj_spread<kEsTaps>);
+    allow_big_smem(k_fu2d_adj_spread<kTaps>);
     allow_big_smem(k_fu2d_cols);
     allow_big_smem(k_fu2d_adj_cols);
     allow_big_smem(k_fu2d_adj_rows);
@@ -926,10 +867,10 @@ void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0) {
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
   const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(double2);
   prof::begin("k_fu1d", stream_);
-  k_fu1d<TIn><<<grid, 256, smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
-                                            static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
-                                            t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(),
-                                            t.z_tw.get());
+  auto kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps> : k_fu1d<TIn, kTaps>;
+  kern<<<grid, 256, smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
+                                     static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
+                                     t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get());
   MLRG_LAUNCH_CHECK("k_fu1d");
   prof::end("k_fu1d", stream_);
 }
@@ -959,7 +900,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int ggrid = (t.ngroups + kGroupWarps - 1) / kGroupWarps;
+  const int ggrid = static_cast<int>((T + kGatherPerCta - 1) / kGatherPerCta);
+  auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
     prof::begin("k_fu2d_rows", stream_);
@@ -979,9 +921,10 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
     prof::begin("k_fu2d_gather", stream_);
-    k_fu2d_gather_warp<<<ggrid, 32 * kGroupWarps, kGroupWarps * sizeof(GatherSmem), stream_>>>(
-        t.Gd.get(), t.ngroups, t.groups.get(), static_cast<int>(g_.w), t.px.logm, t.py.logm, nb, t.g_tidx.get(),
-        t.g_dr.get(), t.g_dc.get(), t.g_w1.get(), t.g_w2.get(), t.g_fac.get(), eo, partials_.dev(), b > 0 ? 1 : 0);
+    gather<<<ggrid, 32 * kGatherWarps, 0, stream_>>>(t.Gd.get(), static_cast<int>(T), static_cast<int>(g_.w),
+                                                     t.px.logm, t.py.logm, nb, t.s_tidx.get(), t.s_r0.get(),
+                                                     t.s_c0.get(), t.s_w1.get(), t.s_w2.get(), t.s_fac.get(), eo,
+                                                     partials_.dev(), b > 0 ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", stream_);
   }
@@ -1001,13 +944,13 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
     prof::end("k_fu2d_adj_prep", stream_);
     prof::begin("k_fu2d_adj_spread", stream_);
-    k_fu2d_adj_spread_warp<<<(t.nitems + kGroupWarps - 1) / kGroupWarps, 32 * kGroupWarps,
-                             kGroupWarps * sizeof(SpreadSmem), stream_>>>(
+    auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
+    spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), stream_>>>(
         t.val.get(), t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
         t.t_w1.get(), t.t_w2.get(), t.Gd.get(), t.partial.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     if (t.nsplit > 0) {
-      k_fu2d_adj_spread_reduce<<<(t.nsplit + kGroupWarps - 1) / kGroupWarps, 32 * kGroupWarps, 0, stream_>>>(
+      k_fu2d_adj_spread_reduce<<<(t.nsplit + kReduceWarps - 1) / kReduceWarps, 32 * kReduceWarps, 0, stream_>>>(
           t.nsplit, t.split.get(), t.py.logm, t.partial.get(), t.Gd.get());
       MLRG_LAUNCH_CHECK("k_fu2d_adj_spread_reduce");
     }

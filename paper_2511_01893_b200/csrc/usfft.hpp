@@ -3,7 +3,8 @@
 // row), and the centred unitary 2D DFT f2d / f2d_adj. All arrays are device
 // complex64 (float2) in the reference's row-major layouts (array.hpp:38-73).
 //
-// Reference operators replaced (numerically, to fp32 rounding):
+// Reference operators replaced (numerically, to fp32 rounding; the spreading
+// kernel is selectable, geometry.hpp):
 //   nufft::fu1d_gridding      nufft.cpp:107-134
 //   nufft::fu1d_adj_gridding  nufft.cpp:136-162
 //   nufft::fu2d_gridding      nufft.cpp:183-225  (+ fused_sub_fu2d, operators.cpp:285-299)
@@ -37,12 +38,13 @@ class Usfft {
  public:
   static constexpr int kRowBatch = 16;  // detector rows per fu2d grid batch
 
-  Usfft(const Geometry& g, cudaStream_t stream);
+  Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel = GridKernel::es);
   ~Usfft();
   Usfft(const Usfft&) = delete;
   Usfft& operator=(const Usfft&) = delete;
 
   const Geometry& geometry() const { return g_; }
+  GridKernel kernel() const { return kernel_; }
   cudaStream_t stream() const { return stream_; }
 
   /// u: contiguous (d0, n0, n2) -> out (d0, h, n2). The volume side may be
@@ -76,6 +78,7 @@ class Usfft {
   struct Tables;
   Geometry g_;
   cudaStream_t stream_;
+  GridKernel kernel_;
   Tables* t_;
   Partials partials_;
 };

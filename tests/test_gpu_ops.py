@@ -9,7 +9,8 @@ import mlr_oracle as O
 from conftest import golden, golden_geometry, rel
 
 pytestmark = pytest.mark.gpu
-TOL = 2e-5  # relative L2, fp32 FFT + 576-tap accumulation
+TOL = 2e-5  # relative L2: complex64 storage of the grids and outputs
+KERNELS = ["es", "gaussian"]  # geometry.hpp: both evaluate the reference's NUDFT
 
 
 def dev(torch, a):
@@ -20,12 +21,13 @@ def host(t):
     return t.cpu().numpy().astype(np.complex128)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("case", ["ops_c16", "ops_ragged", "ops_c32"])
-def test_usfft_ops_match_reference(mlrg, torch_cuda, case):
+def test_usfft_ops_match_reference(mlrg, torch_cuda, case, kernel):
     torch = torch_cuda
     z = golden(case)
     n1, n0, n2, nt, h, w = golden_geometry(z)
-    ctx = mlrg.Context(n1, n0, n2, nt, h, w)
+    ctx = mlrg.Context(n1, n0, n2, nt, h, w, kernel=kernel)
     u, mid, pf, dh = (dev(torch, z[k]) for k in ("in_u", "in_mid", "in_projf", "in_dhat"))
     e = lambda *s: torch.empty(s, dtype=torch.complex64, device="cuda")
     out = ctx.fu1d(u, e(n1, h, n2))
@@ -45,12 +47,13 @@ def test_usfft_ops_match_reference(mlrg, torch_cuda, case):
     assert rel(host(out), z["fu2d_adj_grid"]) < TOL
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("case", ["ops_c16", "ops_ragged", "ops_c32"])
-def test_f2d_forward_adjoint_L_match_reference(mlrg, torch_cuda, case):
+def test_f2d_forward_adjoint_L_match_reference(mlrg, torch_cuda, case, kernel):
     torch = torch_cuda
     z = golden(case)
     n1, n0, n2, nt, h, w = golden_geometry(z)
-    ctx = mlrg.Context(n1, n0, n2, nt, h, w)
+    ctx = mlrg.Context(n1, n0, n2, nt, h, w, kernel=kernel)
     e = lambda *s: torch.empty(s, dtype=torch.complex64, device="cuda")
     ps, pf, u = dev(torch, z["in_projs"]), dev(torch, z["in_projf"]), dev(torch, z["in_u"])
     o = ctx.f2d(ps, e(nt, h, w))
@@ -83,12 +86,12 @@ def test_grad_div_match_reference(mlrg, torch_cuda):
     assert rel(host(out), z["div"]) < 1e-6
 
 
-@pytest.mark.parametrize("n,nt", [(64, 48), (128, 128)])
-def test_ops_vs_restatement_and_adjointness(mlrg, torch_cuda, n, nt):
+@pytest.mark.parametrize("n,nt,kernel", [(64, 48, "es"), (128, 128, "es"), (64, 48, "gaussian")])
+def test_ops_vs_restatement_and_adjointness(mlrg, torch_cuda, n, nt, kernel):
     torch = torch_cuda
     rng = np.random.default_rng(n)
     g = O.Geometry(n, n, n, nt, n, n)
-    ctx = mlrg.Context(n, n, n, nt, n, n)
+    ctx = mlrg.Context(n, n, n, nt, n, n, kernel=kernel)
     cplx = lambda *s: (rng.standard_normal(s) + 1j * rng.standard_normal(s))
     u, v, p = cplx(n, n, n), cplx(n, n, n), cplx(nt, n, n)
     e = lambda *s: torch.empty(s, dtype=torch.complex64, device="cuda")

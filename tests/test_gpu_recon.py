@@ -15,15 +15,19 @@ def ref_rows(z):
     return [[float(v) for v in l.split(",")] for l in lines[1:]]
 
 
-def config_text(n, nt, n_outer, memo):
+def config_text(n, nt, n_outer, memo, kernel="es"):
     return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
-            f"memoization={memo}\nnudft_path=gridding\n")
+            f"memoization={memo}\nnudft_path=gridding\ngridding_kernel={kernel}\n")
 
 
-@pytest.mark.parametrize("case,memo", [("recon_c16_memo_grid", "local"), ("recon_c32_memo_grid", "local"),
-                                       ("recon_c32_off_grid", "off"), ("recon_c64_off_grid", "off"),
-                                       ("recon_cfg1_memo_direct", "local")])
-def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo):
+@pytest.mark.parametrize("case,memo,kernel", [("recon_c16_memo_grid", "local", "es"),
+                                              ("recon_c32_memo_grid", "local", "es"),
+                                              ("recon_c32_off_grid", "off", "es"),
+                                              ("recon_c64_off_grid", "off", "es"),
+                                              ("recon_cfg1_memo_direct", "local", "es"),
+                                              ("recon_c32_memo_grid", "local", "gaussian"),
+                                              ("recon_c64_off_grid", "off", "gaussian")])
+def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo, kernel):
     torch = torch_cuda
     z = golden(case)
     n = z["phantom"].shape[0]
@@ -31,7 +35,7 @@ def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo):
     d = torch.from_numpy(z["data"]).cuda()
     ref = torch.from_numpy(z["phantom"]).cuda()
     u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
-    r = mlrg.reconstruct_device(config_text(n, nt, 10, memo), d, u, reference=ref)
+    r = mlrg.reconstruct_device(config_text(n, nt, 10, memo, kernel), d, u, reference=ref)
     aborted = bool(int(str(z["txt_aborted_txt"]).split()[0]))
     assert r.aborted == aborted
     if memo != "off":
