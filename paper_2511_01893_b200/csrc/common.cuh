@@ -1,6 +1,5 @@
 // Shared device helpers for the sm_100a kernels: complex arithmetic on
-// float2/double2, bit reversal for the in-place FFTs, block reductions and the
-// shared-memory FFT cores.
+// float2/double2, block reductions and the shared-memory Stockham FFT.
 //
 // Precision: the transforms store their big intermediates (oversampled
 // grids) in complex64 but compute every FFT butterfly, twiddle and long
@@ -49,11 +48,6 @@ __device__ __forceinline__ double2 to_d(float2 a) { return make_double2(a.x, a.y
 __device__ __forceinline__ double2 to_d(double2 a) { return a; }
 __device__ __forceinline__ float2 to_f(double2 a) { return make_float2(static_cast<float>(a.x), static_cast<float>(a.y)); }
 
-// Position of frequency k inside a length-2^logm DIF output (bit-reversed order).
-__device__ __forceinline__ int brev(int k, int logm) {
-  return static_cast<int>(__brev(static_cast<unsigned>(k)) >> (32 - logm));
-}
-
 // Sum of NV doubles across the block; result valid in thread 0. `scratch`
 // needs blockDim.x/32 * NV doubles of shared memory.
 template <int NV>
@@ -78,99 +72,105 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
   __syncthreads();
 }
 
-// In-place radix-4/radix-2 decimation-in-frequency FFT over shared memory.
-// Element (m, c) of the batch lives at s[m * sm + c]; the natural-order input
-// is replaced by its unnormalised transform X[k] = sum_m x[m] e^{SIGN 2 pi i mk/M}
-// stored at position brev(k). `tw` holds e^{+2 pi i k/M} for k < M/2.
-// Lanes run along c first, so rows stay contiguous across a warp.
-template <int SIGN, class T>
-__device__ void fft_dif(T* s, int logm, int ncols, int sm, const T* __restrict__ tw) {
-  const int m = 1 << logm;
-  int span = m;  // current sub-transform size
-  while (span >= 4) {
-    const int l = span >> 2;
-    const int tws1 = m / span;         // w_{4L}^j -> tw[j * m/(4L)]
-    const int tws2 = (m << 1) / span;  // w_{2L}^j -> tw[j * m/(2L)]
-    const int nbf = (m >> 2) * ncols;
-    for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
-      const int c = idx % ncols, bf = idx / ncols;
-      const int j = bf % l, base = (bf / l) * span + j;
-      T* p = s + base * sm + c;
-      const T a0 = p[0], a1 = p[l * sm], a2 = p[2 * l * sm], a3 = p[3 * l * sm];
-      T w4 = tw[j * tws1];
-      T w2 = tw[j * tws2];
-      if (SIGN < 0) {
-        w4.y = -w4.y;
-        w2.y = -w2.y;
-      }
-      const T y0 = cadd(a0, a2), y1 = cadd(a1, a3);
-      const T y2 = cmul(csub(a0, a2), w4);
-      const T y3 = cmul(cmul_i<SIGN>(csub(a1, a3)), w4);  // w_{4L}^{j+L} = w_{4L}^j * (SIGN i)
-      p[0] = cadd(y0, y1);
-      p[l * sm] = cmul(csub(y0, y1), w2);
-      p[2 * l * sm] = cadd(y2, y3);
-      p[3 * l * sm] = cmul(csub(y2, y3), w2);
-    }
-    __syncthreads();
-    span = l;
-  }
-  if (span == 2) {
-    const int nbf = (m >> 1) * ncols;
-    for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
-      const int c = idx % ncols, bf = idx / ncols;
-      T* p = s + (bf * 2) * sm + c;
-      const T a0 = p[0], a1 = p[sm];
-      p[0] = cadd(a0, a1);
-      p[sm] = csub(a0, a1);
-    }
-    __syncthreads();
+// ---- batched Stockham FFT over a shared-memory tile ------------------------------------
+// The tile holds nb independent columns of length m = 2^logm: element (row,
+// b) at s[row * ld + b]. The transform is in place and self-sorting (natural
+// order in and out): X[k] = sum_j x[j] e^{SIGN 2 pi i jk/m}. It runs one
+// radix-2 or radix-4 pass (logm % 3 != 0) followed by radix-8 passes, each
+// thread owning 8 elements per pass in registers, so a 512-point column
+// costs three passes and six block barriers. The block must have exactly
+// nb * m / 8 threads (m >= 8); thread t works on column b = t % nb and
+// butterfly group g = t / nb. `tw` holds e^{+2 pi i k/m} for k < m.
+template <int SIGN>
+__device__ __forceinline__ void fft4_reg(double2& a0, double2& a1, double2& a2, double2& a3) {
+  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3);
+  const double2 d13 = cmul_i<SIGN>(csub(a1, a3));
+  a0 = cadd(s02, s13);
+  a1 = cadd(d02, d13);
+  a2 = csub(s02, s13);
+  a3 = csub(d02, d13);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void fft8_reg(double2* v) {
+  fft4_reg<SIGN>(v[0], v[2], v[4], v[6]);  // E[k] at v[2k]
+  fft4_reg<SIGN>(v[1], v[3], v[5], v[7]);  // O[k] at v[2k+1]
+  constexpr double c = 0.70710678118654752440;
+  const double2 o1 = v[3], o3 = v[7];
+  // w8 = c (1 + SIGN i), w8^2 = SIGN i, w8^3 = c (-1 + SIGN i)
+  const double2 t1 = make_double2(c * (o1.x - SIGN * o1.y), c * (o1.y + SIGN * o1.x));
+  const double2 t2 = cmul_i<SIGN>(v[5]);
+  const double2 t3 = make_double2(c * (-o3.x - SIGN * o3.y), c * (-o3.y + SIGN * o3.x));
+  const double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], o0 = v[1];
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, t1);
+  v[5] = csub(e1, t1);
+  v[2] = cadd(e2, t2);
+  v[6] = csub(e2, t2);
+  v[3] = cadd(e3, t3);
+  v[7] = csub(e3, t3);
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void fft_reg(double2* v) {
+  if constexpr (R == 8) {
+    fft8_reg<SIGN>(v);
+  } else if constexpr (R == 4) {
+    fft4_reg<SIGN>(v[0], v[1], v[2], v[3]);
+  } else {
+    const double2 a = v[0];
+    v[0] = cadd(a, v[1]);
+    v[1] = csub(a, v[1]);
   }
 }
 
-// In-place radix-2/radix-4 decimation-in-time FFT over shared memory: the
-// input sits at bit-reversed positions (x[m] at brev(m)), the output X[k] is
-// left in natural order. Same layout and twiddle table as fft_dif.
-template <int SIGN, class T>
-__device__ void fft_dit(T* s, int logm, int ncols, int sm, const T* __restrict__ tw) {
-  const int m = 1 << logm;
-  int l = 1;  // size of the sub-transforms being combined
-  if (logm & 1) {
-    const int nbf = (m >> 1) * ncols;
-    for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
-      const int c = idx % ncols, bf = idx / ncols;
-      T* p = s + (bf * 2) * sm + c;
-      const T a0 = p[0], a1 = p[sm];
-      p[0] = cadd(a0, a1);
-      p[sm] = csub(a0, a1);
-    }
-    __syncthreads();
-    l = 2;
+template <int R, int LOGR, int SIGN>
+__device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, int logm, int logns,
+                                              const double2* __restrict__ tw) {
+  constexpr int PER = 8 / R;
+  const int m8 = 1 << (logm - 3), stride = 1 << (logm - LOGR), ns = 1 << logns;
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int gg = g + q * m8;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q * R + r] = s[(gg + r * stride) * ld + b];
   }
-  for (; l < m; l <<= 2) {
-    const int span = l << 2;
-    const int tws2 = (m << 1) / span;  // w_{2L}^j
-    const int tws4 = m / span;         // w_{4L}^j
-    const int nbf = (m >> 2) * ncols;
-    for (int idx = threadIdx.x; idx < nbf; idx += blockDim.x) {
-      const int c = idx % ncols, bf = idx / ncols;
-      const int j = bf % l, base = (bf / l) * span + j;
-      T* p = s + base * sm + c;
-      T t = tw[j * tws2];
-      T u = tw[j * tws4];
-      if (SIGN < 0) {
-        t.y = -t.y;
-        u.y = -u.y;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int gg = g + q * m8;
+    const int k = gg & (ns - 1);
+    if (logns > 0) {
+      const int step = k << (logm - logns - LOGR);  // k m / (ns R)
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 w = tw[step * r];
+        if (SIGN < 0) w.y = -w.y;
+        v[q * R + r] = cmul(v[q * R + r], w);
       }
-      const T a0 = p[0], a1 = cmul(p[l * sm], t), a2 = p[2 * l * sm], a3 = cmul(p[3 * l * sm], t);
-      const T y0 = cadd(a0, a1), y1 = csub(a0, a1), y2 = cadd(a2, a3), y3 = csub(a2, a3);
-      const T uy2 = cmul(y2, u), uy3 = cmul_i<SIGN>(cmul(y3, u));
-      p[0] = cadd(y0, uy2);
-      p[2 * l * sm] = csub(y0, uy2);
-      p[l * sm] = cadd(y1, uy3);
-      p[3 * l * sm] = csub(y1, uy3);
     }
-    __syncthreads();
+    fft_reg<R, SIGN>(v + q * R);
+    const int base = ((gg >> logns) << (logns + LOGR)) + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[(base + (r << logns)) * ld + b] = v[q * R + r];
   }
+  __syncthreads();
+}
+
+template <int SIGN>
+__device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw) {
+  const int b = threadIdx.x % nb, g = threadIdx.x / nb;
+  int logns = 0;
+  if (logm % 3 == 1) {
+    stockham_pass<2, 1, SIGN>(s, ld, b, g, logm, 0, tw);
+    logns = 1;
+  } else if (logm % 3 == 2) {
+    stockham_pass<4, 2, SIGN>(s, ld, b, g, logm, 0, tw);
+    logns = 2;
+  }
+  for (; logns < logm; logns += 3) stockham_pass<8, 3, SIGN>(s, ld, b, g, logm, logns, tw);
 }
 
 }  // namespace mlrg

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <numbers>
 #include <vector>
 
@@ -30,14 +31,30 @@ namespace {
 
 constexpr int KB = Usfft::kRowBatch;
 
-// k-columns per CTA of a 2D-grid FFT pass over length m (double smem <= ~140 KB).
-int pass_cols(std::int64_t m) { return static_cast<int>(std::clamp<std::int64_t>(8192 / m, 2, KB)); }
+// Complex elements per CTA of the shared-memory FFT passes (double: 16 B each).
+// 2048 (32 KB) lets ~6 CTAs share an SM so one CTA's loads overlap another's
+// butterflies; MLRG_FFT_ELEMS overrides it for tuning.
+std::int64_t fft_elems() {
+  static const std::int64_t e = [] {
+    const char* v = std::getenv("MLRG_FFT_ELEMS");
+    std::int64_t n = v ? std::max<std::int64_t>(std::atoll(v), 64) : std::int64_t{2048};
+    while (n & (n - 1)) n &= n - 1;
+    return n;
+  }();
+  return e;
+}
+// k-columns per CTA of a 2D-grid FFT pass over length m.
+int pass_cols(std::int64_t m) {
+  int c = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / m, 2, KB));
+  while (c & (c - 1)) c &= c - 1;  // a power of two dividing KB
+  return c;
+}
 
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
 template <class TIn, int W>
-__global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
+__global__ void __launch_bounds__(512) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
                                               const double* __restrict__ wts, const double2* __restrict__ fac,
@@ -55,7 +72,7 @@ __global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2*
     sd[idx] = v;
   }
   __syncthreads();
-  fft_dif<+1>(sd, logm, ncol, ncol, tw);
+  fft_stockham<+1>(sd, logm, ncol, ncol, tw);
   float2* oi = out + static_cast<long long>(blockIdx.y) * h * n2;
   for (int idx = threadIdx.x; idx < h * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
@@ -66,7 +83,7 @@ __global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2*
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
     for (int a = 0; a < W; ++a) {
-      const double2 g = sd[brev((st + a) & mask, logm) * ncol + c];
+      const double2 g = sd[((st + a) & mask) * ncol + c];
       const double wa = __ldg(wk + a);
       acc.x = fma(g.x, wa, acc.x);
       acc.y = fma(g.y, wa, acc.y);
@@ -76,7 +93,7 @@ __global__ void __launch_bounds__(256) k_fu1d(const TIn* __restrict__ u, float2*
 }
 
 template <class TOut>
-__global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, TOut* __restrict__ out, int n0,
+__global__ void __launch_bounds__(512) k_fu1d_adj(const float2* __restrict__ v, TOut* __restrict__ out, int n0,
                                                   int n2, int h, int logm, int center, int ncol,
                                                   const double2* __restrict__ cphase,
                                                   const int* __restrict__ cell_ptr, const int* __restrict__ cell_k,
@@ -107,14 +124,14 @@ __global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, 
     sd[idx] = acc;
   }
   __syncthreads();
-  fft_dif<-1>(sd, logm, ncol, ncol, tw);
+  fft_stockham<-1>(sd, logm, ncol, ncol, tw);
   TOut* oi = out + static_cast<long long>(blockIdx.y) * n0 * n2;
   for (int idx = threadIdx.x; idx < n0 * ncol; idx += blockDim.x) {
     const int mode = idx / ncol, c = idx - mode * ncol;
     const int j = j0 + c;
     if (j >= n2) continue;
     const int slot = (mode - center) & mask;
-    const double2 r = cscale(sd[brev(slot, logm) * ncol + c], pdeconv[mode]);
+    const double2 r = cscale(sd[slot * ncol + c], pdeconv[mode]);
     TOut& o = oi[static_cast<long long>(mode) * n2 + j];
     o.x = static_cast<decltype(o.x)>(r.x);
     o.y = static_cast<decltype(o.y)>(r.y);
@@ -125,12 +142,12 @@ __global__ void __launch_bounds__(256) k_fu1d_adj(const float2* __restrict__ v, 
 // fu2d forward: row pass, column pass, gather
 // ------------------------------------------------------------------------------------------
 // S[i][c'][KB]: row FFT of v[i, k0+kk, :] * dx[i] * dy[:] placed at wrapped slots.
-__global__ void __launch_bounds__(256) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
+__global__ void __launch_bounds__(512) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
                                                    const double2* __restrict__ tw2, float2* __restrict__ S) {
   extern __shared__ double2 sd[];
-  const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
+  const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
   const double di = dx[i];
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
@@ -142,7 +159,7 @@ __global__ void __launch_bounds__(256) k_fu2d_rows(const float2* __restrict__ v,
     sd[r * sm + kk] = val;
   }
   __syncthreads();
-  fft_dif<+1>(sd, logm2, ks_n, sm, tw2);
+  fft_stockham<+1>(sd, logm2, ks_n, sm, tw2);
   float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
@@ -151,7 +168,7 @@ __global__ void __launch_bounds__(256) k_fu2d_rows(const float2* __restrict__ v,
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
-__global__ void __launch_bounds__(256) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(512) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
                                                    float2* __restrict__ G) {
   extern __shared__ double2 sd[];
@@ -163,7 +180,7 @@ __global__ void __launch_bounds__(256) k_fu2d_cols(const float2* __restrict__ S,
     sd[idx] = i < n1 ? to_d(S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk]) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_dif<+1>(sd, logm1, ks_n, ks_n, tw1);
+  fft_stockham<+1>(sd, logm1, ks_n, ks_n, tw1);
   for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
     const int r = idx / ks_n, kk = idx - r * ks_n;
     G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(sd[idx]);
@@ -214,17 +231,29 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
 #pragma unroll
     for (int j = 0; j < WH; ++j) {
       const int b = 2 * j + ph;
-      coff[j] = brev((c0 + b) & mask2, logm2) * KB + kk;
+      coff[j] = ((c0 + b) & mask2) * KB + kk;
       w2r[j] = s_w2[static_cast<long long>(s) * W + b];
     }
     const double* w1p = s_w1 + static_cast<long long>(s) * W;
     double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 2
+    // rows are software-pipelined one ahead: the next row's W/2 loads are in
+    // flight while the current row is summed
+    float2 nxt[WH];
+    {
+      const float2* gr = G + (r0 & mask1) * row_stride;
+#pragma unroll
+      for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
+    }
+#pragma unroll
     for (int a = 0; a < W; ++a) {
-      const float2* gr = G + brev((r0 + a) & mask1, logm1) * row_stride;
       float2 v[WH];
 #pragma unroll
-      for (int j = 0; j < WH; ++j) v[j] = __ldg(gr + coff[j]);
+      for (int j = 0; j < WH; ++j) v[j] = nxt[j];
+      if (a + 1 < W) {
+        const float2* gr = G + ((r0 + a + 1) & mask1) * row_stride;
+#pragma unroll
+        for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
+      }
       double2 racc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int j = 0; j < WH; ++j) {
@@ -460,7 +489,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
-__global__ void __launch_bounds__(256) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(512) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
                                                        int logm2, int ks_n, const double2* __restrict__ tw1,
                                                        float2* __restrict__ S) {
   extern __shared__ double2 sd[];
@@ -471,17 +500,17 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_cols(const float2* __restrict_
     sd[idx] = to_d(G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk]);
   }
   __syncthreads();
-  fft_dif<-1>(sd, logm1, ks_n, ks_n, tw1);
+  fft_stockham<-1>(sd, logm1, ks_n, ks_n, tw1);
   for (int idx = threadIdx.x; idx < n1 * ks_n; idx += blockDim.x) {
     const int i = idx / ks_n, kk = idx - i * ks_n;
     const int slot = (i - center1) & mask1;
-    S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = to_f(sd[brev(slot, logm1) * ks_n + kk]);
+    S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = to_f(sd[slot * ks_n + kk]);
   }
 }
 
 // Row FFT(-1) (DIT from bit-reversed placement, natural output) and the
 // final deconvolution into out[i, k0_out+kk, j].
-__global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
+__global__ void __launch_bounds__(512) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
@@ -492,10 +521,10 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict_
   const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
     const int c = idx / ks_n, kk = idx - c * ks_n;
-    sd[brev(c, logm2) * sm + kk] = to_d(Si[static_cast<long long>(c) * KB + kk]);
+    sd[c * sm + kk] = to_d(Si[static_cast<long long>(c) * KB + kk]);
   }
   __syncthreads();
-  fft_dit<-1>(sd, logm2, ks_n, sm, tw2);
+  fft_stockham<-1>(sd, logm2, ks_n, sm, tw2);
   const double pi = pdx[i];
   for (int idx = threadIdx.x; idx < ks_n * n2; idx += blockDim.x) {
     const int kk = idx / n2, j = idx - kk * n2;
@@ -512,7 +541,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_rows(const float2* __restrict_
 // ------------------------------------------------------------------------------------------
 // FFT along the contiguous axis of `rows` rows of length m (one CTA per ncol rows).
 template <int SIGN>
-__global__ void __launch_bounds__(256) k_center_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
+__global__ void __launch_bounds__(512) k_center_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
                                                          long long rows, int logm, int ncol, double scale,
                                                          const double2* __restrict__ tw) {
   extern __shared__ double2 sd[];
@@ -528,18 +557,18 @@ __global__ void __launch_bounds__(256) k_center_fft_rows(const float2* __restric
     sd[n * sm + c] = x;
   }
   __syncthreads();
-  fft_dif<SIGN>(sd, logm, ncol, sm, tw);
+  fft_stockham<SIGN>(sd, logm, ncol, sm, tw);
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int c = idx / m, k = idx - c * m;
     if (r0 + c >= rows) continue;
     const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    out[(r0 + c) * m + k] = to_f(cscale(sd[brev(k, logm) * sm + c], sg));
+    out[(r0 + c) * m + k] = to_f(cscale(sd[k * sm + c], sg));
   }
 }
 
 // FFT along the middle axis of [outer][m][inner] (one CTA per outer x ncol inner).
 template <int SIGN>
-__global__ void __launch_bounds__(256) k_center_fft_cols(const float2* in, float2* out, int inner, int logm, int ncol,
+__global__ void __launch_bounds__(512) k_center_fft_cols(const float2* in, float2* out, int inner, int logm, int ncol,
                                                          double scale, const double2* __restrict__ tw) {
   extern __shared__ double2 sd[];
   const int m = 1 << logm;
@@ -556,13 +585,13 @@ __global__ void __launch_bounds__(256) k_center_fft_cols(const float2* in, float
     sd[idx] = x;
   }
   __syncthreads();
-  fft_dif<SIGN>(sd, logm, ncol, ncol, tw);
+  fft_stockham<SIGN>(sd, logm, ncol, ncol, tw);
   float2* oo = out + o * m * inner;
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
     if (c0 + c >= inner) continue;
     const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    oo[static_cast<long long>(k) * inner + c0 + c] = to_f(cscale(sd[brev(k, logm) * ncol + c], sg));
+    oo[static_cast<long long>(k) * inner + c0 + c] = to_f(cscale(sd[k * ncol + c], sg));
   }
 }
 
@@ -583,9 +612,10 @@ __global__ void k_dense_dft(const float2* __restrict__ in, float2* __restrict__ 
   }
 }
 
+// e^{2 pi i k/m} for k < m (the Stockham passes index the full circle).
 std::vector<double2> twiddles(std::int64_t m) {
-  std::vector<double2> t(static_cast<std::size_t>(std::max<std::int64_t>(m / 2, 1)));
-  for (std::int64_t k = 0; k < m / 2; ++k) {
+  std::vector<double2> t(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)));
+  for (std::int64_t k = 0; k < m; ++k) {
     const double a = 2.0 * std::numbers::pi * static_cast<double>(k) / static_cast<double>(m);
     t[static_cast<std::size_t>(k)] = make_double2(std::cos(a), std::sin(a));
   }
@@ -656,7 +686,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   t.pz = DimPlan::make(g_.n0, fg.nu_z, kernel_);
   const int W = t.pz.taps;
   const DimPlan& pz = t.pz;
-  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(4096 / pz.m, 1, 64));
+  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / pz.m, 1, 64));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
   t.z_deconv.upload(pz.deconv, stream_);
   std::vector<double> pdec(pz.deconv.size());
@@ -810,7 +840,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   t.val.resize(T * KB);
 
   // ---- f2d (operators.cpp:20-74) ----
-  t.f2d_fft = is_pow2(g_.h) && is_pow2(g_.w) && g_.h >= 4 && g_.w >= 4;
+  t.f2d_fft = is_pow2(g_.h) && is_pow2(g_.w) && g_.h >= 8 && g_.w >= 8;
   if (t.f2d_fft) {
     t.h_tw.upload(twiddles(g_.h), stream_);
     t.w_tw.upload(twiddles(g_.w), stream_);
@@ -868,7 +898,7 @@ void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0) {
   const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(double2);
   prof::begin("k_fu1d", stream_);
   auto kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps> : k_fu1d<TIn, kTaps>;
-  kern<<<grid, 256, smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
+  kern<<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                      static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
                                      t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get());
   MLRG_LAUNCH_CHECK("k_fu1d");
@@ -883,7 +913,7 @@ void Usfft::fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0) {
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
   const std::size_t smem = static_cast<std::size_t>((t.pz.m + g_.h) * ncol) * sizeof(double2);
   prof::begin("k_fu1d_adj", stream_);
-  k_fu1d_adj<TOut><<<grid, 256, smem, stream_>>>(v, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
+  k_fu1d_adj<TOut><<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(v, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                                  static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center),
                                                  ncol, t.z_cphase.get(), t.z_cell_ptr.get(), t.z_cell_k.get(),
                                                  t.z_cell_w.get(), t.z_pdeconv.get(), t.z_tw.get());
@@ -905,14 +935,14 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
     prof::begin("k_fu2d_rows", stream_);
-    k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), 256,
+    k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
                   static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
         t.y_deconv.get(), t.y_tw.get(), t.S.get());
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", stream_);
     prof::begin("k_fu2d_cols", stream_);
-    k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), 256,
+    k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
                   static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
         t.S.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(),
         t.Gd.get());
@@ -956,14 +986,14 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     }
     prof::end("k_fu2d_adj_spread", stream_);
     prof::begin("k_fu2d_adj_cols", stream_);
-    k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), 256,
+    k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
                       static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
         t.Gd.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1,
         t.x_tw.get(), t.S.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     prof::end("k_fu2d_adj_cols", stream_);
     prof::begin("k_fu2d_adj_rows", stream_);
-    k_fu2d_adj_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), 256,
+    k_fu2d_adj_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
                       static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
         t.S.get(), nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
         t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b);
@@ -979,21 +1009,23 @@ void Usfft::f2d(const float2* p, float2* out, std::int64_t count, bool adjoint) 
   if (t.f2d_fft) {
     // rows (along w) into out, then columns (along h) in place
     const int lw = ilog2(w), lh = ilog2(h);
-    const int ncr = static_cast<int>(std::clamp<std::int64_t>(4096 / w, 1, 64));
+    const int ncr = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / w, 1, 64));
     const std::int64_t rows = count * h;
     const std::size_t smr = static_cast<std::size_t>(w * (ncr + 1)) * sizeof(double2);
     const double sw = 1.0 / std::sqrt(static_cast<double>(w)), sh = 1.0 / std::sqrt(static_cast<double>(h));
     const unsigned gr = static_cast<unsigned>((rows + ncr - 1) / ncr);
-    if (adjoint) k_center_fft_rows<+1><<<gr, 256, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
-    else k_center_fft_rows<-1><<<gr, 256, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
+    const unsigned tr = static_cast<unsigned>(ncr * w / 8);
+    if (adjoint) k_center_fft_rows<+1><<<gr, tr, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
+    else k_center_fft_rows<-1><<<gr, tr, smr, stream_>>>(p, out, rows, lw, ncr, sw, t.w_tw.get());
     MLRG_LAUNCH_CHECK("k_center_fft_rows");
-    const int ncc = static_cast<int>(std::clamp<std::int64_t>(4096 / h, 1, std::min<std::int64_t>(64, w)));
+    const int ncc = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / h, 1, std::min<std::int64_t>(64, w)));
     const dim3 gc(static_cast<unsigned>((w + ncc - 1) / ncc), static_cast<unsigned>(count));
     const std::size_t smc = static_cast<std::size_t>(h * ncc) * sizeof(double2);
+    const unsigned tc = static_cast<unsigned>(ncc * h / 8);
     if (adjoint)
-      k_center_fft_cols<+1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
+      k_center_fft_cols<+1><<<gc, tc, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
     else
-      k_center_fft_cols<-1><<<gc, 256, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
+      k_center_fft_cols<-1><<<gc, tc, smc, stream_>>>(out, out, static_cast<int>(w), lh, ncc, sh, t.h_tw.get());
     MLRG_LAUNCH_CHECK("k_center_fft_cols");
     return;
   }

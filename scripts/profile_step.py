@@ -1,0 +1,49 @@
+"""One ADMM outer iteration of the device solver between cudaProfilerStart/Stop,
+for `ncu --profile-from-start off` (launch lists and --set full captures).
+
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
+        --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py --n 256
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2511_01893_b200 as m  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--memo", default="off")
+    ap.add_argument("--kernel", default="es")
+    a = ap.parse_args()
+    n = a.n
+    stream = torch.cuda.current_stream()
+    ph = torch.from_numpy(m.make_phantom("blocks", n, n, n, 1).numpy().astype("complex64")).cuda()
+    ctx = m.Context(n, n, n, n, n, n, stream=stream.cuda_stream, kernel=a.kernel)
+    d = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+    ctx.forward_L(ph, d)
+    ctx.sync()
+    del ctx
+    cfg = (f"n1={n}\nn0={n}\nn2={n}\nn_theta={n}\nh={n}\nw={n}\nn_outer=1000\nmemoization={a.memo}\n"
+           f"nudft_path=gridding\ngridding_kernel={a.kernel}\n")
+    s = m.Solver(cfg, d, reference=ph, stream=stream.cuda_stream)
+    for _ in range(a.warmup):
+        s.step()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    for _ in range(a.steps):
+        s.step()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    print("profiled", a.steps, "step(s) at", n)
+
+
+if __name__ == "__main__":
+    main()
