@@ -125,9 +125,12 @@ __device__ __forceinline__ void fft_reg(double2* v) {
   }
 }
 
-template <int R, int LOGR, int SIGN>
+// One pass. GIN: the pass reads its inputs through load(row, b) (global
+// memory, the transform's first pass) instead of the tile; GOUT: it writes
+// through store(row, b, value) (the last pass) instead of the tile.
+template <int R, int LOGR, int SIGN, bool GIN, bool GOUT, class Load, class Store>
 __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, int logm, int logns,
-                                              const double2* __restrict__ tw) {
+                                              const double2* __restrict__ tw, const Load& load, const Store& store) {
   constexpr int PER = 8 / R;
   const int m8 = 1 << (logm - 3), stride = 1 << (logm - LOGR), ns = 1 << logns;
   double2 v[8];
@@ -135,9 +138,13 @@ __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, 
   for (int q = 0; q < PER; ++q) {
     const int gg = g + q * m8;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[q * R + r] = s[(gg + r * stride) * ld + b];
+    for (int r = 0; r < R; ++r) {
+      const int row = gg + r * stride;
+      if constexpr (GIN) v[q * R + r] = load(row, b);
+      else v[q * R + r] = s[row * ld + b];
+    }
   }
-  __syncthreads();
+  if constexpr (!GIN || GOUT) __syncthreads();  // in place: every read precedes any write
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int gg = g + q * m8;
@@ -154,23 +161,50 @@ __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, 
     fft_reg<R, SIGN>(v + q * R);
     const int base = ((gg >> logns) << (logns + LOGR)) + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[(base + (r << logns)) * ld + b] = v[q * R + r];
+    for (int r = 0; r < R; ++r) {
+      const int row = base + (r << logns);
+      if constexpr (GOUT) store(row, b, v[q * R + r]);
+      else s[row * ld + b] = v[q * R + r];
+    }
   }
-  __syncthreads();
+  if constexpr (!GOUT) __syncthreads();
 }
 
-template <int SIGN>
-__device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw) {
+struct NoLoad {
+  __device__ double2 operator()(int, int) const { return make_double2(0.0, 0.0); }
+};
+struct NoStore {
+  __device__ void operator()(int, int, double2) const {}
+};
+
+// Full transform. With GIN the tile's initial contents are ignored and the
+// first pass reads load(row, b) for row < m (natural input order); with GOUT
+// the last pass hands X[row] of column b to store(row, b, X) and the tile is
+// left as scratch; otherwise the tile holds the input / output.
+template <int SIGN, bool GIN = false, bool GOUT = false, class Load = NoLoad, class Store = NoStore>
+__device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw,
+                                             const Load& load = Load(), const Store& store = Store()) {
   const int b = threadIdx.x % nb, g = threadIdx.x / nb;
-  int logns = 0;
+  const int npass = (logm + 2) / 3;
+  int logns = 0, p = 0;
   if (logm % 3 == 1) {
-    stockham_pass<2, 1, SIGN>(s, ld, b, g, logm, 0, tw);
+    if (npass == 1) stockham_pass<2, 1, SIGN, GIN, GOUT>(s, ld, b, g, logm, 0, tw, load, store);
+    else stockham_pass<2, 1, SIGN, GIN, false>(s, ld, b, g, logm, 0, tw, load, store);
     logns = 1;
+    p = 1;
   } else if (logm % 3 == 2) {
-    stockham_pass<4, 2, SIGN>(s, ld, b, g, logm, 0, tw);
+    if (npass == 1) stockham_pass<4, 2, SIGN, GIN, GOUT>(s, ld, b, g, logm, 0, tw, load, store);
+    else stockham_pass<4, 2, SIGN, GIN, false>(s, ld, b, g, logm, 0, tw, load, store);
     logns = 2;
+    p = 1;
   }
-  for (; logns < logm; logns += 3) stockham_pass<8, 3, SIGN>(s, ld, b, g, logm, logns, tw);
+  for (; logns < logm; logns += 3, ++p) {
+    const bool first = p == 0, last = p == npass - 1;
+    if (first && last) stockham_pass<8, 3, SIGN, GIN, GOUT>(s, ld, b, g, logm, logns, tw, load, store);
+    else if (first) stockham_pass<8, 3, SIGN, GIN, false>(s, ld, b, g, logm, logns, tw, load, store);
+    else if (last) stockham_pass<8, 3, SIGN, false, GOUT>(s, ld, b, g, logm, logns, tw, load, store);
+    else stockham_pass<8, 3, SIGN, false, false>(s, ld, b, g, logm, logns, tw, load, store);
+  }
 }
 
 }  // namespace mlrg

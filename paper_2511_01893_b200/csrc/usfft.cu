@@ -197,7 +197,11 @@ struct GatherOut {
   int reduce;
 };
 
-// ---- gather: one warp per target ---------------------------------------------------------
+// ---- gather: one warp per target class ---------------------------------------------------
+// A class is a set of detector samples with the same frequency (the tilted
+// geometry samples every frequency twice: (theta, q) and (theta + pi, w - q)
+// coincide, and q = w/2 is the origin for every angle): its 2D sum is
+// computed once and multiplied by each member's phase (Usfft::Tables).
 // Lane l owns batch row l % 16 and the window columns of parity l / 16, so a
 // half warp reads one 128 B grid cell (16 rows x complex64) per tap: every
 // load is a full coalesced line, no tap is wasted and no lane idles. The
@@ -209,13 +213,15 @@ struct GatherOut {
 // processed in a spatially sorted order, kGatherPerCta per CTA, so the warps
 // of a CTA share their windows' cells in L1.
 constexpr int kGatherWarps = 8;
+constexpr std::size_t kClassMax = 4;
 constexpr int kGatherPerCta = 64;
 
 template <int W>
 __global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
-    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_tidx,
-    const int* __restrict__ s_r0, const int* __restrict__ s_c0, const double* __restrict__ s_w1,
-    const double* __restrict__ s_w2, const double2* __restrict__ s_fac, GatherOut eo, double* __restrict__ partials,
+    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
+    const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
+    const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
+    double* __restrict__ partials,
     int accumulate) {
   constexpr int WH = W / 2;
   __shared__ double red_scratch[kGatherWarps * 2];
@@ -267,16 +273,19 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
     if (ph == 0 && kk < nk) {
-      const int tq = s_tidx[s];
-      const int t = tq / w, q = tq - t * w;
-      double2 val = cmul(acc, s_fac[s]);
-      if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
-      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
-      if (eo.reduce) {
-        red[0] += val.x * val.x + val.y * val.y;
-        if (eo.dot) {
-          const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
-          red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
+      // every detector sample of the class gets the shared sum times its own phase
+      for (int e = m_first[s], e1 = m_first[s + 1]; e < e1; ++e) {
+        const int tq = m_tidx[e];
+        const int t = tq / w, q = tq - t * w;
+        double2 val = cmul(acc, m_fac[e]);
+        if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
+        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
+        if (eo.reduce) {
+          red[0] += val.x * val.x + val.y * val.y;
+          if (eo.dot) {
+            const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
+            red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
+          }
         }
       }
     }
@@ -465,27 +474,23 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_fu2d_adj_spread_reduce(
 // ------------------------------------------------------------------------------------------
 // fu2d adjoint: prep, column pass, row pass (the spread is above)
 // ------------------------------------------------------------------------------------------
-// val[t][KB] = p[t_, k0+kk, q_] * conj(phase product), zero for kk >= nk.
+// val[c][kk] = sum over the members e of class c of p[t_e, k0+kk, q_e] *
+// conj(phase_e), in member order (deterministic); zero for kk >= nk.
 __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict__ p, long long ld, long long k0,
-                                                       int nk, int T, int w, const double2* __restrict__ cfac,
-                                                       float2* __restrict__ val) {
-  __shared__ float2 tile[32][KB + 1];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
-  const int t = blockIdx.x * 32 + tx;
-  for (int kk = ty; kk < KB; kk += 8) {
-    float2 x = make_float2(0.f, 0.f);
-    if (t < T && kk < nk) {
-      const int ta = t / w, q = t - ta * w;
-      x = to_f(cmul(to_d(p[(ta * ld + k0 + kk) * w + q]), cfac[t]));
+                                                       int nk, int C, int w, const int* __restrict__ m_first,
+                                                       const int* __restrict__ m_tidx,
+                                                       const double2* __restrict__ m_cfac, float2* __restrict__ val) {
+  const int kk = threadIdx.x & (KB - 1);
+  const int c = blockIdx.x * (blockDim.x / KB) + threadIdx.x / KB;
+  if (c >= C) return;
+  double2 acc = make_double2(0.0, 0.0);
+  if (kk < nk)
+    for (int e = m_first[c], e1 = m_first[c + 1]; e < e1; ++e) {
+      const int tq = m_tidx[e];
+      const int t = tq / w, q = tq - t * w;
+      acc = cadd(acc, cmul(to_d(p[(t * ld + k0 + kk) * w + q]), m_cfac[e]));
     }
-    tile[tx][kk] = x;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 32 * KB; e += blockDim.x) {
-    const int tt = e / KB, kk = e - tt * KB;
-    const long long tg = static_cast<long long>(blockIdx.x) * 32 + tt;
-    if (tg < T) val[tg * KB + kk] = tile[tt][kk];
-  }
+  val[static_cast<long long>(c) * KB + kk] = to_f(acc);
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
@@ -658,14 +663,13 @@ struct Usfft::Tables {
   // fu2d
   DimPlan px, py;
   DeviceBuffer<double> x_deconv, x_pdeconv, y_deconv;
-  DeviceBuffer<double> t_w1, t_w2;  // [T][W] in target order (spread)
-  DeviceBuffer<int> t_r0, t_c0;
-  DeviceBuffer<double2> t_fac, t_cfac, x_tw, y_tw;
-  DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint values
-  // gather: targets in spatially sorted order
-  DeviceBuffer<int> s_tidx, s_r0, s_c0;
-  DeviceBuffer<double> s_w1, s_w2;
-  DeviceBuffer<double2> s_fac;
+  // target classes (coincident frequencies), spatially sorted: window origin
+  // and weights per class, member lists with each member's phase factors
+  int nclass = 0;
+  DeviceBuffer<int> t_r0, t_c0, m_first, m_tidx;
+  DeviceBuffer<double> t_w1, t_w2;  // [C][W]
+  DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
+  DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint class values
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
   int nitems = 0, nsplit = 0;
   DeviceBuffer<int> patch_t;
@@ -731,10 +735,6 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   std::vector<double> pdx(px.deconv.size());
   for (std::size_t i = 0; i < pdx.size(); ++i) pdx[i] = px.pref * py.pref * px.deconv[i];
   t.x_pdeconv.upload(pdx, stream_);
-  t.t_r0.upload(std::vector<int>(px.start.begin(), px.start.end()), stream_);
-  t.t_c0.upload(std::vector<int>(py.start.begin(), py.start.end()), stream_);
-  t.t_w1.upload(px.weights, stream_);
-  t.t_w2.upload(py.weights, stream_);
   std::vector<double2> tf(T), tcf(T);
   for (std::size_t q = 0; q < T; ++q) {
     const std::complex<double> ph = std::complex<double>(px.phase_re[q], px.phase_im[q]) *
@@ -743,45 +743,85 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     tf[q] = make_double2(f.real(), f.imag());
     tcf[q] = make_double2(ph.real(), -ph.imag());
   }
-  t.t_fac.upload(tf, stream_);
-  t.t_cfac.upload(tcf, stream_);
-  {  // gather order: 16 x 16 bins of the window origin, row-major inside a bin
-    std::vector<int> order(T);
-    for (std::size_t q = 0; q < T; ++q) order[q] = static_cast<int>(q);
-    std::vector<std::uint64_t> key(T);
-    for (std::size_t q = 0; q < T; ++q) {
-      const std::uint64_t r = static_cast<std::uint64_t>(px.start[q]), c = static_cast<std::uint64_t>(py.start[q]);
-      key[q] = ((r / 16) << 48) | ((c / 16) << 32) | (r << 16) | c;
+  // Classes of coincident targets: equal window origins and kernel weights
+  // within 1e-13 (the duplicates differ only by the rounding of cos/sin of
+  // theta and theta + pi), at most kClassMax members (the n_theta samples of
+  // the origin would otherwise serialise one warp), ordered by 16 x 16 bins
+  // of the window origin.
+  std::vector<int> order(T);
+  for (std::size_t q = 0; q < T; ++q) order[q] = static_cast<int>(q);
+  std::vector<std::uint64_t> key(T);
+  for (std::size_t q = 0; q < T; ++q) {
+    const std::uint64_t r = static_cast<std::uint64_t>(px.start[q]), c = static_cast<std::uint64_t>(py.start[q]);
+    key[q] = ((r / 16) << 48) | ((c / 16) << 32) | (r << 16) | c;
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
+  auto same_weights = [&](std::size_t a, std::size_t b) {
+    for (std::size_t k = 0; k < WS; ++k)
+      if (std::abs(px.weights[a * WS + k] - px.weights[b * WS + k]) > 1e-13 ||
+          std::abs(py.weights[a * WS + k] - py.weights[b * WS + k]) > 1e-13)
+        return false;
+    return true;
+  };
+  std::vector<int> rep_of;                   // class representative (lowest target index)
+  std::vector<std::vector<int>> members;
+  for (std::size_t i = 0; i < T;) {
+    std::size_t j = i;
+    while (j < T && key[static_cast<std::size_t>(order[j])] == key[static_cast<std::size_t>(order[i])]) ++j;
+    std::vector<int> run(order.begin() + static_cast<std::ptrdiff_t>(i), order.begin() + static_cast<std::ptrdiff_t>(j));
+    std::sort(run.begin(), run.end());
+    const std::size_t first_class = members.size();
+    for (const int q : run) {
+      std::size_t c = first_class;
+      while (c < members.size() && (members[c].size() >= kClassMax ||
+                                    !same_weights(static_cast<std::size_t>(rep_of[c]), static_cast<std::size_t>(q))))
+        ++c;
+      if (c == members.size()) {
+        rep_of.push_back(q);
+        members.emplace_back();
+      }
+      members[c].push_back(q);
     }
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
-    std::vector<int> tidx(T), r0(T), c0(T);
-    std::vector<double> sw1(T * WS), sw2(T * WS);
-    std::vector<double2> sfac(T);
-    for (std::size_t s = 0; s < T; ++s) {
-      const std::size_t q = static_cast<std::size_t>(order[s]);
-      tidx[s] = static_cast<int>(q);
-      r0[s] = px.start[q];
-      c0[s] = py.start[q];
+    i = j;
+  }
+  const std::size_t C = members.size();
+  t.nclass = static_cast<int>(C);
+  {
+    std::vector<int> r0(C), c0(C), mfirst(C + 1, 0), mtidx;
+    std::vector<double> w1(C * WS), w2(C * WS);
+    std::vector<double2> mfac, mcfac;
+    for (std::size_t c = 0; c < C; ++c) {
+      const std::size_t q = static_cast<std::size_t>(rep_of[c]);
+      r0[c] = px.start[q];
+      c0[c] = py.start[q];
       std::copy_n(px.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
-                  sw1.begin() + static_cast<std::ptrdiff_t>(s * WS));
+                  w1.begin() + static_cast<std::ptrdiff_t>(c * WS));
       std::copy_n(py.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
-                  sw2.begin() + static_cast<std::ptrdiff_t>(s * WS));
-      sfac[s] = tf[q];
+                  w2.begin() + static_cast<std::ptrdiff_t>(c * WS));
+      for (const int e : members[c]) {
+        mtidx.push_back(e);
+        mfac.push_back(tf[static_cast<std::size_t>(e)]);
+        mcfac.push_back(tcf[static_cast<std::size_t>(e)]);
+      }
+      mfirst[c + 1] = static_cast<int>(mtidx.size());
     }
-    t.s_tidx.upload(tidx, stream_);
-    t.s_r0.upload(r0, stream_);
-    t.s_c0.upload(c0, stream_);
-    t.s_w1.upload(sw1, stream_);
-    t.s_w2.upload(sw2, stream_);
-    t.s_fac.upload(sfac, stream_);
+    t.t_r0.upload(r0, stream_);
+    t.t_c0.upload(c0, stream_);
+    t.t_w1.upload(w1, stream_);
+    t.t_w2.upload(w2, stream_);
+    t.m_first.upload(mfirst, stream_);
+    t.m_tidx.upload(mtidx, stream_);
+    t.m_fac.upload(mfac, stream_);
+    t.m_cfac.upload(mcfac, stream_);
   }
   {  // spread patches: 8x4 cells -> targets whose W x W window touches them (targets ascending)
     const std::int64_t npr = px.m / kPatchR, npc = py.m / kPatchC;
     const int npatch = static_cast<int>(npr * npc);
     // patches touched by a target's W x W window (dedup within the target)
     std::vector<int> touched;
-    auto patches_of = [&](std::size_t q) {
+    auto patches_of = [&](std::size_t c) {
+      const std::size_t q = static_cast<std::size_t>(rep_of[c]);
       touched.clear();
       for (int a = 0; a < W; ++a) {
         const std::int64_t pr = ((px.start[q] + a) % px.m) / kPatchR;
@@ -799,11 +839,11 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
         pos.assign(cnt.begin(), cnt.end() - 1);
         lst.resize(static_cast<std::size_t>(cnt.back()));
       }
-      for (std::size_t q = 0; q < T; ++q) {
-        patches_of(q);
+      for (std::size_t c = 0; c < C; ++c) {
+        patches_of(c);
         for (const int p : touched) {
           if (pass == 0) cnt[static_cast<std::size_t>(p) + 1]++;
-          else lst[static_cast<std::size_t>(pos[static_cast<std::size_t>(p)]++)] = static_cast<int>(q);
+          else lst[static_cast<std::size_t>(pos[static_cast<std::size_t>(p)]++)] = static_cast<int>(c);
         }
       }
     }
@@ -837,7 +877,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   t.y_tw.upload(twiddles(py.m), stream_);
   t.S.resize(static_cast<std::size_t>(px.m * py.m * KB));
   t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB));
-  t.val.resize(T * KB);
+  t.val.resize(C * KB);
 
   // ---- f2d (operators.cpp:20-74) ----
   t.f2d_fft = is_pow2(g_.h) && is_pow2(g_.w) && g_.h >= 8 && g_.w >= 8;
@@ -930,7 +970,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int ggrid = static_cast<int>((T + kGatherPerCta - 1) / kGatherPerCta);
+  const int ggrid = (t.nclass + kGatherPerCta - 1) / kGatherPerCta;
   auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
@@ -951,10 +991,10 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
     prof::begin("k_fu2d_gather", stream_);
-    gather<<<ggrid, 32 * kGatherWarps, 0, stream_>>>(t.Gd.get(), static_cast<int>(T), static_cast<int>(g_.w),
-                                                     t.px.logm, t.py.logm, nb, t.s_tidx.get(), t.s_r0.get(),
-                                                     t.s_c0.get(), t.s_w1.get(), t.s_w2.get(), t.s_fac.get(), eo,
-                                                     partials_.dev(), b > 0 ? 1 : 0);
+    gather<<<ggrid, 32 * kGatherWarps, 0, stream_>>>(t.Gd.get(), t.nclass, static_cast<int>(g_.w), t.px.logm,
+                                                     t.py.logm, nb, t.t_r0.get(), t.t_c0.get(), t.t_w1.get(),
+                                                     t.t_w2.get(), t.m_first.get(), t.m_tidx.get(), t.m_fac.get(),
+                                                     eo, partials_.dev(), b > 0 ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", stream_);
   }
@@ -969,8 +1009,9 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
     prof::begin("k_fu2d_adj_prep", stream_);
-    k_fu2d_adj_prep<<<static_cast<unsigned>((T + 31) / 32), 256, 0, stream_>>>(
-        p, ld, k0 + b, nb, static_cast<int>(T), static_cast<int>(g_.w), t.t_cfac.get(), t.val.get());
+    k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, stream_>>>(
+        p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(),
+        t.val.get());
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
     prof::end("k_fu2d_adj_prep", stream_);
     prof::begin("k_fu2d_adj_spread", stream_);

@@ -36,13 +36,14 @@ for n, nt in [(64, 48)]:
     print("fu2d vs oracle", rel(c, O.fu2d_gridding(v[:, :4].astype(np.complex64).astype(complex), g)))
     c = host(ctx.fu2d(dev(v), e(nt, n, n))); d = host(ctx.fu2d_adj(dev(p), e(n, n, n)))
     print("adj fu2d", abs(np.vdot(p, c) - np.vdot(d, v)) / (np.linalg.norm(c) * np.linalg.norm(p)), flush=True)
-for case, memo in [("recon_c32_off_grid", "off"), ("recon_c32_memo_grid", "local"), ("recon_c64_off_grid", "off"), ("recon_cfg1_memo_direct", "local")]:
+KERNELS = os.environ.get("DIAG_KERNELS", "es").split(",")
+for case, memo, kern in [(c, mm, k) for k in KERNELS for c, mm in [("recon_c32_off_grid", "off"), ("recon_c32_memo_grid", "local"), ("recon_c64_off_grid", "off"), ("recon_cfg1_memo_direct", "local")]]:
     z = golden(case); n = z["phantom"].shape[0]; nt = z["data"].shape[0]
     u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
-    cfg = f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer=10\nmemoization={memo}\n"
+    cfg = f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer=10\nmemoization={memo}\ngridding_kernel={kern}\n"
     r = m.reconstruct_device(cfg, torch.from_numpy(z["data"]).cuda(), u, reference=torch.from_numpy(z["phantom"]).cuda())
     rows = m.parse_csv(r.csv); ref = [[float(x) for x in l.split(",")] for l in str(z["txt_report_csv"]).strip().splitlines()[1:]]
-    print(case, "aborted", r.aborted, "rows", len(rows), len(ref), "u rel", f"{rel(u.cpu().numpy(), z['u']):.2e}")
+    print(case, kern, "aborted", r.aborted, "rows", len(rows), len(ref), "u rel", f"{rel(u.cpu().numpy(), z['u']):.2e}")
     if memo != "off":
         meta, _ = r.audit(); print("  audit equal:", meta.shape == z["audit_int"].shape and np.array_equal(meta, z["audit_int"]),
                                     "first diff:", None if meta.shape != z["audit_int"].shape else np.argwhere((meta != z["audit_int"]).any(1))[:3].ravel())
