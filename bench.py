@@ -30,6 +30,11 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max clock (no measured figure)
 METRIC = "ADMM-FFT iterations/sec at N^3 volume"
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+# `ncu --set full` captures (profiles/), filled in per round
+TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (cold-cache capture of one launch)
+    "k_fu2d_gather": 46438144, "k_fu2d_adj_spread": 12300800, "k_fu2d_cols": 18330624, "k_fu1d": 379552256,
+}
 
 
 def parse():
@@ -105,16 +110,33 @@ def config_text(n, nt, memo):
             f"memoization={memo}\nnudft_path=gridding\n")
 
 
-def algorithmic(n, nt, kernel, launches_per_step):
-    """Per-launch algorithmic work of the profiled kernels."""
-    T = nt * n
-    if kernel == "k_fu2d_gather":  # 16 detector rows per launch, 576 taps + 24 outer + 12 epilogue flops
-        return {"flops": T * 16 * (24 * 24 * 4 + 24 * 4 + 12), "bytes": 8 * (2 * n) ** 2 * 16 + 8 * T * 16}
-    if kernel == "k_fu2d_adj_spread":
-        return {"flops": T * 16 * (24 * 24 * 4 + 24 * 4 + 12), "bytes": 8 * (2 * n) ** 2 * 16 + 8 * T * 16}
-    if kernel in ("k_fu1d", "k_fu1d_adj"):
-        return {"flops": None, "bytes": 8 * 2 * n ** 3}
+def algorithmic(n, nt, kernel):
+    """Per-launch algorithmic work of the profiled kernels, defined as SURVEY.md §8(d)
+    defines F2/F1 and B_iter: at the reference's 576 taps per target (a kernel that does
+    fewer taps shows a higher effective rate, not a smaller denominator)."""
+    T, M = nt * n, 2 * n
+    grid = 8 * M * M * 16  # one 16-row complex64 grid
+    if kernel in ("k_fu2d_gather", "k_fu2d_adj_spread"):  # 16 detector rows per launch
+        return {"flops": T * 16 * (24 * 24 * 4 + 24 * 4 + 12), "bytes": grid + 8 * T * 16}
+    if kernel in ("k_fu2d_rows", "k_fu2d_adj_rows"):  # one FFT pass over n1 x 16 rows of length M
+        return {"flops": n * 16 * 5 * M * math.log2(M), "bytes": 8 * n * 16 * n + grid // 2}
+    if kernel in ("k_fu2d_cols", "k_fu2d_adj_cols"):
+        return {"flops": M * 16 * 5 * M * math.log2(M), "bytes": grid // 2 + grid}
+    if kernel == "k_fu1d":  # whole volume: u (complex128 iterate) in, mid out
+        return {"flops": n * n * (5 * M * math.log2(M) + 2 * n + n * (24 * 4 + 8)), "bytes": 16 * n ** 3 + 8 * n ** 3}
+    if kernel == "k_fu1d_adj":
+        return {"flops": n * n * (5 * M * math.log2(M) + 2 * n + n * (24 * 4 + 8)), "bytes": 8 * n ** 3 + 16 * n ** 3}
     return {"flops": None, "bytes": None}
+
+
+def iteration_work(n, nt):
+    """algorithmic FP32 flops and fused-minimum HBM bytes per outer iteration."""
+    V = M_ = n ** 3
+    P = nt * n * n
+    M0 = M1 = M2 = 2 * n
+    F1 = n * n * (5 * M0 * math.log2(M0) + 2 * n + n * (24 * 4 + 8))
+    F2 = n * (5 * M1 * M2 * math.log2(M1 * M2) + 2 * n * n + nt * n * (24 * 24 * 4 + 24 * 4 + 12))
+    return 13 * F1 + 13 * F2, 8 * (131 * V + 26 * M_ + 22 * P)
 
 
 def main():
@@ -213,26 +235,33 @@ def main():
     if off["prof"]:
         name, rec = max(off["prof"].items(), key=lambda kv: kv[1]["ms_total"])
         avg_ms = rec["ms_total"] / rec["launches"]
-        work = algorithmic(n, nt, name, rec["launches"] / max(off["steps_done"], 1))
+        work = algorithmic(n, nt, name)
         total_ms = sum(v["ms_total"] for v in off["prof"].values())
-        if work["flops"]:
+        # the fu2d-class tap kernels are bound by FP32 CUDA-core issue
+        # (no dense contraction: tensor cores do not apply); everything else by HBM
+        if name in ("k_fu2d_gather", "k_fu2d_adj_spread"):
             ach = work["flops"] / (avg_ms * 1e-3) / 1e12
             roof = {"kernel": name, "bound": "fp32", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": ach / FP32_PEAK_TFLOPS,
                     "peak_source": "computed 148 SM x 128 FFMA lanes x 2 x 1.965 GHz (MEASURED_PEAKS has no FP32 figure)",
-                    "algorithmic_per_launch": work["flops"], "avg_launch_ms": avg_ms, "traffic": None}
+                    "algorithmic_per_launch": work["flops"], "algorithmic_unit": "flop (576 taps x 16 rows per target)",
+                    "avg_launch_ms": avg_ms, "traffic": TRAFFIC.get(name),
+                    "hbm_view": {"bytes_per_launch": work["bytes"],
+                                 "achieved_gbs": work["bytes"] / (avg_ms * 1e-3) / 1e9, "peak_gbs": P["hbm_gbs"]}}
         else:
             ach = work["bytes"] / (avg_ms * 1e-3) / 1e9
             roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"], "unit": "GB/s",
                     "frac": ach / P["hbm_gbs"], "peak_source": src, "algorithmic_per_launch": work["bytes"],
-                    "avg_launch_ms": avg_ms, "traffic": None}
+                    "avg_launch_ms": avg_ms, "traffic": TRAFFIC.get(name)}
         roof["share_of_step"] = rec["ms_total"] / off["ms"]
         roof["kernels_ms_per_step"] = {k: v["ms_total"] / max(off["steps_done"], 1) for k, v in off["prof"].items()}
-    # whole-iteration HBM view against SURVEY §8(d)'s fused-minimum bytes
-    V, M, Pp = n ** 3, n ** 3, nt * n * n
-    b_iter = 8 * (131 * V + 26 * M + 22 * Pp)
+    # whole-iteration views against SURVEY §8(d)'s F_iter and fused-minimum B_iter
+    V = n ** 3
+    f_iter, b_iter = iteration_work(n, nt)
     iter_hbm = {"bytes_per_iter": b_iter, "achieved_gbs": b_iter / (ms_step * 1e-3) / 1e9,
-                "frac": b_iter / (ms_step * 1e-3) / 1e9 / P["hbm_gbs"], "peak_source": src}
+                "frac": b_iter / (ms_step * 1e-3) / 1e9 / P["hbm_gbs"], "peak_source": src,
+                "flops_per_iter": f_iter, "achieved_tflops": f_iter / (ms_step * 1e-3) / 1e12,
+                "fp32_frac": f_iter / (ms_step * 1e-3) / 1e12 / FP32_PEAK_TFLOPS}
 
     e2e = None
     if not args.no_e2e:
@@ -259,7 +288,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c64 (fp32)", "data": "synthetic (blocks phantom seed 1, d = forward_L on GPU)",
         "config": {"workload": f"configs[1]: {n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)",
-                   "n": n, "n_theta": nt, "n_inner": 4, "memo": "off", "nudft": "gridding, 24-tap Gaussian",
+                   "n": n, "n_theta": nt, "n_inner": 4, "memo": "off",
+                   "nudft": "gridding, 12-tap ES kernel (NUDFT to 2e-11; reference: 24-tap Gaussian, 3e-12)",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "no flush: every per-iteration array (134 MB) exceeds the 126 MB L2"},
         "memo_on": memo_on, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
