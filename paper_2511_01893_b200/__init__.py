@@ -18,7 +18,7 @@ __all__ = ["lib", "LIB_PATH", "MlrError", "Config", "Array", "Result", "make_pha
            "reconstruct", "array_from_numpy", "Context", "DeviceRecon", "reconstruct_device", "Solver",
            "Memo", "projection_matrix", "slot_mix"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmlr.so")
+LIB_PATH = os.environ.get("MLRG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmlr.so")
 _LIB = None
 
 MLR_OK, MLR_ERR_CONFIG, MLR_ERR_IO, MLR_ERR_RUNTIME, MLR_ERR_ABORTED = range(5)

@@ -31,13 +31,19 @@ namespace {
 
 constexpr int KB = Usfft::kRowBatch;
 
+// minimum resident CTAs per SM for the 256-thread 2D grid FFT passes (register cap)
+#ifndef MLRG_FFT_MINB
+#define MLRG_FFT_MINB 4
+#endif
+
 // Complex elements per CTA of the shared-memory FFT passes (double: 16 B each).
 // 2048 (32 KB) lets ~6 CTAs share an SM so one CTA's loads overlap another's
 // butterflies; MLRG_FFT_ELEMS overrides it for tuning.
 std::int64_t fft_elems() {
   static const std::int64_t e = [] {
     const char* v = std::getenv("MLRG_FFT_ELEMS");
-    std::int64_t n = v ? std::max<std::int64_t>(std::atoll(v), 64) : std::int64_t{2048};
+    // <= 2048: the 2D passes run 256-thread CTAs (m * nb / 8 threads)
+    std::int64_t n = v ? std::clamp<std::int64_t>(std::atoll(v), 64, 2048) : std::int64_t{2048};
     while (n & (n - 1)) n &= n - 1;
     return n;
   }();
@@ -45,7 +51,7 @@ std::int64_t fft_elems() {
 }
 // k-columns per CTA of a 2D-grid FFT pass over length m.
 int pass_cols(std::int64_t m) {
-  int c = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / m, 2, KB));
+  int c = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / m, 1, KB));
   while (c & (c - 1)) c &= c - 1;  // a power of two dividing KB
   return c;
 }
@@ -63,16 +69,16 @@ __global__ void __launch_bounds__(512) k_fu1d(const TIn* __restrict__ u, float2*
   const int m = 1 << logm, mask = m - 1;
   const int j0 = blockIdx.x * ncol;
   const TIn* ui = u + static_cast<long long>(blockIdx.y) * n0 * n2;
-  for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
-    const int r = idx / ncol, c = idx - r * ncol;
-    const int mode = (r + center) & mask;  // grid slot r holds mode (r + center) mod m
-    const int j = j0 + c;
-    double2 v = make_double2(0.0, 0.0);
-    if (mode < n0 && j < n2) v = cscale(to_d(ui[static_cast<long long>(mode) * n2 + j]), deconv[mode]);
-    sd[idx] = v;
-  }
-  __syncthreads();
-  fft_stockham<+1>(sd, logm, ncol, ncol, tw);
+  // grid slot r holds mode (r + center) mod m, deconvolved. Loads are
+  // unconditional (clamped address) so a pass issues its 8 back to back.
+  auto load = [&](int r, int c) {
+    const int mode = (r + center) & mask, j = j0 + c;
+    const bool ok = mode < n0 && j < n2;
+    const double2 x = to_d(ui[ok ? static_cast<long long>(mode) * n2 + j : 0]);
+    const double dc = deconv[ok ? mode : 0];
+    return ok ? cscale(x, dc) : make_double2(0.0, 0.0);
+  };
+  fft_stockham<+1, true, false>(sd, logm, ncol, ncol, tw, load);
   float2* oi = out + static_cast<long long>(blockIdx.y) * h * n2;
   for (int idx = threadIdx.x; idx < h * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
@@ -124,25 +130,23 @@ __global__ void __launch_bounds__(512) k_fu1d_adj(const float2* __restrict__ v, 
     sd[idx] = acc;
   }
   __syncthreads();
-  fft_stockham<-1>(sd, logm, ncol, ncol, tw);
   TOut* oi = out + static_cast<long long>(blockIdx.y) * n0 * n2;
-  for (int idx = threadIdx.x; idx < n0 * ncol; idx += blockDim.x) {
-    const int mode = idx / ncol, c = idx - mode * ncol;
-    const int j = j0 + c;
-    if (j >= n2) continue;
-    const int slot = (mode - center) & mask;
-    const double2 r = cscale(sd[slot * ncol + c], pdeconv[mode]);
+  auto store = [&](int slot, int c, double2 x) {
+    const int mode = (slot + center) & mask, j = j0 + c;
+    if (mode >= n0 || j >= n2) return;
+    const double2 r = cscale(x, pdeconv[mode]);
     TOut& o = oi[static_cast<long long>(mode) * n2 + j];
     o.x = static_cast<decltype(o.x)>(r.x);
     o.y = static_cast<decltype(o.y)>(r.y);
-  }
+  };
+  fft_stockham<-1, false, true>(sd, logm, ncol, ncol, tw, NoLoad(), store);
 }
 
 // ------------------------------------------------------------------------------------------
 // fu2d forward: row pass, column pass, gather
 // ------------------------------------------------------------------------------------------
 // S[i][c'][KB]: row FFT of v[i, k0+kk, :] * dx[i] * dy[:] placed at wrapped slots.
-__global__ void __launch_bounds__(512) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
+__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
                                                    const double2* __restrict__ tw2, float2* __restrict__ S) {
@@ -150,41 +154,33 @@ __global__ void __launch_bounds__(512) k_fu2d_rows(const float2* __restrict__ v,
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
   const double di = dx[i];
-  for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
-    const int kk = idx / m2, r = idx - kk * m2;
+  auto load = [&](int r, int kk) {
     const int j = (r + center2) & mask2;
-    double2 val = make_double2(0.0, 0.0);
-    if (j < n2 && ks + kk < nk)
-      val = cscale(to_d(v[(static_cast<long long>(i) * ld + k0 + ks + kk) * n2 + j]), di * dy[j]);
-    sd[r * sm + kk] = val;
-  }
-  __syncthreads();
-  fft_stockham<+1>(sd, logm2, ks_n, sm, tw2);
+    const bool ok = j < n2 && ks + kk < nk;
+    const double2 x = to_d(v[ok ? (static_cast<long long>(i) * ld + k0 + ks + kk) * n2 + j : 0]);
+    const double f = di * dy[ok ? j : 0];
+    return ok ? cscale(x, f) : make_double2(0.0, 0.0);
+  };
   float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
-  for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
-    const int r = idx / ks_n, kk = idx - r * ks_n;
-    Si[static_cast<long long>(r) * KB + kk] = to_f(sd[r * sm + kk]);
-  }
+  auto store = [&](int r, int kk, double2 x) { Si[static_cast<long long>(r) * KB + kk] = to_f(x); };
+  fft_stockham<+1, true, true>(sd, logm2, ks_n, sm, tw2, load, store);
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
-__global__ void __launch_bounds__(512) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
                                                    float2* __restrict__ G) {
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
-  for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
-    const int r = idx / ks_n, kk = idx - r * ks_n;
+  auto load = [&](int r, int kk) {
     const int i = (r + center1) & mask1;
-    sd[idx] = i < n1 ? to_d(S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk]) : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  fft_stockham<+1>(sd, logm1, ks_n, ks_n, tw1);
-  for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
-    const int r = idx / ks_n, kk = idx - r * ks_n;
-    G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(sd[idx]);
-  }
+    const bool ok = i < n1;
+    const double2 x = to_d(S[(static_cast<long long>(ok ? i : 0) * m2 + c) * KB + ks + kk]);
+    return ok ? x : make_double2(0.0, 0.0);
+  };
+  auto store = [&](int r, int kk, double2 x) { G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(x); };
+  fft_stockham<+1, true, true>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
 struct GatherOut {
@@ -210,27 +206,33 @@ struct GatherOut {
 // them, sums them against the column weights (double) and adds the row
 // weight times that sum, which is the reference's order of summation
 // (inner over columns, outer over rows, nufft.cpp:205-216). Targets are
-// processed in a spatially sorted order, kGatherPerCta per CTA, so the warps
+// processed in a spatially sorted order, gather_per_cta() per CTA, so the warps
 // of a CTA share their windows' cells in L1.
 constexpr int kGatherWarps = 8;
 constexpr std::size_t kClassMax = 4;
-constexpr int kGatherPerCta = 64;
+// classes per gather CTA (MLRG_GATHER_PER_CTA overrides, for tuning)
+int gather_per_cta() {
+  static const int v = [] {
+    const char* e = std::getenv("MLRG_GATHER_PER_CTA");
+    return e ? std::max(8, std::atoi(e)) : 16;
+  }();
+  return v;
+}
 
 template <int W>
 __global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
     const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
     const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
     const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
-    double* __restrict__ partials,
-    int accumulate) {
+    int per_cta, double* __restrict__ partials, int accumulate) {
   constexpr int WH = W / 2;
   __shared__ double red_scratch[kGatherWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, kk = lane & 15, ph = lane >> 4;
   const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1;
   const long long row_stride = static_cast<long long>(KB) << logm2;  // complex64 per grid row
   double red[2] = {0.0, 0.0};
-  const int s_end = min(T, static_cast<int>(blockIdx.x + 1) * kGatherPerCta);
-  for (int s = blockIdx.x * kGatherPerCta + warp; s < s_end; s += kGatherWarps) {
+  const int s_end = min(T, static_cast<int>(blockIdx.x + 1) * per_cta);
+  for (int s = blockIdx.x * per_cta + warp; s < s_end; s += kGatherWarps) {
     const int r0 = s_r0[s], c0 = s_c0[s];
     int coff[WH];
     double w2r[WH];
@@ -494,28 +496,22 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
-__global__ void __launch_bounds__(512) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
                                                        int logm2, int ks_n, const double2* __restrict__ tw1,
                                                        float2* __restrict__ S) {
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
-  for (int idx = threadIdx.x; idx < m1 * ks_n; idx += blockDim.x) {
-    const int r = idx / ks_n, kk = idx - r * ks_n;
-    sd[idx] = to_d(G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk]);
-  }
-  __syncthreads();
-  fft_stockham<-1>(sd, logm1, ks_n, ks_n, tw1);
-  for (int idx = threadIdx.x; idx < n1 * ks_n; idx += blockDim.x) {
-    const int i = idx / ks_n, kk = idx - i * ks_n;
-    const int slot = (i - center1) & mask1;
-    S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = to_f(sd[slot * ks_n + kk]);
-  }
+  auto load = [&](int r, int kk) { return to_d(G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk]); };
+  auto store = [&](int slot, int kk, double2 x) {  // keep the n1 slots that map to modes
+    const int i = (slot + center1) & mask1;
+    if (i < n1) S[(static_cast<long long>(i) * m2 + c) * KB + ks + kk] = to_f(x);
+  };
+  fft_stockham<-1, true, true>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
-// Row FFT(-1) (DIT from bit-reversed placement, natural output) and the
-// final deconvolution into out[i, k0_out+kk, j].
-__global__ void __launch_bounds__(512) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
+// Row FFT(-1) and the final deconvolution into out[i, k0_out+kk, j].
+__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
@@ -524,19 +520,14 @@ __global__ void __launch_bounds__(512) k_fu2d_adj_rows(const float2* __restrict_
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
   const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
-  for (int idx = threadIdx.x; idx < m2 * ks_n; idx += blockDim.x) {
-    const int c = idx / ks_n, kk = idx - c * ks_n;
-    sd[c * sm + kk] = to_d(Si[static_cast<long long>(c) * KB + kk]);
-  }
-  __syncthreads();
-  fft_stockham<-1>(sd, logm2, ks_n, sm, tw2);
   const double pi = pdx[i];
-  for (int idx = threadIdx.x; idx < ks_n * n2; idx += blockDim.x) {
-    const int kk = idx / n2, j = idx - kk * n2;
-    if (ks + kk >= nk) continue;
-    const int slot = (j - center2) & mask2;
-    out[(static_cast<long long>(i) * ld_out + k0_out + ks + kk) * n2 + j] = to_f(cscale(sd[slot * sm + kk], pi * dy[j]));
-  }
+  auto load = [&](int c, int kk) { return to_d(Si[static_cast<long long>(c) * KB + kk]); };
+  auto store = [&](int slot, int kk, double2 x) {
+    const int j = (slot + center2) & mask2;
+    if (j < n2 && ks + kk < nk)
+      out[(static_cast<long long>(i) * ld_out + k0_out + ks + kk) * n2 + j] = to_f(cscale(x, pi * dy[j]));
+  };
+  fft_stockham<-1, true, true>(sd, logm2, ks_n, sm, tw2, load, store);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -552,23 +543,17 @@ __global__ void __launch_bounds__(512) k_center_fft_rows(const float2* __restric
   extern __shared__ double2 sd[];
   const int m = 1 << logm, sm = ncol + 1;
   const long long r0 = static_cast<long long>(blockIdx.x) * ncol;
-  for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
-    const int c = idx / m, n = idx - c * m;
-    double2 x = make_double2(0.0, 0.0);
-    if (r0 + c < rows) {
-      x = to_d(in[(r0 + c) * m + n]);
-      if (n & 1) x = make_double2(-x.x, -x.y);
-    }
-    sd[n * sm + c] = x;
-  }
-  __syncthreads();
-  fft_stockham<SIGN>(sd, logm, ncol, sm, tw);
-  for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
-    const int c = idx / m, k = idx - c * m;
-    if (r0 + c >= rows) continue;
+  auto load = [&](int n, int c) {
+    const bool ok = r0 + c < rows;
+    const double2 x = to_d(in[ok ? (r0 + c) * m + n : 0]);
+    return !ok ? make_double2(0.0, 0.0) : (n & 1) ? make_double2(-x.x, -x.y) : x;
+  };
+  auto store = [&](int k, int c, double2 x) {
+    if (r0 + c >= rows) return;
     const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    out[(r0 + c) * m + k] = to_f(cscale(sd[k * sm + c], sg));
-  }
+    out[(r0 + c) * m + k] = to_f(cscale(x, sg));
+  };
+  fft_stockham<SIGN, true, true>(sd, logm, ncol, sm, tw, load, store);
 }
 
 // FFT along the middle axis of [outer][m][inner] (one CTA per outer x ncol inner).
@@ -580,24 +565,18 @@ __global__ void __launch_bounds__(512) k_center_fft_cols(const float2* in, float
   const long long o = blockIdx.y;
   const int c0 = blockIdx.x * ncol;
   const float2* io = in + o * m * inner;
-  for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
-    const int n = idx / ncol, c = idx - n * ncol;
-    double2 x = make_double2(0.0, 0.0);
-    if (c0 + c < inner) {
-      x = to_d(io[static_cast<long long>(n) * inner + c0 + c]);
-      if (n & 1) x = make_double2(-x.x, -x.y);
-    }
-    sd[idx] = x;
-  }
-  __syncthreads();
-  fft_stockham<SIGN>(sd, logm, ncol, ncol, tw);
   float2* oo = out + o * m * inner;
-  for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
-    const int k = idx / ncol, c = idx - k * ncol;
-    if (c0 + c >= inner) continue;
+  auto load = [&](int n, int c) {
+    const bool ok = c0 + c < inner;
+    const double2 x = to_d(io[ok ? static_cast<long long>(n) * inner + c0 + c : 0]);
+    return !ok ? make_double2(0.0, 0.0) : (n & 1) ? make_double2(-x.x, -x.y) : x;
+  };
+  auto store = [&](int k, int c, double2 x) {  // in place is safe: all loads precede the first store
+    if (c0 + c >= inner) return;
     const double sg = ((k + (m >> 1)) & 1) ? -scale : scale;
-    oo[static_cast<long long>(k) * inner + c0 + c] = to_f(cscale(sd[k * ncol + c], sg));
-  }
+    oo[static_cast<long long>(k) * inner + c0 + c] = to_f(cscale(x, sg));
+  };
+  fft_stockham<SIGN, true, true>(sd, logm, ncol, ncol, tw, load, store);
 }
 
 // out[o, k, in] = sum_m W[k, m] x[o, m, in] (dense centred DFT along the middle axis).
@@ -727,6 +706,9 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   // ---- fu2d plans (nufft.cpp:185-187) ----
   t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
   t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
+  // the 2D grid passes run 256-thread CTAs (launch bounds 256 x 4): m * nb / 8 <= 256
+  if (t.px.m > 2048 || t.py.m > 2048)
+    throw std::invalid_argument("fu2d: n1 and n2 up to 1024 are supported on one device");
   const std::size_t WS = static_cast<std::size_t>(W);
   const DimPlan &px = t.px, &py = t.py;
   const std::size_t T = fg.nu_x.size();
@@ -970,7 +952,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int ggrid = (t.nclass + kGatherPerCta - 1) / kGatherPerCta;
+  const int per_cta = gather_per_cta();
+  const int ggrid = (t.nclass + per_cta - 1) / per_cta;
   auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
   for (std::int64_t b = 0; b < nk; b += KB) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
@@ -994,7 +977,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     gather<<<ggrid, 32 * kGatherWarps, 0, stream_>>>(t.Gd.get(), t.nclass, static_cast<int>(g_.w), t.px.logm,
                                                      t.py.logm, nb, t.t_r0.get(), t.t_c0.get(), t.t_w1.get(),
                                                      t.t_w2.get(), t.m_first.get(), t.m_tidx.get(), t.m_fac.get(),
-                                                     eo, partials_.dev(), b > 0 ? 1 : 0);
+                                                     eo, per_cta, partials_.dev(), b > 0 ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", stream_);
   }
