@@ -35,6 +35,9 @@ constexpr int KB = Usfft::kRowBatch;
 #ifndef MLRG_FFT_MINB
 #define MLRG_FFT_MINB 4
 #endif
+#ifndef MLRG_GATHER_MINB
+#define MLRG_GATHER_MINB 3
+#endif
 
 // Complex elements per CTA of the shared-memory FFT passes (double: 16 B each).
 // 2048 (32 KB) lets ~6 CTAs share an SM so one CTA's loads overlap another's
@@ -220,7 +223,7 @@ int gather_per_cta() {
 }
 
 template <int W>
-__global__ void __launch_bounds__(32 * kGatherWarps) k_fu2d_gather(
+__global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_gather(
     const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
     const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
     const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
