@@ -105,8 +105,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def config_text(n, nt, memo):
-    return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer=1000000\n"
+def config_text(n, nt, memo, n_outer=1000000):
+    return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
             f"memoization={memo}\nnudft_path=gridding\n")
 
 
@@ -171,15 +171,19 @@ def main():
     ctx.sync()
     del ctx
 
-    def timed_run(memo: str, profile: bool):
-        solver = m.Solver(config_text(n, nt, memo), d, reference=phantom, stream=stream.cuda_stream)
+    def timed_run(memo: str, profile_steps: int):
+        """W warm-up steps, K timed steps (CUDA events on the solver's stream, no
+        profiling hooks), then `profile_steps` more with per-kernel event timers."""
+        # n_outer = the iterations this run makes (sizes the memo value arena, reserved at setup)
+        solver = m.Solver(config_text(n, nt, memo, args.warmup + args.steps + profile_steps), d, reference=phantom,
+                          stream=stream.cuda_stream)
         for _ in range(args.warmup):
             solver.step()
-        m.lib().mlrg_prof_reset()
-        m.lib().mlrg_prof_enable(1 if profile else 0)
+        m.lib().mlrg_prof_enable(0)
         c0 = solver.counters()
         launches0 = m.lib().mlrg_launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        step_ms = []
         with ClockSampler(local) as clocks:
             if world > 1:
                 dist.barrier()
@@ -187,19 +191,28 @@ def main():
             ev0.record(stream)
             done = 0
             for _ in range(args.steps):
+                t0 = time.perf_counter()
                 if not solver.step():
                     break
+                step_ms.append(1e3 * (time.perf_counter() - t0))
                 done += 1
             ev1.record(stream)
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-        m.lib().mlrg_prof_enable(0)
         ms = ev0.elapsed_time(ev1)
         launches = m.lib().mlrg_launch_count() - launches0
         c1 = solver.counters()
-        prof = {}
-        if profile:
+        prof, prof_steps = {}, 0
+        if profile_steps:
+            m.lib().mlrg_prof_reset()
+            m.lib().mlrg_prof_enable(1)
+            for _ in range(profile_steps):
+                if not solver.step():
+                    break
+                prof_steps += 1
+            torch.cuda.synchronize()
+            m.lib().mlrg_prof_enable(0)
             for k in ("k_fu2d_gather", "k_fu2d_adj_spread", "k_fu2d_rows", "k_fu2d_cols", "k_fu2d_adj_cols",
                       "k_fu2d_adj_rows", "k_fu2d_adj_prep", "k_fu1d", "k_fu1d_adj"):
                 tot, cnt = m.prof_query(k)
@@ -208,9 +221,10 @@ def main():
         csv = solver.csv
         del solver
         return dict(ms=ms, steps_done=done, launches=launches, clocks=clocks.summary(), prof=prof,
-                    counters={k: c1[k] - c0[k] for k in c1}, csv=csv)
+                    prof_steps=prof_steps, counters={k: c1[k] - c0[k] for k in c1}, csv=csv,
+                    step_ms=[round(x, 2) for x in step_ms])
 
-    off = timed_run("off", profile=True)
+    off = timed_run("off", profile_steps=3)
     ms_step = off["ms"] / max(off["steps_done"], 1)
     if world > 1:
         t = torch.tensor([ms_step], device="cuda")
@@ -220,14 +234,14 @@ def main():
 
     memo_on = None
     if not args.no_memo_run:
-        on = timed_run("local", profile=False)
+        on = timed_run("local", profile_steps=0)
         c = on["counters"]
         hits = c["remote_hits"] + c["cache_hits"]
         memo_on = {"value": 1000.0 * on["steps_done"] / on["ms"] if on["steps_done"] else None,
                    "steps_done": on["steps_done"], "lookups": c["lookups"], "misses": c["misses"],
                    "remote_hits": c["remote_hits"], "cache_hits": c["cache_hits"],
                    "hit_rate": hits / c["lookups"] if c["lookups"] else None,
-                   "aborted": on["steps_done"] < args.steps}
+                   "aborted": on["steps_done"] < args.steps, "step_ms": on["step_ms"]}
 
     # dominant kernel roofline from the live CUDA-event timers
     P, src = peaks()
@@ -253,8 +267,9 @@ def main():
             roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"], "unit": "GB/s",
                     "frac": ach / P["hbm_gbs"], "peak_source": src, "algorithmic_per_launch": work["bytes"],
                     "avg_launch_ms": avg_ms, "traffic": TRAFFIC.get(name)}
-        roof["share_of_step"] = rec["ms_total"] / off["ms"]
-        roof["kernels_ms_per_step"] = {k: v["ms_total"] / max(off["steps_done"], 1) for k, v in off["prof"].items()}
+        ps = max(off["prof_steps"], 1)
+        roof["share_of_step"] = rec["ms_total"] / ps / ms_step
+        roof["kernels_ms_per_step"] = {k: v["ms_total"] / ps for k, v in off["prof"].items()}
     # whole-iteration views against SURVEY §8(d)'s F_iter and fused-minimum B_iter
     V = n ** 3
     f_iter, b_iter = iteration_work(n, nt)

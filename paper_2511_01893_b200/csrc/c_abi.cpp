@@ -116,7 +116,17 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s);
   if (rc.encoder.variant != mlrg::EncoderConfig::Variant::projection)
     throw std::invalid_argument("encoder_variant=cnn is not provided by the B200 build (projection only)");
-  auto client = std::make_shared<mlrg::MemoClient>(rc.memo, std::make_shared<mlrg::MemoStore>());
+  auto store = std::make_shared<mlrg::MemoStore>();
+  // HBM for the values the solve can insert: n_outer x the per-iteration insert
+  // cap x the largest slab value (complex64), at most 45% of free HBM
+  const std::int64_t e = ec.chunk_extent;
+  const std::int64_t slab = std::max({e * g.h * g.n2, e * g.n0 * g.n2, g.n_theta * e * g.w, g.n1 * e * g.n2});
+  std::size_t free_b = 0, total_b = 0;
+  MLRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double want = static_cast<double>(rc.admm.n_outer) * static_cast<double>(rc.memo.insert_queue_cap) *
+                      static_cast<double>(slab) * sizeof(float2);
+  store->arena().reserve(static_cast<std::size_t>(std::min(want, 0.45 * static_cast<double>(free_b))));
+  auto client = std::make_shared<mlrg::MemoClient>(rc.memo, store);
   auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
   return std::make_unique<mlrg::Engine>(g, ec, s, enc, client);
 }

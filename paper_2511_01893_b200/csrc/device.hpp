@@ -26,6 +26,20 @@ bool enabled();
 /// Brackets one launch of `name` on `s` with events when profiling is on.
 void begin(const char* name, cudaStream_t s);
 void end(const char* name, cudaStream_t s);
+/// Accumulates a host-side phase's wall time under `name` when profiling is on.
+void host_add(const char* name, double ms);
+/// RAII wall timer for host_add.
+class HostSpan {
+ public:
+  explicit HostSpan(const char* name);
+  ~HostSpan();
+  HostSpan(const HostSpan&) = delete;
+  HostSpan& operator=(const HostSpan&) = delete;
+
+ private:
+  const char* name_;
+  long long t0_;
+};
 }  // namespace prof
 
 #define MLRG_CUDA(call) ::mlrg::cuda_check((call), #call)

@@ -109,14 +109,25 @@ void encode(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns
             double* work, float* keys, double* norms2, cudaStream_t s);
 std::size_t encode_work_doubles(int ns, int kd);
 
-/// out[slab] = value * scale - sub[slab] (sub may be null) (scalerun.cpp:250-255).
-void slab_materialize(float2* out, SlabGeom g, const float2* value, double scale, const float2* sub, cudaStream_t s);
-void slab_materialize(double2* out, SlabGeom g, const float2* value, double scale, cudaStream_t s);
-/// value = out[slab] (contiguous chunk order, complex64).
-void slab_store(const float2* out, SlabGeom g, float2* value, cudaStream_t s);
-void slab_store(const double2* out, SlabGeom g, float2* value, cudaStream_t s);
-/// out[slab] -= sub[slab].
-void slab_sub(float2* out, SlabGeom g, const float2* sub, cudaStream_t s);
+/// A list of slabs of one SlabGeom (start/extent per entry) for the batched
+/// copies: hits read `value[q]` scaled by `scale[q]`, stores write `dst[q]`.
+constexpr int kSlabBatch = 64;
+struct SlabBatch {
+  std::int64_t start[kSlabBatch];
+  std::int64_t extent[kSlabBatch];
+  const float2* value[kSlabBatch];
+  float2* dst[kSlabBatch];
+  double scale[kSlabBatch];
+};
+
+/// out[slab_q] = value_q * scale_q - sub[slab_q] for every listed slab (sub may
+/// be null) (scalerun.cpp:250-255).
+void slab_materialize(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s);
+void slab_materialize(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream_t s);
+/// dst_q = out[slab_q] (contiguous chunk order, complex64; dst_q may be null)
+/// and then out[slab_q] -= sub[slab_q] when sub is set (scalerun.cpp:276-283).
+void slab_store(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s);
+void slab_store(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream_t s);
 
 }  // namespace ops
 }  // namespace mlrg

@@ -37,6 +37,9 @@ class ValueArena {
  public:
   explicit ValueArena(std::size_t chunk_bytes = std::size_t{1} << 30) : chunk_(chunk_bytes) {}
   float2* alloc(std::int64_t count);
+  /// Maps `bytes` of HBM up front (one allocation) so the solve itself never
+  /// calls cudaMalloc (which maps and clears pages at ~30 ms/GiB on B200).
+  void reserve(std::size_t bytes);
   std::size_t bytes_used() const { return used_; }
 
  private:

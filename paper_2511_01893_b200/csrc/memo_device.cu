@@ -12,8 +12,6 @@ namespace mlrg::ops {
 
 namespace {
 
-constexpr int kEncThreads = 256;
-constexpr int kChunk = 32;   // K elements per smem stage
 constexpr int kMaxSlabs = 64;
 constexpr int kRows = 64;    // key rows padded (key_dim <= 64)
 
@@ -30,149 +28,262 @@ __device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long st
   return (i * g.d1 + start + kl) * g.d2 + (rem - kl * g.d2);
 }
 
-// Split-K GEMM keys[s][r] = sum_k P[r][k] X[s][k] over K = 2n, with P stored
-// interleaved on the device (column 2i weights Re x_i, 2i+1 weights Im x_i;
-// the reference's row layout is [re block | im block], encoder.cpp:414-419).
-// Thread (ty, tx) owns slabs {ty + 16 q} x rows {tx + 16 p}
-// (q < SG, p < 4); each CTA walks K chunks grid-stride and writes its double
-// partial tile. The first row slot past kd accumulates |x|^2.
-template <int SG, class TX>
-__global__ void __launch_bounds__(kEncThreads) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
-                                                        const float* __restrict__ P, long long n, int kd,
-                                                        double* __restrict__ part) {
-  __shared__ float xs[kChunk][16 * SG + 1];
-  __shared__ float ps[kChunk][kRows + 1];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[SG][4];
-  double nrm_acc[SG];
-#pragma unroll
-  for (int q = 0; q < SG; ++q) {
-    nrm_acc[q] = 0.0;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) acc[q][p] = 0.0;
+// Split-K skinny GEMM keys[s][r] = sum_k P[r][k] X[s][k] over K = 2n for up
+// to 16 slabs per launch, with P in the reference's row layout but interleaved
+// columns (column 2i weights Re x_i, 2i+1 weights Im x_i; the reference's row
+// is [re block | im block], encoder.cpp:414-419). The GEMM is HBM-bound on
+// streaming P (60 x 2n floats) once per call.
+//
+// Every warp owns 32-column chunks of K (grid-stride over warps) and stages
+// them in warp-private double-buffered shared memory: P by cp.async (60 rows x
+// 128 B), x through registers (converted to float once). Lane (sg, rg) holds a
+// 4-slab x 8-row register tile (rows rg, rg+8, ..., rg+56): per pair of K
+// columns 2 LDS.128 (x) + 8 LDS.64 (P) feed 64 FMAs. Products are summed in
+// float within a chunk and in double across chunks (the reference accumulates
+// in double, encoder.cpp:416-420); slot kd of each slab carries sum |x|^2.
+constexpr int kEncWarps = 4;
+constexpr int kPStride = 36;  // floats per staged P row: 16 B aligned, conflict-free LDS.64 across rg
+struct EncStage {
+  float x[32][16];           // [column kk][slab]
+  float p[kRows][kPStride];  // [row][column kk]
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+
+template <class TX>
+__global__ void __launch_bounds__(kEncWarps * 32) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
+                                                           const float* __restrict__ P, long long n, int kd,
+                                                           bool p_vec, double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char enc_smem[];
+  EncStage(*stage)[2] = reinterpret_cast<EncStage(*)[2]>(enc_smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sg = lane >> 3, rg = lane & 7;
+  EncStage* st = stage[warp];
+  // rows >= kd stay zero in both buffers
+  for (int e = lane; e < 2 * (kRows - kd) * kPStride; e += 32) {
+    const int b = e / ((kRows - kd) * kPStride), r = e % ((kRows - kd) * kPStride);
+    st[b].p[kd + r / kPStride][r % kPStride] = 0.f;
   }
   const long long K = 2 * n;
-  const long long nchunks = (K + kChunk - 1) / kChunk;
-  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const long long k0 = ch * kChunk;
-    for (int e = threadIdx.x; e < (kChunk / 2) * 16 * SG; e += blockDim.x) {
-      const int s = e / (kChunk / 2), ee = e - s * (kChunk / 2);
-      const long long ce = k0 / 2 + ee;
-      float xr = 0.f, xi = 0.f;
-      if (s < ns && ce < n) {
-        const TX xv = x[slab_offset(g, sl.start[s], ce)];
-        xr = static_cast<float>(xv.x);
-        xi = static_cast<float>(xv.y);
+  const long long nchunks = (K + 31) / 32;
+  const long long gw = static_cast<long long>(blockIdx.x) * kEncWarps + warp;
+  const long long W = static_cast<long long>(gridDim.x) * kEncWarps;
+  // x staging: lane owns complex element e = lane & 15 of slabs (lane >> 4) + 2j
+  const int xe = lane & 15, xs0 = lane >> 4;
+  float2 xr[8];
+  auto load_x = [&](long long ch) {
+    const long long ce = ch * 16 + xe;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int sidx = xs0 + 2 * j;
+      xr[j] = make_float2(0.f, 0.f);
+      if (sidx < ns && ce < n) {
+        const TX v = x[slab_offset(g, sl.start[sidx], ce)];
+        xr[j] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
       }
-      xs[2 * ee][s] = xr;
-      xs[2 * ee + 1][s] = xi;
     }
-    for (int e = threadIdx.x; e < kChunk * kRows; e += blockDim.x) {
-      const int r = e / kChunk, kk = e - r * kChunk;
-      const long long k = k0 + kk;
-      ps[kk][r] = (r < kd && k < K) ? P[static_cast<long long>(r) * K + k] : 0.f;
+  };
+  auto store_x = [&](EncStage& b) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      b.x[2 * xe][xs0 + 2 * j] = xr[j].x;
+      b.x[2 * xe + 1][xs0 + 2 * j] = xr[j].y;
     }
-    __syncthreads();
-    float fa[SG][4];
-    float fn[SG];
+  };
+  auto load_p = [&](EncStage& b, long long ch) {
+    const long long k0 = ch * 32;
+    if (p_vec) {  // 8 x 16 B per row
+      for (int e = lane; e < kd * 8; e += 32) {
+        const int r = e >> 3, q = e & 7;
+        const long long k = k0 + 4 * q;
+        const int bytes = k >= K ? 0 : static_cast<int>(min(16LL, (K - k) * 4));
+        cp_async16z(&b.p[r][4 * q], P + (bytes ? static_cast<long long>(r) * K + k : 0), bytes);
+      }
+    } else {
+      const long long k = k0 + lane;
+      const int bytes = k < K ? 4 : 0;
+      for (int r = 0; r < kd; ++r) cp_async4(&b.p[r][lane], P + (bytes ? static_cast<long long>(r) * K + k : 0), bytes);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  double acc[4][8], nrm[4];
 #pragma unroll
-    for (int q = 0; q < SG; ++q) {
-      fn[q] = 0.f;
+  for (int a = 0; a < 4; ++a) {
+    nrm[a] = 0.0;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) fa[q][p] = 0.f;
+    for (int i = 0; i < 8; ++i) acc[a][i] = 0.0;
+  }
+  int buf = 0;
+  if (gw < nchunks) {
+    load_p(st[0], gw);
+    load_x(gw);
+    store_x(st[0]);
+  }
+  for (long long ch = gw; ch < nchunks; ch += W) {
+    const bool more = ch + W < nchunks;
+    if (more) {
+      load_p(st[buf ^ 1], ch + W);
+      load_x(ch + W);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncwarp();
+    const EncStage& b = st[buf];
+    float fa[4][8], fn[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      fn[a] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fa[a][i] = 0.f;
     }
 #pragma unroll 4
-    for (int kk = 0; kk < kChunk; ++kk) {
-      float xv[SG], pv[4];
+    for (int kk = 0; kk < 32; kk += 2) {
+      const float4 x0 = *reinterpret_cast<const float4*>(&b.x[kk][4 * sg]);
+      const float4 x1 = *reinterpret_cast<const float4*>(&b.x[kk + 1][4 * sg]);
+      const float xa0[4] = {x0.x, x0.y, x0.z, x0.w}, xa1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-      for (int q = 0; q < SG; ++q) xv[q] = xs[kk][ty + 16 * q];
+      for (int i = 0; i < 8; ++i) {
+        const float2 pv = *reinterpret_cast<const float2*>(&b.p[8 * i + rg][kk]);
 #pragma unroll
-      for (int p = 0; p < 4; ++p) pv[p] = ps[kk][tx + 16 * p];
-#pragma unroll
-      for (int q = 0; q < SG; ++q) {
-#pragma unroll
-        for (int p = 0; p < 4; ++p) fa[q][p] = fmaf(pv[p], xv[q], fa[q][p]);
-        fn[q] = fmaf(xv[q], xv[q], fn[q]);
+        for (int a = 0; a < 4; ++a) fa[a][i] = fmaf(pv.y, xa1[a], fmaf(pv.x, xa0[a], fa[a][i]));
       }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) fn[a] = fmaf(xa1[a], xa1[a], fmaf(xa0[a], xa0[a], fn[a]));
     }
 #pragma unroll
-    for (int q = 0; q < SG; ++q) {
-      nrm_acc[q] += fn[q];
+    for (int a = 0; a < 4; ++a) {
+      nrm[a] += fn[a];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) acc[q][p] += fa[q][p];
+      for (int i = 0; i < 8; ++i) acc[a][i] += fa[a][i];
     }
-    __syncthreads();
+    __syncwarp();
+    if (more) store_x(st[buf ^ 1]);
+    buf ^= 1;
   }
-  // partial tile layout: [block][slab][kd + 1]
+  // CTA reduction over warps (fixed order) into the partial tile [block][slab][kd + 1]
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(enc_smem);  // [warp][16][kRows + 1]
+  constexpr int kRS = kRows + 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[(warp * 16 + 4 * sg + a) * kRS + 8 * i + rg] = acc[a][i];
+    if (rg == 0) red[(warp * 16 + 4 * sg + a) * kRS + kRows] = nrm[a];
+  }
+  __syncthreads();
   double* pb = part + static_cast<long long>(blockIdx.x) * ns * (kd + 1);
-#pragma unroll
-  for (int q = 0; q < SG; ++q) {
-    const int s = ty + 16 * q;
-    if (s >= ns) continue;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = tx + 16 * p;
-      if (r < kd) pb[s * (kd + 1) + r] = acc[q][p];
-    }
-    if (tx == 0) pb[s * (kd + 1) + kd] = nrm_acc[q];
+  for (int e = threadIdx.x; e < ns * (kd + 1); e += blockDim.x) {
+    const int slab = e / (kd + 1), r = e - slab * (kd + 1);
+    const int col = r < kd ? r : kRows;
+    double v = 0.0;
+    for (int w = 0; w < kEncWarps; ++w) v += red[(w * 16 + slab) * kRS + col];
+    pb[e] = v;
   }
 }
 
+// One warp per output value: lanes stride over the CTA partials, then a fixed
+// shuffle tree (deterministic).
 __global__ void k_encode_reduce(const double* __restrict__ part, int nblocks, int ns, int kd,
                                 float* __restrict__ keys, double* __restrict__ norms2) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int per = ns * (kd + 1);
   if (e >= per) return;
   double s = 0.0;
-  for (int b = 0; b < nblocks; ++b) s += part[static_cast<long long>(b) * per + e];
+  for (int b = lane; b < nblocks; b += 32) s += part[static_cast<long long>(b) * per + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
   const int slab = e / (kd + 1), r = e - slab * (kd + 1);
   if (r < kd) keys[slab * kd + r] = static_cast<float>(s);
   else norms2[slab] = s;
 }
 
+// Slab copies between full arrays and the value arena, batched: blockIdx.y
+// selects the slab of the list, blockIdx.x strides over its elements.
+// A slab is `runs` contiguous runs of `run_len` elements in the full array
+// (axis 0: extent planes; axis 1: one run of extent*d2 per index of axis 0),
+// stored back to back in the value.
+constexpr long long kSeg = 4096;  // elements per block iteration
+struct SlabRuns {
+  long long runs, run_len, first, stride;  // run r starts at first + r * stride
+};
+__device__ __forceinline__ SlabRuns slab_runs(const SlabGeom& g, long long start, long long extent) {
+  if (g.axis == 0) return {extent, g.d1 * g.d2, start * g.d1 * g.d2, g.d1 * g.d2};
+  return {g.d0, extent * g.d2, start * g.d2, g.d1 * g.d2};
+}
+
+// Slab copies between full arrays and the value arena, batched: blockIdx.y
+// selects the slab of the list; warps stride over (run, element) pairs.
 template <class TO>
-__global__ void k_slab_materialize(TO* __restrict__ out, SlabGeom g, const float2* __restrict__ value, double scale,
-                                   const float2* __restrict__ sub) {
-  const long long n = g.count();
-  for (long long ce = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ce < n;
-       ce += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long o = slab_offset(g, g.start, ce);
-    const float2 v = value[ce];
-    double re = v.x * scale, im = v.y * scale;
-    if (sub) {
-      re -= sub[o].x;
-      im -= sub[o].y;
+__global__ void __launch_bounds__(256) k_slab_materialize(TO* __restrict__ out, SlabGeom g, SlabBatch b,
+                                                          const float2* __restrict__ sub) {
+  const int q = blockIdx.y;
+  const SlabRuns sr = slab_runs(g, b.start[q], b.extent[q]);
+  const float2* __restrict__ value = b.value[q];
+  const double scale = b.scale[q];
+  const long long segs = (sr.run_len + kSeg - 1) / kSeg;
+  for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
+    const long long r = t / segs, e0 = (t - r * segs) * kSeg;
+    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
+    const long long e1 = min(sr.run_len, e0 + kSeg);
+    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const long long o = o0 + e;
+      const float2 v = value[v0 + e];
+      double re = v.x * scale, im = v.y * scale;
+      if (sub) {
+        const float2 sv = sub[o];
+        re -= sv.x;
+        im -= sv.y;
+      }
+      TO res;
+      res.x = static_cast<decltype(res.x)>(re);
+      res.y = static_cast<decltype(res.y)>(im);
+      out[o] = res;
     }
-    out[o].x = static_cast<decltype(out[o].x)>(re);
-    out[o].y = static_cast<decltype(out[o].y)>(im);
   }
 }
 
+// value = out[slab] and, when `sub` is set, out[slab] -= sub[slab] afterwards
+// (the fused op stores the linear part and keeps out = fu2d(v) - d_hat).
 template <class TO>
-__global__ void k_slab_store(const TO* __restrict__ out, SlabGeom g, float2* __restrict__ value) {
-  const long long n = g.count();
-  for (long long ce = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ce < n;
-       ce += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const TO v = out[slab_offset(g, g.start, ce)];
-    value[ce] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
-  }
-}
-
-__global__ void k_slab_sub(float2* __restrict__ out, SlabGeom g, const float2* __restrict__ sub) {
-  const long long n = g.count();
-  for (long long ce = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; ce < n;
-       ce += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long o = slab_offset(g, g.start, ce);
-    out[o] = csub(out[o], sub[o]);
+__global__ void __launch_bounds__(256) k_slab_store(TO* __restrict__ out, SlabGeom g, SlabBatch b,
+                                                    const float2* __restrict__ sub) {
+  const int q = blockIdx.y;
+  const SlabRuns sr = slab_runs(g, b.start[q], b.extent[q]);
+  float2* __restrict__ value = b.dst[q];
+  const long long segs = (sr.run_len + kSeg - 1) / kSeg;
+  for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
+    const long long r = t / segs, e0 = (t - r * segs) * kSeg;
+    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
+    const long long e1 = min(sr.run_len, e0 + kSeg);
+    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const long long o = o0 + e;
+      const TO v = out[o];
+      if (value) value[v0 + e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+      if constexpr (sizeof(TO) == sizeof(float2)) {
+        if (sub) out[o] = csub(v, sub[o]);
+      }
+    }
   }
 }
 
 int enc_blocks() { return 2 * sm_count(); }
+constexpr int kEncSlabs = 16;  // slabs per launch (one 4 x 8 register tile per lane)
 
 }  // namespace
 
 std::size_t encode_work_doubles(int ns, int kd) {
-  return static_cast<std::size_t>(enc_blocks()) * static_cast<std::size_t>(std::min(ns, kMaxSlabs)) *
+  return static_cast<std::size_t>(enc_blocks()) * static_cast<std::size_t>(std::min(ns, kEncSlabs)) *
          static_cast<std::size_t>(kd + 1);
 }
 
@@ -182,19 +293,26 @@ void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns
                  double* work, float* keys, double* norms2, cudaStream_t s) {
   if (kd > kRows - 1) throw std::invalid_argument("encode: key_dim must be < 64");
   const long long n = shape.count();
-  for (int b = 0; b < ns; b += kMaxSlabs) {
-    const int nb = std::min(kMaxSlabs, ns - b);
+  constexpr std::size_t smem = sizeof(EncStage) * 2 * kEncWarps;
+  static_assert(smem >= sizeof(double) * kEncWarps * 16 * (kRows + 1), "reduction scratch must fit");
+  static bool attr = false;
+  if (!attr) {
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const bool p_vec = (2 * n) % 4 == 0 && reinterpret_cast<std::uintptr_t>(P) % 16 == 0;
+  for (int b = 0; b < ns; b += kEncSlabs) {
+    const int nb = std::min(kEncSlabs, ns - b);
     SlabList sl{};
     for (int q = 0; q < nb; ++q) sl.start[q] = starts[b + q];
     const int blocks = enc_blocks();
     prof::begin("k_encode", s);
-    if (nb <= 16) k_encode<1, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
-    else if (nb <= 32) k_encode<2, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
-    else k_encode<4, TX><<<blocks, kEncThreads, 0, s>>>(x, shape, sl, nb, P, n, kd, work);
+    k_encode<TX><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
     MLRG_LAUNCH_CHECK("k_encode");
     prof::end("k_encode", s);
     const int per = nb * (kd + 1);
-    k_encode_reduce<<<(per + 255) / 256, 256, 0, s>>>(work, blocks, nb, kd, keys + b * kd, norms2 + b);
+    k_encode_reduce<<<(per * 32 + 255) / 256, 256, 0, s>>>(work, blocks, nb, kd, keys + b * kd, norms2 + b);
     MLRG_LAUNCH_CHECK("k_encode_reduce");
   }
 }
@@ -210,29 +328,37 @@ void encode(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns
   encode_impl(x, shape, starts, ns, P, kd, work, keys, norms2, s);
 }
 
-void slab_materialize(float2* out, SlabGeom g, const float2* value, double scale, const float2* sub, cudaStream_t s) {
-  k_slab_materialize<float2><<<2 * sm_count(), 256, 0, s>>>(out, g, value, scale, sub);
+namespace {
+dim3 batch_grid(int nb) {
+  return dim3(static_cast<unsigned>(std::max(1, 8 * sm_count() / std::max(nb, 1))), static_cast<unsigned>(nb));
+}
+template <class TO>
+void materialize_impl(TO* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {
+  if (nb <= 0) return;
+  if (nb > kSlabBatch) throw std::logic_error("slab batch too large");
+  k_slab_materialize<TO><<<batch_grid(nb), 256, 0, s>>>(out, g, b, sub);
   MLRG_LAUNCH_CHECK("k_slab_materialize");
 }
-
-void slab_materialize(double2* out, SlabGeom g, const float2* value, double scale, cudaStream_t s) {
-  k_slab_materialize<double2><<<2 * sm_count(), 256, 0, s>>>(out, g, value, scale, nullptr);
-  MLRG_LAUNCH_CHECK("k_slab_materialize");
-}
-
-void slab_store(const float2* out, SlabGeom g, float2* value, cudaStream_t s) {
-  k_slab_store<float2><<<2 * sm_count(), 256, 0, s>>>(out, g, value);
+template <class TO>
+void store_impl(TO* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {
+  if (nb <= 0) return;
+  if (nb > kSlabBatch) throw std::logic_error("slab batch too large");
+  k_slab_store<TO><<<batch_grid(nb), 256, 0, s>>>(out, g, b, sub);
   MLRG_LAUNCH_CHECK("k_slab_store");
 }
+}  // namespace
 
-void slab_store(const double2* out, SlabGeom g, float2* value, cudaStream_t s) {
-  k_slab_store<double2><<<2 * sm_count(), 256, 0, s>>>(out, g, value);
-  MLRG_LAUNCH_CHECK("k_slab_store");
+void slab_materialize(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {
+  materialize_impl(out, g, b, nb, sub, s);
 }
-
-void slab_sub(float2* out, SlabGeom g, const float2* sub, cudaStream_t s) {
-  k_slab_sub<<<2 * sm_count(), 256, 0, s>>>(out, g, sub);
-  MLRG_LAUNCH_CHECK("k_slab_sub");
+void slab_materialize(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream_t s) {
+  materialize_impl(out, g, b, nb, static_cast<const float2*>(nullptr), s);
+}
+void slab_store(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {
+  store_impl(out, g, b, nb, sub, s);
+}
+void slab_store(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream_t s) {
+  store_impl(out, g, b, nb, static_cast<const float2*>(nullptr), s);
 }
 
 }  // namespace mlrg::ops

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -150,9 +151,12 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
                   enc_norms_.get() + c0, s_);
     c0 = c1;
   }
-  MLRG_CUDA(cudaMemcpyAsync(keys_host_.get(), enc_keys_.get(), sizeof(float) * n * kd, cudaMemcpyDeviceToHost, s_));
-  MLRG_CUDA(cudaMemcpyAsync(norms_host_.get(), enc_norms_.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s_));
-  MLRG_CUDA(cudaStreamSynchronize(s_));
+  {
+    prof::HostSpan span("host:memo_key_sync");
+    MLRG_CUDA(cudaMemcpyAsync(keys_host_.get(), enc_keys_.get(), sizeof(float) * n * kd, cudaMemcpyDeviceToHost, s_));
+    MLRG_CUDA(cudaMemcpyAsync(norms_host_.get(), enc_norms_.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s_));
+    MLRG_CUDA(cudaStreamSynchronize(s_));
+  }
 
   std::vector<MemoKey> keys(static_cast<std::size_t>(n));
   std::vector<std::size_t> value_bytes(static_cast<std::size_t>(n));
@@ -170,7 +174,11 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     out_counts[static_cast<std::size_t>(c)] = oc;
     value_bytes[static_cast<std::size_t>(c)] = 8 + static_cast<std::size_t>(oc) * 16;
   }
-  const std::vector<MemoDecision> dec = memo_->lookup_batch(keys, value_bytes);
+  std::vector<MemoDecision> dec;
+  {
+    prof::HostSpan span("host:memo_lookup");
+    dec = memo_->lookup_batch(keys, value_bytes);
+  }
 
   // ---- misses: computed in contiguous runs (linear fu2d for fused, d_hat after staging) ----
   for (int c0 = 0; c0 < n;) {
@@ -185,42 +193,60 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     compute(op, false, in, in_d, nullptr, out, out_d, starts[static_cast<std::size_t>(c0)], extent);
     c0 = c1;
   }
-  // ---- hits: value * (live norm / stored norm), minus the live d_hat slab when fused ----
+  // ---- hits: value * (live norm / stored norm), minus the live d_hat slab when fused (one launch) ----
+  const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, 0, 0};
+  auto batch = std::make_unique<ops::SlabBatch>();
+  int nb = 0;
+  auto flush_hits = [&]() {
+    if (out_d) ops::slab_materialize(static_cast<double2*>(out), og, *batch, nb, s_);
+    else ops::slab_materialize(static_cast<float2*>(out), og, *batch, nb, fused ? d_hat : nullptr, s_);
+    nb = 0;
+  };
   for (int c = 0; c < n; ++c) {
     const MemoDecision& d = dec[static_cast<std::size_t>(c)];
-    const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)],
-                           ext[static_cast<std::size_t>(c)]};
     if (d.outcome != MemoOutcome::miss) {
       const ValueRef& v = memo_->store().value(d.value_id);
       const double live = in_norms[static_cast<std::size_t>(c)];
-      const double scale = (v.norm > 0.0 && live > 0.0) ? live / v.norm : 1.0;
-      if (out_d) ops::slab_materialize(static_cast<double2*>(out), og, v.dev, scale, s_);
-      else ops::slab_materialize(static_cast<float2*>(out), og, v.dev, scale, fused ? d_hat : nullptr, s_);
+      batch->start[nb] = starts[static_cast<std::size_t>(c)];
+      batch->extent[nb] = ext[static_cast<std::size_t>(c)];
+      batch->value[nb] = v.dev;
+      batch->scale[nb] = (v.norm > 0.0 && live > 0.0) ? live / v.norm : 1.0;
+      if (++nb == ops::kSlabBatch) flush_hits();
     }
     audit_.push_back(ChunkAudit{op, axis, c, ext[static_cast<std::size_t>(c)], d.outcome, d.cs, iteration_, -1.0f});
   }
-  // ---- stage the miss values (the linear part for fused), then apply d_hat ----
+  flush_hits();
+  // ---- stage the miss values (the linear part for fused), then apply d_hat (one launch) ----
+  auto flush_stores = [&]() {
+    if (out_d) ops::slab_store(static_cast<double2*>(out), og, *batch, nb, s_);
+    else ops::slab_store(static_cast<float2*>(out), og, *batch, nb, fused ? d_hat : nullptr, s_);
+    nb = 0;
+  };
   for (int c = 0; c < n; ++c) {
     if (dec[static_cast<std::size_t>(c)].outcome != MemoOutcome::miss) continue;
-    const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, starts[static_cast<std::size_t>(c)],
-                           ext[static_cast<std::size_t>(c)]};
+    float2* dst = nullptr;
     memo_->insert_async(keys[static_cast<std::size_t>(c)], [&]() {
       ValueRef v;
       v.count = out_counts[static_cast<std::size_t>(c)];
-      float2* dst = memo_->store().arena().alloc(v.count);
-      if (out_d) ops::slab_store(static_cast<const double2*>(out), og, dst, s_);
-      else ops::slab_store(static_cast<const float2*>(out), og, dst, s_);
+      prof::HostSpan span("host:memo_alloc");
+      dst = memo_->store().arena().alloc(v.count);
       v.dev = dst;
       v.norm = in_norms[static_cast<std::size_t>(c)];
       v.bytes = value_bytes[static_cast<std::size_t>(c)];
       return v;
     });
-    if (fused) ops::slab_sub(static_cast<float2*>(out), og, d_hat, s_);
+    if (!dst && !fused) continue;  // dropped insert, nothing to do for this slab
+    batch->start[nb] = starts[static_cast<std::size_t>(c)];
+    batch->extent[nb] = ext[static_cast<std::size_t>(c)];
+    batch->dst[nb] = dst;
+    if (++nb == ops::kSlabBatch) flush_stores();
   }
+  flush_stores();
   if (cfg_.flush_after_apply) memo_->flush_inserts();
 }
 
 void Engine::flush_inserts() {
+  prof::HostSpan span("host:memo_flush");
   if (memo_) memo_->flush_inserts();
 }
 

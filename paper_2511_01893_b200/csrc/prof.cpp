@@ -2,6 +2,7 @@
 // are recorded on the launching stream, so a timer measures exactly the
 // kernel's device time span even when the host runs ahead.
 #include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
@@ -29,7 +30,28 @@ std::map<std::string, cudaEvent_t>& open_events() {
   static std::map<std::string, cudaEvent_t> m;
   return m;
 }
+std::map<std::string, std::pair<double, std::int64_t>>& host_spans() {
+  static std::map<std::string, std::pair<double, std::int64_t>> m;
+  return m;
+}
 }  // namespace
+
+void host_add(const char* name, double ms) {
+  if (!enabled()) return;
+  std::lock_guard<std::mutex> lk(g_mx);
+  auto& e = host_spans()[name];
+  e.first += ms;
+  ++e.second;
+}
+
+HostSpan::HostSpan(const char* name)
+    : name_(name), t0_(enabled() ? std::chrono::steady_clock::now().time_since_epoch().count() : 0) {}
+HostSpan::~HostSpan() {
+  if (!t0_) return;
+  const long long t1 = std::chrono::steady_clock::now().time_since_epoch().count();
+  host_add(name_, static_cast<double>(t1 - t0_) * 1e3 * std::chrono::steady_clock::period::num /
+                      std::chrono::steady_clock::period::den);
+}
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool enabled() { return g_enabled.load(std::memory_order_relaxed); }
@@ -71,12 +93,19 @@ void mlrg_prof_reset(void) {
       cudaEventDestroy(s.b);
     }
   mlrg::prof::spans().clear();
+  mlrg::prof::host_spans().clear();
 }
 
 int mlrg_prof_query(const char* name, double* total_ms, int64_t* count) {
   std::lock_guard<std::mutex> lk(mlrg::prof::g_mx);
   double tot = 0.0;
   int64_t n = 0;
+  auto ht = mlrg::prof::host_spans().find(name ? name : "");
+  if (ht != mlrg::prof::host_spans().end()) {  // host-side phase ("host:..."): wall ms
+    if (total_ms) *total_ms = ht->second.first;
+    if (count) *count = ht->second.second;
+    return 0;
+  }
   auto it = mlrg::prof::spans().find(name ? name : "");
   if (it != mlrg::prof::spans().end())
     for (auto& s : it->second) {

@@ -7,6 +7,7 @@ for `ncu --profile-from-start off` (launch lists and --set full captures).
 import argparse
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -31,18 +32,26 @@ def main():
     ctx.forward_L(ph, d)
     ctx.sync()
     del ctx
-    cfg = (f"n1={n}\nn0={n}\nn2={n}\nn_theta={n}\nh={n}\nw={n}\nn_outer=1000\nmemoization={a.memo}\n"
+    cfg = (f"n1={n}\nn0={n}\nn2={n}\nn_theta={n}\nh={n}\nw={n}\nn_outer={a.warmup + a.steps}\nmemoization={a.memo}\n"
            f"nudft_path=gridding\ngridding_kernel={a.kernel}\n")
     s = m.Solver(cfg, d, reference=ph, stream=stream.cuda_stream)
     for _ in range(a.warmup):
         s.step()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
+    m.lib().mlrg_prof_reset()
+    m.lib().mlrg_prof_enable(1)
     for _ in range(a.steps):
+        t0 = time.perf_counter()
         s.step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        print(f"step {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
     torch.cuda.cudart().cudaProfilerStop()
-    print("profiled", a.steps, "step(s) at", n)
+    m.lib().mlrg_prof_enable(0)
+    for k in ("host:memo_key_sync", "host:memo_lookup", "host:memo_alloc", "host:memo_flush", "k_encode"):
+        tot, cnt = m.prof_query(k)
+        print(f"{k}: {tot:.2f} ms over {cnt}")
+    print("profiled", a.steps, "step(s) at", n, s.counters())
 
 
 if __name__ == "__main__":
