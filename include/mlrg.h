@@ -96,6 +96,31 @@ int mlrg_solver_counters(const mlrg_solver* s, uint64_t out[11]);
 int64_t mlrg_solver_audit(const mlrg_solver* s, int32_t* meta4, float* cs, int64_t cap);
 void mlrg_solver_free(mlrg_solver* s);
 
+/* ---- z-slab sharded solver across the GPUs of one node ----
+ * One process per GPU. mlrg_comm_create joins the node-local communicator
+ * `name` (POSIX shared memory; rank 0 creates it, every rank passes the same
+ * name and world; blocks until all ranks joined or timeout_s). Pure host: no
+ * CUDA calls. The sharded solver splits the volume along axis 0 and the
+ * detector rows along axis 1 in whole 16-slabs with the reference's assign()
+ * (scalerun.cpp:14-27); d and reference are the FULL arrays on every rank's
+ * device; mlrg_solver_volume then returns this rank's planes [a, b) and
+ * mlrg_solver_shard reports {a, b, c, d}. The CSV, counters and audit are the
+ * global ones on every rank. A comm of world 1 (or NULL) is mlrg_solver_new. */
+typedef struct mlrg_comm mlrg_comm;
+mlrg_comm* mlrg_comm_create(const char* name, int rank, int world, double timeout_s);
+void mlrg_comm_free(mlrg_comm* c);
+int mlrg_comm_barrier(mlrg_comm* c);
+/* v[i] = sum over ranks, added in rank order (bit-identical on every rank). */
+int mlrg_comm_allreduce(mlrg_comm* c, double* v, int n);
+/* out = every rank's `bytes` bytes, concatenated in rank order (bytes <= 1 MiB). */
+int mlrg_comm_allgather(mlrg_comm* c, const void* in, uint64_t bytes, void* out);
+/* Per rank r: out[4r..4r+3] = {a, b, c, d}: planes [a, b) of axis 0 (n1) and
+ * detector rows [c, d) of axis 1 (h). */
+int mlrg_partition(int64_t n1, int64_t h, int64_t chunk, int world, int64_t* out);
+mlrg_solver* mlrg_solver_new_sharded(const char* config_text, const void* d, const void* reference, void* stream,
+                                     mlrg_comm* comm);
+int mlrg_solver_shard(const mlrg_solver* s, int64_t out[4]);
+
 /* ---- host memo decision logic (memoclient.cpp + memostore.cpp), for replay tests ---- */
 mlrg_memo* mlrg_memo_new(float tau, int nprobe, uint64_t insert_cap, uint64_t coalesce_bytes, int global_cache,
                          int nlist, int train_size);

@@ -97,6 +97,14 @@ _SIGS = {
     "mlrg_solver_counters": (C.c_int, [_P, _P]),
     "mlrg_solver_audit": (_I64, [_P, _P, _P, _I64]),
     "mlrg_solver_free": (None, [_P]),
+    "mlrg_solver_new_sharded": (_P, [C.c_char_p, _P, _P, _P, _P]),
+    "mlrg_solver_shard": (C.c_int, [_P, _P]),
+    "mlrg_comm_create": (_P, [C.c_char_p, C.c_int, C.c_int, _D]),
+    "mlrg_comm_free": (None, [_P]),
+    "mlrg_comm_barrier": (C.c_int, [_P]),
+    "mlrg_comm_allreduce": (C.c_int, [_P, _P, C.c_int]),
+    "mlrg_comm_allgather": (C.c_int, [_P, _P, _U64, _P]),
+    "mlrg_partition": (C.c_int, [_I64, _I64, _I64, C.c_int, _P]),
     "mlrg_memo_new": (_P, [C.c_float, C.c_int, _U64, _U64, C.c_int, C.c_int, C.c_int]),
     "mlrg_memo_free": (None, [_P]),
     "mlrg_memo_lookup": (C.c_int, [_P, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
@@ -418,13 +426,73 @@ def reconstruct_device(config_text: str, d, u_out, reference=None, stream=None) 
     return DeviceRecon(h)
 
 
-class Solver:
-    """mlrg_solver: the ADMM outer loop on the device, one outer iteration per step()."""
+class Comm:
+    """mlrg_comm: the node-local communicator of the sharded solver (one process
+    per GPU; every rank passes the same `name` and `world`)."""
 
-    def __init__(self, config_text: str, d, reference=None, stream=None):
-        self._h = lib().mlrg_solver_new(config_text.encode(), _dp(d), _dp(reference), _default_stream(stream))
+    def __init__(self, name: str, rank: int, world: int, timeout_s: float = 120.0):
+        self.rank, self.world = rank, world
+        self._h = lib().mlrg_comm_create(name.encode(), rank, world, timeout_s)
         if not self._h:
             raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
+
+    @classmethod
+    def from_torch(cls, timeout_s: float = 120.0):
+        """Joins with the ranks of the default torch.distributed group (any backend):
+        rank 0 picks a fresh segment name and broadcasts it."""
+        import os
+        import uuid
+
+        import torch.distributed as dist
+
+        name = [f"mlrg-{os.getpid()}-{uuid.uuid4().hex[:12]}" if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(name, src=0)
+        return cls(name[0], dist.get_rank(), dist.get_world_size(), timeout_s)
+
+    def barrier(self):
+        _gcheck(lib().mlrg_comm_barrier(self._h))
+
+    def allreduce(self, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _gcheck(lib().mlrg_comm_allreduce(self._h, v.ctypes.data, v.size))
+        return v
+
+    def allgather(self, b: bytes) -> list:
+        out = C.create_string_buffer(len(b) * self.world)
+        _gcheck(lib().mlrg_comm_allgather(self._h, b, len(b), out))
+        raw = out.raw
+        return [raw[r * len(b):(r + 1) * len(b)] for r in range(self.world)]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.mlrg_comm_free(self._h)
+            self._h = None
+
+
+def partition(n1: int, h: int, world: int, chunk: int = 16) -> np.ndarray:
+    """[world, 4] = per rank {a, b, c, d}: planes [a, b) and detector rows [c, d)
+    (the reference's assign() over 16-slabs, scalerun.cpp:14-27)."""
+    out = np.zeros((world, 4), np.int64)
+    _gcheck(lib().mlrg_partition(n1, h, chunk, world, out.ctypes.data))
+    return out
+
+
+class Solver:
+    """mlrg_solver: the ADMM outer loop on the device, one outer iteration per step().
+    With `comm` (world > 1) the solve is z-slab sharded: d and reference are the full
+    arrays on this rank's device, volume() returns this rank's planes (shard())."""
+
+    def __init__(self, config_text: str, d, reference=None, stream=None, comm: "Comm" = None):
+        self._comm = comm  # keep the communicator alive as long as the solver
+        self._h = lib().mlrg_solver_new_sharded(config_text.encode(), _dp(d), _dp(reference),
+                                                _default_stream(stream), comm._h if comm else None)
+        if not self._h:
+            raise MlrError(MLR_ERR_RUNTIME, (lib().mlrg_last_error() or b"").decode())
+
+    def shard(self):
+        out = np.zeros(4, np.int64)
+        _gcheck(lib().mlrg_solver_shard(self._h, out.ctypes.data))
+        return tuple(int(x) for x in out)
 
     def step(self) -> bool:
         ab = C.c_int(0)
@@ -458,6 +526,7 @@ class Solver:
         if getattr(self, "_h", None) and _LIB is not None:
             _LIB.mlrg_solver_free(self._h)
             self._h = None
+        self._comm = None
 
 
 class Memo:

@@ -63,6 +63,9 @@ struct mlrg_solver {
     if (own) cudaStreamDestroy(own);
   }
 };
+struct mlrg_comm {
+  std::shared_ptr<mlrg::HostComm> c;
+};
 struct mlrg_memo {
   std::shared_ptr<mlrg::MemoStore> store;
   std::unique_ptr<mlrg::MemoClient> client;
@@ -110,10 +113,11 @@ void need(bool ok, const char* what) {
 /// Engine assembly per reconstruction (capi.cpp:70-86). Both memo modes use
 /// the device-resident store: "distributed" keeps the reference's decision
 /// semantics (its transport only adds timeouts) without a TCP memory node.
-std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg::Geometry& g, cudaStream_t s) {
+std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg::Geometry& g, cudaStream_t s,
+                                           std::shared_ptr<mlrg::HostComm> comm = nullptr) {
   mlrg::EngineConfig ec = rc.engine;
   ec.memo_enabled = rc.admm.memoization != mlrg::MemoMode::off;
-  if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s);
+  if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s, nullptr, nullptr, std::move(comm));
   if (rc.encoder.variant != mlrg::EncoderConfig::Variant::projection)
     throw std::invalid_argument("encoder_variant=cnn is not provided by the B200 build (projection only)");
   auto store = std::make_shared<mlrg::MemoStore>();
@@ -123,12 +127,24 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   const std::int64_t slab = std::max({e * g.h * g.n2, e * g.n0 * g.n2, g.n_theta * e * g.w, g.n1 * e * g.n2});
   std::size_t free_b = 0, total_b = 0;
   MLRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double want = static_cast<double>(rc.admm.n_outer) * static_cast<double>(rc.memo.insert_queue_cap) *
-                      static_cast<double>(slab) * sizeof(float2);
-  store->arena().reserve(static_cast<std::size_t>(std::min(want, 0.45 * static_cast<double>(free_b))));
+  double per_iter = static_cast<double>(rc.memo.insert_queue_cap);
+  if (comm && comm->world() > 1) {  // a rank stores only its own slabs' values
+    const mlrg::Shard sh = mlrg::Shard::make(g, e, comm);
+    std::int64_t most = 0;
+    for (int r = 0; r < sh.world; ++r) {
+      const auto& pl = sh.planes[static_cast<std::size_t>(r)];
+      const auto& rw = sh.rows[static_cast<std::size_t>(r)];
+      most = std::max({most, (pl.second - pl.first + e - 1) / e, (rw.second - rw.first + e - 1) / e});
+    }
+    per_iter = std::min(per_iter, static_cast<double>(4 * rc.admm.n_inner * most));
+  }
+  const double want = static_cast<double>(rc.admm.n_outer) * per_iter * static_cast<double>(slab) * sizeof(float2);
+  const std::size_t bytes = static_cast<std::size_t>(std::min(want, 0.45 * static_cast<double>(free_b)));
+  if (comm && comm->world() > 1) ec.memo_arena_bytes = bytes;
+  else store->arena().reserve(bytes);
   auto client = std::make_shared<mlrg::MemoClient>(rc.memo, store);
   auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
-  return std::make_unique<mlrg::Engine>(g, ec, s, enc, client);
+  return std::make_unique<mlrg::Engine>(g, ec, s, enc, client, std::move(comm));
 }
 
 struct StreamGuard {
@@ -630,6 +646,11 @@ int mlrg_recon_counters(const mlrg_recon* r, uint64_t out[11]) {
 void mlrg_recon_free(mlrg_recon* r) { delete r; }
 
 mlrg_solver* mlrg_solver_new(const char* config_text, const void* d, const void* reference, void* stream) {
+  return mlrg_solver_new_sharded(config_text, d, reference, stream, nullptr);
+}
+
+mlrg_solver* mlrg_solver_new_sharded(const char* config_text, const void* d, const void* reference, void* stream,
+                                     mlrg_comm* comm) {
   return guarded_ptr<mlrg_solver>([&] {
     need(config_text && d, "mlrg_solver_new: bad argument");
     const mlrg::RunConfig rc = mlrg::RunConfig::from_text(config_text);
@@ -637,11 +658,22 @@ mlrg_solver* mlrg_solver_new(const char* config_text, const void* d, const void*
     const mlrg::Geometry g = rc.make_geometry();
     auto sv = std::make_unique<mlrg_solver>();
     cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
-    sv->eng = build_engine(rc, g, s);
+    sv->eng = build_engine(rc, g, s, comm ? comm->c : nullptr);
     sv->solver = std::make_unique<mlrg::Solver>(static_cast<const float2*>(d), rc.admm, *sv->eng,
                                                 static_cast<const float2*>(reference));
     MLRG_CUDA(cudaStreamSynchronize(s));
     return sv.release();
+  });
+}
+
+int mlrg_solver_shard(const mlrg_solver* s, int64_t out[4]) {
+  return guarded([&] {
+    need(s && out, "null argument");
+    const mlrg::Shard& sh = s->eng->shard();
+    out[0] = sh.a();
+    out[1] = sh.b();
+    out[2] = sh.c();
+    out[3] = sh.d();
   });
 }
 
@@ -657,7 +689,7 @@ int mlrg_solver_step(mlrg_solver* s, int* aborted) {
 int mlrg_solver_volume(mlrg_solver* s, void* u_out) {
   return guarded([&] {
     need(s && u_out, "null argument");
-    const std::int64_t n = s->eng->geometry().volume_shape().count();
+    const std::int64_t n = s->eng->shard().np() * s->eng->geometry().n0 * s->eng->geometry().n2;  // this rank's planes
     mlrg::ops::c128_to_c64(s->solver->u(), static_cast<float2*>(u_out), n, s->eng->stream());
     MLRG_CUDA(cudaStreamSynchronize(s->eng->stream()));
   });
@@ -778,6 +810,71 @@ int mlrg_slot_mix(float* key, int key_dim, uint64_t seed, int64_t location, int 
   return guarded([&] {
     need(key != nullptr, "null key");
     mlrg::slot_mix(key, key_dim, seed, location, static_cast<mlrg::OpId>(op));
+  });
+}
+
+/* ---- node-local communicator and partition (sharded solver) ---- */
+
+mlrg_comm* mlrg_comm_create(const char* name, int rank, int world, double timeout_s) {
+  return guarded_ptr<mlrg_comm>([&] {
+    need(name && *name, "mlrg_comm_create: empty name");
+    auto c = std::make_unique<mlrg_comm>();
+    c->c = std::make_shared<mlrg::HostComm>(name, rank, world, timeout_s > 0 ? timeout_s : 120.0);
+    return c.release();
+  });
+}
+
+void mlrg_comm_free(mlrg_comm* c) { delete c; }
+
+int mlrg_comm_barrier(mlrg_comm* c) {
+  return guarded([&] {
+    need(c != nullptr, "null comm");
+    c->c->barrier();
+  });
+}
+
+int mlrg_comm_allreduce(mlrg_comm* c, double* v, int n) {
+  return guarded([&] {
+    need(c && (v || n == 0), "null argument");
+    c->c->allreduce_sum(v, n);
+  });
+}
+
+int mlrg_comm_allgather(mlrg_comm* c, const void* in, uint64_t bytes, void* out) {
+  return guarded([&] {
+    need(c && in && out, "null argument");
+    c->c->allgather(in, static_cast<std::size_t>(bytes), out);
+  });
+}
+
+int mlrg_partition(int64_t n1, int64_t h, int64_t chunk, int world, int64_t* out) {
+  return guarded([&] {
+    need(out != nullptr && world >= 1 && chunk > 0, "mlrg_partition: bad argument");
+    mlrg::Geometry g;
+    g.n1 = n1;
+    g.h = h;
+    mlrg::Shard sh = mlrg::Shard::whole(g, chunk);
+    if (world > 1) {
+      // the same assign() split Shard::make uses, without a communicator
+      auto ranges = [&](std::int64_t len) {
+        const std::int64_t ns = (len + chunk - 1) / chunk;
+        if (ns < world) throw std::invalid_argument("mlrg_partition: fewer slabs than ranks");
+        auto r = mlrg::assign_ranges(ns, world);
+        for (auto& [lo, hi] : r) {
+          lo = std::min(len, lo * chunk);
+          hi = std::min(len, hi * chunk);
+        }
+        return r;
+      };
+      sh.planes = ranges(n1);
+      sh.rows = ranges(h);
+    }
+    for (int r = 0; r < world; ++r) {
+      out[4 * r + 0] = sh.planes[static_cast<std::size_t>(r)].first;
+      out[4 * r + 1] = sh.planes[static_cast<std::size_t>(r)].second;
+      out[4 * r + 2] = sh.rows[static_cast<std::size_t>(r)].first;
+      out[4 * r + 3] = sh.rows[static_cast<std::size_t>(r)].second;
+    }
   });
 }
 

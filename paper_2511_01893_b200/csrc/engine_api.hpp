@@ -17,6 +17,7 @@
 #include "encoder.hpp"
 #include "geometry.hpp"
 #include "memo.hpp"
+#include "shard.hpp"
 #include "usfft.hpp"
 
 namespace mlrg {
@@ -27,6 +28,7 @@ struct EngineConfig {  // scalerun.hpp:27-42
   bool memo_enabled = false;
   bool flush_after_apply = false;
   GridKernel kernel = GridKernel::es;  // B200 extension key `gridding_kernel` (geometry.hpp)
+  std::size_t memo_arena_bytes = 0;    // sharded memo: HBM reserved per rank for values
 };
 
 struct ChunkAudit {  // scalerun.hpp:45-54
@@ -42,12 +44,20 @@ struct ChunkAudit {  // scalerun.hpp:45-54
 /// Partition axis of each operator's input (scalerun.cpp:29-42).
 int chunk_axis_of(OpId op);
 
+/// Sharded mode (a HostComm of world > 1): the volume-side arrays the engine
+/// reads and writes are this rank's planes [a, b) (Shard), the detector-side
+/// arrays its rows [c, d); fu1d writes the engine-owned mid() block (all
+/// planes, rows [c, d)) of every rank and fu2d_adj the mid2() block (planes
+/// [a, b), all rows). Memo keys are all-gathered so every rank makes the
+/// reference's global decisions (SURVEY.md §8(e) "Memo under sharding").
 class Engine {
  public:
   Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_ptr<Encoder> enc = nullptr,
-         std::shared_ptr<MemoClient> memo = nullptr);
+         std::shared_ptr<MemoClient> memo = nullptr, std::shared_ptr<HostComm> comm = nullptr);
+  ~Engine();
 
   const Geometry& geometry() const { return g_; }
+  const Shard& shard() const { return shard_; }
   Usfft& usfft() { return usfft_; }
   cudaStream_t stream() const { return s_; }
   MemoClient* memo() const { return memo_.get(); }
@@ -55,6 +65,12 @@ class Engine {
   void set_iteration(int it) { iteration_ = it; }
   void flush_inserts();
   const std::vector<ChunkAudit>& audit_log() const { return audit_; }
+
+  /// Sharded mode: the exchange targets (nullptr when unsharded).
+  float2* mid() const { return mid_.get(); }
+  float2* mid2() const { return mid2_.get(); }
+  /// Sums `v` over the ranks in rank order (no-op unsharded).
+  void allreduce(double* v, int n) const;
 
   // Full-array applications (scalerun.hpp:77-92).
   // The volume side (fu1d input, fu1d_adj output) is the solver's complex128
@@ -71,7 +87,7 @@ class Engine {
 
   /// Non-memoized fu2d whose output is only reduced: {sum |fu2d(v) - sub|^2,
   /// Re<dot, fu2d(v) - sub>} (line search terms admm.cpp:95-102 and the data
-  /// term of objective(), admm.cpp:190-195).
+  /// term of objective(), admm.cpp:190-195); summed over ranks.
   std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot);
 
  private:
@@ -79,13 +95,17 @@ class Engine {
              bool memoize);
   void compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
                std::int64_t start, std::int64_t extent);
-  Shape3 in_shape(OpId op) const;
-  Shape3 out_shape(OpId op) const;
+  Shape3 in_shape(OpId op) const;   // this rank's input array
+  Shape3 out_shape(OpId op) const;  // this rank's output array
+  std::int64_t slab0(int axis, OpId op) const;  // global index of this rank's first slab
   void register_shapes();
+  void exchange_fence();  // stream sync + barrier across ranks
+  float2* value_slot(int owner, std::int64_t count);
 
   Geometry g_;
   EngineConfig cfg_;
   cudaStream_t s_;
+  Shard shard_;
   Usfft usfft_;
   std::shared_ptr<Encoder> enc_;
   std::shared_ptr<MemoClient> memo_;
@@ -95,6 +115,13 @@ class Engine {
   DeviceBuffer<float> enc_keys_;
   PinnedBuffer<float> keys_host_;
   PinnedBuffer<double> norms_host_;
+  // sharded mode
+  DeviceBuffer<float2> mid_, mid2_, stage1_, stage2_;
+  std::unique_ptr<PeerMemory> mid_peers_, mid2_peers_;
+  DeviceBuffer<char> arena_;
+  std::unique_ptr<PeerMemory> arena_peers_;
+  std::size_t arena_cap_ = 0;
+  std::vector<std::size_t> arena_next_;
 };
 
 }  // namespace mlrg

@@ -46,6 +46,17 @@ using CDField3 = CField3T<double2>;
 
 namespace ops {
 
+/// Neighbour planes of this rank's axis-0 range in sharded mode (SURVEY.md
+/// §8(e)): plane a-1 ("lo") and plane b ("hi") of the global volume, each
+/// (n0, n2). Null = the global boundary (or unsharded).
+struct Halo {
+  const double2* u_lo = nullptr;
+  const double2* u_hi = nullptr;
+  const double2* g0_lo = nullptr;  // axis-0 component of g at plane a-1
+  const double2* G_hi = nullptr;
+  const double2* pp_hi = nullptr;  // p_prev at plane b
+};
+
 /// g = psi - lambda * lc (admm.cpp:64 with the lazy lambda scale folded in lc).
 void g_init(CDField3 psi, CDField3 lam, DField3 g, std::int64_t n, double lc, cudaStream_t s);
 
@@ -53,12 +64,12 @@ void g_init(CDField3 psi, CDField3 lam, DField3 g, std::int64_t n, double lc, cu
 /// [|grad u - g|^2, |G|^2, Re<p_prev, G - G_prev>] (the last one only when
 /// p_prev/G_prev are non-null).
 int grad_update(const double2* u, CDField3 g, double2* G, const double2* p_prev, const double2* G_prev, Dims d,
-                double rho, double* partials, cudaStream_t s);
+                double rho, double* partials, cudaStream_t s, const Halo& halo = {});
 
 /// p = -G + beta * p_prev (admm.cpp:86-93) with partials
 /// [|grad p|^2, Re<grad u - g, grad p>] (admm.cpp:95-102).
 int direction(const double2* G, const double2* p_prev, double beta, const double2* u, CDField3 g, double2* p,
-              Dims d, double* partials, cudaStream_t s);
+              Dims d, double* partials, cudaStream_t s, const Halo& halo = {});
 
 /// y += a * x (admm.cpp:108-110).
 void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s);
@@ -67,10 +78,10 @@ void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s
 /// psi_new = shrink(grad u + lam*lc, thr); lam += rho_over_lam_scale * (grad u - psi_new).
 /// Partials [|grad u - psi_new|^2, |psi_new - psi_old|^2].
 int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
-                   double rho_over_scale, double* partials, cudaStream_t s);
+                   double rho_over_scale, double* partials, cudaStream_t s, const Halo& halo = {});
 
 /// Isotropic TV: partials [sum sqrt(sum_c |grad_c u|^2)] (admm.cpp:39-46).
-int tv_norm(const double2* u, Dims d, double* partials, cudaStream_t s);
+int tv_norm(const double2* u, Dims d, double* partials, cudaStream_t s, const Halo& halo = {});
 
 /// Partials [|a - b|^2, |a|^2] (b may be null).
 int norm2_diff(const float2* a, const float2* b, std::int64_t n, double* partials, cudaStream_t s);

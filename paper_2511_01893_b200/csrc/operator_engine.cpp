@@ -2,8 +2,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.hpp"
 
@@ -34,13 +36,63 @@ Shape3 with_axis(Shape3 s, int axis, std::int64_t e) {
 }  // namespace
 
 Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_ptr<Encoder> enc,
-               std::shared_ptr<MemoClient> memo)
-    : g_(g), cfg_(cfg), s_(s), usfft_(g, s, cfg.kernel), enc_(std::move(enc)), memo_(std::move(memo)) {
+               std::shared_ptr<MemoClient> memo, std::shared_ptr<HostComm> comm)
+    : g_(g),
+      cfg_(cfg),
+      s_(s),
+      shard_(Shard::make(g, cfg.chunk_extent, std::move(comm))),
+      usfft_(g, s, cfg.kernel),
+      enc_(std::move(enc)),
+      memo_(std::move(memo)) {
   if (cfg_.workers <= 0) throw std::invalid_argument("OperatorEngine: workers must be positive");
   if (cfg_.chunk_extent <= 0) throw std::invalid_argument("OperatorEngine: chunk_extent must be positive");
   if (cfg_.memo_enabled && (!enc_ || !memo_))
     throw std::invalid_argument("OperatorEngine: memoization needs an encoder and a client");
   if (cfg_.memo_enabled) register_shapes();
+  if (shard_.sharded()) {
+    HostComm& c = *shard_.comm;
+    const std::int64_t np = shard_.np(), nr = shard_.nr();
+    mid_.resize(static_cast<std::size_t>(g_.n1 * nr * g_.n2));
+    mid2_.resize(static_cast<std::size_t>(np * g_.h * g_.n2));
+    stage1_.resize(static_cast<std::size_t>(np * g_.h * g_.n2));
+    stage2_.resize(static_cast<std::size_t>(g_.n1 * nr * g_.n2));
+    mid_peers_ = std::make_unique<PeerMemory>(c, mid_.get());
+    mid2_peers_ = std::make_unique<PeerMemory>(c, mid2_.get());
+    if (cfg_.memo_enabled) {
+      // every rank reserves the same capacity (the smallest request), so the
+      // replicated per-owner bump offsets agree everywhere
+      double cap = static_cast<double>(cfg_.memo_arena_bytes);
+      std::vector<double> caps(static_cast<std::size_t>(shard_.world));
+      c.allgather(&cap, sizeof(cap), caps.data());
+      arena_cap_ = static_cast<std::size_t>(*std::min_element(caps.begin(), caps.end()));
+      arena_cap_ = std::max<std::size_t>(arena_cap_, 256);
+      arena_.resize(arena_cap_);
+      arena_peers_ = std::make_unique<PeerMemory>(c, arena_.get());
+      arena_next_.assign(static_cast<std::size_t>(shard_.world), 0);
+    }
+  }
+}
+
+Engine::~Engine() = default;
+
+void Engine::allreduce(double* v, int n) const {
+  if (shard_.sharded()) shard_.comm->allreduce_sum(v, n);
+}
+
+void Engine::exchange_fence() {
+  MLRG_CUDA(cudaStreamSynchronize(s_));
+  shard_.comm->barrier();
+}
+
+float2* Engine::value_slot(int owner, std::int64_t count) {
+  const std::size_t bytes = (static_cast<std::size_t>(count) * sizeof(float2) + 255) & ~std::size_t{255};
+  std::size_t& next = arena_next_[static_cast<std::size_t>(owner)];
+  if (next + bytes > arena_cap_)
+    throw std::runtime_error("memo value arena of rank " + std::to_string(owner) + " exhausted (" +
+                             std::to_string(arena_cap_) + " bytes reserved)");
+  float2* p = reinterpret_cast<float2*>(static_cast<char*>(arena_peers_->at(owner)) + next);
+  next += bytes;
+  return p;
 }
 
 void Engine::register_shapes() {  // scalerun.cpp:109-124
@@ -57,11 +109,12 @@ void Engine::register_shapes() {  // scalerun.cpp:109-124
 }
 
 Shape3 Engine::in_shape(OpId op) const {
+  const std::int64_t np = shard_.np(), nr = shard_.nr();
   switch (op) {
-    case OpId::fu1d: return g_.volume_shape();
-    case OpId::fu1d_adj: return g_.mid_shape();
-    case OpId::fu2d: return g_.mid_shape();
-    case OpId::fu2d_adj: return g_.projection_shape();
+    case OpId::fu1d: return {np, g_.n0, g_.n2};
+    case OpId::fu1d_adj: return {np, g_.h, g_.n2};
+    case OpId::fu2d: return {g_.n1, nr, g_.n2};
+    case OpId::fu2d_adj: return {g_.n_theta, nr, g_.w};
     case OpId::f2d:
     case OpId::f2d_adj: return g_.projection_shape();
   }
@@ -69,20 +122,26 @@ Shape3 Engine::in_shape(OpId op) const {
 }
 
 Shape3 Engine::out_shape(OpId op) const {
+  const std::int64_t np = shard_.np(), nr = shard_.nr();
   switch (op) {
-    case OpId::fu1d: return g_.mid_shape();
-    case OpId::fu1d_adj: return g_.volume_shape();
-    case OpId::fu2d: return g_.projection_shape();
-    case OpId::fu2d_adj: return g_.mid_shape();
+    case OpId::fu1d: return {np, g_.h, g_.n2};
+    case OpId::fu1d_adj: return {np, g_.n0, g_.n2};
+    case OpId::fu2d: return {g_.n_theta, nr, g_.w};
+    case OpId::fu2d_adj: return {g_.n1, nr, g_.n2};
     case OpId::f2d:
     case OpId::f2d_adj: return g_.projection_shape();
   }
   throw std::invalid_argument("out_shape: unknown operator");
 }
 
+std::int64_t Engine::slab0(int axis, OpId op) const {
+  if (op == OpId::f2d || op == OpId::f2d_adj) return 0;
+  return (axis == 0 ? shard_.a() : shard_.c()) / cfg_.chunk_extent;
+}
+
 void Engine::compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
                      std::int64_t start, std::int64_t extent) {
-  const std::int64_t n0 = g_.n0, n2 = g_.n2, h = g_.h, w = g_.w;
+  const std::int64_t n0 = g_.n0, n2 = g_.n2, h = g_.h, w = g_.w, nr = shard_.nr();
   switch (op) {
     case OpId::fu1d:
       if (in_d) usfft_.fu1d(static_cast<const double2*>(in) + start * n0 * n2, static_cast<float2*>(out) + start * h * n2, extent);
@@ -95,18 +154,18 @@ void Engine::compute(OpId op, bool fused, const void* in, bool in_d, const float
     case OpId::fu2d: {
       Fu2dEpilogue e;
       e.out = static_cast<float2*>(out);
-      e.ld_out = h;
+      e.ld_out = nr;
       e.k0_out = start;
       if (fused) {
         e.sub = d_hat;
-        e.ld_sub = h;
+        e.ld_sub = nr;
         e.k0_sub = start;
       }
-      usfft_.fu2d(static_cast<const float2*>(in), h, start, extent, e);
+      usfft_.fu2d(static_cast<const float2*>(in), nr, start, extent, e);
       return;
     }
     case OpId::fu2d_adj:
-      usfft_.fu2d_adj(static_cast<const float2*>(in), h, start, extent, static_cast<float2*>(out), h, start);
+      usfft_.fu2d_adj(static_cast<const float2*>(in), nr, start, extent, static_cast<float2*>(out), nr, start);
       return;
     case OpId::f2d:
     case OpId::f2d_adj:
@@ -126,10 +185,13 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     compute(op, fused, in, in_d, d_hat, out, out_d, 0, len);
     return;
   }
-  // ---- encode every slab (one GEMM per distinct slab shape) ----
+  if (shard_.sharded() && (op == OpId::f2d || op == OpId::f2d_adj))
+    throw std::invalid_argument("OperatorEngine: f2d is not memoized in sharded mode (pipeline=optimized)");
+  // ---- encode this rank's slabs (one GEMM per distinct slab shape) ----
   const std::vector<std::int64_t> ext = slab_extents(len, cfg_.chunk_extent);
   const int n = static_cast<int>(ext.size());
   const int kd = enc_->key_dim();
+  const std::int64_t g0 = slab0(axis, op);  // global location of local slab 0
   enc_keys_.resize(static_cast<std::size_t>(n * kd));
   enc_norms_.resize(static_cast<std::size_t>(n));
   keys_host_.reserve(static_cast<std::size_t>(n * kd));
@@ -157,20 +219,49 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     MLRG_CUDA(cudaMemcpyAsync(norms_host_.get(), enc_norms_.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s_));
     MLRG_CUDA(cudaStreamSynchronize(s_));
   }
-
-  std::vector<MemoKey> keys(static_cast<std::size_t>(n));
-  std::vector<std::size_t> value_bytes(static_cast<std::size_t>(n));
-  std::vector<double> in_norms(static_cast<std::size_t>(n));
-  std::vector<std::int64_t> out_counts(static_cast<std::size_t>(n));
+  // ---- local keys -> the global key list (slot-mixed with the global location) ----
+  std::vector<float> kv(static_cast<std::size_t>(n * kd));
+  std::vector<double> nv(static_cast<std::size_t>(n));
   for (int c = 0; c < n; ++c) {
+    std::copy(keys_host_.get() + static_cast<std::size_t>(c) * kd, keys_host_.get() + static_cast<std::size_t>(c + 1) * kd,
+              kv.begin() + static_cast<std::ptrdiff_t>(c) * kd);
+    slot_mix(kv.data() + static_cast<std::size_t>(c) * kd, kd, enc_->seed(), g0 + c, op);
+    nv[static_cast<std::size_t>(c)] = std::sqrt(norms_host_.get()[c]);
+  }
+  const Shape3 gin = op == OpId::fu1d || op == OpId::fu1d_adj ? with_axis(ishape, 0, g_.n1)
+                     : op == OpId::fu2d || op == OpId::fu2d_adj ? with_axis(ishape, 1, g_.h)
+                                                                : ishape;
+  const std::vector<std::int64_t> gext = slab_extents(gin.extent(axis), cfg_.chunk_extent);
+  const int N = static_cast<int>(gext.size());
+  if (shard_.sharded()) {  // all-gather keys and norms in rank (= slab) order
+    std::vector<unsigned char> buf(kv.size() * sizeof(float) + nv.size() * sizeof(double));
+    std::memcpy(buf.data(), nv.data(), nv.size() * sizeof(double));
+    std::memcpy(buf.data() + nv.size() * sizeof(double), kv.data(), kv.size() * sizeof(float));
+    std::vector<std::size_t> counts;
+    const std::vector<unsigned char> all = shard_.comm->allgatherv(buf.data(), buf.size(), &counts);
+    kv.clear();
+    nv.clear();
+    std::size_t at = 0;
+    for (const std::size_t bytes : counts) {
+      const std::size_t m = bytes / (sizeof(double) + sizeof(float) * static_cast<std::size_t>(kd));
+      const double* np_ = reinterpret_cast<const double*>(all.data() + at);
+      const float* kp = reinterpret_cast<const float*>(all.data() + at + m * sizeof(double));
+      nv.insert(nv.end(), np_, np_ + m);
+      kv.insert(kv.end(), kp, kp + m * static_cast<std::size_t>(kd));
+      at += bytes;
+    }
+    if (static_cast<int>(nv.size()) != N) throw std::logic_error("sharded memo: global slab count mismatch");
+  }
+  std::vector<MemoKey> keys(static_cast<std::size_t>(N));
+  std::vector<std::size_t> value_bytes(static_cast<std::size_t>(N));
+  std::vector<std::int64_t> out_counts(static_cast<std::size_t>(N));
+  const Shape3 gout = with_axis(oshape, axis, 1);
+  for (int c = 0; c < N; ++c) {
     MemoKey& k = keys[static_cast<std::size_t>(c)];
-    k.values.assign(keys_host_.get() + static_cast<std::size_t>(c) * kd,
-                    keys_host_.get() + static_cast<std::size_t>(c + 1) * kd);
+    k.values.assign(kv.begin() + static_cast<std::ptrdiff_t>(c) * kd, kv.begin() + static_cast<std::ptrdiff_t>(c + 1) * kd);
     k.location = c;
     k.op = op;
-    slot_mix(k.values.data(), kd, enc_->seed(), c, op);
-    in_norms[static_cast<std::size_t>(c)] = std::sqrt(norms_host_.get()[c]);
-    const std::int64_t oc = with_axis(oshape, axis, ext[static_cast<std::size_t>(c)]).count();
+    const std::int64_t oc = with_axis(gout, axis, gext[static_cast<std::size_t>(c)]).count();
     out_counts[static_cast<std::size_t>(c)] = oc;
     value_bytes[static_cast<std::size_t>(c)] = 8 + static_cast<std::size_t>(oc) * 16;
   }
@@ -179,21 +270,21 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     prof::HostSpan span("host:memo_lookup");
     dec = memo_->lookup_batch(keys, value_bytes);
   }
+  auto local_dec = [&](int c) -> const MemoDecision& { return dec[static_cast<std::size_t>(g0 + c)]; };
 
-  // ---- misses: computed in contiguous runs (linear fu2d for fused, d_hat after staging) ----
+  // ---- local misses: computed in contiguous runs (linear fu2d for fused, d_hat after staging) ----
   for (int c0 = 0; c0 < n;) {
-    if (dec[static_cast<std::size_t>(c0)].outcome != MemoOutcome::miss) {
+    if (local_dec(c0).outcome != MemoOutcome::miss) {
       ++c0;
       continue;
     }
     int c1 = c0;
     std::int64_t extent = 0;
-    while (c1 < n && dec[static_cast<std::size_t>(c1)].outcome == MemoOutcome::miss)
-      extent += ext[static_cast<std::size_t>(c1++)];
+    while (c1 < n && local_dec(c1).outcome == MemoOutcome::miss) extent += ext[static_cast<std::size_t>(c1++)];
     compute(op, false, in, in_d, nullptr, out, out_d, starts[static_cast<std::size_t>(c0)], extent);
     c0 = c1;
   }
-  // ---- hits: value * (live norm / stored norm), minus the live d_hat slab when fused (one launch) ----
+  // ---- local hits: value * (live norm / stored norm), minus the live d_hat slab when fused (one launch) ----
   const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, 0, 0};
   auto batch = std::make_unique<ops::SlabBatch>();
   int nb = 0;
@@ -203,57 +294,82 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
     nb = 0;
   };
   for (int c = 0; c < n; ++c) {
-    const MemoDecision& d = dec[static_cast<std::size_t>(c)];
-    if (d.outcome != MemoOutcome::miss) {
-      const ValueRef& v = memo_->store().value(d.value_id);
-      const double live = in_norms[static_cast<std::size_t>(c)];
-      batch->start[nb] = starts[static_cast<std::size_t>(c)];
-      batch->extent[nb] = ext[static_cast<std::size_t>(c)];
-      batch->value[nb] = v.dev;
-      batch->scale[nb] = (v.norm > 0.0 && live > 0.0) ? live / v.norm : 1.0;
-      if (++nb == ops::kSlabBatch) flush_hits();
-    }
-    audit_.push_back(ChunkAudit{op, axis, c, ext[static_cast<std::size_t>(c)], d.outcome, d.cs, iteration_, -1.0f});
+    const MemoDecision& d = local_dec(c);
+    if (d.outcome == MemoOutcome::miss) continue;
+    const ValueRef& v = memo_->store().value(d.value_id);
+    const double live = nv[static_cast<std::size_t>(g0 + c)];
+    batch->start[nb] = starts[static_cast<std::size_t>(c)];
+    batch->extent[nb] = ext[static_cast<std::size_t>(c)];
+    batch->value[nb] = v.dev;  // this rank's arena or a peer's (IPC mapping)
+    batch->scale[nb] = (v.norm > 0.0 && live > 0.0) ? live / v.norm : 1.0;
+    if (++nb == ops::kSlabBatch) flush_hits();
   }
   flush_hits();
-  // ---- stage the miss values (the linear part for fused), then apply d_hat (one launch) ----
+  for (int c = 0; c < N; ++c) {
+    const MemoDecision& d = dec[static_cast<std::size_t>(c)];
+    audit_.push_back(ChunkAudit{op, axis, c, gext[static_cast<std::size_t>(c)], d.outcome, d.cs, iteration_, -1.0f});
+  }
+  // ---- stage the miss values in global order (the linear part for fused); the
+  // owner copies its slabs, then applies d_hat (one launch) ----
   auto flush_stores = [&]() {
     if (out_d) ops::slab_store(static_cast<double2*>(out), og, *batch, nb, s_);
     else ops::slab_store(static_cast<float2*>(out), og, *batch, nb, fused ? d_hat : nullptr, s_);
     nb = 0;
   };
-  for (int c = 0; c < n; ++c) {
+  for (int c = 0; c < N; ++c) {
     if (dec[static_cast<std::size_t>(c)].outcome != MemoOutcome::miss) continue;
+    const bool mine = c >= g0 && c < g0 + n;
+    const int owner = !shard_.sharded() ? 0
+                      : axis == 0       ? shard_.owner_of_plane(c * cfg_.chunk_extent)
+                                        : shard_.owner_of_row(c * cfg_.chunk_extent);
     float2* dst = nullptr;
     memo_->insert_async(keys[static_cast<std::size_t>(c)], [&]() {
+      prof::HostSpan span("host:memo_alloc");
       ValueRef v;
       v.count = out_counts[static_cast<std::size_t>(c)];
-      prof::HostSpan span("host:memo_alloc");
-      dst = memo_->store().arena().alloc(v.count);
-      v.dev = dst;
-      v.norm = in_norms[static_cast<std::size_t>(c)];
+      float2* slot = shard_.sharded() ? value_slot(owner, v.count) : memo_->store().arena().alloc(v.count);
+      if (mine) dst = slot;
+      v.dev = slot;
+      v.norm = nv[static_cast<std::size_t>(c)];
       v.bytes = value_bytes[static_cast<std::size_t>(c)];
       return v;
     });
-    if (!dst && !fused) continue;  // dropped insert, nothing to do for this slab
-    batch->start[nb] = starts[static_cast<std::size_t>(c)];
-    batch->extent[nb] = ext[static_cast<std::size_t>(c)];
+    if (!mine || (!dst && !fused)) continue;  // another rank's slab, or a dropped insert
+    batch->start[nb] = starts[static_cast<std::size_t>(c - g0)];
+    batch->extent[nb] = ext[static_cast<std::size_t>(c - g0)];
     batch->dst[nb] = dst;
     if (++nb == ops::kSlabBatch) flush_stores();
   }
   flush_stores();
-  if (cfg_.flush_after_apply) memo_->flush_inserts();
+  if (cfg_.flush_after_apply) flush_inserts();
 }
 
 void Engine::flush_inserts() {
   prof::HostSpan span("host:memo_flush");
-  if (memo_) memo_->flush_inserts();
+  if (!memo_) return;
+  // sharded: a value is read by its first hit only after this flush; the owner's
+  // copy must be complete on its stream before any rank publishes the key
+  if (shard_.sharded()) exchange_fence();
+  memo_->flush_inserts();
 }
 
 void Engine::fu1d(const double2* u, float2* out, bool memoize) {
-  apply(OpId::fu1d, false, u, true, nullptr, out, false, memoize);
+  if (!shard_.sharded()) return apply(OpId::fu1d, false, u, true, nullptr, out, false, memoize);
+  if (out != mid_.get()) throw std::invalid_argument("sharded fu1d: output must be the engine's mid()");
+  exchange_fence();  // every rank is done reading its mid block
+  apply(OpId::fu1d, false, u, true, nullptr, stage1_.get(), false, memoize);
+  ops::RankTable t;
+  t.world = shard_.world;
+  for (int r = 0; r < shard_.world; ++r) {
+    t.lo[r] = shard_.rows[static_cast<std::size_t>(r)].first;
+    t.hi[r] = shard_.rows[static_cast<std::size_t>(r)].second;
+    t.dst[r] = static_cast<float2*>(mid_peers_->at(r));
+  }
+  ops::scatter_planes_to_rows(stage1_.get(), shard_.np(), shard_.a(), g_.n1, g_.h, g_.n2, t, s_);
+  exchange_fence();  // every rank's mid block is complete
 }
 void Engine::fu1d(const float2* u, float2* out, bool memoize) {
+  if (shard_.sharded()) throw std::invalid_argument("sharded fu1d takes the complex128 iterate");
   apply(OpId::fu1d, false, u, false, nullptr, out, false, memoize);
 }
 void Engine::fu1d_adj(const float2* v, double2* out, bool memoize) {
@@ -269,7 +385,19 @@ void Engine::fu2d_fused(const float2* v, const float2* d_hat, float2* out, bool 
   apply(OpId::fu2d, true, v, false, d_hat, out, false, memoize);
 }
 void Engine::fu2d_adj(const float2* p, float2* out, bool memoize) {
-  apply(OpId::fu2d_adj, false, p, false, nullptr, out, false, memoize);
+  if (!shard_.sharded()) return apply(OpId::fu2d_adj, false, p, false, nullptr, out, false, memoize);
+  if (out != mid2_.get()) throw std::invalid_argument("sharded fu2d_adj: output must be the engine's mid2()");
+  exchange_fence();
+  apply(OpId::fu2d_adj, false, p, false, nullptr, stage2_.get(), false, memoize);
+  ops::RankTable t;
+  t.world = shard_.world;
+  for (int r = 0; r < shard_.world; ++r) {
+    t.lo[r] = shard_.planes[static_cast<std::size_t>(r)].first;
+    t.hi[r] = shard_.planes[static_cast<std::size_t>(r)].second;
+    t.dst[r] = static_cast<float2*>(mid2_peers_->at(r));
+  }
+  ops::scatter_rows_to_planes(stage2_.get(), shard_.nr(), shard_.c(), g_.n1, g_.h, g_.n2, t, s_);
+  exchange_fence();
 }
 void Engine::f2d(const float2* p, float2* out, bool memoize) {
   apply(OpId::f2d, false, p, false, nullptr, out, false, memoize);
@@ -279,14 +407,16 @@ void Engine::f2d_adj(const float2* p, float2* out, bool memoize) {
 }
 
 std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot) {
+  const std::int64_t nr = shard_.nr();
   Fu2dEpilogue e;
   e.sub = sub;
-  e.ld_sub = g_.h;
+  e.ld_sub = nr;
   e.dot = dot;
-  e.ld_dot = g_.h;
+  e.ld_dot = nr;
   e.reduce = true;
-  const int slots = usfft_.fu2d(v, g_.h, 0, g_.h, e);
-  const std::vector<double> r = usfft_.partials().sum(slots, 2, s_);
+  const int slots = usfft_.fu2d(v, nr, 0, nr, e);
+  std::vector<double> r = usfft_.partials().sum(slots, 2, s_);
+  allreduce(r.data(), 2);
   return {r[0], r[1]};
 }
 

@@ -5,10 +5,12 @@
 #include <cstdlib>
 #include <cmath>
 #include <iomanip>
+#include <memory>
 #include <sstream>
 #include <utility>
 
 #include "kernels.hpp"
+#include "shard.hpp"
 
 namespace mlrg {
 
@@ -35,18 +37,28 @@ namespace {
 /// Device ADMM state (admm.hpp:38-49). lambda is stored scaled: the true
 /// multiplier is lam * lam_scale, with lam_scale a power of two, so the
 /// residual-balancing rescale (admm.cpp:173-180) is exact and costs no pass.
+/// Sharded: volume-side arrays hold this rank's planes [a, b), detector-side
+/// arrays its rows [c, d); mid/mid2 are the engine's exchange blocks.
 struct State {
-  std::int64_t V, M, P;
+  std::int64_t V, P, P0;  // local volume / detector sizes, one axis-0 plane
   DeviceBuffer<double2> u, G, G_prev, p, p_prev;       // volume side, complex128
   DeviceBuffer<double2> psi[3], psi_prev[3], lam[3], g[3];
   DeviceBuffer<double2> ref;                            // accuracy reference (optional)
-  DeviceBuffer<float2> mid, mid2, rhat, dhat, dpred, fu2d_out;  // operator side, complex64
+  DeviceBuffer<float2> mid_own, mid2_own, rhat, dhat, dpred, fu2d_out;  // operator side, complex64
+  float2 *mid = nullptr, *mid2 = nullptr;
+  // sharded: halo inboxes (written by the neighbours) and their peer mappings
+  DeviceBuffer<double2> in_u_lo, in_u_hi, in_g0_lo, in_G_hi, in_pp_hi;
+  std::unique_ptr<PeerMemory> pm_u_lo, pm_u_hi, pm_g0_lo, pm_G_hi, pm_pp_hi;
   double rho = 1.0, lam_scale = 1.0;
   bool have_direction = false;
   std::vector<double> inner_losses;
 
-  State(const Geometry& geo, bool baseline, cudaStream_t s)
-      : V(geo.volume_shape().count()), M(geo.mid_shape().count()), P(geo.projection_shape().count()) {
+  State(const Geometry& geo, const Engine& eng, bool baseline, cudaStream_t s) {
+    const Shard& sh = eng.shard();
+    P0 = geo.n0 * geo.n2;
+    V = sh.np() * P0;
+    P = geo.n_theta * sh.nr() * geo.w;
+    const std::int64_t M = geo.mid_shape().count();
     auto vz = [&](auto& b, std::int64_t n) {
       b.resize(static_cast<std::size_t>(n));
       b.zero(s);
@@ -58,8 +70,24 @@ struct State {
       vz(lam[c], V);
       vz(g[c], V);
     }
-    vz(mid, M);
-    vz(mid2, M);
+    if (sh.sharded()) {
+      if (baseline) throw std::invalid_argument("admm: pipeline=baseline runs on one GPU only (sharded: optimized)");
+      mid = eng.mid();
+      mid2 = eng.mid2();
+      for (auto* b : {&in_u_lo, &in_u_hi, &in_g0_lo, &in_G_hi, &in_pp_hi}) vz(*b, P0);
+      HostComm& c = *sh.comm;
+      MLRG_CUDA(cudaStreamSynchronize(s));
+      pm_u_lo = std::make_unique<PeerMemory>(c, in_u_lo.get());
+      pm_u_hi = std::make_unique<PeerMemory>(c, in_u_hi.get());
+      pm_g0_lo = std::make_unique<PeerMemory>(c, in_g0_lo.get());
+      pm_G_hi = std::make_unique<PeerMemory>(c, in_G_hi.get());
+      pm_pp_hi = std::make_unique<PeerMemory>(c, in_pp_hi.get());
+    } else {
+      vz(mid_own, M);
+      vz(mid2_own, M);
+      mid = mid_own.get();
+      mid2 = mid2_own.get();
+    }
     vz(rhat, P);
     vz(dhat, P);
     if (baseline) {
@@ -70,7 +98,7 @@ struct State {
   DField3 f(DeviceBuffer<double2> (&a)[3]) { return DField3{{a[0].get(), a[1].get(), a[2].get()}}; }
 };
 
-std::int64_t geo_count(const Engine& e) { return e.geometry().volume_shape().count(); }
+std::int64_t local_count(const Engine& e) { return e.shard().np() * e.geometry().n0 * e.geometry().n2; }
 
 bool trace_on() {  // MLRG_TRACE=1: per-step solver scalars on stderr (diagnostics)
   static const bool on = [] {
@@ -95,15 +123,53 @@ struct SolverState : State {
   MemoCounters prev;
   int outer = 0;
   SolverState(const float2* d_, const AdmmConfig& c, Engine& e, const float2* ref)
-      : State(e.geometry(), c.pipeline == Pipeline::baseline, e.stream()),
+      : State(e.geometry(), e, c.pipeline == Pipeline::baseline, e.stream()),
         d(d_),
         has_reference(ref != nullptr),
         cfg(c),
         eng(e) {
-    if (ref) {
+    if (ref) {  // this rank's planes of the full reference volume
       this->ref.resize(static_cast<std::size_t>(V));
-      ops::c64_to_c128(ref, this->ref.get(), V, e.stream());
+      ops::c64_to_c128(ref + e.shard().a() * P0, this->ref.get(), V, e.stream());
     }
+  }
+
+  // ---- halo exchange (sharded): push this rank's boundary planes into the
+  // neighbours' inboxes; completion is published by the next fence/allreduce ----
+  const Shard& sh() const { return eng.shard(); }
+  void push(const double2* plane, const PeerMemory* pm, int to) {
+    MLRG_CUDA(cudaMemcpyAsync(pm->at(to), plane, static_cast<std::size_t>(P0) * sizeof(double2), cudaMemcpyDefault,
+                              eng.stream()));
+  }
+  void push_u() {
+    if (!sh().sharded()) return;
+    const int r = sh().rank;
+    if (r > 0) push(u.get(), pm_u_hi.get(), r - 1);
+    if (r + 1 < sh().world) push(u.get() + (sh().np() - 1) * P0, pm_u_lo.get(), r + 1);
+  }
+  void push_g0() {
+    if (!sh().sharded() || sh().rank + 1 >= sh().world) return;
+    push(g[0].get() + (sh().np() - 1) * P0, pm_g0_lo.get(), sh().rank + 1);
+  }
+  void push_G_pp() {
+    if (!sh().sharded() || sh().rank == 0) return;
+    push(G.get(), pm_G_hi.get(), sh().rank - 1);
+    push(p_prev.get(), pm_pp_hi.get(), sh().rank - 1);
+  }
+  ops::Halo halo() const {
+    ops::Halo h;
+    if (!sh().sharded()) return h;
+    const bool lo = sh().rank > 0, hi = sh().rank + 1 < sh().world;
+    if (lo) {
+      h.u_lo = in_u_lo.get();
+      h.g0_lo = in_g0_lo.get();
+    }
+    if (hi) {
+      h.u_hi = in_u_hi.get();
+      h.G_hi = in_G_hi.get();
+      h.pp_hi = in_pp_hi.get();
+    }
+    return h;
   }
 };
 
@@ -111,7 +177,19 @@ Solver::Solver(const float2* d, const AdmmConfig& cfg, Engine& eng, const float2
   cfg.validate();
   st_ = new SolverState(d, cfg, eng, reference);
   st_->rho = cfg.rho0;
-  eng.f2d(d, st_->dhat.get(), false);  // admm.cpp:220
+  const Shard& sh = eng.shard();
+  if (!sh.sharded()) {
+    eng.f2d(d, st_->dhat.get(), false);  // admm.cpp:220
+  } else {  // d_hat of the full data, then this rank's rows (n_theta, [c, d), w)
+    const Geometry& g = eng.geometry();
+    DeviceBuffer<float2> full(static_cast<std::size_t>(g.projection_shape().count()));
+    eng.f2d(d, full.get(), false);
+    MLRG_CUDA(cudaMemcpy2DAsync(st_->dhat.get(), static_cast<std::size_t>(sh.nr() * g.w) * sizeof(float2),
+                                full.get() + sh.c() * g.w, static_cast<std::size_t>(g.h * g.w) * sizeof(float2),
+                                static_cast<std::size_t>(sh.nr() * g.w) * sizeof(float2),
+                                static_cast<std::size_t>(g.n_theta), cudaMemcpyDeviceToDevice, eng.stream()));
+    MLRG_CUDA(cudaStreamSynchronize(eng.stream()));
+  }
   st_->prev = eng.memo() ? eng.memo()->counters() : MemoCounters{};
 }
 
@@ -128,11 +206,15 @@ bool Solver::step() {
   const Geometry& geo = eng.geometry();
   cudaStream_t s = eng.stream();
   Partials& part = eng.usfft().partials();
-  const Dims dims{geo.n1, geo.n0, geo.n2};
+  const Dims dims{eng.shard().np(), geo.n0, geo.n2};  // this rank's planes
   const bool baseline = cfg.pipeline == Pipeline::baseline;
   const float2* d = st.d;
   using clock = std::chrono::steady_clock;
-  auto sum = [&](int slots, int nv) { return part.sum(slots, nv, s); };
+  auto sum = [&](int slots, int nv) {  // CTA partials -> this rank's sums -> summed over ranks
+    std::vector<double> v = part.sum(slots, nv, s);
+    eng.allreduce(v.data(), nv);
+    return v;
+  };
   const int outer = st.outer++;
   {
     eng.set_iteration(outer);
@@ -142,28 +224,31 @@ bool Solver::step() {
       const auto t0 = clock::now();
       // ---- LSP (admm.cpp:59-118, 122-152) ----
       ops::g_init(CDField3(st.f(st.psi)), CDField3(st.f(st.lam)), st.f(st.g), st.V, st.lam_scale / st.rho, s);
+      st.push_g0();
       st.have_direction = false;
       const std::size_t phase_start = st.inner_losses.size();
       for (int inner = 0; inner < cfg.n_inner; ++inner) {
         // gradient(u): r_hat, loss terms, G
         double rr = 0.0;
-        eng.fu1d(st.u.get(), st.mid.get());
+        st.push_u();  // published by fu1d's exchange fences
+        eng.fu1d(st.u.get(), st.mid);
         if (baseline) {
-          eng.fu2d(st.mid.get(), st.fu2d_out.get());
+          eng.fu2d(st.mid, st.fu2d_out.get());
           eng.f2d_adj(st.fu2d_out.get(), st.dpred.get());
           rr = sum(ops::sub_norm(st.dpred.get(), d, st.P, part.dev(), s), 1)[0];
           eng.f2d(st.dpred.get(), st.rhat.get());
         } else {
-          eng.fu2d_fused(st.mid.get(), st.dhat.get(), st.rhat.get());
+          eng.fu2d_fused(st.mid, st.dhat.get(), st.rhat.get());
           rr = sum(ops::norm2_diff(st.rhat.get(), nullptr, st.P, part.dev(), s), 2)[1];
         }
-        eng.fu2d_adj(st.rhat.get(), st.mid2.get());
-        eng.fu1d_adj(st.mid2.get(), st.G.get());
+        eng.fu2d_adj(st.rhat.get(), st.mid2);
+        eng.fu1d_adj(st.mid2, st.G.get());
         const bool hd = st.have_direction;
-        const std::vector<double> gu = sum(
+        const int gu_slots =
             ops::grad_update(st.u.get(), CDField3(st.f(st.g)), st.G.get(), hd ? st.p_prev.get() : nullptr,
-                             hd ? st.G_prev.get() : nullptr, dims, st.rho, part.dev(), s),
-            3);
+                             hd ? st.G_prev.get() : nullptr, dims, st.rho, part.dev(), s, st.halo());
+        st.push_G_pp();  // published by the allreduce below
+        const std::vector<double> gu = sum(gu_slots, 3);
         const double loss = 0.5 * rr + 0.5 * st.rho * gu[0];
         st.inner_losses.push_back(loss);
         const std::size_t n = st.inner_losses.size();
@@ -177,11 +262,12 @@ bool Solver::step() {
         double beta = 0.0;
         if (hd && gu[2] > 0.0) beta = normG2 / gu[2];
         auto step_terms = [&](double bt, double& a, double& b) {
-          const std::vector<double> dr = sum(ops::direction(st.G.get(), st.p_prev.get(), bt, st.u.get(),
-                                                            CDField3(st.f(st.g)), st.p.get(), dims, part.dev(), s),
-                                             2);
-          eng.fu1d(st.p.get(), st.mid.get(), false);
-          const std::array<double, 2> q = eng.fu2d_reduce(st.mid.get(), nullptr, st.rhat.get());
+          const std::vector<double> dr =
+              sum(ops::direction(st.G.get(), st.p_prev.get(), bt, st.u.get(), CDField3(st.f(st.g)), st.p.get(), dims,
+                                 part.dev(), s, st.halo()),
+                  2);
+          eng.fu1d(st.p.get(), st.mid, false);
+          const std::array<double, 2> q = eng.fu2d_reduce(st.mid, nullptr, st.rhat.get());
           a = q[0] + st.rho * dr[0];
           b = q[1] + st.rho * dr[1];
         };
@@ -199,9 +285,15 @@ bool Solver::step() {
       MLRG_CUDA(cudaStreamSynchronize(s));
       const auto t1 = clock::now();
       // ---- RSP + multiplier/penalty, one fused pass (admm.cpp:154-181) ----
+      st.push_u();
+      if (eng.shard().sharded()) {  // publish the u halos
+        MLRG_CUDA(cudaStreamSynchronize(s));
+        eng.shard().comm->barrier();
+      }
       const std::vector<double> rs =
           sum(ops::rsp_multiplier(st.u.get(), st.f(st.lam), CDField3(st.f(st.psi)), st.f(st.psi_prev), dims,
-                                  st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s),
+                                  st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s,
+                                  st.halo()),
               2);
       for (int c = 0; c < 3; ++c) std::swap(st.psi[c], st.psi_prev[c]);  // psi_prev <- old psi
       const auto t2 = clock::now();
@@ -228,9 +320,9 @@ bool Solver::step() {
     }
     eng.flush_inserts();  // admm.cpp:251-254
     // objective (admm.cpp:190-195), not memoized
-    eng.fu1d(st.u.get(), st.mid.get(), false);
-    const std::array<double, 2> data = eng.fu2d_reduce(st.mid.get(), st.dhat.get(), nullptr);
-    const double tv = sum(ops::tv_norm(st.u.get(), dims, part.dev(), s), 1)[0];
+    eng.fu1d(st.u.get(), st.mid, false);
+    const std::array<double, 2> data = eng.fu2d_reduce(st.mid, st.dhat.get(), nullptr);
+    const double tv = sum(ops::tv_norm(st.u.get(), dims, part.dev(), s, st.halo()), 1)[0];
     row.loss = 0.5 * data[0] + cfg.alpha * tv;
     if (st.has_reference) {  // accuracy(reference, u), admm.cpp:183-188
       const std::vector<double> nd = sum(ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev(), s), 2);
@@ -255,7 +347,7 @@ ReconReport reconstruct(const float2* d, const AdmmConfig& cfg, Engine& eng, con
   for (int outer = 0; outer < cfg.n_outer; ++outer)
     if (!solver.step()) break;
   cudaStream_t s = eng.stream();
-  ops::c128_to_c64(solver.u(), u_out, geo_count(eng), s);
+  ops::c128_to_c64(solver.u(), u_out, local_count(eng), s);
   MLRG_CUDA(cudaStreamSynchronize(s));
   return solver.report();
 }

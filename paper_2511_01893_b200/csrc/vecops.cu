@@ -78,26 +78,46 @@ __global__ void __launch_bounds__(kThreads) k_g_init(CDField3 psi, CDField3 lam,
   }
 }
 
+// Axis-0 neighbours across the shard boundary: plane i+1 / i-1 of the local
+// range, else the halo plane (pl = offset within a plane), else absent.
+__device__ __forceinline__ bool has_fwd(int i, int n1, const double2* hi) { return i + 1 < n1 || hi != nullptr; }
+__device__ __forceinline__ bool has_bwd(int i, const double2* lo) { return i > 0 || lo != nullptr; }
+__device__ __forceinline__ double2 fwd0(const double2* __restrict__ a, const double2* __restrict__ hi, int i, int n1,
+                                        long long idx, long long s0, long long pl) {
+  return i + 1 < n1 ? a[idx + s0] : hi[pl];
+}
+__device__ __forceinline__ double2 bwd0(const double2* __restrict__ a, const double2* __restrict__ lo, int i,
+                                        long long idx, long long s0, long long pl) {
+  return i > 0 ? a[idx - s0] : lo[pl];
+}
+
 __global__ void __launch_bounds__(kThreads) k_grad_update(const double2* __restrict__ u, CDField3 g,
                                                           double2* __restrict__ G,
                                                           const double2* __restrict__ p_prev,
                                                           const double2* __restrict__ G_prev, DevDims d,
-                                                          double rho, double* __restrict__ partials) {
+                                                          double rho, double* __restrict__ partials, Halo hl) {
   double red[3] = {0.0, 0.0, 0.0};
   const int len[3] = {d.n1, d.n0, d.n2};
   const long long st[3] = {d.s0, d.s1, 1};
   for_voxels(d, [&](long long idx, int i, int m, int j) {
     const int pos[3] = {i, m, j};
+    const long long pl = static_cast<long long>(m) * d.n2 + j;
     const double2 u0 = u[idx];
     double2 dv = zero2();
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const bool fwd = pos[ax] + 1 < len[ax];
-      const double2 gu = fwd ? dsub(u[idx + st[ax]], u0) : zero2();
+      const bool fwd = ax == 0 ? has_fwd(i, d.n1, hl.u_hi) : pos[ax] + 1 < len[ax];
+      const double2 un = !fwd ? zero2() : ax == 0 ? fwd0(u, hl.u_hi, i, d.n1, idx, st[0], pl) : u[idx + st[ax]];
+      const double2 gu = fwd ? dsub(un, u0) : zero2();
       const double2 gd = dsub(gu, g.c[ax][idx]);  // (grad u - g)_ax at idx
       red[0] += dnrm(gd);
       if (fwd) dv = dadd(dv, gd);
-      if (pos[ax] > 0) dv = dsub(dv, dsub(dsub(u0, u[idx - st[ax]]), g.c[ax][idx - st[ax]]));
+      const bool bwd = ax == 0 ? has_bwd(i, hl.u_lo) : pos[ax] > 0;
+      if (bwd) {
+        const double2 ub = ax == 0 ? bwd0(u, hl.u_lo, i, idx, st[0], pl) : u[idx - st[ax]];
+        const double2 gb = ax == 0 ? bwd0(g.c[0], hl.g0_lo, i, idx, st[0], pl) : g.c[ax][idx - st[ax]];
+        dv = dsub(dv, dsub(dsub(u0, ub), gb));
+      }
     }
     const double2 Gn = dfma(-rho, dv, G[idx]);
     G[idx] = Gn;
@@ -118,20 +138,31 @@ __global__ void __launch_bounds__(kThreads) k_direction(const double2* __restric
                                                         const double2* __restrict__ p_prev, double beta,
                                                         const double2* __restrict__ u, CDField3 g,
                                                         double2* __restrict__ p, DevDims d,
-                                                        double* __restrict__ partials) {
+                                                        double* __restrict__ partials, Halo hl) {
   double red[2] = {0.0, 0.0};
   const int len[3] = {d.n1, d.n0, d.n2};
   const long long st[3] = {d.s0, d.s1, 1};
   for_voxels(d, [&](long long idx, int i, int m, int j) {
     const int pos[3] = {i, m, j};
+    const long long pl = static_cast<long long>(m) * d.n2 + j;
     const double2 p0 = dir_at(G, p_prev, beta, idx);
     p[idx] = p0;
     const double2 u0 = u[idx];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const bool fwd = pos[ax] + 1 < len[ax];
-      const double2 gp = fwd ? dsub(dir_at(G, p_prev, beta, idx + st[ax]), p0) : zero2();
-      const double2 gu = fwd ? dsub(u[idx + st[ax]], u0) : zero2();
+      const bool fwd = ax == 0 ? has_fwd(i, d.n1, hl.u_hi) : pos[ax] + 1 < len[ax];
+      double2 pn = zero2(), un = zero2();
+      if (fwd) {
+        if (ax == 0 && i + 1 >= d.n1) {
+          pn = dir_at(hl.G_hi, hl.pp_hi, beta, pl);
+          un = hl.u_hi[pl];
+        } else {
+          pn = dir_at(G, p_prev, beta, idx + st[ax]);
+          un = u[idx + st[ax]];
+        }
+      }
+      const double2 gp = fwd ? dsub(pn, p0) : zero2();
+      const double2 gu = fwd ? dsub(un, u0) : zero2();
       const double2 gd = dsub(gu, g.c[ax][idx]);
       red[0] += dnrm(gp);
       red[1] += dredot(gd, gp);
@@ -148,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) k_axpy(double2* __restrict__ y, cons
 __global__ void __launch_bounds__(kThreads) k_rsp_multiplier(const double2* __restrict__ u, DField3 lam,
                                                              CDField3 psi_old, DField3 psi_new, DevDims d,
                                                              double lc, double thr, double rho_s,
-                                                             double* __restrict__ partials) {
+                                                             double* __restrict__ partials, Halo hl) {
   double red[2] = {0.0, 0.0};
   const int len[3] = {d.n1, d.n0, d.n2};
   const long long st[3] = {d.s0, d.s1, 1};
@@ -159,7 +190,12 @@ __global__ void __launch_bounds__(kThreads) k_rsp_multiplier(const double2* __re
     double msq = 0.0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      gu[ax] = pos[ax] + 1 < len[ax] ? dsub(u[idx + st[ax]], u0) : zero2();
+      if (ax == 0)
+        gu[ax] = has_fwd(i, d.n1, hl.u_hi)
+                     ? dsub(fwd0(u, hl.u_hi, i, d.n1, idx, st[0], static_cast<long long>(m) * d.n2 + j), u0)
+                     : zero2();
+      else
+        gu[ax] = pos[ax] + 1 < len[ax] ? dsub(u[idx + st[ax]], u0) : zero2();
       l[ax] = lam.c[ax][idx];
       z[ax] = dadd(gu[ax], dscale(l[ax], lc));
       msq += dnrm(z[ax]);
@@ -180,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_rsp_multiplier(const double2* __re
 }
 
 __global__ void __launch_bounds__(kThreads) k_tv(const double2* __restrict__ u, DevDims d,
-                                                 double* __restrict__ partials) {
+                                                 double* __restrict__ partials, Halo hl) {
   double red[1] = {0.0};
   const int len[3] = {d.n1, d.n0, d.n2};
   const long long st[3] = {d.s0, d.s1, 1};
@@ -189,8 +225,14 @@ __global__ void __launch_bounds__(kThreads) k_tv(const double2* __restrict__ u, 
     const double2 u0 = u[idx];
     double acc = 0.0;
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax)
-      if (pos[ax] + 1 < len[ax]) acc += dnrm(dsub(u[idx + st[ax]], u0));
+    for (int ax = 0; ax < 3; ++ax) {
+      if (ax == 0) {
+        if (has_fwd(i, d.n1, hl.u_hi))
+          acc += dnrm(dsub(fwd0(u, hl.u_hi, i, d.n1, idx, st[0], static_cast<long long>(m) * d.n2 + j), u0));
+      } else if (pos[ax] + 1 < len[ax]) {
+        acc += dnrm(dsub(u[idx + st[ax]], u0));
+      }
+    }
     red[0] += sqrt(acc);
   });
   write_partials<1>(red, partials);
@@ -285,15 +327,15 @@ void g_init(CDField3 psi, CDField3 lam, DField3 g, std::int64_t n, double lc, cu
 }
 
 int grad_update(const double2* u, CDField3 g, double2* G, const double2* p_prev, const double2* G_prev, Dims d,
-                double rho, double* partials, cudaStream_t s) {
-  k_grad_update<<<grid_blocks(), kThreads, 0, s>>>(u, g, G, p_prev, G_prev, dev_dims(d), rho, partials);
+                double rho, double* partials, cudaStream_t s, const Halo& halo) {
+  k_grad_update<<<grid_blocks(), kThreads, 0, s>>>(u, g, G, p_prev, G_prev, dev_dims(d), rho, partials, halo);
   MLRG_LAUNCH_CHECK("k_grad_update");
   return 3 * grid_blocks();
 }
 
 int direction(const double2* G, const double2* p_prev, double beta, const double2* u, CDField3 g, double2* p,
-              Dims d, double* partials, cudaStream_t s) {
-  k_direction<<<grid_blocks(), kThreads, 0, s>>>(G, p_prev, beta, u, g, p, dev_dims(d), partials);
+              Dims d, double* partials, cudaStream_t s, const Halo& halo) {
+  k_direction<<<grid_blocks(), kThreads, 0, s>>>(G, p_prev, beta, u, g, p, dev_dims(d), partials, halo);
   MLRG_LAUNCH_CHECK("k_direction");
   return 2 * grid_blocks();
 }
@@ -304,15 +346,15 @@ void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s
 }
 
 int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
-                   double rho_over_scale, double* partials, cudaStream_t s) {
+                   double rho_over_scale, double* partials, cudaStream_t s, const Halo& halo) {
   k_rsp_multiplier<<<grid_blocks(), kThreads, 0, s>>>(u, lam, psi_old, psi_new, dev_dims(d), lc, thr,
-                                                      rho_over_scale, partials);
+                                                      rho_over_scale, partials, halo);
   MLRG_LAUNCH_CHECK("k_rsp_multiplier");
   return 2 * grid_blocks();
 }
 
-int tv_norm(const double2* u, Dims d, double* partials, cudaStream_t s) {
-  k_tv<<<grid_blocks(), kThreads, 0, s>>>(u, dev_dims(d), partials);
+int tv_norm(const double2* u, Dims d, double* partials, cudaStream_t s, const Halo& halo) {
+  k_tv<<<grid_blocks(), kThreads, 0, s>>>(u, dev_dims(d), partials, halo);
   MLRG_LAUNCH_CHECK("k_tv");
   return grid_blocks();
 }
