@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-memo-run", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-offload-run", action="store_true")
     ap.add_argument("--same-gpu", action="store_true",
                     help="testing: every rank on cuda:0 with a gloo group (exercises the sharded path on one GPU)")
     return ap.parse_args()
@@ -109,9 +110,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def config_text(n, nt, memo, n_outer=1000000):
+def config_text(n, nt, memo, n_outer=1000000, offload="off"):
     return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
-            f"memoization={memo}\nnudft_path=gridding\n")
+            f"memoization={memo}\nnudft_path=gridding\noffload={offload}\n")
 
 
 def algorithmic(n, nt, kernel):
@@ -189,12 +190,13 @@ def main():
     ctx.sync()
     del ctx
 
-    def timed_run(memo: str, profile_steps: int):
+    def timed_run(memo: str, profile_steps: int, offload: str = "off", steps: int = 0):
         """W warm-up steps, K timed steps (CUDA events on the solver's stream, no
         profiling hooks), then `profile_steps` more with per-kernel event timers."""
         # n_outer = the iterations this run makes (sizes the memo value arena, reserved at setup)
-        solver = m.Solver(config_text(n, nt, memo, args.warmup + args.steps + profile_steps), d, reference=phantom,
-                          stream=stream.cuda_stream, comm=comm)
+        steps = steps or args.steps
+        solver = m.Solver(config_text(n, nt, memo, args.warmup + steps + profile_steps, offload), d,
+                          reference=phantom, stream=stream.cuda_stream, comm=comm)
         for _ in range(args.warmup):
             solver.step()
         m.lib().mlrg_prof_enable(0)
@@ -208,7 +210,7 @@ def main():
             torch.cuda.synchronize()
             ev0.record(stream)
             done = 0
-            for _ in range(args.steps):
+            for _ in range(steps):
                 t0 = time.perf_counter()
                 if not solver.step():
                     break
@@ -258,6 +260,15 @@ def main():
                    "remote_hits": c["remote_hits"], "cache_hits": c["cache_hits"],
                    "hit_rate": hits / c["lookups"] if c["lookups"] else None,
                    "aborted": on["steps_done"] < args.steps, "step_ms": on["step_ms"]}
+
+    offload = None
+    if not args.no_offload_run:
+        # ADMM-Offload: psi, psi_prev, lambda (9 V complex128) in pinned
+        # host memory, streamed through 16-plane chunks on a side stream; bit-identical results
+        of = timed_run("off", profile_steps=0, offload="host", steps=min(args.steps, 5))
+        offload = {"value": 1000.0 * of["steps_done"] / allmax(of["ms"]), "steps": of["steps_done"],
+                   "hbm_bytes_moved_to_host": 9 * 16 * n ** 3 // max(world, 1),
+                   "pcie_bytes_per_iter": 3 * 6 * 16 * n ** 3 // max(world, 1)}
 
     # dominant kernel roofline from the live CUDA-event timers
     P, src = peaks()
@@ -350,7 +361,7 @@ def main():
                    "parallelism": f"z-slab sharded x{world} (16-slab assign(), P2P all-to-all)" if world > 1
                    else "1 GPU",
                    "l2": "no flush: every per-iteration array (134 MB) exceeds the 126 MB L2"},
-        "memo_on": memo_on, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
+        "memo_on": memo_on, "offload": offload, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": off["launches"], "clocks": off["clocks"],
     }
     if rank == 0:

@@ -109,6 +109,10 @@ const std::map<std::string, Setter>& setters() {
        [](RunConfig& c, const std::string& k, const std::string& v) {
          c.engine.kernel = pick<GridKernel>(k, v, {{"es", GridKernel::es}, {"gaussian", GridKernel::gaussian}});
        }},
+      {"offload",  // B200 extension: off (default) | host -- psi, psi_prev, lambda in pinned host memory
+       [](RunConfig& c, const std::string& k, const std::string& v) {
+         c.admm.offload = pick<bool>(k, v, {{"off", false}, {"host", true}});
+       }},
       {"flush_after_apply",
        [](RunConfig& c, const std::string& k, const std::string& v) { c.engine.flush_after_apply = to_bool(k, v); }},
       {"key_dim", [](RunConfig& c, const std::string& k, const std::string& v) { c.encoder.key_dim = to_int(k, v); }},
@@ -214,6 +218,7 @@ std::string RunConfig::str() const {  // config.cpp:160-189
     << "\ninsert_queue_cap = " << memo.insert_queue_cap << "\ncoalesce_bytes = " << memo.coalesce_bytes
     << "\nglobal_cache = " << (memo.global_cache ? "true" : "false") << "\n";
   if (engine.kernel == GridKernel::gaussian) o << "gridding_kernel = gaussian\n";
+  if (admm.offload) o << "offload = host\n";
   return o.str();
 }
 

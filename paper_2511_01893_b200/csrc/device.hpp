@@ -100,6 +100,15 @@ class PinnedBuffer {
   }
   PinnedBuffer(const PinnedBuffer&) = delete;
   PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  PinnedBuffer(PinnedBuffer&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+  PinnedBuffer& operator=(PinnedBuffer&& o) noexcept {
+    if (this != &o) {
+      if (p_) cudaFreeHost(p_);
+      p_ = std::exchange(o.p_, nullptr);
+      n_ = std::exchange(o.n_, 0);
+    }
+    return *this;
+  }
   void reserve(std::size_t n) {
     if (n <= n_) return;
     if (p_) cudaFreeHost(p_);
@@ -118,7 +127,7 @@ class PinnedBuffer {
 /// CTA order, so every reduction is deterministic (no float atomics).
 class Partials {
  public:
-  static constexpr int kMaxSlots = 1 << 16;
+  static constexpr int kMaxSlots = 1 << 20;
   Partials() {
     dev_.resize(static_cast<std::size_t>(kMaxSlots));
     host_.reserve(static_cast<std::size_t>(kMaxSlots));
@@ -128,6 +137,7 @@ class Partials {
   /// of a [count / nv][nv] table.
   std::vector<double> sum(int count, int nv, cudaStream_t s) {
     if (count > kMaxSlots) throw std::logic_error("Partials: too many slots");
+    if (count % nv) throw std::logic_error("Partials: count is not a multiple of nv");
     MLRG_CUDA(cudaMemcpyAsync(host_.get(), dev_.get(), static_cast<std::size_t>(count) * sizeof(double),
                               cudaMemcpyDeviceToHost, s));
     MLRG_CUDA(cudaStreamSynchronize(s));

@@ -25,7 +25,7 @@ namespace mlrg {
 
 constexpr int kSpread = 12;         // nufft.cpp:12
 constexpr int kTaps = 2 * kSpread;  // 24 wrapped grid points per target and dimension (gaussian)
-constexpr int kEsTaps = 12;         // es kernel width (grid cells)
+constexpr int kEsTaps = 10;         // es kernel width (grid cells)
 constexpr double kEsBeta = 2.30 * kEsTaps;
 
 enum class GridKernel : std::uint8_t { es = 0, gaussian = 1 };

@@ -3,6 +3,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <iomanip>
 #include <memory>
@@ -53,7 +54,27 @@ struct State {
   bool have_direction = false;
   std::vector<double> inner_losses;
 
-  State(const Geometry& geo, const Engine& eng, bool baseline, cudaStream_t s) {
+  // ---- ADMM-Offload (AdmmConfig::offload): psi / lambda in pinned host memory ----
+  static constexpr std::int64_t kChunk = 16;  // planes per g_init / RSP launch (both modes)
+  bool offload = false;
+  std::int64_t nchunks = 0;
+  PinnedBuffer<double2> h_psi[3], h_psi_new[3], h_lam[3];
+  DeviceBuffer<double2> c_psi[2][3], c_psi_new[2][3], c_lam[2][3];
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out = nullptr;
+
+  ~State() {
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+    }
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t e : {ev_in[b], ev_done[b]})
+        if (e) cudaEventDestroy(e);
+    if (ev_out) cudaEventDestroy(ev_out);
+  }
+
+  State(const Geometry& geo, const Engine& eng, bool baseline, bool offload_, cudaStream_t s) : offload(offload_) {
     const Shard& sh = eng.shard();
     P0 = geo.n0 * geo.n2;
     V = sh.np() * P0;
@@ -64,11 +85,30 @@ struct State {
       b.zero(s);
     };
     for (auto* b : {&u, &G, &G_prev, &p, &p_prev}) vz(*b, V);
-    for (int c = 0; c < 3; ++c) {
-      vz(psi[c], V);
-      vz(psi_prev[c], V);
-      vz(lam[c], V);
-      vz(g[c], V);
+    for (int c = 0; c < 3; ++c) vz(g[c], V);
+    const std::int64_t np = sh.np();
+    nchunks = (np + kChunk - 1) / kChunk;
+    if (!offload) {
+      for (int c = 0; c < 3; ++c) {
+        vz(psi[c], V);
+        vz(psi_prev[c], V);
+        vz(lam[c], V);
+      }
+    } else {  // pinned host residency + double-buffered device chunks
+      for (int c = 0; c < 3; ++c) {
+        for (auto* hb : {&h_psi[c], &h_psi_new[c], &h_lam[c]}) {
+          hb->reserve(static_cast<std::size_t>(V));
+          std::memset(hb->get(), 0, static_cast<std::size_t>(V) * sizeof(double2));
+        }
+      }
+      const std::int64_t cn = std::min<std::int64_t>(kChunk, np) * P0;
+      for (int b = 0; b < 2; ++b)
+        for (int c = 0; c < 3; ++c)
+          for (auto* db : {&c_psi[b][c], &c_psi_new[b][c], &c_lam[b][c]}) db->resize(static_cast<std::size_t>(cn));
+      MLRG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t* e : {&ev_in[b], &ev_done[b]}) MLRG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      MLRG_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
     }
     if (sh.sharded()) {
       if (baseline) throw std::invalid_argument("admm: pipeline=baseline runs on one GPU only (sharded: optimized)");
@@ -123,7 +163,7 @@ struct SolverState : State {
   MemoCounters prev;
   int outer = 0;
   SolverState(const float2* d_, const AdmmConfig& c, Engine& e, const float2* ref)
-      : State(e.geometry(), e, c.pipeline == Pipeline::baseline, e.stream()),
+      : State(e.geometry(), e, c.pipeline == Pipeline::baseline, c.offload, e.stream()),
         d(d_),
         has_reference(ref != nullptr),
         cfg(c),
@@ -156,6 +196,84 @@ struct SolverState : State {
     push(G.get(), pm_G_hi.get(), sh().rank - 1);
     push(p_prev.get(), pm_pp_hi.get(), sh().rank - 1);
   }
+  // ---- g_init and the fused RSP/multiplier pass, in 16-plane chunks (both modes,
+  // so offload on and off launch identical kernels and reduce identically) ----
+  std::int64_t chunk_planes(std::int64_t k) const { return std::min(kChunk, sh().np() - k * kChunk); }
+  std::size_t chunk_bytes(std::int64_t k) const {
+    return static_cast<std::size_t>(chunk_planes(k) * P0) * sizeof(double2);
+  }
+  void h2d(DeviceBuffer<double2> (&dst)[3], PinnedBuffer<double2> (&src)[3], std::int64_t k) {
+    for (int c = 0; c < 3; ++c)
+      MLRG_CUDA(cudaMemcpyAsync(dst[c].get(), src[c].get() + k * kChunk * P0, chunk_bytes(k), cudaMemcpyHostToDevice,
+                                side));
+  }
+  void d2h(PinnedBuffer<double2> (&dst)[3], DeviceBuffer<double2> (&src)[3], std::int64_t k) {
+    for (int c = 0; c < 3; ++c)
+      MLRG_CUDA(cudaMemcpyAsync(dst[c].get() + k * kChunk * P0, src[c].get(), chunk_bytes(k), cudaMemcpyDeviceToHost,
+                                side));
+  }
+  static DField3 at(DeviceBuffer<double2> (&a)[3], std::int64_t off) {
+    return DField3{{a[0].get() + off, a[1].get() + off, a[2].get() + off}};
+  }
+
+  void g_init_chunks(double lc, cudaStream_t s) {  // g = psi - lambda * lc (admm.cpp:64)
+    for (std::int64_t k = 0; k < nchunks; ++k) {
+      const std::int64_t off = k * kChunk * P0, n = chunk_planes(k) * P0;
+      if (!offload) {
+        ops::g_init(CDField3(at(psi, off)), CDField3(at(lam, off)), at(g, off), n, lc, s);
+        continue;
+      }
+      const int b = static_cast<int>(k & 1);
+      MLRG_CUDA(cudaStreamWaitEvent(side, ev_done[b], 0));  // chunk k-2 is done with buffer b
+      h2d(c_psi[b], h_psi, k);
+      h2d(c_lam[b], h_lam, k);
+      MLRG_CUDA(cudaEventRecord(ev_in[b], side));
+      MLRG_CUDA(cudaStreamWaitEvent(s, ev_in[b], 0));
+      ops::g_init(CDField3(at(c_psi[b], 0)), CDField3(at(c_lam[b], 0)), at(g, off), n, lc, s);
+      MLRG_CUDA(cudaEventRecord(ev_done[b], s));
+    }
+  }
+
+  /// Returns the partial-slot count written (chunk-major).
+  int rsp_chunks(double lc, double thr, double rho_s, double* partials, cudaStream_t s, const Geometry& geo) {
+    int slots = 0;
+    const ops::Halo rank_halo = halo();
+    for (std::int64_t k = 0; k < nchunks; ++k) {
+      const std::int64_t off = k * kChunk * P0, np = chunk_planes(k);
+      const Dims dk{np, geo.n0, geo.n2};
+      ops::Halo hk;  // the plane above the chunk: the next chunk's first, or the rank halo
+      hk.u_hi = k + 1 < nchunks ? u.get() + off + np * P0 : rank_halo.u_hi;
+      if (!offload) {
+        slots += ops::rsp_multiplier(u.get() + off, at(lam, off), CDField3(at(psi, off)), at(psi_prev, off), dk, lc,
+                                     thr, rho_s, partials + slots, s, hk);
+        continue;
+      }
+      const int b = static_cast<int>(k & 1);
+      MLRG_CUDA(cudaStreamWaitEvent(side, ev_done[b], 0));
+      h2d(c_psi[b], h_psi, k);
+      h2d(c_lam[b], h_lam, k);
+      MLRG_CUDA(cudaEventRecord(ev_in[b], side));
+      MLRG_CUDA(cudaStreamWaitEvent(s, ev_in[b], 0));
+      slots += ops::rsp_multiplier(u.get() + off, at(c_lam[b], 0), CDField3(at(c_psi[b], 0)), at(c_psi_new[b], 0), dk,
+                                   lc, thr, rho_s, partials + slots, s, hk);
+      MLRG_CUDA(cudaEventRecord(ev_done[b], s));
+      MLRG_CUDA(cudaStreamWaitEvent(side, ev_done[b], 0));
+      d2h(h_lam, c_lam[b], k);
+      d2h(h_psi_new, c_psi_new[b], k);
+    }
+    if (offload) {  // the host copies are complete before anything reads them
+      MLRG_CUDA(cudaEventRecord(ev_out, side));
+      MLRG_CUDA(cudaStreamWaitEvent(s, ev_out, 0));
+    }
+    return slots;
+  }
+  void swap_psi() {  // psi_prev <- old psi; psi <- new
+    for (int c = 0; c < 3; ++c) {
+      if (offload) std::swap(h_psi[c], h_psi_new[c]);
+      else std::swap(psi[c], psi_prev[c]);
+    }
+  }
+
   ops::Halo halo() const {
     ops::Halo h;
     if (!sh().sharded()) return h;
@@ -223,7 +341,7 @@ bool Solver::step() {
     try {
       const auto t0 = clock::now();
       // ---- LSP (admm.cpp:59-118, 122-152) ----
-      ops::g_init(CDField3(st.f(st.psi)), CDField3(st.f(st.lam)), st.f(st.g), st.V, st.lam_scale / st.rho, s);
+      st.g_init_chunks(st.lam_scale / st.rho, s);
       st.push_g0();
       st.have_direction = false;
       const std::size_t phase_start = st.inner_losses.size();
@@ -290,12 +408,9 @@ bool Solver::step() {
         MLRG_CUDA(cudaStreamSynchronize(s));
         eng.shard().comm->barrier();
       }
-      const std::vector<double> rs =
-          sum(ops::rsp_multiplier(st.u.get(), st.f(st.lam), CDField3(st.f(st.psi)), st.f(st.psi_prev), dims,
-                                  st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s,
-                                  st.halo()),
-              2);
-      for (int c = 0; c < 3; ++c) std::swap(st.psi[c], st.psi_prev[c]);  // psi_prev <- old psi
+      const std::vector<double> rs = sum(
+          st.rsp_chunks(st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s, geo), 2);
+      st.swap_psi();
       const auto t2 = clock::now();
       const double r = std::sqrt(rs[0]);
       const double sres = st.rho * std::sqrt(rs[1]);

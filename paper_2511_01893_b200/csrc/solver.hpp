@@ -28,6 +28,11 @@ struct AdmmConfig {  // admm.hpp:19-30
   Pipeline pipeline = Pipeline::optimized;
   MemoMode memoization = MemoMode::off;
   bool freeze_rho = false;
+  /// B200 extension (ADMM-Offload): psi, psi_prev and
+  /// lambda live in pinned host memory and stream through the device in
+  /// 16-plane chunks on a side stream around g_init and the RSP/multiplier pass;
+  /// results are bit-identical to offload off.
+  bool offload = false;
   void validate() const;
 };
 

@@ -1,7 +1,7 @@
 """The spreading-kernel claim of DESIGN.md §4: the reference's 24-tap Gaussian
-gridding and the B200 build's default 12-tap exponential-of-semicircle (ES)
+gridding and the B200 build's default 10-tap exponential-of-semicircle (ES)
 kernel both reproduce the direct NUDFT (operators.cpp:133-200), to 3e-12 and
-2e-11 respectively. The ES plan below restates csrc/geometry.cpp DimPlan::make
+2e-9 respectively (10x below the complex64 rounding of the outputs, 2.6e-8). The ES plan below restates csrc/geometry.cpp DimPlan::make
 (kernel = es) in numpy; CPU only."""
 import math
 
@@ -9,7 +9,7 @@ import numpy as np
 
 import mlr_oracle as O
 
-W, BETA = 12, 2.30 * 12
+W, BETA = 10, 2.30 * 10
 
 
 def es_plan(n, freqs):
@@ -52,4 +52,4 @@ def test_gaussian_and_es_gridding_match_direct_nudft():
     exact = O.fu2d_direct(v, g)
     rel = lambda a: np.linalg.norm(a - exact) / np.linalg.norm(exact)
     assert rel(O.fu2d_gridding(v, g)) < 1e-11
-    assert rel(fu2d_es(v, g)) < 1e-10
+    assert rel(fu2d_es(v, g)) < 5e-9
