@@ -151,11 +151,25 @@ __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, 
     const int k = gg & (ns - 1);
     if (logns > 0) {
       const int step = k << (logm - logns - LOGR);  // k m / (ns R)
+      // w^r for r < R from the table entries w, w^2, w^4 and products (the
+      // twiddle loads share the L1/shared-memory pipe with the data, which
+      // bounds these passes; the products are exact to a few double ulps)
+      double2 w[8];
+      w[1] = tw[step];
+      if constexpr (R >= 4) {
+        w[2] = tw[2 * step];
+        w[3] = cmul(w[1], w[2]);
+      }
+      if constexpr (R == 8) {
+        w[4] = tw[4 * step];
+        w[5] = cmul(w[4], w[1]);
+        w[6] = cmul(w[4], w[2]);
+        w[7] = cmul(w[4], w[3]);
+      }
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 w = tw[step * r];
-        if (SIGN < 0) w.y = -w.y;
-        v[q * R + r] = cmul(v[q * R + r], w);
+        if (SIGN < 0) w[r].y = -w[r].y;
+        v[q * R + r] = cmul(v[q * R + r], w[r]);
       }
     }
     fft_reg<R, SIGN>(v + q * R);

@@ -63,7 +63,7 @@ int pass_cols(std::int64_t m) {
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
 template <class TIn, int W>
-__global__ void __launch_bounds__(512) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
+__global__ void __launch_bounds__(512, 2) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
                                               const double* __restrict__ wts, const double2* __restrict__ fac,
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(512) k_fu1d(const TIn* __restrict__ u, float2*
 }
 
 template <class TOut>
-__global__ void __launch_bounds__(512) k_fu1d_adj(const float2* __restrict__ v, TOut* __restrict__ out, int n0,
+__global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ v, TOut* __restrict__ out, int n0,
                                                   int n2, int h, int logm, int center, int ncol,
                                                   const double2* __restrict__ cphase,
                                                   const int* __restrict__ cell_ptr, const int* __restrict__ cell_k,
@@ -637,7 +637,7 @@ int sm_count() {
 struct Usfft::Tables {
   // fu1d
   DimPlan pz;
-  int z_ncol = 0;
+  int z_ncol = 0, z_ncol_adj = 0;
   DeviceBuffer<double> z_deconv, z_pdeconv;
   DeviceBuffer<double> z_w, z_cell_w;
   DeviceBuffer<int> z_start, z_cell_ptr, z_cell_k;
@@ -673,7 +673,16 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   const int W = t.pz.taps;
   const DimPlan& pz = t.pz;
   t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / pz.m, 1, 64));
+  t.z_ncol_adj = t.z_ncol;
+  // fu1d: 8 columns per CTA (512 threads at m = 512) make every global row
+  // segment a full 128 B line and every shared-memory phase one grid row
+  // (conflict-free taps); fu1d_adj keeps the smaller tile (its spread stage
+  // holds h extra rows per column).
+  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(4096 / pz.m, 1, 64));
+  if (const char* e = std::getenv("MLRG_FU1D_NCOL"))  // tuning override (threads = ncol * m / 8 <= 512)
+    t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 4096 / pz.m)));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
+  t.z_ncol_adj = static_cast<int>(std::min<std::int64_t>(t.z_ncol_adj, g_.n2));
   t.z_deconv.upload(pz.deconv, stream_);
   std::vector<double> pdec(pz.deconv.size());
   for (std::size_t i = 0; i < pdec.size(); ++i) pdec[i] = pz.pref * pz.deconv[i];
@@ -934,7 +943,7 @@ template <class TOut>
 void Usfft::fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0) {
   if (d0 <= 0) return;
   const Tables& t = *t_;
-  const int ncol = t.z_ncol;
+  const int ncol = t.z_ncol_adj;
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
   const std::size_t smem = static_cast<std::size_t>((t.pz.m + g_.h) * ncol) * sizeof(double2);
   prof::begin("k_fu1d_adj", stream_);
