@@ -357,6 +357,20 @@ void Engine::fu1d(const double2* u, float2* out, bool memoize) {
   if (!shard_.sharded()) return apply(OpId::fu1d, false, u, true, nullptr, out, false, memoize);
   if (out != mid_.get()) throw std::invalid_argument("sharded fu1d: output must be the engine's mid()");
   exchange_fence();  // every rank is done reading its mid block
+  if (!(memoize && cfg_.memo_enabled) && shard_.world <= PeerOut::kMax) {
+    // fused: k_fu1d stores each detector row straight into its owner's mid block
+    PeerOut po;
+    po.world = shard_.world;
+    po.off = shard_.a();
+    for (int r = 0; r < shard_.world; ++r) {
+      po.lo[r] = shard_.rows[static_cast<std::size_t>(r)].first;
+      po.hi[r] = shard_.rows[static_cast<std::size_t>(r)].second;
+      po.dst[r] = static_cast<float2*>(mid_peers_->at(r));
+    }
+    usfft_.fu1d(u, nullptr, shard_.np(), &po);
+    exchange_fence();
+    return;
+  }
   apply(OpId::fu1d, false, u, true, nullptr, stage1_.get(), false, memoize);
   ops::RankTable t;
   t.world = shard_.world;
@@ -388,6 +402,21 @@ void Engine::fu2d_adj(const float2* p, float2* out, bool memoize) {
   if (!shard_.sharded()) return apply(OpId::fu2d_adj, false, p, false, nullptr, out, false, memoize);
   if (out != mid2_.get()) throw std::invalid_argument("sharded fu2d_adj: output must be the engine's mid2()");
   exchange_fence();
+  if (!(memoize && cfg_.memo_enabled) && shard_.world <= PeerOut::kMax) {
+    // fused: the row pass stores each plane straight into its owner's mid2 block
+    PeerOut po;
+    po.world = shard_.world;
+    po.off = shard_.c();
+    po.h = g_.h;
+    for (int r = 0; r < shard_.world; ++r) {
+      po.lo[r] = shard_.planes[static_cast<std::size_t>(r)].first;
+      po.hi[r] = shard_.planes[static_cast<std::size_t>(r)].second;
+      po.dst[r] = static_cast<float2*>(mid2_peers_->at(r));
+    }
+    usfft_.fu2d_adj(p, shard_.nr(), 0, shard_.nr(), nullptr, 0, 0, &po);
+    exchange_fence();
+    return;
+  }
   apply(OpId::fu2d_adj, false, p, false, nullptr, stage2_.get(), false, memoize);
   ops::RankTable t;
   t.world = shard_.world;

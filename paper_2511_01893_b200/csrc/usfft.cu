@@ -20,6 +20,7 @@
 #include <complex>
 #include <cstdlib>
 #include <numbers>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -62,12 +63,12 @@ int pass_cols(std::int64_t m) {
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
-template <class TIn, int W>
+template <class TIn, int W, bool PEER>
 __global__ void __launch_bounds__(512, 2) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
                                               const double* __restrict__ wts, const double2* __restrict__ fac,
-                                              const double2* __restrict__ tw) {
+                                              const double2* __restrict__ tw, PeerOut po) {
   extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
   const int j0 = blockIdx.x * ncol;
@@ -97,7 +98,13 @@ __global__ void __launch_bounds__(512, 2) k_fu1d(const TIn* __restrict__ u, floa
       acc.x = fma(g.x, wa, acc.x);
       acc.y = fma(g.y, wa, acc.y);
     }
-    oi[static_cast<long long>(k) * n2 + j] = to_f(cmul(acc, fac[k]));
+    float2* dst = oi + static_cast<long long>(k) * n2;
+    if constexpr (PEER) {  // fused all-to-all: detector row k goes to the rank that owns it
+      int r = 0;
+      while (r + 1 < po.world && k >= po.hi[r]) ++r;
+      dst = po.dst[r] + ((po.off + blockIdx.y) * (po.hi[r] - po.lo[r]) + (k - po.lo[r])) * n2;
+    }
+    dst[j] = to_f(cmul(acc, fac[k]));
   }
 }
 
@@ -514,21 +521,29 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const floa
 }
 
 // Row FFT(-1) and the final deconvolution into out[i, k0_out+kk, j].
+template <bool PEER>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
-                                                       long long k0_out) {
+                                                       long long k0_out, PeerOut po) {
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
   const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   const double pi = pdx[i];
+  // plane i of the output: local, or (fused all-to-all) in the HBM of the rank owning plane i
+  float2* oplane = out + static_cast<long long>(i) * ld_out * n2;
+  if constexpr (PEER) {
+    int r = 0;
+    while (r + 1 < po.world && i >= po.hi[r]) ++r;
+    oplane = po.dst[r] + (i - po.lo[r]) * po.h * n2;
+    k0_out += po.off;
+  }
   auto load = [&](int c, int kk) { return to_d(Si[static_cast<long long>(c) * KB + kk]); };
   auto store = [&](int slot, int kk, double2 x) {
     const int j = (slot + center2) & mask2;
-    if (j < n2 && ks + kk < nk)
-      out[(static_cast<long long>(i) * ld_out + k0_out + ks + kk) * n2 + j] = to_f(cscale(x, pi * dy[j]));
+    if (j < n2 && ks + kk < nk) oplane[(k0_out + ks + kk) * n2 + j] = to_f(cscale(x, pi * dy[j]));
   };
   fft_stockham<-1, true, true>(sd, logm2, ks_n, sm, tw2, load, store);
 }
@@ -898,10 +913,12 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   MLRG_CUDA(cudaStreamSynchronize(stream_));
   static bool smem_set = [] {
-    allow_big_smem(k_fu1d<float2, kEsTaps>);
-    allow_big_smem(k_fu1d<double2, kEsTaps>);
-    allow_big_smem(k_fu1d<float2, kTaps>);
-    allow_big_smem(k_fu1d<double2, kTaps>);
+    allow_big_smem(k_fu1d<float2, kEsTaps, false>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, false>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, true>);
+    allow_big_smem(k_fu1d<float2, kTaps, false>);
+    allow_big_smem(k_fu1d<double2, kTaps, false>);
+    allow_big_smem(k_fu1d<double2, kTaps, true>);
     allow_big_smem(k_fu1d_adj<float2>);
     allow_big_smem(k_fu1d_adj<double2>);
     allow_big_smem(k_fu2d_rows);
@@ -909,7 +926,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     allow_big_smem(k_fu2d_adj_spread<kTaps>);
     allow_big_smem(k_fu2d_cols);
     allow_big_smem(k_fu2d_adj_cols);
-    allow_big_smem(k_fu2d_adj_rows);
+    allow_big_smem(k_fu2d_adj_rows<false>);
+    allow_big_smem(k_fu2d_adj_rows<true>);
     allow_big_smem(k_center_fft_rows<+1>);
     allow_big_smem(k_center_fft_rows<-1>);
     allow_big_smem(k_center_fft_cols<+1>);
@@ -924,17 +942,20 @@ Usfft::~Usfft() { delete t_; }
 int Usfft::reduce_grid() const { return 4 * sm_count(); }
 
 template <class TIn>
-void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0) {
+void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0, const PeerOut* peer) {
   if (d0 <= 0) return;
   const Tables& t = *t_;
   const int ncol = t.z_ncol;
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
   const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(double2);
   prof::begin("k_fu1d", stream_);
-  auto kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps> : k_fu1d<TIn, kTaps>;
+  auto kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps, false> : k_fu1d<TIn, kTaps, false>;
+  if constexpr (std::is_same_v<TIn, double2>)
+    if (peer) kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps, true> : k_fu1d<TIn, kTaps, true>;
   kern<<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                      static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
-                                     t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get());
+                                     t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get(),
+                                     peer ? *peer : PeerOut{});
   MLRG_LAUNCH_CHECK("k_fu1d");
   prof::end("k_fu1d", stream_);
 }
@@ -955,8 +976,8 @@ void Usfft::fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0) {
   prof::end("k_fu1d_adj", stream_);
 }
 
-void Usfft::fu1d(const float2* u, float2* out, std::int64_t d0) { fu1d_t(u, out, d0); }
-void Usfft::fu1d(const double2* u, float2* out, std::int64_t d0) { fu1d_t(u, out, d0); }
+void Usfft::fu1d(const float2* u, float2* out, std::int64_t d0) { fu1d_t(u, out, d0, nullptr); }
+void Usfft::fu1d(const double2* u, float2* out, std::int64_t d0, const PeerOut* peer) { fu1d_t(u, out, d0, peer); }
 void Usfft::fu1d_adj(const float2* v, float2* out, std::int64_t d0) { fu1d_adj_t(v, out, d0); }
 void Usfft::fu1d_adj(const float2* v, double2* out, std::int64_t d0) { fu1d_adj_t(v, out, d0); }
 
@@ -997,7 +1018,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
 }
 
 void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
-                     std::int64_t ld_out, std::int64_t k0_out) {
+                     std::int64_t ld_out, std::int64_t k0_out, const PeerOut* peer) {
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
@@ -1029,10 +1050,10 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     prof::end("k_fu2d_adj_cols", stream_);
     prof::begin("k_fu2d_adj_rows", stream_);
-    k_fu2d_adj_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
+    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
                       static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
         t.S.get(), nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
-        t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b);
+        t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b, peer ? *peer : PeerOut{});
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
     prof::end("k_fu2d_adj_rows", stream_);
   }

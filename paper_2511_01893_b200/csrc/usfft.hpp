@@ -34,6 +34,19 @@ struct Fu2dEpilogue {
   bool reduce = false;
 };
 
+/// Sharded output of fu1d / fu2d_adj (the fused all-to-all):
+/// the producing kernel stores every output row straight into the HBM of the
+/// rank that owns it (CUDA IPC mappings, P2P over NVLink), so the exchange
+/// overlaps the transform tile by tile. world == 0: plain local output.
+struct PeerOut {
+  static constexpr int kMax = 8;
+  int world = 0;
+  std::int64_t lo[kMax] = {}, hi[kMax] = {};  // owned range per rank (rows for fu1d, planes for fu2d_adj)
+  float2* dst[kMax] = {};                     // each rank's destination block
+  std::int64_t off = 0;  // fu1d: global plane of local plane 0; fu2d_adj: global row of local row 0
+  std::int64_t h = 0;    // fu2d_adj: detector rows of the destination blocks
+};
+
 class Usfft {
  public:
   static constexpr int kRowBatch = 16;  // detector rows per fu2d grid batch
@@ -50,7 +63,7 @@ class Usfft {
   /// u: contiguous (d0, n0, n2) -> out (d0, h, n2). The volume side may be
   /// complex128 (the solver's iterate); the transform runs in complex64.
   void fu1d(const float2* u, float2* out, std::int64_t d0);
-  void fu1d(const double2* u, float2* out, std::int64_t d0);
+  void fu1d(const double2* u, float2* out, std::int64_t d0, const PeerOut* peer = nullptr);
   /// v: contiguous (d0, h, n2) -> out (d0, n0, n2).
   void fu1d_adj(const float2* v, float2* out, std::int64_t d0);
   void fu1d_adj(const float2* v, double2* out, std::int64_t d0);
@@ -62,7 +75,7 @@ class Usfft {
   /// Rows [k0, k0+nk) of an (n_theta, ld, w) array -> rows [k0_out, k0_out+nk)
   /// of an (n1, ld_out, n2) array.
   void fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
-                std::int64_t ld_out, std::int64_t k0_out);
+                std::int64_t ld_out, std::int64_t k0_out, const PeerOut* peer = nullptr);
 
   /// Centred unitary 2D DFT of `count` contiguous (h, w) planes.
   void f2d(const float2* p, float2* out, std::int64_t count, bool adjoint);
@@ -72,7 +85,7 @@ class Usfft {
 
  private:
   template <class TIn>
-  void fu1d_t(const TIn* u, float2* out, std::int64_t d0);
+  void fu1d_t(const TIn* u, float2* out, std::int64_t d0, const PeerOut* peer);
   template <class TOut>
   void fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0);
   struct Tables;
