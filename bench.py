@@ -357,7 +357,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "c64 (fp32)", "data": "synthetic (blocks phantom seed 1, d = forward_L on GPU)",
         "config": {"workload": f"configs[1]: {n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)",
                    "n": n, "n_theta": nt, "n_inner": 4, "memo": "off",
-                   "nudft": "gridding, 12-tap ES kernel (NUDFT to 2e-11; reference: 24-tap Gaussian, 3e-12)",
+                   "nudft": "gridding, 10-tap ES kernel (NUDFT to 2e-9; reference: 24-tap Gaussian, 3e-12)",
                    "parallelism": f"z-slab sharded x{world} (16-slab assign(), P2P all-to-all)" if world > 1
                    else "1 GPU",
                    "l2": "no flush: every per-iteration array (134 MB) exceeds the 126 MB L2"},

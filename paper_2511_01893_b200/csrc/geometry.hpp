@@ -8,10 +8,10 @@
 //             dimension, tau = pi*12 / (n^2 sigma (sigma - 1/2)); it matches
 //             the direct NUDFT to ~3e-12 relative.
 //   es        exponential-of-semicircle kernel exp(beta (sqrt(1 - z^2) - 1)),
-//             12 taps, beta = 2.30 * 12, same oversampled grid (sigma = 2),
+//             10 taps, beta = 2.30 * 10, same oversampled grid (sigma = 2),
 //             deconvolved by its Fourier transform (Gauss-Legendre quadrature):
-//             ~2e-11 relative to the direct NUDFT, i.e. within 3e-11 of the
-//             reference's gridding, with 4x fewer taps in two dimensions. Its
+//             ~2e-9 relative to the direct NUDFT (10x below the complex64
+//             rounding of the outputs), with 5.8x fewer taps in two dimensions. Its
 //             deconvolution spans 4.8x per dimension instead of the Gaussian's
 //             23x, so the complex64 grid rounding is amplified less.
 #pragma once
