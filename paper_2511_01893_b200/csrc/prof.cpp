@@ -62,7 +62,7 @@ void begin(const char* name, cudaStream_t s) {
   MLRG_CUDA(cudaEventCreate(&e));
   MLRG_CUDA(cudaEventRecord(e, s));
   std::lock_guard<std::mutex> lk(g_mx);
-  open_events()[name] = e;
+  open_events()[std::string(name) + "@" + std::to_string(reinterpret_cast<std::uintptr_t>(s))] = e;
 }
 
 void end(const char* name, cudaStream_t s) {
@@ -71,7 +71,7 @@ void end(const char* name, cudaStream_t s) {
   MLRG_CUDA(cudaEventCreate(&e));
   MLRG_CUDA(cudaEventRecord(e, s));
   std::lock_guard<std::mutex> lk(g_mx);
-  auto it = open_events().find(name);
+  auto it = open_events().find(std::string(name) + "@" + std::to_string(reinterpret_cast<std::uintptr_t>(s)));
   if (it == open_events().end()) return;
   spans()[name].push_back({it->second, e});
   open_events().erase(it);

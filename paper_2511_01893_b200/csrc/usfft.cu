@@ -53,6 +53,14 @@ std::int64_t fft_elems() {
   }();
   return e;
 }
+// fu2d row batches alternate between two streams (MLRG_FU2D_PIPE=0 disables).
+bool pipelined() {
+  static const bool on = [] {
+    const char* e = std::getenv("MLRG_FU2D_PIPE");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
 // k-columns per CTA of a 2D-grid FFT pass over length m.
 int pass_cols(std::int64_t m) {
   int c = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / m, 1, KB));
@@ -667,6 +675,13 @@ struct Usfft::Tables {
   DeviceBuffer<double> t_w1, t_w2;  // [C][W]
   DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint class values
+  // fu2d runs its row batches on two streams (the second set of grids and
+  // partial slots belongs to the side stream) so one batch's gather overlaps the
+  // next batch's FFT passes
+  DeviceBuffer<float2> S2, Gd2, val2;
+  DeviceBuffer<double2> partial2;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
   int nitems = 0, nsplit = 0;
   DeviceBuffer<int> patch_t;
@@ -937,7 +952,25 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   (void)smem_set;
 }
 
-Usfft::~Usfft() { delete t_; }
+void Usfft::ensure_side() {
+  Tables& t = *t_;
+  if (t.side) return;
+  MLRG_CUDA(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
+  MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
+  MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_join, cudaEventDisableTiming));
+  t.S2.resize(t.S.size());
+  t.Gd2.resize(t.Gd.size());
+}
+
+Usfft::~Usfft() {
+  if (t_->side) {
+    cudaStreamSynchronize(t_->side);
+    cudaStreamDestroy(t_->side);
+  }
+  if (t_->ev_fork) cudaEventDestroy(t_->ev_fork);
+  if (t_->ev_join) cudaEventDestroy(t_->ev_join);
+  delete t_;
+}
 
 int Usfft::reduce_grid() const { return 4 * sm_count(); }
 
@@ -988,74 +1021,112 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const int per_cta = gather_per_cta();
   const int ggrid = (t.nclass + per_cta - 1) / per_cta;
   auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
-  for (std::int64_t b = 0; b < nk; b += KB) {
+  Tables& tm = *t_;
+  const bool pipe = nk > KB && pipelined();
+  if (pipe) {
+    ensure_side();
+    MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));  // inputs and partial slots ready
+    MLRG_CUDA(cudaStreamWaitEvent(tm.side, tm.ev_fork, 0));
+  }
+  int bi = 0;
+  for (std::int64_t b = 0; b < nk; b += KB, ++bi) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
-    prof::begin("k_fu2d_rows", stream_);
+    const bool alt = pipe && (bi & 1);
+    cudaStream_t s = alt ? tm.side : stream_;
+    float2* S = alt ? tm.S2.get() : t.S.get();
+    float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
+    prof::begin("k_fu2d_rows", s);
     k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
-                  static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
+                  static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), s>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
-        t.y_deconv.get(), t.y_tw.get(), t.S.get());
+        t.y_deconv.get(), t.y_tw.get(), S);
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
-    prof::end("k_fu2d_rows", stream_);
-    prof::begin("k_fu2d_cols", stream_);
+    prof::end("k_fu2d_rows", s);
+    prof::begin("k_fu2d_cols", s);
     k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
-                  static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
-        t.S.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(),
-        t.Gd.get());
+                  static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+        S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd);
     MLRG_LAUNCH_CHECK("k_fu2d_cols");
-    prof::end("k_fu2d_cols", stream_);
+    prof::end("k_fu2d_cols", s);
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
-    prof::begin("k_fu2d_gather", stream_);
-    gather<<<ggrid, 32 * kGatherWarps, 0, stream_>>>(t.Gd.get(), t.nclass, static_cast<int>(g_.w), t.px.logm,
-                                                     t.py.logm, nb, t.t_r0.get(), t.t_c0.get(), t.t_w1.get(),
-                                                     t.t_w2.get(), t.m_first.get(), t.m_tidx.get(), t.m_fac.get(),
-                                                     eo, per_cta, partials_.dev(), b > 0 ? 1 : 0);
+    prof::begin("k_fu2d_gather", s);
+    // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
+    gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(Gd, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
+                                               t.t_r0.get(), t.t_c0.get(), t.t_w1.get(), t.t_w2.get(),
+                                               t.m_first.get(), t.m_tidx.get(), t.m_fac.get(), eo, per_cta,
+                                               partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
-    prof::end("k_fu2d_gather", stream_);
+    prof::end("k_fu2d_gather", s);
   }
-  return epi.reduce && nk > 0 ? 2 * ggrid : 0;
+  if (pipe) {
+    MLRG_CUDA(cudaEventRecord(tm.ev_join, tm.side));
+    MLRG_CUDA(cudaStreamWaitEvent(stream_, tm.ev_join, 0));
+  }
+  return epi.reduce && nk > 0 ? (pipe ? 4 : 2) * ggrid : 0;
 }
 
 void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
                      std::int64_t ld_out, std::int64_t k0_out, const PeerOut* peer) {
   const Tables& t = *t_;
-  const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  for (std::int64_t b = 0; b < nk; b += KB) {
+  Tables& tm = *t_;
+  const bool pipe = nk > KB && pipelined();  // row batches alternate between two streams, as in fu2d
+  if (pipe) {
+    ensure_side();
+    if (tm.val2.size() != tm.val.size()) {
+      tm.val2.resize(tm.val.size());
+      tm.partial2.resize(tm.partial.size());
+    }
+    MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));
+    MLRG_CUDA(cudaStreamWaitEvent(tm.side, tm.ev_fork, 0));
+  }
+  int bi = 0;
+  for (std::int64_t b = 0; b < nk; b += KB, ++bi) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
-    prof::begin("k_fu2d_adj_prep", stream_);
-    k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, stream_>>>(
-        p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(),
-        t.val.get());
+    const bool alt = pipe && (bi & 1);
+    cudaStream_t s = alt ? tm.side : stream_;
+    float2* S = alt ? tm.S2.get() : t.S.get();
+    float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
+    float2* val = alt ? tm.val2.get() : t.val.get();
+    double2* partial = alt ? tm.partial2.get() : t.partial.get();
+    prof::begin("k_fu2d_adj_prep", s);
+    k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, s>>>(
+        p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(), val);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
-    prof::end("k_fu2d_adj_prep", stream_);
-    prof::begin("k_fu2d_adj_spread", stream_);
+    prof::end("k_fu2d_adj_prep", s);
+    prof::begin("k_fu2d_adj_spread", s);
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
-    spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), stream_>>>(
-        t.val.get(), t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
-        t.t_w1.get(), t.t_w2.get(), t.Gd.get(), t.partial.get());
+    spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
+                                                               t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
+                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     if (t.nsplit > 0) {
-      k_fu2d_adj_spread_reduce<<<(t.nsplit + kReduceWarps - 1) / kReduceWarps, 32 * kReduceWarps, 0, stream_>>>(
-          t.nsplit, t.split.get(), t.py.logm, t.partial.get(), t.Gd.get());
+      k_fu2d_adj_spread_reduce<<<(t.nsplit + kReduceWarps - 1) / kReduceWarps, 32 * kReduceWarps, 0, s>>>(
+          t.nsplit, t.split.get(), t.py.logm, partial, Gd);
       MLRG_LAUNCH_CHECK("k_fu2d_adj_spread_reduce");
     }
-    prof::end("k_fu2d_adj_spread", stream_);
-    prof::begin("k_fu2d_adj_cols", stream_);
+    prof::end("k_fu2d_adj_spread", s);
+    prof::begin("k_fu2d_adj_cols", s);
     k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
-                      static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), stream_>>>(
-        t.Gd.get(), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1,
-        t.x_tw.get(), t.S.get());
+                      static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+        Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
-    prof::end("k_fu2d_adj_cols", stream_);
-    prof::begin("k_fu2d_adj_rows", stream_);
-    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
-                      static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), stream_>>>(
-        t.S.get(), nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
+    prof::end("k_fu2d_adj_cols", s);
+    prof::begin("k_fu2d_adj_rows", s);
+    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2),
+                                                              static_cast<unsigned>(ks2 * t.py.m / 8),
+                                                              static_cast<std::size_t>(t.py.m * (ks2 + 1)) *
+                                                                  sizeof(double2),
+                                                              s>>>(
+        S, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
         t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b, peer ? *peer : PeerOut{});
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
-    prof::end("k_fu2d_adj_rows", stream_);
+    prof::end("k_fu2d_adj_rows", s);
+  }
+  if (pipe) {
+    MLRG_CUDA(cudaEventRecord(tm.ev_join, tm.side));
+    MLRG_CUDA(cudaStreamWaitEvent(stream_, tm.ev_join, 0));
   }
 }
 

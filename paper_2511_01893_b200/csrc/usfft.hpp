@@ -88,6 +88,7 @@ class Usfft {
   void fu1d_t(const TIn* u, float2* out, std::int64_t d0, const PeerOut* peer);
   template <class TOut>
   void fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0);
+  void ensure_side();  // second stream + grids for the pipelined row batches
   struct Tables;
   Geometry g_;
   cudaStream_t stream_;
