@@ -140,7 +140,17 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   }
   const double want = static_cast<double>(rc.admm.n_outer) * per_iter * static_cast<double>(slab) * sizeof(float2);
   const std::size_t bytes = static_cast<std::size_t>(std::min(want, 0.45 * static_cast<double>(free_b)));
-  if (comm && comm->world() > 1) ec.memo_arena_bytes = bytes;
+  // one GPU: the lookups run on the device (memo_gpu.hpp) unless the config needs
+  // the host client (global cache, baseline pipeline's memoized f2d, other slab
+  // sizes) or MLRG_DEVICE_MEMO=0 asks for it
+  const char* dm = std::getenv("MLRG_DEVICE_MEMO");
+  ec.device_memo = !(comm && comm->world() > 1) && !(dm && *dm == '0') && !rc.memo.global_cache &&
+                   rc.admm.pipeline == mlrg::Pipeline::optimized && ec.chunk_extent == 16 && rc.encoder.key_dim <= 64;
+  ec.memo_max_keys = std::min<std::int64_t>(
+      std::int64_t{1} << 20,
+      static_cast<std::int64_t>(rc.admm.n_outer) * static_cast<std::int64_t>(rc.memo.insert_queue_cap) +
+          static_cast<std::int64_t>(rc.memo.insert_queue_cap) + 1);
+  if ((comm && comm->world() > 1) || ec.device_memo) ec.memo_arena_bytes = bytes;
   else store->arena().reserve(bytes);
   auto client = std::make_shared<mlrg::MemoClient>(rc.memo, store);
   auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);

@@ -17,6 +17,7 @@
 #include "encoder.hpp"
 #include "geometry.hpp"
 #include "memo.hpp"
+#include "memo_gpu.hpp"
 #include "shard.hpp"
 #include "usfft.hpp"
 
@@ -28,7 +29,9 @@ struct EngineConfig {  // scalerun.hpp:27-42
   bool memo_enabled = false;
   bool flush_after_apply = false;
   GridKernel kernel = GridKernel::es;  // B200 extension key `gridding_kernel` (geometry.hpp)
-  std::size_t memo_arena_bytes = 0;    // sharded memo: HBM reserved per rank for values
+  std::size_t memo_arena_bytes = 0;    // HBM reserved for memo values (sharded: per rank)
+  bool device_memo = false;            // lookups on the device (memo_gpu.hpp); set by the assembler
+  std::int64_t memo_max_keys = 0;      // device key index capacity
 };
 
 struct ChunkAudit {  // scalerun.hpp:45-54
@@ -64,6 +67,10 @@ class Engine {
 
   void set_iteration(int it) { iteration_ = it; }
   void flush_inserts();
+  /// Device-side memo: moves the decisions made so far into audit_log() and the
+  /// client's counters without publishing the staged inserts (an aborted
+  /// iteration). No-op otherwise.
+  void drain_memo_log();
   const std::vector<ChunkAudit>& audit_log() const { return audit_; }
 
   /// Sharded mode: the exchange targets (nullptr when unsharded).
@@ -93,6 +100,10 @@ class Engine {
  private:
   void apply(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
              bool memoize);
+  void apply_device_memo(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d);
+  void encode_slabs(OpId op, const void* in, bool in_d, int axis, const Shape3& ishape,
+                    const std::vector<std::int64_t>& ext, const std::vector<std::int64_t>& starts);
+  void take_device_audit(bool publish);
   void compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
                std::int64_t start, std::int64_t extent);
   Shape3 in_shape(OpId op) const;   // this rank's input array
@@ -122,6 +133,7 @@ class Engine {
   std::unique_ptr<PeerMemory> arena_peers_;
   std::size_t arena_cap_ = 0;
   std::vector<std::size_t> arena_next_;
+  std::unique_ptr<DeviceMemo> dmemo_;
 };
 
 }  // namespace mlrg

@@ -22,6 +22,8 @@
 
 namespace mlrg {
 
+struct DevSlab;  // memo_gpu.hpp
+
 /// Volume extents for the stencil kernels (row-major (n1, n0, n2)).
 struct Dims {
   std::int64_t n1 = 0, n0 = 0, n2 = 0;
@@ -139,6 +141,16 @@ void slab_materialize(double2* out, SlabGeom g, const SlabBatch& b, int nb, cuda
 /// and then out[slab_q] -= sub[slab_q] when sub is set (scalerun.cpp:276-283).
 void slab_store(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s);
 void slab_store(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream_t s);
+
+/// Device-side memo: the same copies driven by the per-slab decisions in HBM
+/// (slab c = [c * chunk, ...) along g.axis): hits get value * scale (- sub),
+/// misses are copied to their arena slot (when accepted) and then get out -= sub.
+void dev_materialize(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+                     cudaStream_t s);
+void dev_materialize(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s);
+void dev_store(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+               cudaStream_t s);
+void dev_store(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s);
 
 }  // namespace ops
 }  // namespace mlrg

@@ -76,6 +76,9 @@ class MemoStore {
   std::uint64_t key_count() const;
   bool trained() const { return trained_; }
   const std::vector<std::vector<float>>& centroids() const { return centroids_; }
+  /// Member ids per IVF cluster (insertion order), for the device mirror.
+  std::vector<std::vector<std::uint64_t>> cluster_ids() const;
+  const IvfConfig& ivf() const { return cfg_; }
   /// Device storage of the values; lives as long as the store.
   ValueArena& arena() { return arena_; }
 
@@ -141,6 +144,8 @@ class MemoClient {
   void flush_inserts();
 
   const MemoCounters& counters() const { return ctr_; }
+  /// The device-side lookup path (memo_gpu.hpp) accounts its decisions here.
+  MemoCounters& counters_mut() { return ctr_; }
   const MemoClientConfig& config() const { return cfg_; }
   MemoStore& store() { return *store_; }
   std::size_t cached_slots() const { return cache_.size(); }

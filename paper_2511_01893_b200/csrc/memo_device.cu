@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "device.hpp"
 #include "kernels.hpp"
+#include "memo_gpu.hpp"
 
 namespace mlrg::ops {
 
@@ -43,8 +44,9 @@ __device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long st
 // in double, encoder.cpp:416-420); slot kd of each slab carries sum |x|^2.
 constexpr int kEncWarps = 4;
 constexpr int kPStride = 36;  // floats per staged P row: 16 B aligned, conflict-free LDS.64 across rg
+constexpr int kXStride = 34;  // floats per staged slab row: conflict-free STS.64 / LDS.64
 struct EncStage {
-  float x[32][16];           // [column kk][slab]
+  float x[16][kXStride];     // [slab][column kk]
   float p[kRows][kPStride];  // [row][column kk]
 };
 
@@ -78,6 +80,14 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const TX* __restrict_
   // x staging: lane owns complex element e = lane & 15 of slabs (lane >> 4) + 2j
   const int xe = lane & 15, xs0 = lane >> 4;
   float2 xr[8];
+  // element ce of slab `start`: axis 0 slabs are contiguous; axis 1 slabs are
+  // runs of extent * d2 (32-bit division: slab sizes stay below 2^31)
+  const unsigned per = static_cast<unsigned>(g.extent * g.d2), d2 = static_cast<unsigned>(g.d2);
+  auto offset = [&](long long start, long long ce) -> long long {
+    if (g.axis == 0) return start * g.d1 * g.d2 + ce;
+    const unsigned c = static_cast<unsigned>(ce), i = c / per, rem = c - i * per, kl = rem / d2;
+    return (static_cast<long long>(i) * g.d1 + start + kl) * g.d2 + (rem - kl * d2);
+  };
   auto load_x = [&](long long ch) {
     const long long ce = ch * 16 + xe;
 #pragma unroll
@@ -85,17 +95,14 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const TX* __restrict_
       const int sidx = xs0 + 2 * j;
       xr[j] = make_float2(0.f, 0.f);
       if (sidx < ns && ce < n) {
-        const TX v = x[slab_offset(g, sl.start[sidx], ce)];
+        const TX v = x[offset(sl.start[sidx], ce)];
         xr[j] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
       }
     }
   };
-  auto store_x = [&](EncStage& b) {
+  auto store_x = [&](EncStage& b) {  // (re, im) of element xe = columns (2 xe, 2 xe + 1)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      b.x[2 * xe][xs0 + 2 * j] = xr[j].x;
-      b.x[2 * xe + 1][xs0 + 2 * j] = xr[j].y;
-    }
+    for (int j = 0; j < 8; ++j) *reinterpret_cast<float2*>(&b.x[xs0 + 2 * j][2 * xe]) = xr[j];
   };
   auto load_p = [&](EncStage& b, long long ch) {
     const long long k0 = ch * 32;
@@ -147,9 +154,13 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const TX* __restrict_
     }
 #pragma unroll 4
     for (int kk = 0; kk < 32; kk += 2) {
-      const float4 x0 = *reinterpret_cast<const float4*>(&b.x[kk][4 * sg]);
-      const float4 x1 = *reinterpret_cast<const float4*>(&b.x[kk + 1][4 * sg]);
-      const float xa0[4] = {x0.x, x0.y, x0.z, x0.w}, xa1[4] = {x1.x, x1.y, x1.z, x1.w};
+      float xa0[4], xa1[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const float2 xv = *reinterpret_cast<const float2*>(&b.x[4 * sg + a][kk]);
+        xa0[a] = xv.x;
+        xa1[a] = xv.y;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float2 pv = *reinterpret_cast<const float2*>(&b.p[8 * i + rg][kk]);
@@ -277,6 +288,63 @@ __global__ void __launch_bounds__(256) k_slab_store(TO* __restrict__ out, SlabGe
   }
 }
 
+__device__ __forceinline__ long long slab_len(const SlabGeom& g) { return g.axis == 0 ? g.d0 : g.d1; }
+
+template <class TO>
+__global__ void __launch_bounds__(256) k_dev_materialize(TO* __restrict__ out, SlabGeom g, const DevSlab* __restrict__ slabs,
+                                                         long long chunk, const float2* __restrict__ sub) {
+  const DevSlab d = slabs[blockIdx.y];
+  if (d.outcome == 0) return;
+  const long long start = blockIdx.y * chunk;
+  const SlabRuns sr = slab_runs(g, start, min(chunk, slab_len(g) - start));
+  const float2* __restrict__ value = d.src;
+  const long long segs = (sr.run_len + kSeg - 1) / kSeg;
+  for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
+    const long long r = t / segs, e0 = (t - r * segs) * kSeg;
+    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
+    const long long e1 = min(sr.run_len, e0 + kSeg);
+    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const long long o = o0 + e;
+      const float2 v = value[v0 + e];
+      double re = v.x * d.scale, im = v.y * d.scale;
+      if (sub) {
+        const float2 sv = sub[o];
+        re -= sv.x;
+        im -= sv.y;
+      }
+      TO res;
+      res.x = static_cast<decltype(res.x)>(re);
+      res.y = static_cast<decltype(res.y)>(im);
+      out[o] = res;
+    }
+  }
+}
+
+template <class TO>
+__global__ void __launch_bounds__(256) k_dev_store(TO* __restrict__ out, SlabGeom g, const DevSlab* __restrict__ slabs,
+                                                   long long chunk, const float2* __restrict__ sub) {
+  const DevSlab d = slabs[blockIdx.y];
+  if (d.outcome != 0) return;
+  const long long start = blockIdx.y * chunk;
+  const SlabRuns sr = slab_runs(g, start, min(chunk, slab_len(g) - start));
+  float2* __restrict__ value = d.dst;
+  if (!value && !sub) return;
+  const long long segs = (sr.run_len + kSeg - 1) / kSeg;
+  for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
+    const long long r = t / segs, e0 = (t - r * segs) * kSeg;
+    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
+    const long long e1 = min(sr.run_len, e0 + kSeg);
+    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const long long o = o0 + e;
+      const TO v = out[o];
+      if (value) value[v0 + e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+      if constexpr (sizeof(TO) == sizeof(float2)) {
+        if (sub) out[o] = csub(v, sub[o]);
+      }
+    }
+  }
+}
+
 int enc_blocks() { return 2 * sm_count(); }
 constexpr int kEncSlabs = 16;  // slabs per launch (one 4 x 8 register tile per lane)
 
@@ -347,6 +415,29 @@ void store_impl(TO* out, SlabGeom g, const SlabBatch& b, int nb, const float2* s
   MLRG_LAUNCH_CHECK("k_slab_store");
 }
 }  // namespace
+
+void dev_materialize(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+                     cudaStream_t s) {
+  if (n <= 0) return;
+  k_dev_materialize<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
+  MLRG_LAUNCH_CHECK("k_dev_materialize");
+}
+void dev_materialize(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
+  if (n <= 0) return;
+  k_dev_materialize<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
+  MLRG_LAUNCH_CHECK("k_dev_materialize");
+}
+void dev_store(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+               cudaStream_t s) {
+  if (n <= 0) return;
+  k_dev_store<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
+  MLRG_LAUNCH_CHECK("k_dev_store");
+}
+void dev_store(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
+  if (n <= 0) return;
+  k_dev_store<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
+  MLRG_LAUNCH_CHECK("k_dev_store");
+}
 
 void slab_materialize(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {
   materialize_impl(out, g, b, nb, sub, s);

@@ -1,0 +1,424 @@
+#include "memo_gpu.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+namespace mlrg {
+
+namespace {
+
+constexpr int kLookupThreads = 128;
+constexpr int kMaxKd = 64;
+constexpr int kMaxProbe = 64;
+
+// memostore.cpp:30-38, in the reference's operation order (no contraction).
+__device__ __forceinline__ double l2_sq_d(const float* a, const float* b, int d) {
+  double acc = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double x = __dsub_rn(static_cast<double>(a[i]), static_cast<double>(b[i]));
+    acc = __dadd_rn(acc, __dmul_rn(x, x));
+  }
+  return acc;
+}
+
+// memostore.cpp:17-28.
+__device__ __forceinline__ double cosine_d(const float* a, const float* b, int d) {
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double x = static_cast<double>(a[i]), y = static_cast<double>(b[i]);
+    dot = __dadd_rn(dot, __dmul_rn(x, y));
+    na = __dadd_rn(na, __dmul_rn(x, x));
+    nb = __dadd_rn(nb, __dmul_rn(y, y));
+  }
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  return __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb)));
+}
+
+struct Best {
+  double d;
+  long long id;
+};
+__device__ __forceinline__ bool better(const Best& a, const Best& b) {  // (l2, lower id)
+  return a.id >= 0 && (b.id < 0 || a.d < b.d || (a.d == b.d && a.id < b.id));
+}
+
+struct LookupArgs {
+  int op, n, kd, nprobe, ncent, trained, max_slabs;
+  float tau;
+  const float* raw;
+  const int* perm;
+  const float* sign;
+  float* qkeys;
+  float* cache_key;
+  long long* cache_vid;
+  const float* keys;
+  const long long* vbytes;
+  const long long* slab_vbytes;
+  const float* cent;
+  const int* cl_ptr;
+  const int* cl_ids;
+  const long long* state;
+  DevSlab* slabs;
+  int* probed;
+  int* queried;
+};
+
+// One CTA per slab: cache probe, then (on a cache miss) the store query.
+__global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
+  __shared__ float q[kMaxKd];
+  __shared__ Best red[kLookupThreads / 32];
+  __shared__ double cd[kMaxProbe];
+  __shared__ int probe[kMaxProbe];
+  __shared__ int done;
+  const int c = blockIdx.x, t = threadIdx.x, kd = a.kd;
+  const long long slot = static_cast<long long>(a.op) * a.max_slabs + c;
+  const int mix = static_cast<int>(slot) * kd;
+  if (t < kd) {  // slot_mix (encoder.cpp:66-86): tables from the host
+    q[t] = a.sign[mix + t] * a.raw[static_cast<long long>(c) * kd + a.perm[mix + t]];
+    a.qkeys[static_cast<long long>(c) * kd + t] = q[t];
+  }
+  __syncthreads();
+  DevSlab& out = a.slabs[c];
+  if (t == 0) {
+    done = 0;
+    const long long vid = a.cache_vid[slot];
+    a.probed[c] = vid >= 0;
+    a.queried[c] = 0;
+    if (vid >= 0) {
+      const float cs = static_cast<float>(cosine_d(q, a.cache_key + slot * kd, kd));
+      if (cs > a.tau && a.vbytes[vid] == a.slab_vbytes[c]) {
+        out.outcome = 2;
+        out.cs = cs;
+        out.vid = vid;
+        done = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (done) return;
+  // ---- store query over the published keys (memostore.cpp:174-222) ----
+  const long long npub = a.state[0];
+  Best b{0.0, -1};
+  if (!a.trained) {
+    for (long long id = t; id < npub; id += kLookupThreads) {
+      const Best cand{l2_sq_d(q, a.keys + id * kd, kd), id};
+      if (better(cand, b)) b = cand;
+    }
+  } else {
+    if (t < a.ncent) cd[t] = l2_sq_d(q, a.cent + static_cast<long long>(t) * kd, kd);
+    __syncthreads();
+    if (t == 0) {  // the nprobe smallest (l2, index) pairs, ascending (std::sort on pairs)
+      const int np = min(a.nprobe, a.ncent);
+      unsigned long long used = 0;
+      for (int p = 0; p < np; ++p) {
+        int arg = -1;
+        for (int k = 0; k < a.ncent; ++k) {
+          if (used >> k & 1ull) continue;
+          if (arg < 0 || cd[k] < cd[arg]) arg = k;
+        }
+        used |= 1ull << arg;
+        probe[p] = arg;
+      }
+      done = np;
+    }
+    __syncthreads();
+    for (int p = 0; p < done; ++p) {
+      const int cl = probe[p];
+      for (int e = a.cl_ptr[cl] + t; e < a.cl_ptr[cl + 1]; e += kLookupThreads) {
+        const long long id = a.cl_ids[e];
+        const Best cand{l2_sq_d(q, a.keys + id * kd, kd), id};
+        if (better(cand, b)) b = cand;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    Best x;
+    x.d = __shfl_xor_sync(0xffffffffu, b.d, o);
+    x.id = __shfl_xor_sync(0xffffffffu, b.id, o);
+    if (better(x, b)) b = x;
+  }
+  if ((t & 31) == 0) red[t >> 5] = b;
+  __syncthreads();
+  if (t != 0) return;
+  for (int w = 1; w < kLookupThreads / 32; ++w)
+    if (better(red[w], b)) b = red[w];
+  a.queried[c] = 1;
+  out.outcome = 0;
+  out.cs = 0.0f;
+  out.vid = -1;
+  if (b.id < 0) return;  // empty store: a miss with cs 0
+  const float cs = static_cast<float>(cosine_d(q, a.keys + b.id * kd, kd));
+  out.cs = cs;
+  if (cs > a.tau && a.vbytes[b.id] == a.slab_vbytes[c]) {  // memoclient.cpp:284-292
+    out.outcome = 1;
+    out.vid = b.id;
+    for (int i = 0; i < kd; ++i) a.cache_key[slot * kd + i] = q[i];  // the QUERY key
+    a.cache_vid[slot] = b.id;
+  }
+}
+
+struct StageArgs {
+  int n, kd, op, iteration, cap;
+  long long arena_bytes, log_cap;
+  const float* qkeys;
+  const double* norms2;
+  const long long* slab_vbytes;
+  const long long* slab_counts;
+  float* keys;
+  long long* vbytes;
+  double* vnorm;
+  const float2** vptr;
+  char* arena;
+  long long* state;
+  DevSlab* slabs;
+  unsigned char* skip;
+  const int* probed;
+  const int* queried;
+  DevLog* log;
+};
+
+// Single warp, slabs in order: hit sources/scales, insert staging (cap per
+// flush window, arena bump allocation), the decision log.
+__global__ void k_memo_stage(StageArgs a) {
+  const int lane = threadIdx.x;
+  for (int c = 0; c < a.n; ++c) {
+    DevSlab& s = a.slabs[c];
+    const double live = __dsqrt_rn(a.norms2[c]);
+    int staged = -1;
+    long long id = -1;
+    if (s.outcome != 0) {
+      if (lane == 0) {
+        const double stored = a.vnorm[s.vid];
+        s.src = a.vptr[s.vid];
+        s.scale = (stored > 0.0 && live > 0.0) ? __ddiv_rn(live, stored) : 1.0;
+        s.dst = nullptr;
+        a.skip[c] = 1;
+      }
+    } else {
+      const long long nst = a.state[1];
+      staged = nst < a.cap ? 1 : 0;
+      if (staged) {
+        id = a.state[0] + nst;
+        const long long bytes = (a.slab_counts[c] * 8 + 255) & ~255LL;
+        const long long off = a.state[2];
+        const bool fits = off + bytes <= a.arena_bytes;
+        for (int i = lane; i < a.kd; i += 32) a.keys[id * a.kd + i] = a.qkeys[static_cast<long long>(c) * a.kd + i];
+        __syncwarp();
+        if (lane == 0) {
+          float2* dst = fits ? reinterpret_cast<float2*>(a.arena + off) : nullptr;
+          if (!fits) a.state[4] = 1;  // overflow: the host fails the flush
+          a.vbytes[id] = a.slab_vbytes[c];
+          a.vnorm[id] = live;
+          a.vptr[id] = dst;
+          s.dst = dst;
+          a.state[1] = nst + 1;
+          a.state[2] = off + (fits ? bytes : 0);
+        }
+      } else if (lane == 0) {
+        s.dst = nullptr;
+        a.state[5] += 1;
+      }
+      if (lane == 0) {
+        s.src = nullptr;
+        s.scale = 1.0;
+        a.skip[c] = 0;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const long long li = a.state[3];
+      if (li < a.log_cap)
+        a.log[li] = DevLog{a.iteration, a.op, c, s.outcome, s.cs, a.probed[c], a.queried[c], staged};
+      a.state[3] = li + 1;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int max_slabs, std::int64_t max_keys,
+                       std::size_t arena_bytes, cudaStream_t s)
+    : client_(client),
+      kd_(key_dim),
+      max_slabs_(max_slabs),
+      max_keys_(max_keys),
+      arena_bytes_((arena_bytes + 255) & ~std::size_t{255}),
+      log_cap_(std::int64_t{1} << 16) {
+  if (kd_ < 1 || kd_ > kMaxKd) throw std::invalid_argument("device memo: key_dim must be in [1, 64]");
+  if (client_.config().global_cache) throw std::invalid_argument("device memo: global_cache is host-only");
+  if (client_.store().ivf().nlist > kMaxProbe) throw std::invalid_argument("device memo: nlist must be <= 64");
+  const std::size_t per_key = 8 + 4 * static_cast<std::size_t>(kd_);
+  batch_keys_ = static_cast<int>((client_.config().coalesce_bytes + per_key - 1) / per_key);
+  keys_.resize(static_cast<std::size_t>(max_keys_ * kd_));
+  vbytes_.resize(static_cast<std::size_t>(max_keys_));
+  vnorm_.resize(static_cast<std::size_t>(max_keys_));
+  vptr_.resize(static_cast<std::size_t>(max_keys_));
+  const std::size_t slots = 4 * static_cast<std::size_t>(max_slabs_);
+  cache_key_.resize(slots * kd_);
+  cache_vid_.resize(slots);
+  std::vector<long long> neg(slots, -1);
+  cache_vid_.upload(neg.data(), neg.size(), s);
+  // slot_mix (encoder.cpp:66-86) as gather tables per (op, location)
+  std::vector<int> perm(slots * kd_);
+  std::vector<float> sign(slots * kd_);
+  for (int op = 0; op < 4; ++op)
+    for (int loc = 0; loc < max_slabs_; ++loc) {
+      const std::size_t base = (static_cast<std::size_t>(op) * max_slabs_ + loc) * kd_;
+      // the mix of a one-hot vector e_i is sign_j at j with perm[j] = i; recover both
+      std::vector<float> probe(static_cast<std::size_t>(kd_));
+      for (int i = 0; i < kd_; ++i) {
+        std::fill(probe.begin(), probe.end(), 0.0f);
+        probe[static_cast<std::size_t>(i)] = 1.0f;
+        slot_mix(probe.data(), kd_, seed, loc, static_cast<OpId>(op));
+        for (int j = 0; j < kd_; ++j)
+          if (probe[static_cast<std::size_t>(j)] != 0.0f) {
+            perm[base + j] = i;
+            sign[base + j] = probe[static_cast<std::size_t>(j)];
+          }
+      }
+    }
+  mix_perm_.upload(perm, s);
+  mix_sign_.upload(sign, s);
+  arena_.resize(arena_bytes_);
+  state_.resize(6);
+  state_.zero(s);
+  slabs_.resize(static_cast<std::size_t>(max_slabs_));
+  skip_.resize(static_cast<std::size_t>(max_slabs_));
+  slab_vbytes_.resize(static_cast<std::size_t>(4 * max_slabs_));
+  slab_counts_.resize(static_cast<std::size_t>(4 * max_slabs_));
+  flags_.resize(static_cast<std::size_t>(2 * max_slabs_));
+  qkeys_.resize(static_cast<std::size_t>(max_slabs_) * kd_);
+  log_.resize(static_cast<std::size_t>(log_cap_));
+  centroids_.resize(static_cast<std::size_t>(client_.store().ivf().nlist) * kd_);
+  cl_ptr_.resize(static_cast<std::size_t>(client_.store().ivf().nlist) + 1);
+  cl_ids_.resize(static_cast<std::size_t>(max_keys_));
+  h_state_.reserve(6);
+  MLRG_CUDA(cudaStreamSynchronize(s));
+}
+
+void DeviceMemo::set_slabs(OpId op, const std::vector<std::size_t>& value_bytes,
+                           const std::vector<std::int64_t>& out_counts, cudaStream_t s) {
+  const int o = static_cast<int>(op);
+  if (o > 3 || static_cast<int>(value_bytes.size()) > max_slabs_) throw std::logic_error("device memo: bad slab table");
+  std::vector<long long> vb(value_bytes.begin(), value_bytes.end()), oc(out_counts.begin(), out_counts.end());
+  MLRG_CUDA(cudaMemcpyAsync(slab_vbytes_.get() + o * max_slabs_, vb.data(), vb.size() * sizeof(long long),
+                            cudaMemcpyHostToDevice, s));
+  MLRG_CUDA(cudaMemcpyAsync(slab_counts_.get() + o * max_slabs_, oc.data(), oc.size() * sizeof(long long),
+                            cudaMemcpyHostToDevice, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));
+}
+
+void DeviceMemo::lookup(OpId op, int n, const float* keys, const double* norms2, int iteration, cudaStream_t s) {
+  const int o = static_cast<int>(op);
+  if (n > max_slabs_) throw std::logic_error("device memo: too many slabs");
+  if (o > 3) throw std::logic_error("device memo: operator not memoizable on the device");
+  const long long* svb = slab_vbytes_.get() + o * max_slabs_;
+  const long long* scn = slab_counts_.get() + o * max_slabs_;
+  LookupArgs la{o, n, kd_, client_.config().nprobe, ncent_, trained_ ? 1 : 0, max_slabs_,
+                client_.config().tau, keys, mix_perm_.get(), mix_sign_.get(), qkeys_.get(), cache_key_.get(),
+                cache_vid_.get(), keys_.get(), vbytes_.get(), svb, centroids_.get(), cl_ptr_.get(),
+                cl_ids_.get(), state_.get(), slabs_.get(), flags_.get(), flags_.get() + max_slabs_};
+  k_memo_lookup<<<n, kLookupThreads, 0, s>>>(la);
+  MLRG_LAUNCH_CHECK("k_memo_lookup");
+  StageArgs sa{n, kd_, o, iteration, static_cast<int>(client_.config().insert_queue_cap),
+               static_cast<long long>(arena_bytes_), log_cap_, qkeys_.get(), norms2, svb, scn, keys_.get(),
+               vbytes_.get(), vnorm_.get(), vptr_.get(), arena_.get(), state_.get(), slabs_.get(), skip_.get(),
+               la.probed, la.queried, log_.get()};
+  k_memo_stage<<<1, 32, 0, s>>>(sa);
+  MLRG_LAUNCH_CHECK("k_memo_stage");
+}
+
+void DeviceMemo::upload_ivf(cudaStream_t s) {
+  const MemoStore& st = client_.store();
+  if (!st.trained()) return;
+  const auto& cents = st.centroids();
+  ncent_ = static_cast<int>(cents.size());
+  std::vector<float> c(static_cast<std::size_t>(ncent_) * kd_);
+  for (int i = 0; i < ncent_; ++i) std::copy(cents[i].begin(), cents[i].end(), c.begin() + static_cast<std::ptrdiff_t>(i) * kd_);
+  const auto lists = st.cluster_ids();
+  std::vector<int> ptr(lists.size() + 1, 0), ids;
+  for (std::size_t i = 0; i < lists.size(); ++i) {
+    ptr[i + 1] = ptr[i] + static_cast<int>(lists[i].size());
+    for (std::uint64_t id : lists[i]) ids.push_back(static_cast<int>(id));
+  }
+  MLRG_CUDA(cudaMemcpyAsync(centroids_.get(), c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  MLRG_CUDA(cudaMemcpyAsync(cl_ptr_.get(), ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (!ids.empty())
+    MLRG_CUDA(cudaMemcpyAsync(cl_ids_.get(), ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));  // the host vectors die here
+  trained_ = true;
+}
+
+void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) {
+  MLRG_CUDA(cudaMemcpyAsync(h_state_.get(), state_.get(), 6 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));
+  long long* st = h_state_.get();
+  const long long npub = st[0], nstaged = publish ? st[1] : 0, nlog = st[3];
+  if (st[4]) throw std::runtime_error("device memo: value arena exhausted (" + std::to_string(arena_bytes_) + " bytes)");
+  if (nlog > log_cap_) throw std::runtime_error("device memo: decision log overflow");
+  std::vector<DevLog> log(static_cast<std::size_t>(nlog));
+  if (nlog) MLRG_CUDA(cudaMemcpyAsync(log.data(), log_.get(), sizeof(DevLog) * nlog, cudaMemcpyDeviceToHost, s));
+  std::vector<float> keys(static_cast<std::size_t>(nstaged) * kd_);
+  std::vector<long long> vb(static_cast<std::size_t>(nstaged));
+  std::vector<double> vn(static_cast<std::size_t>(nstaged));
+  std::vector<const float2*> vp(static_cast<std::size_t>(nstaged));
+  if (nstaged) {
+    MLRG_CUDA(cudaMemcpyAsync(keys.data(), keys_.get() + npub * kd_, keys.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaMemcpyAsync(vb.data(), vbytes_.get() + npub, vb.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaMemcpyAsync(vn.data(), vnorm_.get() + npub, vn.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaMemcpyAsync(vp.data(), vptr_.get() + npub, vp.size() * sizeof(void*), cudaMemcpyDeviceToHost, s));
+  }
+  MLRG_CUDA(cudaStreamSynchronize(s));
+  // ---- replay the decisions into the client's counters and the audit ----
+  MemoCounters& ctr = client_.counters_mut();
+  long long queried_in_call = 0;
+  for (std::size_t i = 0; i < log.size(); ++i) {
+    const DevLog& e = log[i];
+    ++ctr.lookups;
+    ctr.cache_probes += static_cast<std::uint64_t>(e.probed);
+    ctr.cache_comparisons += static_cast<std::uint64_t>(e.probed);
+    if (e.outcome == 2) ++ctr.cache_hits;
+    else if (e.outcome == 1) ++ctr.remote_hits;
+    else ++ctr.misses;
+    if (e.staged == 1) ++ctr.inserts_enqueued;
+    if (e.staged == 0) ++ctr.inserts_dropped;
+    queried_in_call += e.queried;
+    const bool call_end = i + 1 == log.size() || log[i + 1].location == 0;
+    if (call_end) {  // coalesced store batches of this call (memoclient.cpp:228-246)
+      ctr.batches_sent += static_cast<std::uint64_t>((queried_in_call + batch_keys_ - 1) / batch_keys_);
+      queried_in_call = 0;
+    }
+    if (audit) audit->push_back(Audit{e.iteration, e.op, e.location, e.outcome, e.cs});
+  }
+  // ---- publish: the host mirror gets the staged keys in order (same ids) ----
+  MemoStore& store = client_.store();
+  const bool was_trained = store.trained();
+  for (long long i = 0; i < nstaged; ++i) {
+    ValueRef v;
+    v.dev = vp[static_cast<std::size_t>(i)];
+    v.norm = vn[static_cast<std::size_t>(i)];
+    v.bytes = static_cast<std::size_t>(vb[static_cast<std::size_t>(i)]);
+    v.count = static_cast<std::int64_t>((v.bytes - 8) / 16);
+    const std::vector<float> k(keys.begin() + i * kd_, keys.begin() + (i + 1) * kd_);
+    const std::uint64_t id = store.insert(k, v);
+    if (static_cast<long long>(id) != npub + i) throw std::logic_error("device memo: id mismatch with the host mirror");
+    ++ctr.inserts_sent;
+  }
+  st[3] = 0;  // the log is drained either way
+  if (publish) {
+    st[0] = npub + nstaged;
+    st[1] = 0;
+    st[5] = 0;
+  }
+  MLRG_CUDA(cudaMemcpyAsync(state_.get(), st, 6 * sizeof(long long), cudaMemcpyHostToDevice, s));
+  MLRG_CUDA(cudaStreamSynchronize(s));
+  if (store.trained() && (nstaged > 0 || !was_trained)) upload_ivf(s);
+  if (st[0] > max_keys_ - static_cast<long long>(client_.config().insert_queue_cap))
+    throw std::runtime_error("device memo: key index full (" + std::to_string(max_keys_) + " keys)");
+}
+
+}  // namespace mlrg

@@ -49,6 +49,25 @@ Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_
   if (cfg_.memo_enabled && (!enc_ || !memo_))
     throw std::invalid_argument("OperatorEngine: memoization needs an encoder and a client");
   if (cfg_.memo_enabled) register_shapes();
+  if (cfg_.memo_enabled && cfg_.device_memo && !shard_.sharded()) {
+    // the device-side lookup needs one memo slab per 16-row fu2d batch
+    if (cfg_.chunk_extent != Usfft::kRowBatch) throw std::invalid_argument("device memo needs chunk_extent = 16");
+    const std::int64_t e = cfg_.chunk_extent;
+    const int max_slabs = static_cast<int>(std::max((g_.n1 + e - 1) / e, (g_.h + e - 1) / e));
+    dmemo_ = std::make_unique<DeviceMemo>(*memo_, enc_->key_dim(), enc_->seed(), max_slabs,
+                                          std::max<std::int64_t>(cfg_.memo_max_keys, 4096), cfg_.memo_arena_bytes, s_);
+    for (OpId op : {OpId::fu1d, OpId::fu2d, OpId::fu1d_adj, OpId::fu2d_adj}) {
+      const int axis = chunk_axis_of(op);
+      const std::vector<std::int64_t> ext = slab_extents(in_shape(op).extent(axis), e);
+      std::vector<std::size_t> vb;
+      std::vector<std::int64_t> oc;
+      for (std::int64_t x : ext) {
+        oc.push_back(with_axis(out_shape(op), axis, x).count());
+        vb.push_back(8 + static_cast<std::size_t>(oc.back()) * 16);
+      }
+      dmemo_->set_slabs(op, vb, oc, s_);
+    }
+  }
   if (shard_.sharded()) {
     HostComm& c = *shard_.comm;
     const std::int64_t np = shard_.np(), nr = shard_.nr();
@@ -187,32 +206,19 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
   }
   if (shard_.sharded() && (op == OpId::f2d || op == OpId::f2d_adj))
     throw std::invalid_argument("OperatorEngine: f2d is not memoized in sharded mode (pipeline=optimized)");
+  if (dmemo_ && op != OpId::f2d && op != OpId::f2d_adj)
+    return apply_device_memo(op, fused, in, in_d, d_hat, out, out_d);
+  if (dmemo_) throw std::invalid_argument("OperatorEngine: device memo does not memoize f2d (pipeline=optimized)");
   // ---- encode this rank's slabs (one GEMM per distinct slab shape) ----
   const std::vector<std::int64_t> ext = slab_extents(len, cfg_.chunk_extent);
   const int n = static_cast<int>(ext.size());
   const int kd = enc_->key_dim();
   const std::int64_t g0 = slab0(axis, op);  // global location of local slab 0
-  enc_keys_.resize(static_cast<std::size_t>(n * kd));
-  enc_norms_.resize(static_cast<std::size_t>(n));
   keys_host_.reserve(static_cast<std::size_t>(n * kd));
   norms_host_.reserve(static_cast<std::size_t>(n));
   std::vector<std::int64_t> starts(static_cast<std::size_t>(n));
   for (int c = 0; c < n; ++c) starts[static_cast<std::size_t>(c)] = static_cast<std::int64_t>(c) * cfg_.chunk_extent;
-  for (int c0 = 0; c0 < n;) {
-    int c1 = c0;
-    while (c1 < n && ext[static_cast<std::size_t>(c1)] == ext[static_cast<std::size_t>(c0)]) ++c1;
-    ops::SlabGeom sg{ishape.d0, ishape.d1, ishape.d2, axis, 0, ext[static_cast<std::size_t>(c0)]};
-    enc_work_.resize(ops::encode_work_doubles(c1 - c0, kd));
-    const float* P = enc_->device_matrix(with_axis(ishape, axis, sg.extent));
-    float* kdst = enc_keys_.get() + static_cast<std::size_t>(c0) * kd;
-    if (in_d)
-      ops::encode(static_cast<const double2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
-                  enc_norms_.get() + c0, s_);
-    else
-      ops::encode(static_cast<const float2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
-                  enc_norms_.get() + c0, s_);
-    c0 = c1;
-  }
+  encode_slabs(op, in, in_d, axis, ishape, ext, starts);
   {
     prof::HostSpan span("host:memo_key_sync");
     MLRG_CUDA(cudaMemcpyAsync(keys_host_.get(), enc_keys_.get(), sizeof(float) * n * kd, cudaMemcpyDeviceToHost, s_));
@@ -344,12 +350,83 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
   if (cfg_.flush_after_apply) flush_inserts();
 }
 
+void Engine::encode_slabs(OpId /*op*/, const void* in, bool in_d, int axis, const Shape3& ishape,
+                          const std::vector<std::int64_t>& ext, const std::vector<std::int64_t>& starts) {
+  const int n = static_cast<int>(ext.size());
+  const int kd = enc_->key_dim();
+  enc_keys_.resize(static_cast<std::size_t>(n * kd));
+  enc_norms_.resize(static_cast<std::size_t>(n));
+  for (int c0 = 0; c0 < n;) {  // one GEMM per distinct slab shape
+    int c1 = c0;
+    while (c1 < n && ext[static_cast<std::size_t>(c1)] == ext[static_cast<std::size_t>(c0)]) ++c1;
+    ops::SlabGeom sg{ishape.d0, ishape.d1, ishape.d2, axis, 0, ext[static_cast<std::size_t>(c0)]};
+    enc_work_.resize(ops::encode_work_doubles(c1 - c0, kd));
+    const float* P = enc_->device_matrix(with_axis(ishape, axis, sg.extent));
+    float* kdst = enc_keys_.get() + static_cast<std::size_t>(c0) * kd;
+    if (in_d)
+      ops::encode(static_cast<const double2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
+                  enc_norms_.get() + c0, s_);
+    else
+      ops::encode(static_cast<const float2*>(in), sg, starts.data() + c0, c1 - c0, P, kd, enc_work_.get(), kdst,
+                  enc_norms_.get() + c0, s_);
+    c0 = c1;
+  }
+}
+
+void Engine::apply_device_memo(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out,
+                               bool out_d) {
+  const int axis = chunk_axis_of(op);
+  const Shape3 ishape = in_shape(op), oshape = out_shape(op);
+  const std::int64_t len = ishape.extent(axis), e = cfg_.chunk_extent;
+  const std::vector<std::int64_t> ext = slab_extents(len, e);
+  const int n = static_cast<int>(ext.size());
+  std::vector<std::int64_t> starts(static_cast<std::size_t>(n));
+  for (int c = 0; c < n; ++c) starts[static_cast<std::size_t>(c)] = static_cast<std::int64_t>(c) * e;
+  // encode -> lookup -> compute (hit slabs skip their CTAs) -> hits -> miss values, all enqueued
+  encode_slabs(op, in, in_d, axis, ishape, ext, starts);
+  dmemo_->lookup(op, n, enc_keys_.get(), enc_norms_.get(), iteration_, s_);
+  usfft_.set_skip(dmemo_->skip());
+  try {
+    compute(op, false, in, in_d, nullptr, out, out_d, 0, len);
+  } catch (...) {
+    usfft_.set_skip(nullptr);
+    throw;
+  }
+  usfft_.set_skip(nullptr);
+  const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, 0, 0};
+  if (out_d) {
+    ops::dev_materialize(static_cast<double2*>(out), og, dmemo_->slabs(), n, e, s_);
+    ops::dev_store(static_cast<double2*>(out), og, dmemo_->slabs(), n, e, s_);
+  } else {
+    ops::dev_materialize(static_cast<float2*>(out), og, dmemo_->slabs(), n, e, fused ? d_hat : nullptr, s_);
+    ops::dev_store(static_cast<float2*>(out), og, dmemo_->slabs(), n, e, fused ? d_hat : nullptr, s_);
+  }
+  if (cfg_.flush_after_apply) flush_inserts();
+}
+
+void Engine::take_device_audit(bool publish) {
+  std::vector<DeviceMemo::Audit> a;
+  dmemo_->flush(s_, &a, publish);
+  for (const DeviceMemo::Audit& x : a) {
+    const OpId op = static_cast<OpId>(x.op);
+    const int axis = chunk_axis_of(op);
+    const std::int64_t len = in_shape(op).extent(axis), e = cfg_.chunk_extent;
+    audit_.push_back(ChunkAudit{op, axis, x.location, std::min(e, len - x.location * e),
+                                static_cast<MemoOutcome>(x.outcome), x.cs, x.iteration, -1.0f});
+  }
+}
+
+void Engine::drain_memo_log() {
+  if (dmemo_) take_device_audit(false);
+}
+
 void Engine::flush_inserts() {
   prof::HostSpan span("host:memo_flush");
   if (!memo_) return;
   // sharded: a value is read by its first hit only after this flush; the owner's
   // copy must be complete on its stream before any rank publishes the key
   if (shard_.sharded()) exchange_fence();
+  if (dmemo_) return take_device_audit(true);
   memo_->flush_inserts();
 }
 

@@ -429,6 +429,7 @@ bool Solver::step() {
       row.ms_rsp = ms_between(t1, t2);
       row.ms_update = ms_between(t2, t3);
     } catch (const AdmmAbort& ex) {
+      eng.drain_memo_log();  // the aborted iteration's decisions stay in the audit, unflushed
       st.rep.aborted = true;
       st.rep.abort_reason = ex.what();
       return false;

@@ -32,6 +32,14 @@ namespace {
 
 constexpr int KB = Usfft::kRowBatch;
 
+// Device-side memo (memo_gpu.hpp): a slab whose lookup hit skips its CTAs.
+// Unit u of a launch belongs to slab (base + u) / div.
+struct Skip {
+  const unsigned char* f = nullptr;
+  int base = 0, div = 1;
+};
+__device__ __forceinline__ bool skipped(const Skip& s, int unit) { return s.f && s.f[(s.base + unit) / s.div]; }
+
 // minimum resident CTAs per SM for the 256-thread 2D grid FFT passes (register cap)
 #ifndef MLRG_FFT_MINB
 #define MLRG_FFT_MINB 4
@@ -76,7 +84,8 @@ __global__ void __launch_bounds__(512, 2) k_fu1d(const TIn* __restrict__ u, floa
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
                                               const double* __restrict__ wts, const double2* __restrict__ fac,
-                                              const double2* __restrict__ tw, PeerOut po) {
+                                              const double2* __restrict__ tw, PeerOut po, Skip sk) {
+  if (skipped(sk, blockIdx.y)) return;
   extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
   const int j0 = blockIdx.x * ncol;
@@ -123,7 +132,8 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
                                                   const int* __restrict__ cell_ptr, const int* __restrict__ cell_k,
                                                   const double* __restrict__ cell_w,
                                                   const double* __restrict__ pdeconv,
-                                                  const double2* __restrict__ tw) {
+                                                  const double2* __restrict__ tw, Skip sk) {
+  if (skipped(sk, blockIdx.y)) return;
   extern __shared__ double2 sd[];
   const int m = 1 << logm, mask = m - 1;
   double2* vt = sd + m * ncol;
@@ -167,7 +177,8 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
-                                                   const double2* __restrict__ tw2, float2* __restrict__ S) {
+                                                   const double2* __restrict__ tw2, float2* __restrict__ S, Skip sk) {
+  if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
@@ -187,7 +198,8 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
-                                                   float2* __restrict__ G) {
+                                                   float2* __restrict__ G, Skip sk) {
+  if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
@@ -242,7 +254,8 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
     const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
     const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
     const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
-    int per_cta, double* __restrict__ partials, int accumulate) {
+    int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
+  if (skipped(sk, 0)) return;
   constexpr int WH = W / 2;
   __shared__ double red_scratch[kGatherWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, kk = lane & 15, ph = lane >> 4;
@@ -410,7 +423,8 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
                                                          const int* __restrict__ patch_t, const int* __restrict__ r0,
                                                          const int* __restrict__ c0, const double* __restrict__ w1,
                                                          const double* __restrict__ w2, float2* __restrict__ G,
-                                                         double2* __restrict__ partial) {
+                                                         double2* __restrict__ partial, Skip sk) {
+  if (skipped(sk, 0)) return;
   extern __shared__ float4 dyn_smem[];
   SpreadShared& sh = *reinterpret_cast<SpreadShared*>(dyn_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1, half = warp & 1;
@@ -475,7 +489,8 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
 // Sums the split patches' partials in item order (deterministic) into the grid.
 __global__ void __launch_bounds__(32 * kReduceWarps) k_fu2d_adj_spread_reduce(
     int nsplit, const int4* __restrict__ split, int logm2, const double2* __restrict__ partial,
-    float2* __restrict__ G) {
+    float2* __restrict__ G, Skip sk) {
+  if (skipped(sk, 0)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int si = blockIdx.x * kReduceWarps + warp;
   if (si >= nsplit) return;
@@ -499,7 +514,8 @@ __global__ void __launch_bounds__(32 * kReduceWarps) k_fu2d_adj_spread_reduce(
 __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict__ p, long long ld, long long k0,
                                                        int nk, int C, int w, const int* __restrict__ m_first,
                                                        const int* __restrict__ m_tidx,
-                                                       const double2* __restrict__ m_cfac, float2* __restrict__ val) {
+                                                       const double2* __restrict__ m_cfac, float2* __restrict__ val, Skip sk) {
+  if (skipped(sk, 0)) return;
   const int kk = threadIdx.x & (KB - 1);
   const int c = blockIdx.x * (blockDim.x / KB) + threadIdx.x / KB;
   if (c >= C) return;
@@ -516,7 +532,8 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
                                                        int logm2, int ks_n, const double2* __restrict__ tw1,
-                                                       float2* __restrict__ S) {
+                                                       float2* __restrict__ S, Skip sk) {
+  if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
   const int c = blockIdx.x, ks = blockIdx.y * ks_n;
@@ -534,7 +551,8 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const floa
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
-                                                       long long k0_out, PeerOut po) {
+                                                       long long k0_out, PeerOut po, Skip sk) {
+  if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.x, ks = blockIdx.y * ks_n;
@@ -988,7 +1006,7 @@ void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0, const PeerOut* pe
   kern<<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                      static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
                                      t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get(),
-                                     peer ? *peer : PeerOut{});
+                                     peer ? *peer : PeerOut{}, Skip{skip_, 0, 16});
   MLRG_LAUNCH_CHECK("k_fu1d");
   prof::end("k_fu1d", stream_);
 }
@@ -1004,7 +1022,8 @@ void Usfft::fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0) {
   k_fu1d_adj<TOut><<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(v, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                                  static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center),
                                                  ncol, t.z_cphase.get(), t.z_cell_ptr.get(), t.z_cell_k.get(),
-                                                 t.z_cell_w.get(), t.z_pdeconv.get(), t.z_tw.get());
+                                                 t.z_cell_w.get(), t.z_pdeconv.get(), t.z_tw.get(),
+                                                 Skip{skip_, 0, 16});
   MLRG_LAUNCH_CHECK("k_fu1d_adj");
   prof::end("k_fu1d_adj", stream_);
 }
@@ -1035,17 +1054,18 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     cudaStream_t s = alt ? tm.side : stream_;
     float2* S = alt ? tm.S2.get() : t.S.get();
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
+    const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_rows", s);
     k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
                   static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), s>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
-        t.y_deconv.get(), t.y_tw.get(), S);
+        t.y_deconv.get(), t.y_tw.get(), S, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", s);
     prof::begin("k_fu2d_cols", s);
     k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
                   static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
-        S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd);
+        S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_cols");
     prof::end("k_fu2d_cols", s);
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
@@ -1055,7 +1075,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(Gd, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
                                                t.t_r0.get(), t.t_c0.get(), t.t_w1.get(), t.t_w2.get(),
                                                t.m_first.get(), t.m_tidx.get(), t.m_fac.get(), eo, per_cta,
-                                               partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0);
+                                               partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0,
+                                               sk);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", s);
   }
@@ -1090,27 +1111,29 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
     float2* val = alt ? tm.val2.get() : t.val.get();
     double2* partial = alt ? tm.partial2.get() : t.partial.get();
+    const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_adj_prep", s);
     k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, s>>>(
-        p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(), val);
+        p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(), val,
+        sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
     prof::end("k_fu2d_adj_prep", s);
     prof::begin("k_fu2d_adj_spread", s);
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
     spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
                                                                t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
-                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial);
+                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     if (t.nsplit > 0) {
       k_fu2d_adj_spread_reduce<<<(t.nsplit + kReduceWarps - 1) / kReduceWarps, 32 * kReduceWarps, 0, s>>>(
-          t.nsplit, t.split.get(), t.py.logm, partial, Gd);
+          t.nsplit, t.split.get(), t.py.logm, partial, Gd, sk);
       MLRG_LAUNCH_CHECK("k_fu2d_adj_spread_reduce");
     }
     prof::end("k_fu2d_adj_spread", s);
     prof::begin("k_fu2d_adj_cols", s);
     k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
                       static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
-        Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S);
+        Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     prof::end("k_fu2d_adj_cols", s);
     prof::begin("k_fu2d_adj_rows", s);
@@ -1120,7 +1143,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
                                                                   sizeof(double2),
                                                               s>>>(
         S, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
-        t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b, peer ? *peer : PeerOut{});
+        t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b, peer ? *peer : PeerOut{}, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
     prof::end("k_fu2d_adj_rows", s);
   }

@@ -81,6 +81,9 @@ class Usfft {
   void f2d(const float2* p, float2* out, std::int64_t count, bool adjoint);
 
   Partials& partials() { return partials_; }
+  /// Device-side memo: per-16-slab skip flags (a hit slab's CTAs exit at entry)
+  /// for the next calls; nullptr clears.
+  void set_skip(const unsigned char* flags) { skip_ = flags; }
   int reduce_grid() const;  // CTAs of an elementwise reduction kernel
 
  private:
@@ -95,6 +98,7 @@ class Usfft {
   GridKernel kernel_;
   Tables* t_;
   Partials partials_;
+  const unsigned char* skip_ = nullptr;
 };
 
 }  // namespace mlrg

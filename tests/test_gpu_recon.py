@@ -108,3 +108,30 @@ def test_offload_is_bit_identical(mlrg, torch_cuda, case, memo):
     if memo != "off":
         assert np.array_equal(a0, a1) and np.array_equal(a0, z["audit_int"])
     assert rel(u1, z["u"]) <= 1e-4
+
+
+@pytest.mark.parametrize("case", ["recon_c16_memo_grid", "recon_c32_memo_grid", "recon_cfg1_memo_direct"])
+def test_device_memo_matches_host_client_and_reference_counters(mlrg, torch_cuda, case, monkeypatch):
+    """The device-side lookup (memo_gpu.cu) against the host MemoClient/MemoStore
+    path of the same build (MLRG_DEVICE_MEMO=0): identical decisions, bit-identical
+    u, and the reference's own counters (memoclient.hpp:42-61)."""
+    torch = torch_cuda
+    z = golden(case)
+    n, nt = z["phantom"].shape[0], z["data"].shape[0]
+    d = torch.from_numpy(z["data"]).cuda()
+    ref = torch.from_numpy(z["phantom"]).cuda()
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MLRG_DEVICE_MEMO", mode)
+        u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+        r = mlrg.reconstruct_device(config_text(n, nt, 10, "local"), d, u, reference=ref)
+        runs[mode] = (u.cpu().numpy(), r.audit(), r.counters(), r.csv)
+    (u0, (m0, c0), k0, csv0), (u1, (m1, c1), k1, csv1) = runs["0"], runs["1"]
+    assert np.array_equal(m1, z["audit_int"]) and np.array_equal(m0, m1)
+    assert np.array_equal(c0, c1)
+    assert np.array_equal(u0, u1)
+    want = dict(l.split("=") for l in str(z["txt_counters_txt"]).split())
+    for k in ("lookups", "cache_hits", "remote_hits", "misses", "cache_comparisons", "cache_probes",
+              "batches_sent", "inserts_enqueued", "inserts_sent", "inserts_dropped"):
+        assert k1[k] == int(want[k]), k
+        assert k0[k] == k1[k], k
