@@ -34,8 +34,9 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max 
 METRIC = "ADMM-FFT iterations/sec at N^3 volume"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
 # `ncu --set full` captures (profiles/), filled in per round
-TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (cold-cache capture of one launch)
-    "k_fu2d_gather": 46438144, "k_fu2d_adj_spread": 12300800, "k_fu2d_cols": 18330624, "k_fu1d": 379552256,
+TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (`ncu --set full`, one launch, cold cache)
+    "k_fu2d_gather": 42822400 + 1037312, "k_fu2d_adj_spread": 10835456 + 120320,
+    "k_fu2d_cols": 17608448 + 8846336, "k_fu1d": 268549376 + 109324288,
 }
 
 

@@ -80,7 +80,7 @@ int pass_cols(std::int64_t m) {
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
 template <class TIn, int W, bool PEER>
-__global__ void __launch_bounds__(512, 2) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
+__global__ void __launch_bounds__(1024, 1) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
                                               const double* __restrict__ wts, const double2* __restrict__ fac,
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* 
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n;
-  const int i = blockIdx.x, ks = blockIdx.y * ks_n;
+  const int i = blockIdx.y, ks = blockIdx.x * ks_n;  // ks groups of one line adjacent in launch order
   const double di = dx[i];
   auto load = [&](int r, int kk) {
     const int j = (r + center2) & mask2;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* 
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
-  const int c = blockIdx.x, ks = blockIdx.y * ks_n;
+  const int c = blockIdx.y, ks = blockIdx.x * ks_n;  // ks groups of one line adjacent in launch order
   auto load = [&](int r, int kk) {
     const int i = (r + center1) & mask1;
     const bool ok = i < n1;
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const floa
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
-  const int c = blockIdx.x, ks = blockIdx.y * ks_n;
+  const int c = blockIdx.y, ks = blockIdx.x * ks_n;  // ks groups of one line adjacent in launch order
   auto load = [&](int r, int kk) { return to_d(G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk]); };
   auto store = [&](int slot, int kk, double2 x) {  // keep the n1 slots that map to modes
     const int i = (slot + center1) & mask1;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const floa
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
-  const int i = blockIdx.x, ks = blockIdx.y * ks_n;
+  const int i = blockIdx.y, ks = blockIdx.x * ks_n;  // ks groups of one line adjacent in launch order
   const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   const double pi = pdx[i];
   // plane i of the output: local, or (fused all-to-all) in the HBM of the rank owning plane i
@@ -722,13 +722,13 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   const DimPlan& pz = t.pz;
   t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(fft_elems() / pz.m, 1, 64));
   t.z_ncol_adj = t.z_ncol;
-  // fu1d: 8 columns per CTA (512 threads at m = 512) make every global row
+  // fu1d: 8 columns per CTA (512 threads at m = 512, 1024 at m = 1024) make every global row
   // segment a full 128 B line and every shared-memory phase one grid row
   // (conflict-free taps); fu1d_adj keeps the smaller tile (its spread stage
   // holds h extra rows per column).
-  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(4096 / pz.m, 1, 64));
-  if (const char* e = std::getenv("MLRG_FU1D_NCOL"))  // tuning override (threads = ncol * m / 8 <= 512)
-    t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 4096 / pz.m)));
+  t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(pz.m >= 1024 ? 8192 / pz.m : 4096 / pz.m, 1, 64));
+  if (const char* e = std::getenv("MLRG_FU1D_NCOL"))  // tuning override (threads = ncol * m / 8 <= 1024)
+    t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 8192 / pz.m)));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
   t.z_ncol_adj = static_cast<int>(std::min<std::int64_t>(t.z_ncol_adj, g_.n2));
   t.z_deconv.upload(pz.deconv, stream_);
@@ -1056,14 +1056,14 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_rows", s);
-    k_fu2d_rows<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2), static_cast<unsigned>(ks2 * t.py.m / 8),
+    k_fu2d_rows<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)), static_cast<unsigned>(ks2 * t.py.m / 8),
                   static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), s>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
         t.y_deconv.get(), t.y_tw.get(), S, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", s);
     prof::begin("k_fu2d_cols", s);
-    k_fu2d_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
+    k_fu2d_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                   static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
         S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_cols");
@@ -1131,13 +1131,13 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     }
     prof::end("k_fu2d_adj_spread", s);
     prof::begin("k_fu2d_adj_cols", s);
-    k_fu2d_adj_cols<<<dim3(static_cast<unsigned>(t.py.m), KB / ks1), static_cast<unsigned>(ks1 * t.px.m / 8),
+    k_fu2d_adj_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                       static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
         Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     prof::end("k_fu2d_adj_cols", s);
     prof::begin("k_fu2d_adj_rows", s);
-    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(static_cast<unsigned>(g_.n1), KB / ks2),
+    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)),
                                                               static_cast<unsigned>(ks2 * t.py.m / 8),
                                                               static_cast<std::size_t>(t.py.m * (ks2 + 1)) *
                                                                   sizeof(double2),
