@@ -11,6 +11,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "solver.hpp"
@@ -326,13 +327,14 @@ mlr_array* mlr_project(const mlr_config* cfg, const mlr_array* volume) {
     upload_c64(volume->a, u, sg.s);
     out.resize(static_cast<std::size_t>(g.projection_shape().count()));
     forward_L(op, u.get(), out.get(), mid, proj);
-    auto* res = new mlr_array{mlrg::HostArray(g.projection_shape(), 0)};
+    auto* res = new mlr_array{mlrg::HostArray(g.projection_shape(), 0, /*zero=*/false)};
     download_c128(out.get(), res->a, sg.s);
     return res;
   });
 }
 
 mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const mlr_array* reference) {
+  mlrg::prof::HostSpan total("host:e2e_total");
   return guarded_ptr<mlr_result>([&] {
     need(cfg && data, "null argument");
     cfg->rc.validate();
@@ -343,20 +345,56 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
     if (reference && !(reference->a.shape == g.volume_shape()))
       throw std::invalid_argument("reference shape " + reference->a.shape.str() +
                                   " does not match the configured geometry " + g.volume_shape().str());
-    StreamGuard sg;
-    std::unique_ptr<mlrg::Engine> eng = build_engine(cfg->rc, g, sg.s);
-    mlrg::DeviceBuffer<float2> d, ref;
-    upload_c64(data->a, d, sg.s);
-    if (reference) upload_c64(reference->a, ref, sg.s);
     auto res = std::make_unique<mlr_result>();
+    // the result volume is allocated and its pages faulted in by host threads
+    // while the device iterates (first-touch faults of hundreds of MB otherwise
+    // land inside the final device-to-host copy)
+    std::thread prefault([&res, shape = g.volume_shape()] {
+      res->u.a = mlrg::HostArray(shape, 0, /*zero=*/false);
+      auto& v = res->u.a.data;
+      const std::size_t n = v.size(), nt = 8, per = (n + nt - 1) / nt;
+      std::vector<std::thread> th;
+      for (std::size_t t = 0; t < nt; ++t)
+        th.emplace_back([&v, n, lo = t * per, per] {
+          for (std::size_t i = lo; i < std::min(n, lo + per); i += 256) v[i] = {0.0, 0.0};
+        });
+      for (auto& x : th) x.join();
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{prefault};
+    auto teardown = std::make_unique<mlrg::prof::HostSpan>("host:e2e_teardown_and_rest");
+    StreamGuard sg;
+    std::unique_ptr<mlrg::Engine> eng;
     {
-      mlrg::Solver solver(d.get(), cfg->rc.admm, *eng, reference ? ref.get() : nullptr);
-      for (int it = 0; it < cfg->rc.admm.n_outer; ++it)
-        if (!solver.step()) break;
-      res->report = solver.report();
-      res->u.a = mlrg::HostArray(g.volume_shape(), 0);
+      mlrg::prof::HostSpan span("host:e2e_engine");
+      eng = build_engine(cfg->rc, g, sg.s);
+    }
+    mlrg::DeviceBuffer<float2> d, ref;
+    {
+      mlrg::prof::HostSpan span("host:e2e_upload");
+      upload_c64(data->a, d, sg.s);
+      if (reference) upload_c64(reference->a, ref, sg.s);
+    }
+    {
+      std::unique_ptr<mlrg::Solver> solver;
+      {
+        mlrg::prof::HostSpan span("host:e2e_solver_setup");
+        solver = std::make_unique<mlrg::Solver>(d.get(), cfg->rc.admm, *eng, reference ? ref.get() : nullptr);
+      }
+      {
+        mlrg::prof::HostSpan span("host:e2e_iterations");
+        for (int it = 0; it < cfg->rc.admm.n_outer; ++it)
+          if (!solver->step()) break;
+      }
+      mlrg::prof::HostSpan span("host:e2e_download");
+      res->report = solver->report();
+      prefault.join();
       // the iterate is complex128 on the device: no rounding on the way out
-      MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver.u(), res->u.a.data.size() * sizeof(double2),
+      MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2),
                                 cudaMemcpyDeviceToHost, sg.s));
       MLRG_CUDA(cudaStreamSynchronize(sg.s));
     }

@@ -28,6 +28,9 @@ void begin(const char* name, cudaStream_t s);
 void end(const char* name, cudaStream_t s);
 /// Accumulates a host-side phase's wall time under `name` when profiling is on.
 void host_add(const char* name, double ms);
+/// Adds the wall time since the previous mark (or HostSpan start) on this
+/// thread under `name` (sub-phases of one span).
+void host_mark(const char* name);
 /// RAII wall timer for host_add.
 class HostSpan {
  public:
@@ -43,6 +46,21 @@ class HostSpan {
 }  // namespace prof
 
 #define MLRG_CUDA(call) ::mlrg::cuda_check((call), #call)
+
+/// Process-wide caching allocator for device and pinned host blocks >= 1 MiB:
+/// cudaMalloc maps (and clears) pages at ~30 ms/GiB on B200, which made every
+/// drop-in mlr_reconstruct pay seconds of setup. Freed blocks stay mapped and
+/// are reused for requests of up to their size (at most 2x larger); a reuse
+/// after any release synchronises the device first, so no kernel of a previous
+/// owner can still be using the block. On cudaErrorMemoryAllocation the cache
+/// is released and the allocation retried.
+namespace alloc {
+void* device(std::size_t bytes);
+void device_free(void* p, std::size_t bytes);
+void* pinned(std::size_t bytes);
+void pinned_free(void* p, std::size_t bytes);
+void release_cache();
+}  // namespace alloc
 #define MLRG_LAUNCH_CHECK(name) (::mlrg::prof::count_launch(), ::mlrg::cuda_check(cudaGetLastError(), name))
 
 /// Owning device allocation (cudaMalloc), movable, zero-length allowed.
@@ -54,20 +72,27 @@ class DeviceBuffer {
   ~DeviceBuffer() { release(); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+  DeviceBuffer(DeviceBuffer&& o) noexcept
+      : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)), cap_(std::exchange(o.cap_, 0)) {}
   DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
     if (this != &o) {
       release();
       p_ = std::exchange(o.p_, nullptr);
       n_ = std::exchange(o.n_, 0);
+      cap_ = std::exchange(o.cap_, 0);
     }
     return *this;
   }
+  /// Grow-only: shrinking keeps the allocation (no release/reallocate churn
+  /// when a caller alternates sizes, e.g. per-call scratch of ragged slabs).
   void resize(std::size_t n) {
-    if (n == n_) return;
+    if (n <= cap_) {
+      n_ = n;
+      return;
+    }
     release();
-    if (n > 0) MLRG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
-    n_ = n;
+    p_ = static_cast<T*>(alloc::device(n * sizeof(T)));
+    n_ = cap_ = n;
   }
   void upload(const T* host, std::size_t n, cudaStream_t s) {
     resize(n);
@@ -82,12 +107,12 @@ class DeviceBuffer {
 
  private:
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) alloc::device_free(p_, cap_ * sizeof(T));
     p_ = nullptr;
-    n_ = 0;
+    n_ = cap_ = 0;
   }
   T* p_ = nullptr;
-  std::size_t n_ = 0;
+  std::size_t n_ = 0, cap_ = 0;
 };
 
 /// Owning page-locked host allocation for D2H of small results.
@@ -96,14 +121,14 @@ class PinnedBuffer {
  public:
   PinnedBuffer() = default;
   ~PinnedBuffer() {
-    if (p_) cudaFreeHost(p_);
+    if (p_) alloc::pinned_free(p_, n_ * sizeof(T));
   }
   PinnedBuffer(const PinnedBuffer&) = delete;
   PinnedBuffer& operator=(const PinnedBuffer&) = delete;
   PinnedBuffer(PinnedBuffer&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
   PinnedBuffer& operator=(PinnedBuffer&& o) noexcept {
     if (this != &o) {
-      if (p_) cudaFreeHost(p_);
+      if (p_) alloc::pinned_free(p_, n_ * sizeof(T));
       p_ = std::exchange(o.p_, nullptr);
       n_ = std::exchange(o.n_, 0);
     }
@@ -111,9 +136,9 @@ class PinnedBuffer {
   }
   void reserve(std::size_t n) {
     if (n <= n_) return;
-    if (p_) cudaFreeHost(p_);
+    if (p_) alloc::pinned_free(p_, n_ * sizeof(T));
     p_ = nullptr;
-    MLRG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    p_ = static_cast<T*>(alloc::pinned(n * sizeof(T)));
     n_ = n;
   }
   T* get() const { return p_; }
@@ -127,7 +152,7 @@ class PinnedBuffer {
 /// CTA order, so every reduction is deterministic (no float atomics).
 class Partials {
  public:
-  static constexpr int kMaxSlots = 1 << 20;
+  static constexpr int kMaxSlots = 1 << 17;
   Partials() {
     dev_.resize(static_cast<std::size_t>(kMaxSlots));
     host_.reserve(static_cast<std::size_t>(kMaxSlots));

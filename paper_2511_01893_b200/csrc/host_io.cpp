@@ -74,7 +74,7 @@ void smooth_noise(HostArray& a, std::uint64_t seed) {
   std::normal_distribution<double> noise(0.0, 1.0);
   for (cd& v : a.data) v = noise(rng);
   const Shape3 s = a.shape;
-  std::vector<cd> tmp(a.data.size());
+  decltype(a.data) tmp(a.data.size());
   for (int axis = 0; axis < 3; ++axis) {
     const std::int64_t len = s.extent(axis);
     for (std::int64_t i = 0; i < s.d0; ++i)

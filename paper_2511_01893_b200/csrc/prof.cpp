@@ -44,8 +44,21 @@ void host_add(const char* name, double ms) {
   ++e.second;
 }
 
+namespace {
+thread_local long long t_last_mark = 0;
+}
+void host_mark(const char* name) {
+  if (!enabled()) return;
+  const long long t = std::chrono::steady_clock::now().time_since_epoch().count();
+  if (t_last_mark)
+    host_add(name, static_cast<double>(t - t_last_mark) * 1e3 * std::chrono::steady_clock::period::num /
+                       std::chrono::steady_clock::period::den);
+  t_last_mark = t;
+}
 HostSpan::HostSpan(const char* name)
-    : name_(name), t0_(enabled() ? std::chrono::steady_clock::now().time_since_epoch().count() : 0) {}
+    : name_(name), t0_(enabled() ? std::chrono::steady_clock::now().time_since_epoch().count() : 0) {
+  t_last_mark = t0_;
+}
 HostSpan::~HostSpan() {
   if (!t0_) return;
   const long long t1 = std::chrono::steady_clock::now().time_since_epoch().count();

@@ -714,6 +714,7 @@ struct Usfft::Tables {
 
 Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     : g_(g), stream_(stream), kernel_(kernel), t_(new Tables) {
+  prof::HostSpan span("host:usfft_tables");
   Tables& t = *t_;
   const FrequencyGrids fg = frequency_grids(g_);
   // ---- fu1d plan (nufft.cpp:109-110) ----
@@ -763,6 +764,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   t.z_tw.upload(twiddles(pz.m), stream_);
 
+  prof::host_mark("host:usfft_fu1d_plan");
   // ---- fu2d plans (nufft.cpp:185-187) ----
   t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
   t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
@@ -785,6 +787,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     tf[q] = make_double2(f.real(), f.imag());
     tcf[q] = make_double2(ph.real(), -ph.imag());
   }
+  prof::host_mark("host:usfft_fu2d_plans");
   // Classes of coincident targets: equal window origins and kernel weights
   // within 1e-13 (the duplicates differ only by the rounding of cos/sin of
   // theta and theta + pi), at most kClassMax members (the n_theta samples of
@@ -857,21 +860,28 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     t.m_fac.upload(mfac, stream_);
     t.m_cfac.upload(mcfac, stream_);
   }
+  prof::host_mark("host:usfft_classes");
   {  // spread patches: 8x4 cells -> targets whose W x W window touches them (targets ascending)
     const std::int64_t npr = px.m / kPatchR, npc = py.m / kPatchC;
     const int npatch = static_cast<int>(npr * npc);
     // patches touched by a target's W x W window (dedup within the target)
     std::vector<int> touched;
+    // the window's distinct patch rows and columns (in first-touch order), then
+    // their product in the row-major order of the full W x W scan
+    std::vector<std::int64_t> prs, pcs;
     auto patches_of = [&](std::size_t c) {
       const std::size_t q = static_cast<std::size_t>(rep_of[c]);
-      touched.clear();
+      prs.clear();
+      pcs.clear();
       for (int a = 0; a < W; ++a) {
-        const std::int64_t pr = ((px.start[q] + a) % px.m) / kPatchR;
-        for (int b = 0; b < W; ++b) {
-          const int p = static_cast<int>(pr * npc + ((py.start[q] + b) % py.m) / kPatchC);
-          if (std::find(touched.begin(), touched.end(), p) == touched.end()) touched.push_back(p);
-        }
+        const std::int64_t pr = ((px.start[q] + a) % px.m + px.m) % px.m / kPatchR;
+        if (std::find(prs.begin(), prs.end(), pr) == prs.end()) prs.push_back(pr);
+        const std::int64_t pc = ((py.start[q] + a) % py.m + py.m) % py.m / kPatchC;
+        if (std::find(pcs.begin(), pcs.end(), pc) == pcs.end()) pcs.push_back(pc);
       }
+      touched.clear();
+      for (const std::int64_t pr : prs)
+        for (const std::int64_t pc : pcs) touched.push_back(static_cast<int>(pr * npc + pc));
     };
     std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0), lst;
     for (int pass = 0; pass < 2; ++pass) {
@@ -917,6 +927,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   t.x_tw.upload(twiddles(px.m), stream_);
   t.y_tw.upload(twiddles(py.m), stream_);
+  prof::host_mark("host:usfft_patches");
   t.S.resize(static_cast<std::size_t>(px.m * py.m * KB));
   t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB));
   t.val.resize(C * KB);
