@@ -91,38 +91,51 @@ __device__ __forceinline__ double2 bwd0(const double2* __restrict__ a, const dou
   return i > 0 ? a[idx - s0] : lo[pl];
 }
 
+// One voxel of k_grad_update; EDGE: plane 0 or n1-1 of this rank (axis-0
+// neighbours from the halo planes or absent), else the interior fast path.
+template <bool EDGE>
+__device__ __forceinline__ void grad_update_voxel(const double2* __restrict__ u, const CDField3& g,
+                                                  double2* __restrict__ G, const double2* __restrict__ p_prev,
+                                                  const double2* __restrict__ G_prev, const DevDims& d, double rho,
+                                                  const Halo& hl, long long idx, int i, int m, int j,
+                                                  double (&red)[3]) {
+  const int pos[3] = {i, m, j};
+  const int len[3] = {d.n1, d.n0, d.n2};
+  const long long st[3] = {d.s0, d.s1, 1};
+  const long long pl = static_cast<long long>(m) * d.n2 + j;
+  const double2 u0 = u[idx];
+  double2 dv = zero2();
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const bool fwd = EDGE && ax == 0 ? has_fwd(i, d.n1, hl.u_hi) : pos[ax] + 1 < len[ax];
+    double2 un = zero2();
+    if (fwd) un = EDGE && ax == 0 ? fwd0(u, hl.u_hi, i, d.n1, idx, st[0], pl) : u[idx + st[ax]];
+    const double2 gu = fwd ? dsub(un, u0) : zero2();
+    const double2 gd = dsub(gu, g.c[ax][idx]);  // (grad u - g)_ax at idx
+    red[0] += dnrm(gd);
+    if (fwd) dv = dadd(dv, gd);
+    const bool bwd = EDGE && ax == 0 ? has_bwd(i, hl.u_lo) : pos[ax] > 0;
+    if (bwd) {
+      const double2 ub = EDGE && ax == 0 ? bwd0(u, hl.u_lo, i, idx, st[0], pl) : u[idx - st[ax]];
+      const double2 gb = EDGE && ax == 0 ? bwd0(g.c[0], hl.g0_lo, i, idx, st[0], pl) : g.c[ax][idx - st[ax]];
+      dv = dsub(dv, dsub(dsub(u0, ub), gb));
+    }
+  }
+  const double2 Gn = dfma(-rho, dv, G[idx]);
+  G[idx] = Gn;
+  red[1] += dnrm(Gn);
+  if (p_prev) red[2] += dredot(p_prev[idx], dsub(Gn, G_prev[idx]));
+}
+
 __global__ void __launch_bounds__(kThreads) k_grad_update(const double2* __restrict__ u, CDField3 g,
                                                           double2* __restrict__ G,
                                                           const double2* __restrict__ p_prev,
                                                           const double2* __restrict__ G_prev, DevDims d,
                                                           double rho, double* __restrict__ partials, Halo hl) {
   double red[3] = {0.0, 0.0, 0.0};
-  const int len[3] = {d.n1, d.n0, d.n2};
-  const long long st[3] = {d.s0, d.s1, 1};
   for_voxels(d, [&](long long idx, int i, int m, int j) {
-    const int pos[3] = {i, m, j};
-    const long long pl = static_cast<long long>(m) * d.n2 + j;
-    const double2 u0 = u[idx];
-    double2 dv = zero2();
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      const bool fwd = ax == 0 ? has_fwd(i, d.n1, hl.u_hi) : pos[ax] + 1 < len[ax];
-      const double2 un = !fwd ? zero2() : ax == 0 ? fwd0(u, hl.u_hi, i, d.n1, idx, st[0], pl) : u[idx + st[ax]];
-      const double2 gu = fwd ? dsub(un, u0) : zero2();
-      const double2 gd = dsub(gu, g.c[ax][idx]);  // (grad u - g)_ax at idx
-      red[0] += dnrm(gd);
-      if (fwd) dv = dadd(dv, gd);
-      const bool bwd = ax == 0 ? has_bwd(i, hl.u_lo) : pos[ax] > 0;
-      if (bwd) {
-        const double2 ub = ax == 0 ? bwd0(u, hl.u_lo, i, idx, st[0], pl) : u[idx - st[ax]];
-        const double2 gb = ax == 0 ? bwd0(g.c[0], hl.g0_lo, i, idx, st[0], pl) : g.c[ax][idx - st[ax]];
-        dv = dsub(dv, dsub(dsub(u0, ub), gb));
-      }
-    }
-    const double2 Gn = dfma(-rho, dv, G[idx]);
-    G[idx] = Gn;
-    red[1] += dnrm(Gn);
-    if (p_prev) red[2] += dredot(p_prev[idx], dsub(Gn, G_prev[idx]));
+    if (i > 0 && i + 1 < d.n1) grad_update_voxel<false>(u, g, G, p_prev, G_prev, d, rho, hl, idx, i, m, j, red);
+    else grad_update_voxel<true>(u, g, G, p_prev, G_prev, d, rho, hl, idx, i, m, j, red);
   });
   write_partials<3>(red, partials);
 }
