@@ -100,3 +100,55 @@ def test_sharded_solver_matches_reference(mlrg, torch_cuda, tmp_path, case, memo
         # the objective cancels 3-4 digits by iteration 10 (see test_gpu_recon.py), so a
         # different summation order moves it ~1e-6 relative while u moves < 1e-8
         assert abs(float(r1[1]) - float(r2[1])) <= 1e-4 * abs(float(r1[1]))
+
+
+def _big_worker(rank, world, port, n, memo, steps, outdir):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_01893_b200 as m
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    comm = m.Comm.from_torch(timeout_s=300) if world > 1 else None
+    s = torch.cuda.current_stream()
+    ph = torch.from_numpy(m.make_phantom("blocks", n, n, n, 1).numpy().astype(np.complex64)).cuda()
+    ctx = m.Context(n, n, n, n, n, n, stream=s.cuda_stream)
+    d = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+    ctx.forward_L(ph, d)
+    ctx.sync()
+    del ctx
+    cfg = (f"n1={n}\nn0={n}\nn2={n}\nn_theta={n}\nh={n}\nw={n}\nn_outer={steps}\nmemoization={memo}\n"
+           f"nudft_path=gridding\n")
+    solver = m.Solver(cfg, d, reference=ph, stream=s.cuda_stream, comm=comm)
+    a, b, _, _ = solver.shard()
+    for _ in range(steps):
+        solver.step()
+    u = torch.empty((b - a, n, n), dtype=torch.complex64, device="cuda")
+    solver.volume(u)
+    meta, _ = solver.audit()
+    np.savez(os.path.join(outdir, f"w{world}_rank{rank}.npz"), u=u.cpu().numpy(), meta=meta, csv=solver.csv)
+    del solver
+    if comm is not None:
+        comm.barrier()
+    del comm
+    dist.destroy_process_group()
+
+
+def test_sharded_512_matches_single_gpu(mlrg, torch_cuda, tmp_path):
+    """configs[2] (512^3, 512 angles) z-slab split, SURVEY.md §8(d) parity gate for
+    cfg3: cross-GPU-count equality. Two ranks (sharing cuda:0) against one rank,
+    2 outer iterations with memoization on: identical memo decisions and u within
+    1e-6 (only the CG/ADMM scalar summation order differs)."""
+    import torch.multiprocessing as mp
+
+    n, steps = 512, 2
+    for world in (1, 2):
+        mp.start_processes(_big_worker, args=(world, free_port(), n, "local", steps, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    one = np.load(tmp_path / "w1_rank0.npz")
+    two = [np.load(tmp_path / f"w2_rank{r}.npz") for r in range(2)]
+    assert np.array_equal(two[0]["meta"], one["meta"]) and np.array_equal(two[1]["meta"], one["meta"])
+    u2 = np.concatenate([p["u"] for p in two], axis=0)
+    assert rel(u2, one["u"]) <= 1e-6
