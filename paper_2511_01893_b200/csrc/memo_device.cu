@@ -42,6 +42,9 @@ __device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long st
 // columns 2 LDS.128 (x) + 8 LDS.64 (P) feed 64 FMAs. Products are summed in
 // float within a chunk and in double across chunks (the reference accumulates
 // in double, encoder.cpp:416-420); slot kd of each slab carries sum |x|^2.
+#ifndef MLRG_ENC_MINB
+#define MLRG_ENC_MINB 2
+#endif
 constexpr int kEncWarps = 4;
 constexpr int kPStride = 36;  // floats per staged P row: 16 B aligned, conflict-free LDS.64 across rg
 constexpr int kXStride = 34;  // floats per staged slab row: conflict-free STS.64 / LDS.64
@@ -60,7 +63,7 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int sr
 }
 
 template <class TX>
-__global__ void __launch_bounds__(kEncWarps * 32) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
+__global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
                                                            const float* __restrict__ P, long long n, int kd,
                                                            bool p_vec, double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char enc_smem[];

@@ -152,3 +152,20 @@ def test_sharded_512_matches_single_gpu(mlrg, torch_cuda, tmp_path):
     assert np.array_equal(two[0]["meta"], one["meta"]) and np.array_equal(two[1]["meta"], one["meta"])
     u2 = np.concatenate([p["u"] for p in two], axis=0)
     assert rel(u2, one["u"]) <= 1e-6
+
+
+@pytest.mark.parametrize("n,world,memo", [(64, 3, "off"), (48, 2, "local"), (80, 3, "local")])
+def test_sharded_uneven_partitions_match_single_gpu(mlrg, torch_cuda, tmp_path, n, world, memo):
+    """Uneven assign() splits (ranks owning 1 or 2 slabs, a short last slab) and
+    more than two ranks: the same decisions and u as one rank."""
+    import torch.multiprocessing as mp
+
+    steps = 4
+    for wsz in (1, world):
+        mp.start_processes(_big_worker, args=(wsz, free_port(), n, memo, steps, str(tmp_path)), nprocs=wsz, join=True,
+                           start_method="spawn")
+    one = np.load(tmp_path / "w1_rank0.npz")
+    parts = [np.load(tmp_path / f"w{world}_rank{r}.npz") for r in range(world)]
+    for p in parts:
+        assert np.array_equal(p["meta"], one["meta"])
+    assert rel(np.concatenate([p["u"] for p in parts], axis=0), one["u"]) <= 1e-6
