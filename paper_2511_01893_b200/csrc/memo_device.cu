@@ -3,6 +3,7 @@
 // streamed from HBM once per call), and the slab copy kernels that
 // materialise hits and capture miss values (scalerun.cpp:86-105, 250-283).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "device.hpp"
@@ -62,7 +63,24 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int sr
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
 }
 
-template <class TX>
+// TC: the chunk products run on the tensor cores (mma.sync m16n8k8 TF32 with the
+// 3xTF32 split a = a_hi + a_lo, products a_hi b_hi + a_hi b_lo + a_lo b_hi, ~2^-21
+// relative per product, fp32 accumulation within the 32-column chunk like the
+// FFMA path), which removes the FMA/shared-load issue limit of the skinny GEMM.
+__device__ __forceinline__ void tf32_split(float v, unsigned& hi, unsigned& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
+  const float r = v - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const unsigned (&a)[4], const unsigned (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <class TX, bool TC>
 __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const TX* __restrict__ x, SlabGeom g, SlabList sl, int ns,
                                                            const float* __restrict__ P, long long n, int kd,
                                                            bool p_vec, double* __restrict__ part) {
@@ -124,6 +142,8 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
     asm volatile("cp.async.commit_group;\n" ::);
   };
 
+  // FFMA path: lane (sg, rg) owns slabs 4 sg + a x rows 8 i + rg; TC path: lane
+  // (gq, tq) owns the mma C fragments, rows 16 mt + gq (+8) x slabs 8 nt + 2 tq (+1)
   double acc[4][8], nrm[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -131,6 +151,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[a][i] = 0.0;
   }
+  const int gq = lane >> 2, tq = lane & 3;
   int buf = 0;
   if (gw < nchunks) {
     load_p(st[0], gw);
@@ -148,36 +169,80 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
     }
     __syncwarp();
     const EncStage& b = st[buf];
-    float fa[4][8], fn[4];
+    if constexpr (TC) {
+      float c[4][2][4], fn[2] = {0.f, 0.f};
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      fn[a] = 0.f;
+      for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fa[a][i] = 0.f;
-    }
-#pragma unroll 4
-    for (int kk = 0; kk < 32; kk += 2) {
-      float xa0[4], xa1[4];
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) c[mt][nt][i] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k0 = 8 * ks;
+        unsigned bh[2][2], bl[2][2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const float b0 = b.x[8 * nt + gq][k0 + tq], b1 = b.x[8 * nt + gq][k0 + tq + 4];
+          fn[nt] = fmaf(b1, b1, fmaf(b0, b0, fn[nt]));
+          tf32_split(b0, bh[nt][0], bl[nt][0]);
+          tf32_split(b1, bh[nt][1], bl[nt][1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const float av[4] = {b.p[16 * mt + gq][k0 + tq], b.p[16 * mt + gq + 8][k0 + tq],
+                               b.p[16 * mt + gq][k0 + tq + 4], b.p[16 * mt + gq + 8][k0 + tq + 4]};
+          unsigned ah[4], al[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) tf32_split(av[i], ah[i], al[i]);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            mma_tf32(c[mt][nt], al, bh[nt]);
+            mma_tf32(c[mt][nt], ah, bl[nt]);
+            mma_tf32(c[mt][nt], ah, bh[nt]);
+          }
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[mt][nt * 4 + i] += c[mt][nt][i];
+      nrm[0] += fn[0];
+      nrm[1] += fn[1];
+    } else {
+      float fa[4][8], fn[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const float2 xv = *reinterpret_cast<const float2*>(&b.x[4 * sg + a][kk]);
-        xa0[a] = xv.x;
-        xa1[a] = xv.y;
+        fn[a] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) fa[a][i] = 0.f;
+      }
+#pragma unroll 4
+      for (int kk = 0; kk < 32; kk += 2) {
+        float xa0[4], xa1[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const float2 xv = *reinterpret_cast<const float2*>(&b.x[4 * sg + a][kk]);
+          xa0[a] = xv.x;
+          xa1[a] = xv.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 pv = *reinterpret_cast<const float2*>(&b.p[8 * i + rg][kk]);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) fa[a][i] = fmaf(pv.y, xa1[a], fmaf(pv.x, xa0[a], fa[a][i]));
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fn[a] = fmaf(xa1[a], xa1[a], fmaf(xa0[a], xa0[a], fn[a]));
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 pv = *reinterpret_cast<const float2*>(&b.p[8 * i + rg][kk]);
+      for (int a = 0; a < 4; ++a) {
+        nrm[a] += fn[a];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a][i] = fmaf(pv.y, xa1[a], fmaf(pv.x, xa0[a], fa[a][i]));
+        for (int i = 0; i < 8; ++i) acc[a][i] += fa[a][i];
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) fn[a] = fmaf(xa1[a], xa1[a], fmaf(xa0[a], xa0[a], fn[a]));
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      nrm[a] += fn[a];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[a][i] += fa[a][i];
     }
     __syncwarp();
     if (more) store_x(st[buf ^ 1]);
@@ -188,11 +253,30 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
   __syncthreads();
   double* red = reinterpret_cast<double*>(enc_smem);  // [warp][16][kRows + 1]
   constexpr int kRS = kRows + 1;
+  if constexpr (TC) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) red[(warp * 16 + 4 * sg + a) * kRS + 8 * i + rg] = acc[a][i];
-    if (rg == 0) red[(warp * 16 + 4 * sg + a) * kRS + kRows] = nrm[a];
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 16 * mt + gq + (i >= 2 ? 8 : 0), slab = 8 * nt + 2 * tq + (i & 1);
+          red[(warp * 16 + slab) * kRS + row] = acc[mt][nt * 4 + i];
+        }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {  // |x|^2: the 4 lanes of a quad hold one slab's columns
+      double v = nrm[nt];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (tq == 0) red[(warp * 16 + 8 * nt + gq) * kRS + kRows] = v;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) red[(warp * 16 + 4 * sg + a) * kRS + 8 * i + rg] = acc[a][i];
+      if (rg == 0) red[(warp * 16 + 4 * sg + a) * kRS + kRows] = nrm[a];
+    }
   }
   __syncthreads();
   double* pb = part + static_cast<long long>(blockIdx.x) * ns * (kd + 1);
@@ -368,8 +452,10 @@ void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns
   static_assert(smem >= sizeof(double) * kEncWarps * 16 * (kRows + 1), "reduction scratch must fit");
   static bool attr = false;
   if (!attr) {
-    MLRG_CUDA(cudaFuncSetAttribute(k_encode<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MLRG_CUDA(cudaFuncSetAttribute(k_encode<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<float2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<double2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<float2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MLRG_CUDA(cudaFuncSetAttribute(k_encode<double2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   const bool p_vec = (2 * n) % 4 == 0 && reinterpret_cast<std::uintptr_t>(P) % 16 == 0;
@@ -379,7 +465,12 @@ void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns
     for (int q = 0; q < nb; ++q) sl.start[q] = starts[b + q];
     const int blocks = enc_blocks();
     prof::begin("k_encode", s);
-    k_encode<TX><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
+    static const bool tc = [] {  // MLRG_ENCODE_TC=0: the FFMA path
+      const char* e = std::getenv("MLRG_ENCODE_TC");
+      return !(e && *e == '0');
+    }();
+    if (tc) k_encode<TX, true><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
+    else k_encode<TX, false><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
     MLRG_LAUNCH_CHECK("k_encode");
     prof::end("k_encode", s);
     const int per = nb * (kd + 1);
