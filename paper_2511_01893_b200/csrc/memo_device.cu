@@ -47,6 +47,10 @@ __device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long st
 #define MLRG_ENC_MINB 2
 #endif
 constexpr int kEncWarps = 4;
+#ifndef MLRG_TC_FLUSH
+#define MLRG_TC_FLUSH 2
+#endif
+constexpr int kTcFlush = MLRG_TC_FLUSH;  // chunks (of 32 columns) summed in fp32 before the double add
 constexpr int kPStride = 36;  // floats per staged P row: 16 B aligned, conflict-free LDS.64 across rg
 constexpr int kXStride = 34;  // floats per staged slab row: conflict-free STS.64 / LDS.64
 struct EncStage {
@@ -152,6 +156,14 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
     for (int i = 0; i < 8; ++i) acc[a][i] = 0.0;
   }
   const int gq = lane >> 2, tq = lane & 3;
+  float tc_c[4][2][4], tc_fn[2] = {0.f, 0.f};  // TC: fp32 chunk-group partials
+  int tc_n = 0;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc_c[mt][nt][i] = 0.f;
   int buf = 0;
   if (gw < nchunks) {
     load_p(st[0], gw);
@@ -170,13 +182,8 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
     __syncwarp();
     const EncStage& b = st[buf];
     if constexpr (TC) {
-      float c[4][2][4], fn[2] = {0.f, 0.f};
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) c[mt][nt][i] = 0.f;
+      auto& c = tc_c;
+      auto& fn = tc_fn;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const int k0 = 8 * ks;
@@ -203,14 +210,22 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
           }
         }
       }
+      // fp32 over kTcFlush chunks, then double
+      if (++tc_n == kTcFlush || !more) {
+        tc_n = 0;
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
+          for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[mt][nt * 4 + i] += c[mt][nt][i];
-      nrm[0] += fn[0];
-      nrm[1] += fn[1];
+            for (int i = 0; i < 4; ++i) {
+              acc[mt][nt * 4 + i] += c[mt][nt][i];
+              c[mt][nt][i] = 0.f;
+            }
+        nrm[0] += fn[0];
+        nrm[1] += fn[1];
+        fn[0] = fn[1] = 0.f;
+      }
     } else {
       float fa[4][8], fn[4];
 #pragma unroll
