@@ -110,6 +110,9 @@ typedef struct mlrg_comm mlrg_comm;
 mlrg_comm* mlrg_comm_create(const char* name, int rank, int world, double timeout_s);
 void mlrg_comm_free(mlrg_comm* c);
 int mlrg_comm_barrier(mlrg_comm* c);
+/* Marks the job failed: every rank in (or entering) a collective returns
+ * MLR_ERR_RUNTIME instead of waiting (a failing mlrg_solver_step does this). */
+int mlrg_comm_abort(mlrg_comm* c);
 /* v[i] = sum over ranks, added in rank order (bit-identical on every rank). */
 int mlrg_comm_allreduce(mlrg_comm* c, double* v, int n);
 /* out = every rank's `bytes` bytes, concatenated in rank order (bytes <= 1 MiB). */

@@ -102,6 +102,7 @@ _SIGS = {
     "mlrg_comm_create": (_P, [C.c_char_p, C.c_int, C.c_int, _D]),
     "mlrg_comm_free": (None, [_P]),
     "mlrg_comm_barrier": (C.c_int, [_P]),
+    "mlrg_comm_abort": (C.c_int, [_P]),
     "mlrg_comm_allreduce": (C.c_int, [_P, _P, C.c_int]),
     "mlrg_comm_allgather": (C.c_int, [_P, _P, _U64, _P]),
     "mlrg_partition": (C.c_int, [_I64, _I64, _I64, C.c_int, _P]),
@@ -451,6 +452,9 @@ class Comm:
 
     def barrier(self):
         _gcheck(lib().mlrg_comm_barrier(self._h))
+
+    def abort(self):
+        _gcheck(lib().mlrg_comm_abort(self._h))
 
     def allreduce(self, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.float64)

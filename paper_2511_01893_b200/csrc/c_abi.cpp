@@ -772,7 +772,13 @@ int mlrg_solver_shard(const mlrg_solver* s, int64_t out[4]) {
 int mlrg_solver_step(mlrg_solver* s, int* aborted) {
   return guarded([&] {
     need(s != nullptr, "null solver");
-    const bool ok = s->solver->step();
+    bool ok = false;
+    try {
+      ok = s->solver->step();
+    } catch (...) {  // sharded: release the peers blocked in a collective
+      if (s->eng->shard().comm) s->eng->shard().comm->abort();
+      throw;
+    }
     MLRG_CUDA(cudaStreamSynchronize(s->eng->stream()));
     if (aborted) *aborted = ok ? 0 : 1;
   });
@@ -922,6 +928,13 @@ int mlrg_comm_barrier(mlrg_comm* c) {
   return guarded([&] {
     need(c != nullptr, "null comm");
     c->c->barrier();
+  });
+}
+
+int mlrg_comm_abort(mlrg_comm* c) {
+  return guarded([&] {
+    need(c != nullptr, "null comm");
+    c->c->abort();
   });
 }
 

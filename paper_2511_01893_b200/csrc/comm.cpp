@@ -112,8 +112,13 @@ HostComm::~HostComm() {
   if (rank_ == 0) shm_unlink(name_.c_str());
 }
 
+void HostComm::abort() {
+  if (hdr_) hdr_->abort.store(1);
+}
+
 void HostComm::barrier() {
   if (world_ == 1) return;
+  if (hdr_->abort.load(std::memory_order_relaxed)) fail("a peer rank failed");
   const std::uint64_t g = hdr_->gen.load(std::memory_order_acquire);
   if (hdr_->count.fetch_add(1, std::memory_order_acq_rel) + 1 == world_) {
     hdr_->count.store(0, std::memory_order_relaxed);

@@ -37,6 +37,9 @@ class HostComm {
   int world() const { return world_; }
 
   void barrier();
+  /// Marks the job failed: every rank blocked in (or entering) a collective
+  /// throws instead of waiting for this one.
+  void abort();
   /// In place: v[i] = sum over ranks (added in rank order, so every rank gets
   /// the bit-identical result).
   void allreduce_sum(double* v, int n);

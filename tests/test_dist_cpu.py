@@ -141,3 +141,27 @@ def _sharded_replay_worker(rank, world, port, case):
 def test_sharded_memo_decisions_match_reference(case):
     golden(case)  # skip when the fixture is absent
     _run(_sharded_replay_worker, case)
+
+
+def _abort_worker(rank, world, port):
+    m, dist = _init(rank, world, port)
+    comm = m.Comm.from_torch(timeout_s=60)
+    comm.barrier()
+    if rank == 0:  # this rank fails; its peers must not wait for it
+        comm.abort()
+    else:
+        import time
+
+        t0 = time.perf_counter()
+        with pytest.raises(m.MlrError, match="peer rank failed"):
+            comm.barrier()
+        assert time.perf_counter() - t0 < 30.0
+    with pytest.raises(m.MlrError):  # payloads above the 1 MiB slot are refused
+        comm.allgather(b"x" * ((1 << 20) + 1))
+    dist.barrier()
+    del comm
+    dist.destroy_process_group()
+
+
+def test_comm_abort_releases_peers():
+    _run(_abort_worker)

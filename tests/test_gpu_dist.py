@@ -102,7 +102,7 @@ def test_sharded_solver_matches_reference(mlrg, torch_cuda, tmp_path, case, memo
         assert abs(float(r1[1]) - float(r2[1])) <= 1e-4 * abs(float(r1[1]))
 
 
-def _big_worker(rank, world, port, n, memo, steps, outdir):
+def _big_worker(rank, world, port, n, memo, steps, outdir, offload="off"):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -120,7 +120,7 @@ def _big_worker(rank, world, port, n, memo, steps, outdir):
     ctx.sync()
     del ctx
     cfg = (f"n1={n}\nn0={n}\nn2={n}\nn_theta={n}\nh={n}\nw={n}\nn_outer={steps}\nmemoization={memo}\n"
-           f"nudft_path=gridding\n")
+           f"nudft_path=gridding\noffload={offload}\n")
     solver = m.Solver(cfg, d, reference=ph, stream=s.cuda_stream, comm=comm)
     a, b, _, _ = solver.shard()
     for _ in range(steps):
@@ -154,16 +154,19 @@ def test_sharded_512_matches_single_gpu(mlrg, torch_cuda, tmp_path):
     assert rel(u2, one["u"]) <= 1e-6
 
 
-@pytest.mark.parametrize("n,world,memo", [(64, 3, "off"), (48, 2, "local"), (80, 3, "local")])
-def test_sharded_uneven_partitions_match_single_gpu(mlrg, torch_cuda, tmp_path, n, world, memo):
-    """Uneven assign() splits (ranks owning 1 or 2 slabs, a short last slab) and
-    more than two ranks: the same decisions and u as one rank."""
+@pytest.mark.parametrize("n,world,memo,offload", [(64, 3, "off", "off"), (48, 2, "local", "off"),
+                                                 (80, 3, "local", "off"), (64, 2, "local", "host")])
+def test_sharded_uneven_partitions_match_single_gpu(mlrg, torch_cuda, tmp_path, n, world, memo, offload):
+    """Uneven assign() splits (ranks owning 1 or 2 slabs, a short last slab), more
+    than two ranks, and ADMM-Offload under sharding: the same decisions and u as
+    one rank without offload."""
     import torch.multiprocessing as mp
 
     steps = 4
     for wsz in (1, world):
-        mp.start_processes(_big_worker, args=(wsz, free_port(), n, memo, steps, str(tmp_path)), nprocs=wsz, join=True,
-                           start_method="spawn")
+        mp.start_processes(_big_worker, args=(wsz, free_port(), n, memo, steps, str(tmp_path),
+                                              offload if wsz > 1 else "off"),
+                           nprocs=wsz, join=True, start_method="spawn")
     one = np.load(tmp_path / "w1_rank0.npz")
     parts = [np.load(tmp_path / f"w{world}_rank{r}.npz") for r in range(world)]
     for p in parts:
