@@ -128,7 +128,11 @@ __device__ __forceinline__ void fft_reg(double2* v) {
 // One pass. GIN: the pass reads its inputs through load(row, b) (global
 // memory, the transform's first pass) instead of the tile; GOUT: it writes
 // through store(row, b, value) (the last pass) instead of the tile.
-template <int R, int LOGR, int SIGN, bool GIN, bool GOUT, class Load, class Store>
+// ZP (zero-padded input, first pass only): the input of slots [m/4, 3m/4) is
+// known to be zero (a length-n signal centred in m = 2n slots: fu1d, the fu2d
+// row and column passes), so a radix-8 first pass never loads its inputs
+// r = 2..5 (rows [m/4, 3m/4) for stride m/8).
+template <int R, int LOGR, int SIGN, bool GIN, bool GOUT, bool ZP, class Load, class Store>
 __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, int logm, int logns,
                                               const double2* __restrict__ tw, const Load& load, const Store& store) {
   constexpr int PER = 8 / R;
@@ -140,8 +144,14 @@ __device__ __forceinline__ void stockham_pass(double2* s, int ld, int b, int g, 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = gg + r * stride;
-      if constexpr (GIN) v[q * R + r] = load(row, b);
-      else v[q * R + r] = s[row * ld + b];
+      if constexpr (GIN && ZP && R == 8) {
+        if (r >= 2 && r < 6) v[q * R + r] = make_double2(0.0, 0.0);
+        else v[q * R + r] = load(row, b);
+      } else if constexpr (GIN) {
+        v[q * R + r] = load(row, b);
+      } else {
+        v[q * R + r] = s[row * ld + b];
+      }
     }
   }
   if constexpr (!GIN || GOUT) __syncthreads();  // in place: every read precedes any write
@@ -195,29 +205,29 @@ struct NoStore {
 // first pass reads load(row, b) for row < m (natural input order); with GOUT
 // the last pass hands X[row] of column b to store(row, b, X) and the tile is
 // left as scratch; otherwise the tile holds the input / output.
-template <int SIGN, bool GIN = false, bool GOUT = false, class Load = NoLoad, class Store = NoStore>
+template <int SIGN, bool GIN = false, bool GOUT = false, bool ZP = false, class Load = NoLoad, class Store = NoStore>
 __device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw,
                                              const Load& load = Load(), const Store& store = Store()) {
   const int b = threadIdx.x % nb, g = threadIdx.x / nb;
   const int npass = (logm + 2) / 3;
   int logns = 0, p = 0;
   if (logm % 3 == 1) {
-    if (npass == 1) stockham_pass<2, 1, SIGN, GIN, GOUT>(s, ld, b, g, logm, 0, tw, load, store);
-    else stockham_pass<2, 1, SIGN, GIN, false>(s, ld, b, g, logm, 0, tw, load, store);
+    if (npass == 1) stockham_pass<2, 1, SIGN, GIN, GOUT, false>(s, ld, b, g, logm, 0, tw, load, store);
+    else stockham_pass<2, 1, SIGN, GIN, false, false>(s, ld, b, g, logm, 0, tw, load, store);
     logns = 1;
     p = 1;
   } else if (logm % 3 == 2) {
-    if (npass == 1) stockham_pass<4, 2, SIGN, GIN, GOUT>(s, ld, b, g, logm, 0, tw, load, store);
-    else stockham_pass<4, 2, SIGN, GIN, false>(s, ld, b, g, logm, 0, tw, load, store);
+    if (npass == 1) stockham_pass<4, 2, SIGN, GIN, GOUT, false>(s, ld, b, g, logm, 0, tw, load, store);
+    else stockham_pass<4, 2, SIGN, GIN, false, false>(s, ld, b, g, logm, 0, tw, load, store);
     logns = 2;
     p = 1;
   }
   for (; logns < logm; logns += 3, ++p) {
     const bool first = p == 0, last = p == npass - 1;
-    if (first && last) stockham_pass<8, 3, SIGN, GIN, GOUT>(s, ld, b, g, logm, logns, tw, load, store);
-    else if (first) stockham_pass<8, 3, SIGN, GIN, false>(s, ld, b, g, logm, logns, tw, load, store);
-    else if (last) stockham_pass<8, 3, SIGN, false, GOUT>(s, ld, b, g, logm, logns, tw, load, store);
-    else stockham_pass<8, 3, SIGN, false, false>(s, ld, b, g, logm, logns, tw, load, store);
+    if (first && last) stockham_pass<8, 3, SIGN, GIN, GOUT, ZP>(s, ld, b, g, logm, logns, tw, load, store);
+    else if (first) stockham_pass<8, 3, SIGN, GIN, false, ZP>(s, ld, b, g, logm, logns, tw, load, store);
+    else if (last) stockham_pass<8, 3, SIGN, false, GOUT, false>(s, ld, b, g, logm, logns, tw, load, store);
+    else stockham_pass<8, 3, SIGN, false, false, false>(s, ld, b, g, logm, logns, tw, load, store);
   }
 }
 

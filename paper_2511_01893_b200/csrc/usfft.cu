@@ -79,7 +79,7 @@ int pass_cols(std::int64_t m) {
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
-template <class TIn, int W, bool PEER>
+template <class TIn, int W, bool PEER, bool ZP>
 __global__ void __launch_bounds__(1024, 1) k_fu1d(const TIn* __restrict__ u, float2* __restrict__ out, int n0, int n2,
                                               int h, int logm, int center, int ncol,
                                               const double* __restrict__ deconv, const int* __restrict__ start,
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(1024, 1) k_fu1d(const TIn* __restrict__ u, flo
     const double dc = deconv[ok ? mode : 0];
     return ok ? cscale(x, dc) : make_double2(0.0, 0.0);
   };
-  fft_stockham<+1, true, false>(sd, logm, ncol, ncol, tw, load);
+  fft_stockham<+1, true, false, ZP>(sd, logm, ncol, ncol, tw, load);
   float2* oi = out + static_cast<long long>(blockIdx.y) * h * n2;
   for (int idx = threadIdx.x; idx < h * ncol; idx += blockDim.x) {
     const int k = idx / ncol, c = idx - k * ncol;
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
 // fu2d forward: row pass, column pass, gather
 // ------------------------------------------------------------------------------------------
 // S[i][c'][KB]: row FFT of v[i, k0+kk, :] * dx[i] * dy[:] placed at wrapped slots.
+template <bool ZP>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
@@ -192,10 +193,11 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* 
   };
   float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
   auto store = [&](int r, int kk, double2 x) { Si[static_cast<long long>(r) * KB + kk] = to_f(x); };
-  fft_stockham<+1, true, true>(sd, logm2, ks_n, sm, tw2, load, store);
+  fft_stockham<+1, true, true, ZP>(sd, logm2, ks_n, sm, tw2, load, store);
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
+template <bool ZP>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
                                                    float2* __restrict__ G, Skip sk) {
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* 
     return ok ? x : make_double2(0.0, 0.0);
   };
   auto store = [&](int r, int kk, double2 x) { G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(x); };
-  fft_stockham<+1, true, true>(sd, logm1, ks_n, ks_n, tw1, load, store);
+  fft_stockham<+1, true, true, ZP>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
 struct GatherOut {
@@ -651,6 +653,9 @@ std::vector<double2> twiddles(std::int64_t m) {
 }
 
 bool is_pow2(std::int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+// A length-n signal placed at the centred slots of an m = 2n grid: the input of
+// slots [m/4, 3m/4) is zero (the ZP first pass of fft_stockham skips it).
+bool zero_padded(const DimPlan& p) { return p.m == 2 * p.n && 2 * p.center == p.n; }
 int ilog2(std::int64_t n) {
   int l = 0;
   while ((std::int64_t{1} << l) < n) ++l;
@@ -957,18 +962,26 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   MLRG_CUDA(cudaStreamSynchronize(stream_));
   static bool smem_set = [] {
-    allow_big_smem(k_fu1d<float2, kEsTaps, false>);
-    allow_big_smem(k_fu1d<double2, kEsTaps, false>);
-    allow_big_smem(k_fu1d<double2, kEsTaps, true>);
-    allow_big_smem(k_fu1d<float2, kTaps, false>);
-    allow_big_smem(k_fu1d<double2, kTaps, false>);
-    allow_big_smem(k_fu1d<double2, kTaps, true>);
+    allow_big_smem(k_fu1d<float2, kEsTaps, false, false>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, false, false>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, true, false>);
+    allow_big_smem(k_fu1d<float2, kTaps, false, false>);
+    allow_big_smem(k_fu1d<double2, kTaps, false, false>);
+    allow_big_smem(k_fu1d<double2, kTaps, true, false>);
+    allow_big_smem(k_fu1d<float2, kEsTaps, false, true>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, false, true>);
+    allow_big_smem(k_fu1d<double2, kEsTaps, true, true>);
+    allow_big_smem(k_fu1d<float2, kTaps, false, true>);
+    allow_big_smem(k_fu1d<double2, kTaps, false, true>);
+    allow_big_smem(k_fu1d<double2, kTaps, true, true>);
     allow_big_smem(k_fu1d_adj<float2>);
     allow_big_smem(k_fu1d_adj<double2>);
-    allow_big_smem(k_fu2d_rows);
+    allow_big_smem(k_fu2d_rows<false>);
+    allow_big_smem(k_fu2d_rows<true>);
     allow_big_smem(k_fu2d_adj_spread<kEsTaps>);
     allow_big_smem(k_fu2d_adj_spread<kTaps>);
-    allow_big_smem(k_fu2d_cols);
+    allow_big_smem(k_fu2d_cols<false>);
+    allow_big_smem(k_fu2d_cols<true>);
     allow_big_smem(k_fu2d_adj_cols);
     allow_big_smem(k_fu2d_adj_rows<false>);
     allow_big_smem(k_fu2d_adj_rows<true>);
@@ -1011,9 +1024,14 @@ void Usfft::fu1d_t(const TIn* u, float2* out, std::int64_t d0, const PeerOut* pe
   const dim3 grid(static_cast<unsigned>((g_.n2 + ncol - 1) / ncol), static_cast<unsigned>(d0));
   const std::size_t smem = static_cast<std::size_t>(t.pz.m * ncol) * sizeof(double2);
   prof::begin("k_fu1d", stream_);
-  auto kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps, false> : k_fu1d<TIn, kTaps, false>;
+  const bool zp = zero_padded(t.pz);
+  auto pick = [&](auto es, auto ga) { return t.pz.taps == kEsTaps ? es : ga; };
+  auto kern = zp ? pick(k_fu1d<TIn, kEsTaps, false, true>, k_fu1d<TIn, kTaps, false, true>)
+                 : pick(k_fu1d<TIn, kEsTaps, false, false>, k_fu1d<TIn, kTaps, false, false>);
   if constexpr (std::is_same_v<TIn, double2>)
-    if (peer) kern = t.pz.taps == kEsTaps ? k_fu1d<TIn, kEsTaps, true> : k_fu1d<TIn, kTaps, true>;
+    if (peer)
+      kern = zp ? pick(k_fu1d<TIn, kEsTaps, true, true>, k_fu1d<TIn, kTaps, true, true>)
+                : pick(k_fu1d<TIn, kEsTaps, true, false>, k_fu1d<TIn, kTaps, true, false>);
   kern<<<grid, static_cast<unsigned>(ncol * t.pz.m / 8), smem, stream_>>>(u, out, static_cast<int>(g_.n0), static_cast<int>(g_.n2),
                                      static_cast<int>(g_.h), t.pz.logm, static_cast<int>(t.pz.center), ncol,
                                      t.z_deconv.get(), t.z_start.get(), t.z_w.get(), t.z_fac.get(), t.z_tw.get(),
@@ -1067,14 +1085,14 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_rows", s);
-    k_fu2d_rows<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)), static_cast<unsigned>(ks2 * t.py.m / 8),
+    (zero_padded(t.py) ? k_fu2d_rows<true> : k_fu2d_rows<false>)<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)), static_cast<unsigned>(ks2 * t.py.m / 8),
                   static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), s>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
         t.y_deconv.get(), t.y_tw.get(), S, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", s);
     prof::begin("k_fu2d_cols", s);
-    k_fu2d_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+    (zero_padded(t.px) ? k_fu2d_cols<true> : k_fu2d_cols<false>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                   static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
         S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_cols");
