@@ -40,8 +40,8 @@ TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (`ncu --set full`, one launc
 }
 # the same captures' per-launch durations (us): ncu serialises launches, while the bench
 # overlaps fu2d row batches on two streams (live durations include the sharing)
-SERIAL_US: dict = {"k_fu2d_gather": 57.28, "k_fu2d_adj_spread": 62.40, "k_fu2d_cols": 29.25, "k_fu2d_rows": 19.26,
-                   "k_fu1d": 321.15, "k_fu1d_adj": 519.42, "k_fu2d_adj_cols": 27.94}
+SERIAL_US: dict = {"k_fu2d_gather": 57.28, "k_fu2d_adj_spread": 62.40, "k_fu2d_cols": 27.33, "k_fu2d_rows": 18.02,
+                   "k_fu1d": 324.99, "k_fu1d_adj": 519.42, "k_fu2d_adj_cols": 27.94}
 
 
 def parse():
