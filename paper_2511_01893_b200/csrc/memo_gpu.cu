@@ -333,6 +333,7 @@ void DeviceMemo::lookup(OpId op, int n, const float* keys, const double* norms2,
 }
 
 void DeviceMemo::upload_ivf(cudaStream_t s) {
+  prof::HostSpan span("host:memo_upload_ivf");
   const MemoStore& st = client_.store();
   if (!st.trained()) return;
   const auto& cents = st.centroids();

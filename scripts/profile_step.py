@@ -41,14 +41,17 @@ def main():
     torch.cuda.cudart().cudaProfilerStart()
     m.lib().mlrg_prof_reset()
     m.lib().mlrg_prof_enable(1)
+    prev_flush = 0.0
     for _ in range(a.steps):
         t0 = time.perf_counter()
         s.step()
         torch.cuda.synchronize()
-        print(f"step {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+        fl = m.prof_query("host:memo_flush")[0]
+        print(f"step {1e3 * (time.perf_counter() - t0):.2f} ms (flush {fl - prev_flush:.2f} ms)", flush=True)
+        prev_flush = fl
     torch.cuda.cudart().cudaProfilerStop()
     m.lib().mlrg_prof_enable(0)
-    for k in ("host:memo_key_sync", "host:memo_lookup", "host:memo_alloc", "host:memo_flush", "k_encode"):
+    for k in ("host:memo_flush", "host:memo_train", "host:memo_upload_ivf", "k_encode"):
         tot, cnt = m.prof_query(k)
         print(f"{k}: {tot:.2f} ms over {cnt}")
     print("profiled", a.steps, "step(s) at", n, s.counters())
