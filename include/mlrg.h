@@ -65,6 +65,14 @@ int mlrg_div(mlrg_ctx* ctx, const void* g0, const void* g1, const void* g2, void
 int mlrg_encode(mlrg_ctx* ctx, int op, const void* x, int64_t chunk_extent, int key_dim, uint64_t seed,
                 float* keys, double* norms, int64_t n_slabs);
 
+/* The CNN key encoder (encoder_variant = cnn, encoder.cpp:95-197) with the seeded
+ * initial weights (init_cnn): raw keys [n_slabs][key_dim] (before slot_mix) and
+ * input norms of every chunk_extent slab of the op's input. */
+int mlrg_encode_cnn(mlrg_ctx* ctx, int op, const void* x, int64_t chunk_extent, int key_dim, uint64_t seed,
+                    float* keys, double* norms, int64_t n_slabs);
+/* init_cnn (encoder.cpp:441-470): conv1 [32][2][5][5], conv2 [64][32][3][3], fc [key_dim][64]. */
+int mlrg_cnn_weights(int key_dim, uint64_t seed, float* c1w, float* c2w, float* fcw);
+
 /* ---- device reconstruction (admm.cpp:208-272) ----
  * config_text: the reference's key=value config text. dev d (n_theta, h, w)
  * space-domain data, optional dev reference (n1, n0, n2), dev u_out. */

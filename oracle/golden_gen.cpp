@@ -139,7 +139,8 @@ int cmd_ops(const std::string& dir, std::int64_t n1, std::int64_t n0, std::int64
 }
 
 int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_outer,
-              const std::string& memo, const std::string& path, int workers) {
+              const std::string& memo, const std::string& path, int workers,
+              const std::string& variant = "projection") {
   mlr::RunConfig rc;
   rc.set("n1", std::to_string(n));
   rc.set("n0", std::to_string(n));
@@ -151,6 +152,7 @@ int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_out
   rc.set("memoization", memo);
   rc.set("nudft_path", path);
   rc.set("workers", std::to_string(workers));
+  rc.set("encoder_variant", variant);
   rc.validate();
   const mlr::Geometry geom = rc.make_geometry();
   const mlr::Volume phantom =
@@ -317,6 +319,41 @@ int cmd_encoder(const std::string& dir) {
   return 0;
 }
 
+// CNN encoder (encoder.cpp:95-197, seeded initial weights init_cnn, 441-470):
+// the weights, and raw and slot-mixed keys of random chunks of three shapes.
+int cmd_cnn(const std::string& dir) {
+  mlr::EncoderConfig ec;
+  ec.variant = mlr::EncoderConfig::Variant::cnn;
+  mlr::Encoder enc(ec);
+  const mlr::CnnWeights& w = enc.cnn_weights();
+  save_npy(dir + "/c1w.npy", w.c1.w.data(), {static_cast<std::size_t>(w.c1.out_ch), 2, 5, 5});
+  save_npy(dir + "/c2w.npy", w.c2.w.data(), {static_cast<std::size_t>(w.c2.out_ch), static_cast<std::size_t>(w.c2.in_ch), 3, 3});
+  save_npy(dir + "/fcw.npy", w.fc_w.data(), {60, static_cast<std::size_t>(w.c2.out_ch)});
+  std::mt19937_64 rng(77);
+  const mlr::Shape3 shapes[] = {{16, 16, 16}, {4, 16, 16}, {16, 8, 12}};
+  int idx = 0;
+  for (const mlr::Shape3& s : shapes) {
+    const std::string tag = std::to_string(idx++);
+    std::vector<float> keys, raw;
+    std::vector<std::int32_t> meta;
+    for (int op = 0; op < 4; ++op) {
+      const std::int64_t loc = op;
+      const mlr::Array3 x = random_array(s, mlr::Domain::space, rng);
+      const mlr::MemoKey k = enc.encode(x, loc, static_cast<mlr::OpId>(op));
+      const mlr::MemoKey r = enc.encode_content_only(x, loc, static_cast<mlr::OpId>(op));
+      keys.insert(keys.end(), k.values.begin(), k.values.end());
+      raw.insert(raw.end(), r.values.begin(), r.values.end());
+      meta.push_back(op);
+      meta.push_back(static_cast<std::int32_t>(loc));
+      save_arr(dir + "/x" + tag + "_op" + std::to_string(op) + ".npy", x);
+    }
+    save_npy(dir + "/keys" + tag + ".npy", keys.data(), {4, 60});
+    save_npy(dir + "/raw" + tag + ".npy", raw.data(), {4, 60});
+    save_npy(dir + "/meta" + tag + ".npy", meta.data(), {4, 2});
+  }
+  return 0;
+}
+
 int cmd_store(const std::string& dir) {
   // Small IVF so the clustered regime is exercised with few keys.
   mlr::IvfConfig ic;
@@ -381,8 +418,9 @@ int main(int argc, char** argv) {
     if (cmd == "ops" && argc == 10) return cmd_ops(dir, I(3), I(4), I(5), I(6), I(7), I(8), I(9));
     if (cmd == "recon" && argc >= 8)
       return cmd_recon(dir, I(3), I(4), static_cast<int>(I(5)), argv[6], argv[7],
-                       argc > 8 ? static_cast<int>(I(8)) : 1);
+                       argc > 8 ? static_cast<int>(I(8)) : 1, argc > 9 ? argv[9] : "projection");
     if (cmd == "encoder") return cmd_encoder(dir);
+    if (cmd == "cnn") return cmd_cnn(dir);
     if (cmd == "trace" && argc == 5) return cmd_trace(I(3), static_cast<int>(I(4)));
     if (cmd == "sens" && argc == 7) return cmd_sens(I(3), static_cast<int>(I(4)), std::stod(argv[5]), argv[6]);
     if (cmd == "store") return cmd_store(dir);

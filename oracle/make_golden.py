@@ -27,12 +27,16 @@ CASES = {
     "ops_ragged": ["ops", "20", "24", "18", "10", "12", "14", "12"],
     "ops_c32": ["ops", "32", "32", "32", "24", "32", "32", "13"],
     "encoder": ["encoder"],
+    "cnn": ["cnn"],
     "store": ["store"],
     # reconstructions (phantom "blocks" seed 1, d = forward_L(phantom))
     "recon_c16_memo_grid": ["recon", "16", "16", "10", "local", "gridding"],
     "recon_c32_memo_grid": ["recon", "32", "32", "10", "local", "gridding"],
     "recon_c32_off_grid": ["recon", "32", "32", "10", "off", "gridding"],
     "recon_c64_off_grid": ["recon", "64", "64", "10", "off", "gridding", "8"],
+    # the CNN key encoder (encoder_variant = cnn, seeded initial weights)
+    "recon_c16_cnn_memo_grid": ["recon", "16", "16", "10", "local", "gridding", "1", "cnn"],
+    "recon_c32_cnn_memo_grid": ["recon", "32", "32", "10", "local", "gridding", "8", "cnn"],
     # BASELINE configs[0] exactly as-is: 64^3, 64 angles, 10 iterations, memo on,
     # default (direct) NUDFT path, 1 worker. ~5 minutes of CPU.
     "recon_cfg1_memo_direct": ["recon", "64", "64", "10", "local", "direct", "1"],

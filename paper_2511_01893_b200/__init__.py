@@ -83,6 +83,8 @@ _SIGS = {
     "mlrg_grad": (C.c_int, [_P, _P, _P, _P, _P]),
     "mlrg_div": (C.c_int, [_P, _P, _P, _P, _P]),
     "mlrg_encode": (C.c_int, [_P, C.c_int, _P, _I64, C.c_int, _U64, _P, _P, _I64]),
+    "mlrg_encode_cnn": (C.c_int, [_P, C.c_int, _P, _I64, C.c_int, _U64, _P, _P, _I64]),
+    "mlrg_cnn_weights": (C.c_int, [C.c_int, _U64, _P, _P, _P]),
     "mlrg_reconstruct": (_P, [C.c_char_p, _P, _P, _P, _P]),
     "mlrg_recon_csv": (_P, [_P]),
     "mlrg_recon_aborted": (C.c_int, [_P]),
@@ -371,6 +373,16 @@ class Context:
                                   keys.ctypes.data, norms.ctypes.data, ns))
         return keys, norms
 
+    def encode_cnn(self, op: str, x, chunk_extent=16, key_dim=60, seed=1337):
+        """Raw CNN keys (before slot_mix) and input norms per slab."""
+        ax = 1 if op in ("fu2d", "fu2d_adj") else 0
+        ns = -(-x.shape[ax] // chunk_extent)
+        keys = np.zeros((ns, key_dim), np.float32)
+        norms = np.zeros(ns, np.float64)
+        _gcheck(lib().mlrg_encode_cnn(self._h, OPS[op], _dp(x), chunk_extent, key_dim, seed,
+                                      keys.ctypes.data, norms.ctypes.data, ns))
+        return keys, norms
+
     def sync(self):
         _gcheck(lib().mlrg_sync(self._h))
 
@@ -580,6 +592,15 @@ def prof_query(name: str):
     ms, n = C.c_double(0), C.c_int64(0)
     _gcheck(lib().mlrg_prof_query(name.encode(), C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def cnn_weights(key_dim=60, seed=1337):
+    """init_cnn weights (conv1, conv2, fc) of the CNN key encoder."""
+    c1 = np.zeros((32, 2, 5, 5), np.float32)
+    c2 = np.zeros((64, 32, 3, 3), np.float32)
+    fc = np.zeros((key_dim, 64), np.float32)
+    _gcheck(lib().mlrg_cnn_weights(key_dim, seed, c1.ctypes.data, c2.ctypes.data, fc.ctypes.data))
+    return c1, c2, fc
 
 
 def projection_matrix(shape, key_dim=60, seed=1337, count=None) -> np.ndarray:

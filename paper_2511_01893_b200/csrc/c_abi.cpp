@@ -20,6 +20,7 @@
 #include "encoder.hpp"
 #include "engine_api.hpp"
 #include "host_io.hpp"
+#include "cnn.hpp"
 #include "kernels.hpp"
 #include "memo.hpp"
 #include "mlr.h"
@@ -120,8 +121,7 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   mlrg::EngineConfig ec = rc.engine;
   ec.memo_enabled = rc.admm.memoization != mlrg::MemoMode::off;
   if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s, nullptr, nullptr, std::move(comm));
-  if (rc.encoder.variant != mlrg::EncoderConfig::Variant::projection)
-    throw std::invalid_argument("encoder_variant=cnn is not provided by the B200 build (projection only)");
+
   auto store = std::make_shared<mlrg::MemoStore>();
   // HBM for the values the solve can insert: n_outer x the per-iteration insert
   // cap x the largest slab value (complex64), at most 45% of free HBM
@@ -155,7 +155,14 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   if ((comm && comm->world() > 1) || ec.device_memo) ec.memo_arena_bytes = bytes;
   else store->arena().reserve(bytes);
   auto client = std::make_shared<mlrg::MemoClient>(rc.memo, store);
-  auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
+  std::shared_ptr<mlrg::Encoder> enc;
+  if (rc.encoder.variant == mlrg::EncoderConfig::Variant::cnn)  // capi.cpp:56-65: file, else seeded init
+    enc = std::make_shared<mlrg::Encoder>(
+        rc.encoder_weights.empty() ? mlrg::CnnWeights::init(rc.encoder.key_dim, rc.encoder.seed)
+                                   : mlrg::CnnWeights::load(rc.encoder_weights, rc.encoder.key_dim, rc.encoder.seed),
+        rc.encoder.seed, s);
+  else
+    enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
   return std::make_unique<mlrg::Engine>(g, ec, s, enc, client, std::move(comm));
 }
 
@@ -650,6 +657,51 @@ int mlrg_div(mlrg_ctx* ctx, const void* g0, const void* g1, const void* g2, void
     f.c[1] = static_cast<const float2*>(g1);
     f.c[2] = static_cast<const float2*>(g2);
     mlrg::ops::div(f, static_cast<float2*>(out), {ctx->g.n1, ctx->g.n0, ctx->g.n2}, ctx->s);
+  });
+}
+
+int mlrg_cnn_weights(int key_dim, uint64_t seed, float* c1w, float* c2w, float* fcw) {
+  return guarded([&] {
+    need(c1w && c2w && fcw && key_dim >= 2, "mlrg_cnn_weights: bad argument");
+    const mlrg::CnnWeights w = mlrg::CnnWeights::init(key_dim, seed);
+    std::memcpy(c1w, w.c1w.data(), w.c1w.size() * sizeof(float));
+    std::memcpy(c2w, w.c2w.data(), w.c2w.size() * sizeof(float));
+    std::memcpy(fcw, w.fcw.data(), w.fcw.size() * sizeof(float));
+  });
+}
+
+int mlrg_encode_cnn(mlrg_ctx* ctx, int op, const void* x, int64_t chunk_extent, int key_dim, uint64_t seed,
+                    float* keys, double* norms, int64_t n_slabs) {
+  return guarded([&] {
+    need(ctx && x && keys && norms && op >= 0 && op <= 5 && chunk_extent >= 1, "mlrg_encode_cnn: bad argument");
+    const mlrg::OpId oid = static_cast<mlrg::OpId>(op);
+    const mlrg::Geometry& g = ctx->g;
+    const mlrg::Shape3 in = oid == mlrg::OpId::fu1d ? g.volume_shape()
+                            : (oid == mlrg::OpId::fu1d_adj || oid == mlrg::OpId::fu2d) ? g.mid_shape()
+                                                                                         : g.projection_shape();
+    const int axis = mlrg::chunk_axis_of(oid);
+    const int64_t len = in.extent(axis);
+    const int64_t ns = (len + chunk_extent - 1) / chunk_extent;
+    need(n_slabs == ns, "mlrg_encode_cnn: n_slabs does not match the slab count");
+    mlrg::Encoder enc(mlrg::CnnWeights::init(key_dim, seed), seed, ctx->s);
+    mlrg::ops::CnnWork work;
+    mlrg::DeviceBuffer<float> dkeys(static_cast<std::size_t>(ns * key_dim));
+    mlrg::DeviceBuffer<double> dnorm(static_cast<std::size_t>(ns));
+    for (int64_t c0 = 0; c0 < ns;) {
+      const int64_t e = std::min(chunk_extent, len - c0 * chunk_extent);
+      int64_t c1 = c0;
+      while (c1 < ns && std::min(chunk_extent, len - c1 * chunk_extent) == e) ++c1;
+      std::vector<int64_t> starts;
+      for (int64_t c = c0; c < c1; ++c) starts.push_back(c * chunk_extent);
+      mlrg::ops::encode_cnn(static_cast<const float2*>(x), {in.d0, in.d1, in.d2, axis, 0, e}, starts.data(),
+                            static_cast<int>(c1 - c0), enc.cnn_device(), dkeys.get() + c0 * key_dim, dnorm.get() + c0,
+                            work, ctx->s);
+      c0 = c1;
+    }
+    MLRG_CUDA(cudaStreamSynchronize(ctx->s));
+    MLRG_CUDA(cudaMemcpy(keys, dkeys.get(), sizeof(float) * ns * key_dim, cudaMemcpyDeviceToHost));
+    MLRG_CUDA(cudaMemcpy(norms, dnorm.get(), sizeof(double) * ns, cudaMemcpyDeviceToHost));
+    for (int64_t c = 0; c < ns; ++c) norms[c] = std::sqrt(norms[c]);  // keys stay raw (before slot_mix)
   });
 }
 

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "device.hpp"
@@ -31,11 +32,33 @@ std::vector<float> projection_matrix(Shape3 shape, int key_dim, std::uint64_t se
 /// encoder.cpp:66-86: signed permutation seeded by (location, op).
 void slot_mix(float* key, int key_dim, std::uint64_t seed, std::int64_t location, OpId op);
 
+/// CNN key encoder weights (encoder.hpp:60-90): conv1 2 -> 32 ch 5x5 stride 2,
+/// conv2 32 -> 64 ch 3x3 stride 2, global average pool, FC 64 -> key_dim.
+struct CnnWeights {
+  int c1_out = 32, c1_k = 5, c2_out = 64, c2_k = 3, key_dim = 60;
+  std::vector<float> c1w, c1b, c2w, c2b, fcw, fcb;
+  /// init_cnn (encoder.cpp:441-470): He-scaled draws from one GaussianStream
+  /// seeded splitmix64(seed ^ 0xC4E1A5), biases zero.
+  static CnnWeights init(int key_dim, std::uint64_t seed);
+  /// Encoder::load_weights (encoder.cpp:636-680): "LENC" v1 file of a cnn encoder.
+  static CnnWeights load(const std::string& path, int key_dim, std::uint64_t seed);
+};
+
+/// Device copies of the CNN weights (kernels in cnn.cu).
+struct CnnDevice {
+  CnnWeights host;
+  DeviceBuffer<float> c1w, c1b, c2w, c2b, fcw, fcb;
+};
+
 class Encoder {
  public:
   Encoder(int key_dim, std::uint64_t seed) : key_dim_(key_dim), seed_(seed) {}
+  /// CNN variant (encoder_variant = cnn).
+  Encoder(const CnnWeights& w, std::uint64_t seed, cudaStream_t s);
   int key_dim() const { return key_dim_; }
   std::uint64_t seed() const { return seed_; }
+  bool cnn() const { return cnn_ != nullptr; }
+  const CnnDevice& cnn_device() const { return *cnn_; }
 
   /// register_shape (encoder.cpp:369-379): builds and uploads once per shape.
   void register_shape(Shape3 shape, cudaStream_t s);
@@ -45,6 +68,7 @@ class Encoder {
  private:
   int key_dim_;
   std::uint64_t seed_;
+  std::shared_ptr<CnnDevice> cnn_;
   std::map<std::array<std::int64_t, 3>, DeviceBuffer<float>> mats_;
 };
 

@@ -17,6 +17,7 @@
 #include "encoder.hpp"
 #include "geometry.hpp"
 #include "memo.hpp"
+#include "cnn.hpp"
 #include "memo_gpu.hpp"
 #include "shard.hpp"
 #include "usfft.hpp"
@@ -134,6 +135,7 @@ class Engine {
   std::size_t arena_cap_ = 0;
   std::vector<std::size_t> arena_next_;
   std::unique_ptr<DeviceMemo> dmemo_;
+  ops::CnnWork cnn_work_;  // encoder_variant = cnn scratch
 };
 
 }  // namespace mlrg

@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "cnn.hpp"
 #include "kernels.hpp"
 
 namespace mlrg {
@@ -356,6 +357,22 @@ void Engine::encode_slabs(OpId /*op*/, const void* in, bool in_d, int axis, cons
   const int kd = enc_->key_dim();
   enc_keys_.resize(static_cast<std::size_t>(n * kd));
   enc_norms_.resize(static_cast<std::size_t>(n));
+  if (enc_->cnn()) {  // encoder_variant = cnn (cnn.cu), per run of equal slab extents
+    for (int c0 = 0; c0 < n;) {
+      int c1 = c0;
+      while (c1 < n && ext[static_cast<std::size_t>(c1)] == ext[static_cast<std::size_t>(c0)]) ++c1;
+      const ops::SlabGeom sg{ishape.d0, ishape.d1, ishape.d2, axis, 0, ext[static_cast<std::size_t>(c0)]};
+      float* kdst = enc_keys_.get() + static_cast<std::size_t>(c0) * kd;
+      if (in_d)
+        ops::encode_cnn(static_cast<const double2*>(in), sg, starts.data() + c0, c1 - c0, enc_->cnn_device(), kdst,
+                        enc_norms_.get() + c0, cnn_work_, s_);
+      else
+        ops::encode_cnn(static_cast<const float2*>(in), sg, starts.data() + c0, c1 - c0, enc_->cnn_device(), kdst,
+                        enc_norms_.get() + c0, cnn_work_, s_);
+      c0 = c1;
+    }
+    return;
+  }
   for (int c0 = 0; c0 < n;) {  // one GEMM per distinct slab shape
     int c1 = c0;
     while (c1 < n && ext[static_cast<std::size_t>(c1)] == ext[static_cast<std::size_t>(c0)]) ++c1;

@@ -127,3 +127,20 @@ def test_encode_keys_match_reference(mlrg, torch_cuda):
             want = O.slot_mix(O.encode_projection(chunk, P), 1337, s, mlrg.OPS[op])
             assert np.allclose(keys[s], want, rtol=1e-5, atol=1e-5 * np.abs(want).max())
             assert abs(norms[s] - np.linalg.norm(chunk)) < 1e-6 * norms[s]
+
+
+@pytest.mark.parametrize("idx,shape", [(0, (16, 16, 16)), (1, (4, 16, 16)), (2, (16, 8, 12))])
+def test_cnn_encoder_matches_reference_keys(mlrg, torch_cuda, idx, shape):
+    """Device CNN keys (cnn.cu) against the reference's (encoder.cpp:95-197) for
+    random chunks: the chunk is the whole projection-shaped input of fu2d_adj
+    (n_theta, h, w) = shape, one slab of extent h."""
+    torch = torch_cuda
+    z = golden("cnn")
+    d0, d1, d2 = shape
+    ctx = mlrg.Context(16, 16, 16, d0, d1, d2)
+    for op in range(4):
+        x = torch.from_numpy(z[f"x{idx}_op{op}"].astype(np.complex64)).cuda()
+        keys, norms = ctx.encode_cnn("fu2d_adj", x, chunk_extent=d1)
+        want = z[f"raw{idx}"][op]
+        assert np.allclose(keys[0], want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
+        assert abs(norms[0] - np.linalg.norm(z[f"x{idx}_op{op}"])) <= 1e-6 * norms[0]

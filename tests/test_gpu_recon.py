@@ -15,9 +15,9 @@ def ref_rows(z):
     return [[float(v) for v in l.split(",")] for l in lines[1:]]
 
 
-def config_text(n, nt, n_outer, memo, kernel="es"):
+def config_text(n, nt, n_outer, memo, kernel="es", encoder="projection"):
     return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
-            f"memoization={memo}\nnudft_path=gridding\ngridding_kernel={kernel}\n")
+            f"memoization={memo}\nnudft_path=gridding\ngridding_kernel={kernel}\nencoder_variant={encoder}\n")
 
 
 @pytest.mark.parametrize("case,memo,kernel", [("recon_c16_memo_grid", "local", "es"),
@@ -135,3 +135,24 @@ def test_device_memo_matches_host_client_and_reference_counters(mlrg, torch_cuda
               "batches_sent", "inserts_enqueued", "inserts_sent", "inserts_dropped"):
         assert k1[k] == int(want[k]), k
         assert k0[k] == k1[k], k
+
+
+@pytest.mark.parametrize("case", ["recon_c16_cnn_memo_grid", "recon_c32_cnn_memo_grid"])
+def test_cnn_encoder_reconstruction_matches_reference(mlrg, torch_cuda, case):
+    """encoder_variant = cnn (seeded init_cnn weights, encoder.cpp:95-197): the
+    untrained CNN maps the iterates to nearly identical keys, so the reference
+    reuses almost every value and its solve drifts away (E grows); the device run
+    must make the same decisions and follow the same trajectory."""
+    torch = torch_cuda
+    z = golden(case)
+    n = z["phantom"].shape[0]
+    nt = z["data"].shape[0]
+    d = torch.from_numpy(z["data"]).cuda()
+    ref = torch.from_numpy(z["phantom"]).cuda()
+    u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+    r = mlrg.reconstruct_device(config_text(n, nt, 10, "local", encoder="cnn"), d, u, reference=ref)
+    meta, cs = r.audit()
+    assert np.array_equal(meta, z["audit_int"]), "memo hit/miss sequence differs from the reference"
+    assert np.allclose(cs, z["audit_cs"], atol=1e-5)
+    assert r.aborted == bool(int(str(z["txt_aborted_txt"]).split()[0]))
+    assert rel(u.cpu().numpy(), z["u"]) <= 1e-4

@@ -155,3 +155,10 @@ def test_memo_decisions_replay_reference(mlrg, case):
     for k in ("lookups", "cache_hits", "remote_hits", "misses", "cache_comparisons", "cache_probes",
               "batches_sent", "inserts_enqueued", "inserts_sent", "inserts_dropped"):
         assert ctr[k] == int(want[k]), k
+
+
+def test_cnn_init_weights_match_reference(mlrg):
+    """init_cnn (encoder.cpp:441-470): one GaussianStream over conv1, conv2, fc."""
+    z = golden("cnn")
+    c1, c2, fc = mlrg.cnn_weights()
+    assert np.array_equal(c1, z["c1w"]) and np.array_equal(c2, z["c2w"]) and np.array_equal(fc, z["fcw"])

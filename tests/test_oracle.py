@@ -95,3 +95,16 @@ def test_recon_memo_c16_matches_reference():
         assert abs(row["loss"] - f[1]) <= 1e-9 * abs(f[1])
         assert (row["miss"], row["remote_hit"], row["cache_hit"]) == (f[4], f[5], f[6])
     assert rel(r["u"], z["u"]) < 1e-6
+
+
+def test_cnn_restatement_matches_reference_keys():
+    """The CNN key encoder (encoder.cpp:95-197, seeded init_cnn weights) restated
+    in numpy against the reference's keys of random chunks (summation order
+    differs: float-rounding level agreement)."""
+    z = golden("cnn")
+    c1w, c2w, fcw = z["c1w"], z["c2w"], z["fcw"]
+    for idx in range(3):
+        raw = z[f"raw{idx}"]
+        for op in range(4):
+            k = O.cnn_forward(z[f"x{idx}_op{op}"], c1w, c2w, fcw)
+            assert np.allclose(k, raw[op], rtol=1e-5, atol=1e-6 * np.abs(raw[op]).max())
