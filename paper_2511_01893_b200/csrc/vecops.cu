@@ -335,34 +335,44 @@ __global__ void k_c64_to_c128(const float2* __restrict__ in, double2* __restrict
 }  // namespace
 
 void g_init(CDField3 psi, CDField3 lam, DField3 g, std::int64_t n, double lc, cudaStream_t s) {
+  prof::begin("k_g_init", s);
   k_g_init<<<grid_blocks(), kThreads, 0, s>>>(psi, lam, g, n, lc);
   MLRG_LAUNCH_CHECK("k_g_init");
+  prof::end("k_g_init", s);
 }
 
 int grad_update(const double2* u, CDField3 g, double2* G, const double2* p_prev, const double2* G_prev, Dims d,
                 double rho, double* partials, cudaStream_t s, const Halo& halo) {
+  prof::begin("k_grad_update", s);
   k_grad_update<<<grid_blocks(), kThreads, 0, s>>>(u, g, G, p_prev, G_prev, dev_dims(d), rho, partials, halo);
   MLRG_LAUNCH_CHECK("k_grad_update");
+  prof::end("k_grad_update", s);
   return 3 * grid_blocks();
 }
 
 int direction(const double2* G, const double2* p_prev, double beta, const double2* u, CDField3 g, double2* p,
               Dims d, double* partials, cudaStream_t s, const Halo& halo) {
+  prof::begin("k_direction", s);
   k_direction<<<grid_blocks(), kThreads, 0, s>>>(G, p_prev, beta, u, g, p, dev_dims(d), partials, halo);
   MLRG_LAUNCH_CHECK("k_direction");
+  prof::end("k_direction", s);
   return 2 * grid_blocks();
 }
 
 void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s) {
+  prof::begin("k_axpy", s);
   k_axpy<<<grid_blocks(), kThreads, 0, s>>>(y, x, a, n);
   MLRG_LAUNCH_CHECK("k_axpy");
+  prof::end("k_axpy", s);
 }
 
 int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
                    double rho_over_scale, double* partials, cudaStream_t s, const Halo& halo) {
+  prof::begin("k_rsp_multiplier", s);
   k_rsp_multiplier<<<grid_blocks(), kThreads, 0, s>>>(u, lam, psi_old, psi_new, dev_dims(d), lc, thr,
                                                       rho_over_scale, partials, halo);
   MLRG_LAUNCH_CHECK("k_rsp_multiplier");
+  prof::end("k_rsp_multiplier", s);
   return 2 * grid_blocks();
 }
 
