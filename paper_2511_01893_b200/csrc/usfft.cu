@@ -76,6 +76,18 @@ int pass_cols(std::int64_t m) {
   return c;
 }
 
+// Four-step column passes (k_cols4_*) for an M-point column FFT: by default
+// from M = 1024, where the 16-row grid batch (M^2 x 128 B) outgrows L2;
+// MLRG_COLS4=0 disables them, MLRG_COLS4=1 uses them from M = 64 (tests).
+bool use_cols4(std::int64_t m) {
+  static const int mode = [] {
+    const char* e = std::getenv("MLRG_COLS4");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (mode == 0) return false;
+  return m >= (mode == 1 ? 64 : 1024) && m <= 4096 && (m & (m - 1)) == 0;
+}
+
 // ------------------------------------------------------------------------------------------
 // fu1d / fu1d_adj
 // ------------------------------------------------------------------------------------------
@@ -547,6 +559,69 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const floa
   fft_stockham<-1, true, true>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
+// ---- four-step column passes (grids beyond L2) --------------------------------------------
+// From M = 1024 the one-pass column kernels hold only 1-2 of a cell's 16 batch
+// rows per CTA (an M-point double column is M x 16 B of shared memory), so
+// every CTA touches 8-16 B of each 128 B cell; once the grid no longer fits L2
+// those partial-line accesses dominate the iteration. With M = A * B the
+// column FFT is X[ka + A kb] = sum_b W_B^{b kb} W_M^{b ka} sum_a x[a B + b] W_A^{a ka}:
+// pass 1 takes the A-point FFTs over rows b, B + b, ... for one b and writes
+// Y[b A + ka] times the twiddle, pass 2 the B-point FFTs over rows ka, A + ka, ...
+// A CTA of either pass holds kCols4 grid columns x all 16 batch rows, a
+// contiguous 512 B block of every grid row it touches, so all traffic is in
+// whole lines at the cost of one more trip through the grid.
+constexpr int kCols4 = 4;
+constexpr int kCols4Lanes = kCols4 * KB;
+
+// FROM_S: the input rows are the S rows of the n1 wrapped slots (forward);
+// otherwise all M natural rows (adjoint).
+template <int SIGN, bool FROM_S>
+__global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict__ in, int n1, int logm1, int center1,
+                                                        int logA, int logm2, const double2* __restrict__ twA,
+                                                        const double2* __restrict__ twM, float2* __restrict__ Y, Skip sk) {
+  if (skipped(sk, 0)) return;
+  extern __shared__ double2 sd[];
+  const int mask1 = (1 << logm1) - 1, m2 = 1 << logm2, logB = logm1 - logA;
+  const int b = blockIdx.x, c0 = blockIdx.y * kCols4;
+  auto load = [&](int a, int l) {
+    const int r = (a << logB) + b;  // one row per warp: the branch is uniform
+    int i = r;
+    if constexpr (FROM_S) {
+      i = (r + center1) & mask1;
+      if (i >= n1) return make_double2(0.0, 0.0);
+    }
+    return to_d(in[(static_cast<long long>(i) * m2 + c0) * KB + l]);
+  };
+  auto store = [&](int ka, int l, double2 x) {
+    double2 w = twM[b * ka];  // b * ka < M
+    if (SIGN < 0) w.y = -w.y;
+    Y[(static_cast<long long>((b << logA) + ka) * m2 + c0) * KB + l] = to_f(cmul(x, w));
+  };
+  fft_stockham<SIGN, true, true>(sd, logA, kCols4Lanes, kCols4Lanes, twA, load, store);
+}
+
+// TO_S: keep the n1 output slots that map to modes, at their S rows (adjoint);
+// otherwise all M rows in natural order (forward).
+template <int SIGN, bool TO_S>
+__global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict__ Y, int n1, int logm1, int center1,
+                                                        int logA, int logm2, const double2* __restrict__ twB,
+                                                        float2* __restrict__ out, Skip sk) {
+  if (skipped(sk, 0)) return;
+  extern __shared__ double2 sd[];
+  const int mask1 = (1 << logm1) - 1, m2 = 1 << logm2, logB = logm1 - logA;
+  const int ka = blockIdx.x, c0 = blockIdx.y * kCols4;
+  auto load = [&](int bb, int l) { return to_d(Y[(static_cast<long long>((bb << logA) + ka) * m2 + c0) * KB + l]); };
+  auto store = [&](int kb, int l, double2 x) {
+    int r = ka + (kb << logA);
+    if constexpr (TO_S) {
+      r = (r + center1) & mask1;
+      if (r >= n1) return;
+    }
+    out[(static_cast<long long>(r) * m2 + c0) * KB + l] = to_f(x);
+  };
+  fft_stockham<SIGN, true, true>(sd, logB, kCols4Lanes, kCols4Lanes, twB, load, store);
+}
+
 // Row FFT(-1) and the final deconvolution into out[i, k0_out+kk, j].
 template <bool PEER>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
@@ -703,6 +778,10 @@ struct Usfft::Tables {
   // next batch's FFT passes
   DeviceBuffer<float2> S2, Gd2, val2;
   DeviceBuffer<double2> partial2;
+  // four-step column passes: M = A * B, A = 2^logA
+  bool cols4 = false;
+  int logA = 0;
+  DeviceBuffer<double2> a_tw, b_tw;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
@@ -932,6 +1011,12 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   t.x_tw.upload(twiddles(px.m), stream_);
   t.y_tw.upload(twiddles(py.m), stream_);
+  t.cols4 = use_cols4(px.m);
+  if (t.cols4) {
+    t.logA = px.logm / 2;
+    t.a_tw.upload(twiddles(std::int64_t{1} << t.logA), stream_);
+    t.b_tw.upload(twiddles(std::int64_t{1} << (px.logm - t.logA)), stream_);
+  }
   prof::host_mark("host:usfft_patches");
   t.S.resize(static_cast<std::size_t>(px.m * py.m * KB));
   t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB));
@@ -983,6 +1068,10 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     allow_big_smem(k_fu2d_cols<false>);
     allow_big_smem(k_fu2d_cols<true>);
     allow_big_smem(k_fu2d_adj_cols);
+    allow_big_smem(k_cols4_pass1<+1, true>);
+    allow_big_smem(k_cols4_pass1<-1, false>);
+    allow_big_smem(k_cols4_pass2<+1, false>);
+    allow_big_smem(k_cols4_pass2<-1, true>);
     allow_big_smem(k_fu2d_adj_rows<false>);
     allow_big_smem(k_fu2d_adj_rows<true>);
     allow_big_smem(k_center_fft_rows<+1>);
@@ -1092,16 +1181,30 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     MLRG_LAUNCH_CHECK("k_fu2d_rows");
     prof::end("k_fu2d_rows", s);
     prof::begin("k_fu2d_cols", s);
-    (zero_padded(t.px) ? k_fu2d_cols<true> : k_fu2d_cols<false>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
-                  static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
-        S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
-    MLRG_LAUNCH_CHECK("k_fu2d_cols");
+    const float2* G = Gd;
+    if (t.cols4) {  // S -> Gd (intermediate) -> S (the grid, all M1 rows)
+      const int A = 1 << t.logA, B = t.px.m >> t.logA;
+      const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
+      k_cols4_pass1<+1, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
+          t.x_tw.get(), Gd, sk);
+      MLRG_LAUNCH_CHECK("k_cols4_pass1");
+      k_cols4_pass2<+1, false><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+          Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S, sk);
+      MLRG_LAUNCH_CHECK("k_cols4_pass2");
+      G = S;
+    } else {
+      (zero_padded(t.px) ? k_fu2d_cols<true> : k_fu2d_cols<false>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+                    static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
+      MLRG_LAUNCH_CHECK("k_fu2d_cols");
+    }
     prof::end("k_fu2d_cols", s);
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
     prof::begin("k_fu2d_gather", s);
     // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
-    gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(Gd, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
+    gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(G, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
                                                t.t_r0.get(), t.t_c0.get(), t.t_w1.get(), t.t_w2.get(),
                                                t.m_first.get(), t.m_tidx.get(), t.m_fac.get(), eo, per_cta,
                                                partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0,
@@ -1160,10 +1263,24 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     }
     prof::end("k_fu2d_adj_spread", s);
     prof::begin("k_fu2d_adj_cols", s);
-    k_fu2d_adj_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
-                      static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
-        Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S, sk);
-    MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
+    const float2* Sc = S;
+    if (t.cols4) {  // Gd -> S (intermediate) -> Gd (rows of the n1 mode slots)
+      const int A = 1 << t.logA, B = t.px.m >> t.logA;
+      const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
+      k_cols4_pass1<-1, false><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+          Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
+          t.x_tw.get(), S, sk);
+      MLRG_LAUNCH_CHECK("k_cols4_pass1");
+      k_cols4_pass2<-1, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd, sk);
+      MLRG_LAUNCH_CHECK("k_cols4_pass2");
+      Sc = Gd;
+    } else {
+      k_fu2d_adj_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+                        static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+          Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S, sk);
+      MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
+    }
     prof::end("k_fu2d_adj_cols", s);
     prof::begin("k_fu2d_adj_rows", s);
     (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)),
@@ -1171,7 +1288,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
                                                               static_cast<std::size_t>(t.py.m * (ks2 + 1)) *
                                                                   sizeof(double2),
                                                               s>>>(
-        S, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
+        Sc, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_pdeconv.get(),
         t.y_deconv.get(), t.y_tw.get(), out, ld_out, k0_out + b, peer ? *peer : PeerOut{}, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
     prof::end("k_fu2d_adj_rows", s);
