@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
 // fu2d forward: row pass, column pass, gather
 // ------------------------------------------------------------------------------------------
 // S[i][c'][KB]: row FFT of v[i, k0+kk, :] * dx[i] * dy[:] placed at wrapped slots.
-template <bool ZP>
+// TS (with the four-step column passes): S[i][KB][c'] instead, so the stores of
+// a CTA holding 1-2 batch rows of a long row are contiguous.
+template <bool ZP, bool TS>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
@@ -203,8 +205,10 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* 
     const double f = di * dy[ok ? j : 0];
     return ok ? cscale(x, f) : make_double2(0.0, 0.0);
   };
-  float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
-  auto store = [&](int r, int kk, double2 x) { Si[static_cast<long long>(r) * KB + kk] = to_f(x); };
+  float2* Si = S + static_cast<long long>(i) * m2 * KB + (TS ? static_cast<long long>(ks) * m2 : ks);
+  auto store = [&](int r, int kk, double2 x) {
+    Si[TS ? static_cast<long long>(kk) * m2 + r : static_cast<long long>(r) * KB + kk] = to_f(x);
+  };
   fft_stockham<+1, true, true, ZP>(sd, logm2, ks_n, sm, tw2, load, store);
 }
 
@@ -573,9 +577,18 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const floa
 constexpr int kCols4 = 4;
 constexpr int kCols4Lanes = kCols4 * KB;
 
+// The block of a grid row a CTA owns: lane l is (column c0 + l / KB, batch row
+// l % KB), at offset l in the [c][KB] layout; with the transposed S layout
+// ([KB][c], TS) lane l is (c0 + l % kCols4, l / kCols4) instead, so both the
+// S side and the grid side of the pass move whole 32 B sectors.
+__device__ __forceinline__ int cols4_off(int l, bool ts) { return ts ? (l % kCols4) * KB + l / kCols4 : l; }
+__device__ __forceinline__ long long cols4_ts(int row, int c0, int l, int m2) {
+  return (static_cast<long long>(row) * KB + l / kCols4) * m2 + c0 + l % kCols4;
+}
+
 // FROM_S: the input rows are the S rows of the n1 wrapped slots (forward);
-// otherwise all M natural rows (adjoint).
-template <int SIGN, bool FROM_S>
+// otherwise all M natural rows (adjoint). TS: S in the transposed layout.
+template <int SIGN, bool FROM_S, bool TS>
 __global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict__ in, int n1, int logm1, int center1,
                                                         int logA, int logm2, const double2* __restrict__ twA,
                                                         const double2* __restrict__ twM, float2* __restrict__ Y, Skip sk) {
@@ -589,20 +602,21 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict
     if constexpr (FROM_S) {
       i = (r + center1) & mask1;
       if (i >= n1) return make_double2(0.0, 0.0);
+      if constexpr (TS) return to_d(in[cols4_ts(i, c0, l, m2)]);
     }
     return to_d(in[(static_cast<long long>(i) * m2 + c0) * KB + l]);
   };
   auto store = [&](int ka, int l, double2 x) {
     double2 w = twM[b * ka];  // b * ka < M
     if (SIGN < 0) w.y = -w.y;
-    Y[(static_cast<long long>((b << logA) + ka) * m2 + c0) * KB + l] = to_f(cmul(x, w));
+    Y[(static_cast<long long>((b << logA) + ka) * m2 + c0) * KB + cols4_off(l, FROM_S && TS)] = to_f(cmul(x, w));
   };
   fft_stockham<SIGN, true, true>(sd, logA, kCols4Lanes, kCols4Lanes, twA, load, store);
 }
 
 // TO_S: keep the n1 output slots that map to modes, at their S rows (adjoint);
-// otherwise all M rows in natural order (forward).
-template <int SIGN, bool TO_S>
+// otherwise all M rows in natural order (forward). TS: S in the transposed layout.
+template <int SIGN, bool TO_S, bool TS>
 __global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict__ Y, int n1, int logm1, int center1,
                                                         int logA, int logm2, const double2* __restrict__ twB,
                                                         float2* __restrict__ out, Skip sk) {
@@ -610,20 +624,23 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict
   extern __shared__ double2 sd[];
   const int mask1 = (1 << logm1) - 1, m2 = 1 << logm2, logB = logm1 - logA;
   const int ka = blockIdx.x, c0 = blockIdx.y * kCols4;
-  auto load = [&](int bb, int l) { return to_d(Y[(static_cast<long long>((bb << logA) + ka) * m2 + c0) * KB + l]); };
+  constexpr bool T = TO_S && TS;
+  auto load = [&](int bb, int l) {
+    return to_d(Y[(static_cast<long long>((bb << logA) + ka) * m2 + c0) * KB + cols4_off(l, T)]);
+  };
   auto store = [&](int kb, int l, double2 x) {
     int r = ka + (kb << logA);
     if constexpr (TO_S) {
       r = (r + center1) & mask1;
       if (r >= n1) return;
     }
-    out[(static_cast<long long>(r) * m2 + c0) * KB + l] = to_f(x);
+    out[T ? cols4_ts(r, c0, l, m2) : (static_cast<long long>(r) * m2 + c0) * KB + l] = to_f(x);
   };
   fft_stockham<SIGN, true, true>(sd, logB, kCols4Lanes, kCols4Lanes, twB, load, store);
 }
 
 // Row FFT(-1) and the final deconvolution into out[i, k0_out+kk, j].
-template <bool PEER>
+template <bool PEER, bool TS>
 __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
@@ -633,7 +650,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const floa
   extern __shared__ double2 sd[];
   const int m2 = 1 << logm2, mask2 = m2 - 1, sm = ks_n + 1;
   const int i = blockIdx.y, ks = blockIdx.x * ks_n;  // ks groups of one line adjacent in launch order
-  const float2* Si = S + static_cast<long long>(i) * m2 * KB + ks;
+  const float2* Si = S + static_cast<long long>(i) * m2 * KB + (TS ? static_cast<long long>(ks) * m2 : ks);
   const double pi = pdx[i];
   // plane i of the output: local, or (fused all-to-all) in the HBM of the rank owning plane i
   float2* oplane = out + static_cast<long long>(i) * ld_out * n2;
@@ -643,7 +660,9 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const floa
     oplane = po.dst[r] + (i - po.lo[r]) * po.h * n2;
     k0_out += po.off;
   }
-  auto load = [&](int c, int kk) { return to_d(Si[static_cast<long long>(c) * KB + kk]); };
+  auto load = [&](int c, int kk) {
+    return to_d(Si[TS ? static_cast<long long>(kk) * m2 + c : static_cast<long long>(c) * KB + kk]);
+  };
   auto store = [&](int slot, int kk, double2 x) {
     const int j = (slot + center2) & mask2;
     if (j < n2 && ks + kk < nk) oplane[(k0_out + ks + kk) * n2 + j] = to_f(cscale(x, pi * dy[j]));
@@ -1061,19 +1080,23 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     allow_big_smem(k_fu1d<double2, kTaps, true, true>);
     allow_big_smem(k_fu1d_adj<float2>);
     allow_big_smem(k_fu1d_adj<double2>);
-    allow_big_smem(k_fu2d_rows<false>);
-    allow_big_smem(k_fu2d_rows<true>);
+    allow_big_smem(k_fu2d_rows<false, false>);
+    allow_big_smem(k_fu2d_rows<true, false>);
+    allow_big_smem(k_fu2d_rows<false, true>);
+    allow_big_smem(k_fu2d_rows<true, true>);
     allow_big_smem(k_fu2d_adj_spread<kEsTaps>);
     allow_big_smem(k_fu2d_adj_spread<kTaps>);
     allow_big_smem(k_fu2d_cols<false>);
     allow_big_smem(k_fu2d_cols<true>);
     allow_big_smem(k_fu2d_adj_cols);
-    allow_big_smem(k_cols4_pass1<+1, true>);
-    allow_big_smem(k_cols4_pass1<-1, false>);
-    allow_big_smem(k_cols4_pass2<+1, false>);
-    allow_big_smem(k_cols4_pass2<-1, true>);
-    allow_big_smem(k_fu2d_adj_rows<false>);
-    allow_big_smem(k_fu2d_adj_rows<true>);
+    allow_big_smem(k_cols4_pass1<+1, true, true>);
+    allow_big_smem(k_cols4_pass1<-1, false, true>);
+    allow_big_smem(k_cols4_pass2<+1, false, true>);
+    allow_big_smem(k_cols4_pass2<-1, true, true>);
+    allow_big_smem(k_fu2d_adj_rows<false, false>);
+    allow_big_smem(k_fu2d_adj_rows<true, false>);
+    allow_big_smem(k_fu2d_adj_rows<false, true>);
+    allow_big_smem(k_fu2d_adj_rows<true, true>);
     allow_big_smem(k_center_fft_rows<+1>);
     allow_big_smem(k_center_fft_rows<-1>);
     allow_big_smem(k_center_fft_cols<+1>);
@@ -1174,7 +1197,9 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_rows", s);
-    (zero_padded(t.py) ? k_fu2d_rows<true> : k_fu2d_rows<false>)<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)), static_cast<unsigned>(ks2 * t.py.m / 8),
+    auto rows = zero_padded(t.py) ? (t.cols4 ? k_fu2d_rows<true, true> : k_fu2d_rows<true, false>)
+                                  : (t.cols4 ? k_fu2d_rows<false, true> : k_fu2d_rows<false, false>);
+    rows<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)), static_cast<unsigned>(ks2 * t.py.m / 8),
                   static_cast<std::size_t>(t.py.m * (ks2 + 1)) * sizeof(double2), s>>>(
         v, ld, k0 + b, nb, static_cast<int>(g_.n2), t.py.logm, static_cast<int>(t.py.center), ks2, t.x_deconv.get(),
         t.y_deconv.get(), t.y_tw.get(), S, sk);
@@ -1185,11 +1210,11 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     if (t.cols4) {  // S -> Gd (intermediate) -> S (the grid, all M1 rows)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<+1, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<+1, true, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
-      k_cols4_pass2<+1, false><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass2<+1, false, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       G = S;
@@ -1267,11 +1292,11 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     if (t.cols4) {  // Gd -> S (intermediate) -> Gd (rows of the n1 mode slots)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<-1, false><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<-1, false, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
-      k_cols4_pass2<-1, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass2<-1, true, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       Sc = Gd;
@@ -1283,7 +1308,9 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     }
     prof::end("k_fu2d_adj_cols", s);
     prof::begin("k_fu2d_adj_rows", s);
-    (peer ? k_fu2d_adj_rows<true> : k_fu2d_adj_rows<false>)<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)),
+    auto arows = peer ? (t.cols4 ? k_fu2d_adj_rows<true, true> : k_fu2d_adj_rows<true, false>)
+                      : (t.cols4 ? k_fu2d_adj_rows<false, true> : k_fu2d_adj_rows<false, false>);
+    arows<<<dim3(KB / ks2, static_cast<unsigned>(g_.n1)),
                                                               static_cast<unsigned>(ks2 * t.py.m / 8),
                                                               static_cast<std::size_t>(t.py.m * (ks2 + 1)) *
                                                                   sizeof(double2),
