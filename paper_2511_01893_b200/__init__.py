@@ -209,6 +209,19 @@ class Array:
         flat = np.ctypeslib.as_array(ptr, shape=(2 * n,)) if n else np.zeros(0)
         return flat.view(np.complex128).reshape(shape).copy()
 
+    def view(self) -> np.ndarray:
+        """Zero-copy read-only complex128 view of the data (mlr_array_data); the
+        view keeps this Array (and a result's owner) alive."""
+        shape = self.shape
+        n = int(np.prod(shape))
+        if n == 0:
+            return np.zeros(shape, dtype=np.complex128)
+        buf = (C.c_double * (2 * n)).from_address(C.cast(lib().mlr_array_data(self._h), C.c_void_p).value)
+        buf._owner = self
+        out = np.frombuffer(buf, dtype=np.complex128).reshape(shape)
+        out.flags.writeable = False
+        return out
+
     def save(self, path: str):
         _check(lib().mlr_array_save(self._h, path.encode()))
 

@@ -65,6 +65,17 @@ def test_shepp_phantom_matches_restatement(mlrg):
     assert np.allclose(ph, O.shepp3d((12, 10, 14)), atol=0)
 
 
+def test_array_view_is_zero_copy_and_keeps_owner_alive(mlrg):
+    a = (np.arange(24) + 1j * np.arange(24)[::-1]).reshape(2, 3, 4)
+    arr = mlrg.array_from_numpy(a)
+    v = arr.view()
+    assert np.array_equal(v, a) and not v.flags.writeable
+    del arr  # the view holds the Array
+    import gc
+    gc.collect()
+    assert np.array_equal(v, a)
+
+
 def test_array_io_roundtrip(mlrg, tmp_path):
     a = (np.arange(24) + 1j * np.arange(24)[::-1]).reshape(2, 3, 4)
     arr = mlrg.array_from_numpy(a)
