@@ -330,7 +330,7 @@ def _default_stream(stream):
 
 class Context:
     """mlrg_ctx: device operator tables for one geometry, bound to a CUDA stream.
-    kernel: "es" (12-tap, default) or "gaussian" (the reference's 24-tap plan)."""
+    kernel: "es" (10-tap, default) or "gaussian" (the reference's 24-tap plan)."""
 
     KERNELS = {"es": 0, "gaussian": 1}
 
