@@ -10,9 +10,11 @@ namespace mlrg {
 
 namespace {
 
-constexpr int kLookupThreads = 128;
+constexpr int kLookupThreads = 256;
 constexpr int kMaxKd = 64;
 constexpr int kMaxProbe = 64;
+constexpr int kStageThreads = 1024;  // one thread per slab (max_slabs <= 1024)
+constexpr int kIlp = 4;              // keys per thread in flight in the distance loop
 
 // memostore.cpp:30-38, in the reference's operation order (no contraction).
 __device__ __forceinline__ double l2_sq_d(const float* a, const float* b, int d) {
@@ -66,12 +68,27 @@ struct LookupArgs {
   int* queried;
 };
 
-// One CTA per slab: cache probe, then (on a cache miss) the store query.
+// Candidate j of the store query: flat, key j; trained, entry j of the
+// concatenated lists of the probed clusters (pre = their prefix sizes).
+__device__ __forceinline__ long long candidate(const LookupArgs& a, long long j, int np, const int* probe,
+                                               const int* pre) {
+  if (!a.trained) return j;
+  int p = 0;
+  while (p + 1 < np && j >= pre[p + 1]) ++p;
+  return a.cl_ids[a.cl_ptr[probe[p]] + (j - pre[p])];
+}
+
+// One CTA per slab: cache probe, then (on a cache miss) the store query. The
+// query's distances are independent per candidate key, so the CTA spreads the
+// candidates over its threads, kIlp interleaved per thread; each distance is
+// still the reference's sequential sum, and the (l2, lower id) minimum does not
+// depend on the visiting order.
 __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
   __shared__ float q[kMaxKd];
   __shared__ Best red[kLookupThreads / 32];
   __shared__ double cd[kMaxProbe];
   __shared__ int probe[kMaxProbe];
+  __shared__ int pre[kMaxProbe + 1];
   __shared__ int done;
   const int c = blockIdx.x, t = threadIdx.x, kd = a.kd;
   const long long slot = static_cast<long long>(a.op) * a.max_slabs + c;
@@ -100,38 +117,51 @@ __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
   __syncthreads();
   if (done) return;
   // ---- store query over the published keys (memostore.cpp:174-222) ----
-  const long long npub = a.state[0];
-  Best b{0.0, -1};
-  if (!a.trained) {
-    for (long long id = t; id < npub; id += kLookupThreads) {
-      const Best cand{l2_sq_d(q, a.keys + id * kd, kd), id};
-      if (better(cand, b)) b = cand;
-    }
-  } else {
+  long long total = a.state[0];
+  int np = 0;
+  if (a.trained) {
+    // the nprobe clusters with the smallest (l2, index), ascending: the rank of
+    // centroid t is the number of centroids ordered before it
     if (t < a.ncent) cd[t] = l2_sq_d(q, a.cent + static_cast<long long>(t) * kd, kd);
     __syncthreads();
-    if (t == 0) {  // the nprobe smallest (l2, index) pairs, ascending (std::sort on pairs)
-      const int np = min(a.nprobe, a.ncent);
-      unsigned long long used = 0;
-      for (int p = 0; p < np; ++p) {
-        int arg = -1;
-        for (int k = 0; k < a.ncent; ++k) {
-          if (used >> k & 1ull) continue;
-          if (arg < 0 || cd[k] < cd[arg]) arg = k;
-        }
-        used |= 1ull << arg;
-        probe[p] = arg;
-      }
-      done = np;
+    np = min(a.nprobe, a.ncent);
+    if (t < a.ncent) {
+      int rank = 0;
+      for (int k = 0; k < a.ncent; ++k) rank += (cd[k] < cd[t] || (cd[k] == cd[t] && k < t)) ? 1 : 0;
+      if (rank < np) probe[rank] = t;
     }
     __syncthreads();
-    for (int p = 0; p < done; ++p) {
-      const int cl = probe[p];
-      for (int e = a.cl_ptr[cl] + t; e < a.cl_ptr[cl + 1]; e += kLookupThreads) {
-        const long long id = a.cl_ids[e];
-        const Best cand{l2_sq_d(q, a.keys + id * kd, kd), id};
-        if (better(cand, b)) b = cand;
+    if (t == 0) {
+      pre[0] = 0;
+      for (int p = 0; p < np; ++p) pre[p + 1] = pre[p] + (a.cl_ptr[probe[p] + 1] - a.cl_ptr[probe[p]]);
+    }
+    __syncthreads();
+    total = pre[np];
+  }
+  Best b{0.0, -1};
+  for (long long j0 = t; j0 < total; j0 += static_cast<long long>(kIlp) * kLookupThreads) {
+    const float* row[kIlp];
+    long long id[kIlp];
+    double acc[kIlp];
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const long long j = j0 + static_cast<long long>(k) * kLookupThreads;
+      id[k] = j < total ? candidate(a, j, np, probe, pre) : -1;
+      row[k] = a.keys + (id[k] < 0 ? 0 : id[k]) * kd;
+      acc[k] = 0.0;
+    }
+    for (int i = 0; i < kd; ++i) {
+      const double qi = static_cast<double>(q[i]);
+#pragma unroll
+      for (int k = 0; k < kIlp; ++k) {
+        const double x = __dsub_rn(qi, static_cast<double>(row[k][i]));
+        acc[k] = __dadd_rn(acc[k], __dmul_rn(x, x));
       }
+    }
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const Best cand{acc[k], id[k]};
+      if (better(cand, b)) b = cand;
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -180,62 +210,79 @@ struct StageArgs {
   DevLog* log;
 };
 
-// Single warp, slabs in order: hit sources/scales, insert staging (cap per
-// flush window, arena bump allocation), the decision log.
-__global__ void k_memo_stage(StageArgs a) {
-  const int lane = threadIdx.x;
-  for (int c = 0; c < a.n; ++c) {
-    DevSlab& s = a.slabs[c];
-    const double live = __dsqrt_rn(a.norms2[c]);
-    int staged = -1;
-    long long id = -1;
-    if (s.outcome != 0) {
-      if (lane == 0) {
-        const double stored = a.vnorm[s.vid];
-        s.src = a.vptr[s.vid];
-        s.scale = (stored > 0.0 && live > 0.0) ? __ddiv_rn(live, stored) : 1.0;
-        s.dst = nullptr;
-        a.skip[c] = 1;
-      }
-    } else {
-      const long long nst = a.state[1];
-      staged = nst < a.cap ? 1 : 0;
-      if (staged) {
-        id = a.state[0] + nst;
-        const long long bytes = (a.slab_counts[c] * 8 + 255) & ~255LL;
-        const long long off = a.state[2];
-        const bool fits = off + bytes <= a.arena_bytes;
-        for (int i = lane; i < a.kd; i += 32) a.keys[id * a.kd + i] = a.qkeys[static_cast<long long>(c) * a.kd + i];
-        __syncwarp();
-        if (lane == 0) {
-          float2* dst = fits ? reinterpret_cast<float2*>(a.arena + off) : nullptr;
-          if (!fits) a.state[4] = 1;  // overflow: the host fails the flush
-          a.vbytes[id] = a.slab_vbytes[c];
-          a.vnorm[id] = live;
-          a.vptr[id] = dst;
-          s.dst = dst;
-          a.state[1] = nst + 1;
-          a.state[2] = off + (fits ? bytes : 0);
-        }
-      } else if (lane == 0) {
-        s.dst = nullptr;
-        a.state[5] += 1;
-      }
-      if (lane == 0) {
-        s.src = nullptr;
-        s.scale = 1.0;
-        a.skip[c] = 0;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const long long li = a.state[3];
-      if (li < a.log_cap)
-        a.log[li] = DevLog{a.iteration, a.op, c, s.outcome, s.cs, a.probed[c], a.queried[c], staged};
-      a.state[3] = li + 1;
-    }
-    __syncwarp();
+// One thread per slab: hit sources/scales, insert staging (cap per flush
+// window, arena bump allocation) and the decision log, in slab order. The only
+// sequential part, the running insert count and arena offset over the misses,
+// runs on one thread over shared memory; every global read and write is issued
+// by the slab's own thread.
+__global__ void __launch_bounds__(kStageThreads) k_memo_stage(StageArgs a) {
+  __shared__ long long s_bytes[kStageThreads], s_off[kStageThreads], s_id[kStageThreads];
+  __shared__ int s_miss[kStageThreads], s_staged[kStageThreads];
+  __shared__ long long st[6];
+  const int c = threadIdx.x;
+  const bool mine = c < a.n;
+  if (c < 6) st[c] = a.state[c];
+  DevSlab s{};
+  double live = 0.0;
+  if (mine) {
+    s = a.slabs[c];
+    live = __dsqrt_rn(a.norms2[c]);
+    s_miss[c] = s.outcome == 0;
+    s_bytes[c] = (a.slab_counts[c] * 8 + 255) & ~255LL;
   }
+  __syncthreads();
+  if (c == 0) {  // memoclient.cpp:302-325: stage up to cap per flush window, in slab order
+    long long nst = st[1], off = st[2], dropped = 0;
+    int overflow = 0;
+    for (int k = 0; k < a.n; ++k) {
+      s_staged[k] = -1;
+      if (!s_miss[k]) continue;
+      if (nst < a.cap) {
+        const bool fits = off + s_bytes[k] <= a.arena_bytes;
+        s_staged[k] = 1;
+        s_off[k] = fits ? off : -1;
+        s_id[k] = st[0] + nst;
+        overflow |= fits ? 0 : 1;
+        off += fits ? s_bytes[k] : 0;
+        ++nst;
+      } else {
+        s_staged[k] = 0;
+        ++dropped;
+      }
+    }
+    a.state[1] = nst;
+    a.state[2] = off;
+    a.state[3] = st[3] + a.n;
+    if (overflow) a.state[4] = 1;  // the host fails the flush
+    a.state[5] = st[5] + dropped;
+  }
+  __syncthreads();
+  if (!mine) return;
+  const int staged = s_staged[c];
+  if (s.outcome != 0) {
+    const double stored = a.vnorm[s.vid];
+    s.src = a.vptr[s.vid];
+    s.scale = (stored > 0.0 && live > 0.0) ? __ddiv_rn(live, stored) : 1.0;
+    s.dst = nullptr;
+    a.skip[c] = 1;
+  } else {
+    s.dst = nullptr;
+    if (staged == 1) {
+      const long long id = s_id[c];
+      float2* dst = s_off[c] >= 0 ? reinterpret_cast<float2*>(a.arena + s_off[c]) : nullptr;
+      for (int i = 0; i < a.kd; ++i) a.keys[id * a.kd + i] = a.qkeys[static_cast<long long>(c) * a.kd + i];
+      a.vbytes[id] = a.slab_vbytes[c];
+      a.vnorm[id] = live;
+      a.vptr[id] = dst;
+      s.dst = dst;
+    }
+    s.src = nullptr;
+    s.scale = 1.0;
+    a.skip[c] = 0;
+  }
+  a.slabs[c] = s;
+  const long long li = st[3] + c;
+  if (li < a.log_cap) a.log[li] = DevLog{a.iteration, a.op, c, s.outcome, s.cs, a.probed[c], a.queried[c], staged};
 }
 
 }  // namespace
@@ -249,6 +296,7 @@ DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int 
       arena_bytes_((arena_bytes + 255) & ~std::size_t{255}),
       log_cap_(std::int64_t{1} << 16) {
   if (kd_ < 1 || kd_ > kMaxKd) throw std::invalid_argument("device memo: key_dim must be in [1, 64]");
+  if (max_slabs_ > kStageThreads) throw std::invalid_argument("device memo: more than 1024 slabs per operator call");
   if (client_.config().global_cache) throw std::invalid_argument("device memo: global_cache is host-only");
   if (client_.store().ivf().nlist > kMaxProbe) throw std::invalid_argument("device memo: nlist must be <= 64");
   const std::size_t per_key = 8 + 4 * static_cast<std::size_t>(kd_);
@@ -328,7 +376,7 @@ void DeviceMemo::lookup(OpId op, int n, const float* keys, const double* norms2,
                static_cast<long long>(arena_bytes_), log_cap_, qkeys_.get(), norms2, svb, scn, keys_.get(),
                vbytes_.get(), vnorm_.get(), vptr_.get(), arena_.get(), state_.get(), slabs_.get(), skip_.get(),
                la.probed, la.queried, log_.get()};
-  k_memo_stage<<<1, 32, 0, s>>>(sa);
+  k_memo_stage<<<1, static_cast<unsigned>((n + 31) / 32 * 32), 0, s>>>(sa);
   MLRG_LAUNCH_CHECK("k_memo_stage");
 }
 

@@ -137,6 +137,31 @@ def test_device_memo_matches_host_client_and_reference_counters(mlrg, torch_cuda
         assert k0[k] == k1[k], k
 
 
+def test_device_memo_ivf_matches_host_client(mlrg, torch_cuda, monkeypatch):
+    """Past 1024 published keys the store trains its IVF index (k-means++, 64
+    lists, memostore.cpp:140-222) and queries probe 8 lists: configs[1]
+    (256^3, 256 angles) inserts ~1200 keys in 10 iterations. The device lookup (parallel candidate scan,
+    rank-selected probes) must make the host store's decisions and give a
+    bit-identical u."""
+    torch = torch_cuda
+    n = 256
+    ph = torch.from_numpy(mlrg.make_phantom("blocks", n, n, n, 1).numpy().astype(np.complex64)).cuda()
+    ctx = mlrg.Context(n, n, n, n, n, n)
+    d = ctx.forward_L(ph, torch.empty((n, n, n), dtype=torch.complex64, device="cuda"))
+    ctx.sync()
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("MLRG_DEVICE_MEMO", mode)
+        u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
+        r = mlrg.reconstruct_device(config_text(n, n, 10, "local"), d, u, reference=ph)
+        runs[mode] = (u.cpu().numpy(), r.audit(), r.counters())
+    (u0, (m0, c0), k0), (u1, (m1, c1), k1) = runs["0"], runs["1"]
+    assert k1["inserts_sent"] > 1024  # the store trained mid-run
+    assert np.array_equal(m0, m1) and np.array_equal(c0, c1)
+    assert k0 == k1
+    assert np.array_equal(u0, u1)
+
+
 @pytest.mark.parametrize("case", ["recon_c16_cnn_memo_grid", "recon_c32_cnn_memo_grid"])
 def test_cnn_encoder_reconstruction_matches_reference(mlrg, torch_cuda, case):
     """encoder_variant = cnn (seeded init_cnn weights, encoder.cpp:95-197): the
