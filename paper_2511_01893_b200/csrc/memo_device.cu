@@ -392,9 +392,16 @@ __global__ void __launch_bounds__(256) k_slab_store(TO* __restrict__ out, SlabGe
 
 __device__ __forceinline__ long long slab_len(const SlabGeom& g) { return g.axis == 0 ? g.d0 : g.d1; }
 
+// Each thread moves kPer elements of a kSeg segment in groups of kInFlight:
+// the group's loads first, then its arithmetic and stores.
+constexpr int kCopyThreads = 256;
+constexpr int kPer = static_cast<int>(kSeg) / kCopyThreads;
+constexpr int kInFlight = 4;
+
 template <class TO>
-__global__ void __launch_bounds__(256) k_dev_materialize(TO* __restrict__ out, SlabGeom g, const DevSlab* __restrict__ slabs,
-                                                         long long chunk, const float2* __restrict__ sub) {
+__global__ void __launch_bounds__(kCopyThreads, 4) k_dev_materialize(TO* __restrict__ out, SlabGeom g,
+                                                                     const DevSlab* __restrict__ slabs,
+                                                                     long long chunk, const float2* __restrict__ sub) {
   const DevSlab d = slabs[blockIdx.y];
   if (d.outcome == 0) return;
   const long long start = blockIdx.y * chunk;
@@ -403,28 +410,38 @@ __global__ void __launch_bounds__(256) k_dev_materialize(TO* __restrict__ out, S
   const long long segs = (sr.run_len + kSeg - 1) / kSeg;
   for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
     const long long r = t / segs, e0 = (t - r * segs) * kSeg;
-    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
-    const long long e1 = min(sr.run_len, e0 + kSeg);
-    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const long long o = o0 + e;
-      const float2 v = value[v0 + e];
-      double re = v.x * d.scale, im = v.y * d.scale;
-      if (sub) {
-        const float2 sv = sub[o];
-        re -= sv.x;
-        im -= sv.y;
+    const long long o0 = sr.first + r * sr.stride + e0, v0 = r * sr.run_len + e0;
+    const int cnt = static_cast<int>(min(kSeg, sr.run_len - e0));
+    for (int i0 = 0; i0 < kPer; i0 += kInFlight) {
+      float2 v[kInFlight], sv[kInFlight];
+#pragma unroll
+      for (int i = 0; i < kInFlight; ++i) {
+        const int e = (i0 + i) * kCopyThreads + threadIdx.x;
+        v[i] = e < cnt ? value[v0 + e] : make_float2(0.f, 0.f);
+        sv[i] = sub && e < cnt ? sub[o0 + e] : make_float2(0.f, 0.f);
       }
-      TO res;
-      res.x = static_cast<decltype(res.x)>(re);
-      res.y = static_cast<decltype(res.y)>(im);
-      out[o] = res;
+#pragma unroll
+      for (int i = 0; i < kInFlight; ++i) {
+        const int e = (i0 + i) * kCopyThreads + threadIdx.x;
+        if (e >= cnt) continue;
+        double re = v[i].x * d.scale, im = v[i].y * d.scale;
+        if (sub) {
+          re -= sv[i].x;
+          im -= sv[i].y;
+        }
+        TO res;
+        res.x = static_cast<decltype(res.x)>(re);
+        res.y = static_cast<decltype(res.y)>(im);
+        out[o0 + e] = res;
+      }
     }
   }
 }
 
 template <class TO>
-__global__ void __launch_bounds__(256) k_dev_store(TO* __restrict__ out, SlabGeom g, const DevSlab* __restrict__ slabs,
-                                                   long long chunk, const float2* __restrict__ sub) {
+__global__ void __launch_bounds__(kCopyThreads, 4) k_dev_store(TO* __restrict__ out, SlabGeom g,
+                                                               const DevSlab* __restrict__ slabs, long long chunk,
+                                                               const float2* __restrict__ sub) {
   const DevSlab d = slabs[blockIdx.y];
   if (d.outcome != 0) return;
   const long long start = blockIdx.y * chunk;
@@ -434,14 +451,23 @@ __global__ void __launch_bounds__(256) k_dev_store(TO* __restrict__ out, SlabGeo
   const long long segs = (sr.run_len + kSeg - 1) / kSeg;
   for (long long t = blockIdx.x; t < sr.runs * segs; t += gridDim.x) {
     const long long r = t / segs, e0 = (t - r * segs) * kSeg;
-    const long long o0 = sr.first + r * sr.stride, v0 = r * sr.run_len;
-    const long long e1 = min(sr.run_len, e0 + kSeg);
-    for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const long long o = o0 + e;
-      const TO v = out[o];
-      if (value) value[v0 + e] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
-      if constexpr (sizeof(TO) == sizeof(float2)) {
-        if (sub) out[o] = csub(v, sub[o]);
+    const long long o0 = sr.first + r * sr.stride + e0, v0 = r * sr.run_len + e0;
+    const int cnt = static_cast<int>(min(kSeg, sr.run_len - e0));
+    for (int i0 = 0; i0 < kPer; i0 += kInFlight) {
+      TO v[kInFlight];
+#pragma unroll
+      for (int i = 0; i < kInFlight; ++i) {
+        const int e = (i0 + i) * kCopyThreads + threadIdx.x;
+        if (e < cnt) v[i] = out[o0 + e];
+      }
+#pragma unroll
+      for (int i = 0; i < kInFlight; ++i) {
+        const int e = (i0 + i) * kCopyThreads + threadIdx.x;
+        if (e >= cnt) continue;
+        if (value) value[v0 + e] = make_float2(static_cast<float>(v[i].x), static_cast<float>(v[i].y));
+        if constexpr (sizeof(TO) == sizeof(float2)) {
+          if (sub) out[o0 + e] = csub(v[i], sub[o0 + e]);
+        }
       }
     }
   }
