@@ -105,22 +105,24 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
   // x staging: lane owns complex element e = lane & 15 of slabs (lane >> 4) + 2j
   const int xe = lane & 15, xs0 = lane >> 4;
   float2 xr[8];
-  // element ce of slab `start`: axis 0 slabs are contiguous; axis 1 slabs are
-  // runs of extent * d2 (32-bit division: slab sizes stay below 2^31)
+  // element ce of slab `start` sits at base(ce) + start * smul: axis 0 slabs
+  // are contiguous; axis 1 slabs are runs of extent * d2 (32-bit division: slab
+  // sizes stay below 2^31), decomposed once per chunk for all the lane's slabs
   const unsigned per = static_cast<unsigned>(g.extent * g.d2), d2 = static_cast<unsigned>(g.d2);
-  auto offset = [&](long long start, long long ce) -> long long {
-    if (g.axis == 0) return start * g.d1 * g.d2 + ce;
-    const unsigned c = static_cast<unsigned>(ce), i = c / per, rem = c - i * per, kl = rem / d2;
-    return (static_cast<long long>(i) * g.d1 + start + kl) * g.d2 + (rem - kl * d2);
-  };
+  const long long smul = g.axis == 0 ? g.d1 * g.d2 : g.d2;
   auto load_x = [&](long long ch) {
     const long long ce = ch * 16 + xe;
+    long long base = ce;
+    if (g.axis != 0) {
+      const unsigned c = static_cast<unsigned>(ce), i = c / per, rem = c - i * per, kl = rem / d2;
+      base = (static_cast<long long>(i) * g.d1 + kl) * g.d2 + (rem - kl * d2);
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int sidx = xs0 + 2 * j;
       xr[j] = make_float2(0.f, 0.f);
       if (sidx < ns && ce < n) {
-        const TX v = x[offset(sl.start[sidx], ce)];
+        const TX v = x[base + sl.start[sidx] * smul];
         xr[j] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
       }
     }
@@ -131,13 +133,13 @@ __global__ void __launch_bounds__(kEncWarps * 32, MLRG_ENC_MINB) k_encode(const 
   };
   auto load_p = [&](EncStage& b, long long ch) {
     const long long k0 = ch * 32;
-    if (p_vec) {  // 8 x 16 B per row
-      for (int e = lane; e < kd * 8; e += 32) {
-        const int r = e >> 3, q = e & 7;
-        const long long k = k0 + 4 * q;
-        const int bytes = k >= K ? 0 : static_cast<int>(min(16LL, (K - k) * 4));
-        cp_async16z(&b.p[r][4 * q], P + (bytes ? static_cast<long long>(r) * K + k : 0), bytes);
-      }
+    if (p_vec) {  // 8 x 16 B per row: lane (r0, q) copies columns 4q.. of rows r0, r0 + 4, ...
+      const int q = lane & 7;
+      const long long k = k0 + 4 * q;
+      const int bytes = k >= K ? 0 : static_cast<int>(min(16LL, (K - k) * 4));
+      const float* src = P + (bytes ? k : 0);
+      for (int r = lane >> 3; r < kd; r += 4)
+        cp_async16z(&b.p[r][4 * q], src + (bytes ? static_cast<long long>(r) * K : 0), bytes);
     } else {
       const long long k = k0 + lane;
       const int bytes = k < K ? 4 : 0;
