@@ -45,7 +45,7 @@ __device__ __forceinline__ bool skipped(const Skip& s, int unit) { return s.f &&
 #define MLRG_FFT_MINB 4
 #endif
 #ifndef MLRG_GATHER_MINB
-#define MLRG_GATHER_MINB 3
+#define MLRG_GATHER_MINB 4
 #endif
 
 // Complex elements per CTA of the shared-memory FFT passes (double: 16 B each).
@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
   if (skipped(sk, 0)) return;
   constexpr int WH = W / 2;
   __shared__ double red_scratch[kGatherWarps * 2];
+  __shared__ double w2s[kGatherWarps][W];  // the class's column weights (half-warp broadcast reads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, kk = lane & 15, ph = lane >> 4;
   const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1;
   const long long row_stride = static_cast<long long>(KB) << logm2;  // complex64 per grid row
@@ -284,13 +285,12 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
   for (int s = blockIdx.x * per_cta + warp; s < s_end; s += kGatherWarps) {
     const int r0 = s_r0[s], c0 = s_c0[s];
     int coff[WH];
-    double w2r[WH];
+    __syncwarp();
+    if (lane < W) w2s[warp][lane] = s_w2[static_cast<long long>(s) * W + lane];
 #pragma unroll
-    for (int j = 0; j < WH; ++j) {
-      const int b = 2 * j + ph;
-      coff[j] = ((c0 + b) & mask2) * KB + kk;
-      w2r[j] = s_w2[static_cast<long long>(s) * W + b];
-    }
+    for (int j = 0; j < WH; ++j) coff[j] = ((c0 + 2 * j + ph) & mask2) * KB + kk;
+    __syncwarp();
+    const double* w2r = &w2s[warp][ph];  // w2r[2 j] = weight of window column 2 j + ph
     const double* w1p = s_w1 + static_cast<long long>(s) * W;
     double2 acc = make_double2(0.0, 0.0);
     // rows are software-pipelined one ahead: the next row's W/2 loads are in
@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
       double2 racc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int j = 0; j < WH; ++j) {
-        racc.x = fma(w2r[j], static_cast<double>(v[j].x), racc.x);
-        racc.y = fma(w2r[j], static_cast<double>(v[j].y), racc.y);
+        const double wj = w2r[2 * j];
+        racc.x = fma(wj, static_cast<double>(v[j].x), racc.x);
+        racc.y = fma(wj, static_cast<double>(v[j].y), racc.y);
       }
       const double wa = w1p[a];
       acc.x = fma(wa, racc.x, acc.x);
