@@ -835,6 +835,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   if (const char* e = std::getenv("MLRG_FU1D_NCOL"))  // tuning override (threads = ncol * m / 8 <= 1024)
     t.z_ncol = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 8192 / pz.m)));
   t.z_ncol = static_cast<int>(std::min<std::int64_t>(t.z_ncol, g_.n2));
+  if (const char* e = std::getenv("MLRG_FU1D_ADJ_NCOL"))  // tuning override (threads = ncol * m / 8 <= 512)
+    t.z_ncol_adj = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 4096 / pz.m)));
   t.z_ncol_adj = static_cast<int>(std::min<std::int64_t>(t.z_ncol_adj, g_.n2));
   t.z_deconv.upload(pz.deconv, stream_);
   std::vector<double> pdec(pz.deconv.size());
