@@ -20,6 +20,7 @@
 #include "encoder.hpp"
 #include "engine_api.hpp"
 #include "host_io.hpp"
+#include "offload_plan.hpp"
 #include "cnn.hpp"
 #include "kernels.hpp"
 #include "memo.hpp"
@@ -490,16 +491,22 @@ int mlr_server_port(const mlr_server*) {
 }
 void mlr_server_stop(mlr_server* s) { delete s; }
 
-char* mlr_plan_offload(const char*, double, const char*) {
-  t_error = "mlr_plan_offload: the ADMM-Offload planner is outside the B200 build's scope";
-  return nullptr;
+// ADMM-Offload planner (capi.cpp:344-380; offload_plan.cpp)
+char* mlr_plan_offload(const char* trace_text, double bandwidth, const char* format) {
+  return guarded_ptr<char>([&] {
+    need(trace_text != nullptr, "trace text is null");
+    return dup_text(mlrg::offload::plan_text(trace_text, bandwidth, format != nullptr ? format : "plan"));
+  });
 }
-char* mlr_lru_baseline(const char*, double, uint64_t) {
-  t_error = "mlr_lru_baseline: the ADMM-Offload planner is outside the B200 build's scope";
-  return nullptr;
+char* mlr_lru_baseline(const char* trace_text, double bandwidth, uint64_t budget_bytes) {
+  return guarded_ptr<char>([&] {
+    need(trace_text != nullptr, "trace text is null");
+    return dup_text(mlrg::offload::lru_text(trace_text, bandwidth, budget_bytes));
+  });
 }
 char* mlr_train_encoder(const mlr_config*, const char*, uint64_t, const char*) {
-  t_error = "mlr_train_encoder: the CNN encoder is outside the B200 build's scope (projection encoder only)";
+  t_error = "mlr_train_encoder: training the CNN encoder is outside the B200 build's scope "
+            "(encoder_variant = cnn runs seeded or LENC-file weights)";
   return nullptr;
 }
 
