@@ -158,11 +158,23 @@ L1TEX_PCT = {"k_fu2d_rows": 76.3, "k_fu2d_cols": 79.2, "k_fu2d_adj_cols": 78.3, 
              "k_fu2d_adj_spread": 87.7, "k_fu2d_gather": 52.8}
 
 
-def kernel_table(prof, n, nt, steps, peaks_gbs):
+def local_share(n, world, rank):
+    """Fraction of the n1 planes this rank owns: assign() over 16-plane slabs
+    (scalerun.cpp:14-27), as the sharded solver partitions the volume."""
+    slabs = -(-n // 16)
+    base, extra = divmod(slabs, world)
+    lo = rank * base + min(rank, extra)
+    cnt = base + (1 if rank < extra else 0)
+    return (min(n, (lo + cnt) * 16) - min(n, lo * 16)) / n
+
+
+def kernel_table(prof, n, nt, steps, peaks_gbs, share=1.0):
     """Every profiled kernel against its own roof: the tap kernels
-    against FP32 CUDA-core flops (algorithmic, 576 taps), everything else against HBM."""
+    against FP32 CUDA-core flops (algorithmic, 576 taps), everything else against HBM.
+    `share`: this rank's fraction of the volume (whole-volume kernels scale with it;
+    the fu2d-class kernels work on one 16-row batch per launch at any rank count)."""
     out = {}
-    V16 = 16 * n ** 3
+    V16 = 16 * n ** 3 * share
     for name, rec in prof.items():
         ms = rec["ms_total"] / max(steps, 1)
         if name in HBM_VOLUMES_PER_ITER:
@@ -172,6 +184,8 @@ def kernel_table(prof, n, nt, steps, peaks_gbs):
                          "bytes_per_step": b, "achieved_gbs": gbs, "frac": gbs / peaks_gbs}
             continue
         work = algorithmic(n, nt, name)
+        if name in ("k_fu1d", "k_fu1d_adj") and work["bytes"]:
+            work = {"flops": work["flops"] * share, "bytes": work["bytes"] * share}
         per = rec["ms_total"] / rec["launches"]
         if name in ("k_fu2d_gather", "k_fu2d_adj_spread") and work["flops"]:
             tf = work["flops"] / (per * 1e-3) / 1e12
@@ -182,10 +196,10 @@ def kernel_table(prof, n, nt, steps, peaks_gbs):
             out[name] = {"ms_per_step": ms, "launches_per_step": rec["launches"] / max(steps, 1),
                          "bound": "l1/shared (ncu)" if name != "k_fu1d" and name != "k_fu1d_adj" else "hbm",
                          "avg_launch_ms": per, "achieved_gbs": gbs, "frac_of_hbm": gbs / peaks_gbs}
-        if name in L1TEX_PCT:
-            out[name]["l1tex_pct_ncu"] = L1TEX_PCT[name]
         else:
             out[name] = {"ms_per_step": ms, "launches_per_step": rec["launches"] / max(steps, 1)}
+        if name in L1TEX_PCT:
+            out[name]["l1tex_pct_ncu"] = L1TEX_PCT[name]
     return out
 
 
@@ -358,7 +372,7 @@ def main():
                                       "source": f"profiles/r1_ncu_{name}.txt"}
         roof["share_of_step"] = rec["ms_total"] / ps / ms_step
         roof["kernels_ms_per_step"] = {k: v["ms_total"] / ps for k, v in off["prof"].items()}
-        roof["kernels"] = kernel_table(off["prof"], n, nt, ps, P["hbm_gbs"])
+        roof["kernels"] = kernel_table(off["prof"], n, nt, ps, P["hbm_gbs"], local_share(n, world, rank))
     # whole-iteration views against SURVEY §8(d)'s F_iter and fused-minimum B_iter
     V = n ** 3
     f_iter, b_iter = iteration_work(n, nt)
