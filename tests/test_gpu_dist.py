@@ -154,6 +154,24 @@ def test_sharded_512_matches_single_gpu(mlrg, torch_cuda, tmp_path):
     assert rel(u2, one["u"]) <= 1e-6
 
 
+def test_sharded_configs1_memo_through_ivf_training(mlrg, torch_cuda, tmp_path):
+    """configs[1] (256^3, 256 angles), memo on for 10 outer iterations: the store
+    passes 1024 published keys and trains its IVF index mid-run. The key index is
+    replicated through the communicator, so two ranks must make the single-GPU
+    decisions before and after training (memo under sharding)."""
+    import torch.multiprocessing as mp
+
+    n, steps = 256, 10
+    for world in (1, 2):
+        mp.start_processes(_big_worker, args=(world, free_port(), n, "local", steps, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    one = np.load(tmp_path / "w1_rank0.npz")
+    two = [np.load(tmp_path / f"w2_rank{r}.npz") for r in range(2)]
+    assert len(one["meta"]) > 2048  # enough decisions to have trained (1024 published keys)
+    assert np.array_equal(two[0]["meta"], one["meta"]) and np.array_equal(two[1]["meta"], one["meta"])
+    assert rel(np.concatenate([p["u"] for p in two], axis=0), one["u"]) <= 1e-6
+
+
 @pytest.mark.parametrize("n,world,memo,offload", [(64, 3, "off", "off"), (48, 2, "local", "off"),
                                                  (80, 3, "local", "off"), (64, 2, "local", "host")])
 def test_sharded_uneven_partitions_match_single_gpu(mlrg, torch_cuda, tmp_path, n, world, memo, offload):
