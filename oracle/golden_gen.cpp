@@ -140,7 +140,7 @@ int cmd_ops(const std::string& dir, std::int64_t n1, std::int64_t n0, std::int64
 
 int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_outer,
               const std::string& memo, const std::string& path, int workers,
-              const std::string& variant = "projection") {
+              const std::string& variant = "projection", const std::string& pipeline = "optimized") {
   mlr::RunConfig rc;
   rc.set("n1", std::to_string(n));
   rc.set("n0", std::to_string(n));
@@ -153,6 +153,7 @@ int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_out
   rc.set("nudft_path", path);
   rc.set("workers", std::to_string(workers));
   rc.set("encoder_variant", variant);
+  rc.set("pipeline", pipeline);
   rc.validate();
   const mlr::Geometry geom = rc.make_geometry();
   const mlr::Volume phantom =
@@ -418,7 +419,8 @@ int main(int argc, char** argv) {
     if (cmd == "ops" && argc == 10) return cmd_ops(dir, I(3), I(4), I(5), I(6), I(7), I(8), I(9));
     if (cmd == "recon" && argc >= 8)
       return cmd_recon(dir, I(3), I(4), static_cast<int>(I(5)), argv[6], argv[7],
-                       argc > 8 ? static_cast<int>(I(8)) : 1, argc > 9 ? argv[9] : "projection");
+                       argc > 8 ? static_cast<int>(I(8)) : 1, argc > 9 ? argv[9] : "projection",
+                       argc > 10 ? argv[10] : "optimized");
     if (cmd == "encoder") return cmd_encoder(dir);
     if (cmd == "cnn") return cmd_cnn(dir);
     if (cmd == "trace" && argc == 5) return cmd_trace(I(3), static_cast<int>(I(4)));

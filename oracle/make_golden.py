@@ -37,6 +37,10 @@ CASES = {
     # the CNN key encoder (encoder_variant = cnn, seeded initial weights)
     "recon_c16_cnn_memo_grid": ["recon", "16", "16", "10", "local", "gridding", "1", "cnn"],
     "recon_c32_cnn_memo_grid": ["recon", "32", "32", "10", "local", "gridding", "8", "cnn"],
+    # pipeline = baseline (admm.cpp:122-138): 6 memoizable operators per inner step,
+    # memoized f2d / f2d_adj included
+    "recon_c16_baseline_memo_grid": ["recon", "16", "16", "6", "local", "gridding", "1", "projection", "baseline"],
+    "recon_c32_baseline_off_grid": ["recon", "32", "32", "6", "off", "gridding", "8", "projection", "baseline"],
     # BASELINE configs[0] exactly as-is: 64^3, 64 angles, 10 iterations, memo on,
     # default (direct) NUDFT path, 1 worker. ~5 minutes of CPU.
     "recon_cfg1_memo_direct": ["recon", "64", "64", "10", "local", "direct", "1"],

@@ -15,9 +15,16 @@ def ref_rows(z):
     return [[float(v) for v in l.split(",")] for l in lines[1:]]
 
 
-def config_text(n, nt, n_outer, memo, kernel="es", encoder="projection"):
+def config_text(n, nt, n_outer, memo, kernel="es", encoder="projection", pipeline="optimized"):
     return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
-            f"memoization={memo}\nnudft_path=gridding\ngridding_kernel={kernel}\nencoder_variant={encoder}\n")
+            f"memoization={memo}\nnudft_path=gridding\ngridding_kernel={kernel}\nencoder_variant={encoder}\n"
+            f"pipeline={pipeline}\n")
+
+
+def ref_config(z):
+    """key = value lines of the reference run's RunConfig::str() (config.txt)."""
+    return dict((k.strip(), v.strip()) for k, v in (l.split("=", 1) for l in str(z["txt_config_txt"]).splitlines()
+                                                     if "=" in l))
 
 
 @pytest.mark.parametrize("case,memo,kernel", [("recon_c16_memo_grid", "local", "es"),
@@ -29,7 +36,11 @@ def config_text(n, nt, n_outer, memo, kernel="es", encoder="projection"):
                                               # amplifies the complex64 grid rounding 23x per dimension
                                               # (es: 4.8x), so larger cases sit near the 1e-4 bound
                                               ("recon_c32_memo_grid", "local", "gaussian"),
-                                              ("recon_c32_off_grid", "off", "gaussian")])
+                                              ("recon_c32_off_grid", "off", "gaussian"),
+                                              # pipeline = baseline (admm.cpp:122-138): six memoizable
+                                              # operators per inner step, memoized f2d / f2d_adj
+                                              ("recon_c16_baseline_memo_grid", "local", "es"),
+                                              ("recon_c32_baseline_off_grid", "off", "es")])
 def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo, kernel):
     torch = torch_cuda
     z = golden(case)
@@ -38,7 +49,9 @@ def test_device_reconstruction_matches_reference(mlrg, torch_cuda, case, memo, k
     d = torch.from_numpy(z["data"]).cuda()
     ref = torch.from_numpy(z["phantom"]).cuda()
     u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
-    r = mlrg.reconstruct_device(config_text(n, nt, 10, memo, kernel), d, u, reference=ref)
+    rc = ref_config(z)
+    r = mlrg.reconstruct_device(config_text(n, nt, int(rc["n_outer"]), memo, kernel, pipeline=rc["pipeline"]), d, u,
+                                reference=ref)
     aborted = bool(int(str(z["txt_aborted_txt"]).split()[0]))
     assert r.aborted == aborted
     if memo != "off":
