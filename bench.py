@@ -413,14 +413,20 @@ def main():
                        nudft_path="gridding")
         ph = m.make_phantom("blocks", n, n, n, 1)
         data = m.project(cfg, ph)
+        warm = m.Config(n1=n, n0=n, n2=n, n_theta=nt, h=n, w=n, n_outer=1, memoization="off",
+                        nudft_path="gridding")
+        m.reconstruct(warm, data, ph).volume.view()  # untimed warm-up call (first-use page mapping)
         t0 = time.perf_counter()
         res = m.reconstruct(cfg, data, ph)
         vol = res.volume.view()  # the host complex128 result, zero-copy
         wall = time.perf_counter() - t0
         k = len(m.parse_csv(res.csv))
-        e2e = {"value": k / wall, "unit": "it/s", "h2d_bytes_per_step": (2 * 16 * V) / max(k, 1),
+        e2e = {"value": k / wall, "unit": "it/s", "h2d_bytes_per_step": (2 * 8 * V) / max(k, 1),
                "d2h_bytes_per_step": 16 * V / max(k, 1), "steps": k, "wall_s": wall,
-               "path": "mlr_reconstruct (drop-in mlr.h) on host complex128 arrays, incl. setup and copies",
+               "path": "mlr_reconstruct (drop-in mlr.h) on host complex128 arrays, incl. setup and copies, "
+                       "after one untimed 1-iteration warm-up call "
+                       "(data and reference rounded to complex64 by the staging threads: 8 B per element "
+                       "over PCIe; the complex128 iterate comes back whole)",
                "checksum": float(np.abs(vol).sum())}
 
     cpu = None

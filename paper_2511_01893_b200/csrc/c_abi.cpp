@@ -178,35 +178,38 @@ struct StreamGuard {
 /// Host -> device copy of pageable memory through a ring of pinned staging
 /// blocks: host threads fill block b + 1 while the copy engine drains block b
 /// (a driver-staged pageable copy runs at ~11 GB/s here; pinned DMA at PCIe rate).
-void h2d_staged(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
-  constexpr std::size_t kBlock = std::size_t{32} << 20;
+/// Host complex128 -> device complex64 through a ring of pinned blocks: host
+/// threads round each block to complex64 while the previous block's DMA runs,
+/// so PCIe carries 8 B per element (the device keeps these arrays in complex64;
+/// round-to-nearest on the host is the device conversion's rounding).
+void upload_c64(const mlrg::HostArray& a, mlrg::DeviceBuffer<float2>& dst, cudaStream_t s) {
+  const std::size_t n = a.data.size();
+  dst.resize(n);
+  constexpr std::size_t kBlock = std::size_t{2} << 20;  // elements (16 MB of complex64)
   constexpr int kRing = 3, kThreads = 8;
-  if (bytes < 2 * kBlock) {
-    MLRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-    return;
-  }
-  mlrg::PinnedBuffer<char> ring[kRing];
+  mlrg::PinnedBuffer<float2> ring[kRing];
   cudaEvent_t done[kRing];
   for (int r = 0; r < kRing; ++r) {
-    ring[r].reserve(kBlock);
+    ring[r].reserve(std::min(kBlock, std::max<std::size_t>(n, 1)));
     MLRG_CUDA(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
   }
   std::exception_ptr err;
   try {
-    for (std::size_t off = 0, i = 0; off < bytes; off += kBlock, ++i) {
+    const auto* src = a.data.data();
+    for (std::size_t off = 0, i = 0; off < n; off += kBlock, ++i) {
       const int r = static_cast<int>(i % kRing);
-      const std::size_t len = std::min(kBlock, bytes - off);
+      const std::size_t len = std::min(kBlock, n - off);
       if (i >= kRing) MLRG_CUDA(cudaEventSynchronize(done[r]));  // the block's previous copy finished
-      std::vector<std::thread> th;
+      float2* buf = ring[r].get();
       const std::size_t per = (len + kThreads - 1) / kThreads;
-      for (int t = 0; t < kThreads; ++t) {
-        const std::size_t lo = std::min(len, t * per), hi = std::min(len, lo + per);
-        th.emplace_back([&, lo, hi] {
-          std::memcpy(ring[r].get() + lo, static_cast<const char*>(src) + off + lo, hi - lo);
+      std::vector<std::thread> th;
+      for (int t = 0; t < kThreads; ++t)
+        th.emplace_back([=] {
+          for (std::size_t e = std::min(len, t * per), e1 = std::min(len, e + per); e < e1; ++e)
+            buf[e] = make_float2(static_cast<float>(src[off + e].real()), static_cast<float>(src[off + e].imag()));
         });
-      }
       for (auto& x : th) x.join();
-      MLRG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ring[r].get(), len, cudaMemcpyHostToDevice, s));
+      MLRG_CUDA(cudaMemcpyAsync(dst.get() + off, buf, len * sizeof(float2), cudaMemcpyHostToDevice, s));
       MLRG_CUDA(cudaEventRecord(done[r], s));
     }
     MLRG_CUDA(cudaStreamSynchronize(s));
@@ -216,16 +219,6 @@ void h2d_staged(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
   }
   for (int r = 0; r < kRing; ++r) cudaEventDestroy(done[r]);
   if (err) std::rethrow_exception(err);
-}
-
-/// Uploads a host complex128 array as device complex64.
-void upload_c64(const mlrg::HostArray& a, mlrg::DeviceBuffer<float2>& dst, cudaStream_t s) {
-  const std::size_t n = a.data.size();
-  mlrg::DeviceBuffer<double2> tmp(n);
-  h2d_staged(tmp.get(), a.data.data(), n * sizeof(double2), s);
-  dst.resize(n);
-  mlrg::ops::c128_to_c64(tmp.get(), dst.get(), static_cast<std::int64_t>(n), s);
-  MLRG_CUDA(cudaStreamSynchronize(s));
 }
 
 void download_c128(const float2* src, mlrg::HostArray& a, cudaStream_t s) {
