@@ -379,13 +379,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // Patches are processed heaviest first.
 constexpr int kPatchR = 8, kPatchC = 4;
 constexpr int KH = KB / 2;
-constexpr int kReduceWarps = 4;
 
 struct SpreadShared {
   double wr[2][2][32][kPatchR];  // [pair][buf][target][patch row]
   double wc[2][2][32][kPatchC];  // [pair][buf][target][patch column]
   float4 vstage[4][2][32][KH / 2];  // per warp, double-buffered half values
   double2 vald[4][32][KH];          // per warp, widened chunk values
+  int last[2];                      // per pair: this item completes its split patch
 };
 
 __device__ __forceinline__ void pair_sync(int pair) {
@@ -393,10 +393,13 @@ __device__ __forceinline__ void pair_sync(int pair) {
 }
 
 // A work item is (patch, a sub-range of its target list): lists longer than
-// kSplit (the cells around nu = 0) are split over several warp pairs whose
-// double partials are summed in item order by k_fu2d_adj_spread_reduce.
+// kSplit (the cells around nu = 0) are split over several warp pairs. Each
+// writes its double partials to its slot; the pair that completes the patch
+// (an atomic count per split group) sums all of the group's slots in slot
+// order (deterministic, whoever finishes last) and writes the grid.
 struct SpreadItem {
   int patch, e0, e1, slot;  // slot < 0: write the grid directly
+  int grp;                  // split group (index into the (patch, first slot, slots) table)
 };
 constexpr int kSplit = 256;
 
@@ -442,7 +445,8 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
                                                          const int* __restrict__ patch_t, const int* __restrict__ r0,
                                                          const int* __restrict__ c0, const double* __restrict__ w1,
                                                          const double* __restrict__ w2, float2* __restrict__ G,
-                                                         double2* __restrict__ partial, Skip sk) {
+                                                         double2* __restrict__ partial, const int4* __restrict__ split,
+                                                         int* __restrict__ split_cnt, Skip sk) {
   if (skipped(sk, 0)) return;
   extern __shared__ float4 dyn_smem[];
   SpreadShared& sh = *reinterpret_cast<SpreadShared*>(dyn_smem);
@@ -495,33 +499,27 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
     double2* pp = partial + (static_cast<long long>(it.slot) * 32 + lane) * KB + half * KH;
 #pragma unroll
     for (int kk = 0; kk < KH; ++kk) pp[kk] = acc[kk];
-    return;
+    __threadfence();  // this pair's partials are visible before its arrival is counted
+    pair_sync(pair);
+    const int4 sp = split[it.grp];  // (patch, first slot, slots, -)
+    if (half == 0 && lane == 0) sh.last[pair] = atomicAdd(split_cnt + it.grp, 1) == sp.z - 1;
+    pair_sync(pair);
+    if (!sh.last[pair]) return;
+    __threadfence();
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) acc[kk] = make_double2(0.0, 0.0);
+    for (int q = 0; q < sp.z; ++q) {  // slot order
+      const double2* src = partial + (static_cast<long long>(sp.y + q) * 32 + lane) * KB + half * KH;
+#pragma unroll
+      for (int kk = 0; kk < KH; ++kk) acc[kk] = cadd(acc[kk], __ldcg(src + kk));
+    }
+    if (half == 0 && lane == 0) split_cnt[it.grp] = 0;  // ready for the next launch
   }
   float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB + half * KH);
 #pragma unroll
   for (int q = 0; q < KH / 2; ++q) {
     const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
     gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
-  }
-}
-
-// Sums the split patches' partials in item order (deterministic) into the grid.
-__global__ void __launch_bounds__(32 * kReduceWarps) k_fu2d_adj_spread_reduce(
-    int nsplit, const int4* __restrict__ split, int logm2, const double2* __restrict__ partial,
-    float2* __restrict__ G, Skip sk) {
-  if (skipped(sk, 0)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int si = blockIdx.x * kReduceWarps + warp;
-  if (si >= nsplit) return;
-  const int4 sp = split[si];  // (patch, first slot, slot count, -)
-  const int m2 = 1 << logm2, npc = m2 / kPatchC;
-  const int r = (sp.x / npc) * kPatchR + lane / kPatchC, c = (sp.x % npc) * kPatchC + lane % kPatchC;
-  float2* gp = G + (static_cast<long long>(r) * m2 + c) * KB;
-#pragma unroll
-  for (int kk = 0; kk < KB; ++kk) {
-    double2 a = make_double2(0.0, 0.0);
-    for (int q = 0; q < sp.z; ++q) a = cadd(a, partial[(static_cast<long long>(sp.y + q) * 32 + lane) * KB + kk]);
-    gp[kk] = to_f(a);
   }
 }
 
@@ -798,6 +796,7 @@ struct Usfft::Tables {
   // next batch's FFT passes
   DeviceBuffer<float2> S2, Gd2, val2;
   DeviceBuffer<double2> partial2;
+  DeviceBuffer<int> split_cnt2;
   // four-step column passes: M = A * B, A = 2^logA
   bool cols4 = false;
   int logA = 0;
@@ -810,6 +809,7 @@ struct Usfft::Tables {
   DeviceBuffer<SpreadItem> items;
   DeviceBuffer<int4> split;
   DeviceBuffer<double2> partial;
+  DeviceBuffer<int> split_cnt;  // arrivals per split group (zero between launches)
   // f2d
   bool f2d_fft = false;
   DeviceBuffer<double2> h_tw, w_tw, Wh, Ww, Whc, Wwc;
@@ -1017,11 +1017,12 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     for (const int p : porder) {  // heaviest first
       const int e0 = cnt[static_cast<std::size_t>(p)], e1 = cnt[static_cast<std::size_t>(p) + 1];
       if (e1 - e0 <= kSplit) {
-        items.push_back(SpreadItem{p, e0, e1, -1});
+        items.push_back(SpreadItem{p, e0, e1, -1, -1});
         continue;
       }
       const int first = slots;
-      for (int e = e0; e < e1; e += kSplit) items.push_back(SpreadItem{p, e, std::min(e1, e + kSplit), slots++});
+      const int grp = static_cast<int>(split.size());
+      for (int e = e0; e < e1; e += kSplit) items.push_back(SpreadItem{p, e, std::min(e1, e + kSplit), slots++, grp});
       split.push_back(make_int4(p, first, slots - first, 0));
     }
     t.nitems = static_cast<int>(items.size());
@@ -1029,6 +1030,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     t.items.upload(items, stream_);
     t.split.upload(split, stream_);
     t.partial.resize(static_cast<std::size_t>(std::max(slots, 1)) * 32 * KB);
+    t.split_cnt.resize(static_cast<std::size_t>(std::max(t.nsplit, 1)));
+    t.split_cnt.zero(stream_);
     t.patch_t.upload(lst, stream_);
   }
   t.x_tw.upload(twiddles(px.m), stream_);
@@ -1258,6 +1261,8 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     if (tm.val2.size() != tm.val.size()) {
       tm.val2.resize(tm.val.size());
       tm.partial2.resize(tm.partial.size());
+      tm.split_cnt2.resize(tm.split_cnt.size());
+      tm.split_cnt2.zero(stream_);
     }
     MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));
     MLRG_CUDA(cudaStreamWaitEvent(tm.side, tm.ev_fork, 0));
@@ -1271,6 +1276,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
     float2* val = alt ? tm.val2.get() : t.val.get();
     double2* partial = alt ? tm.partial2.get() : t.partial.get();
+    int* split_cnt = alt ? tm.split_cnt2.get() : tm.split_cnt.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_adj_prep", s);
     k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, s>>>(
@@ -1282,13 +1288,9 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
     spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
                                                                t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
-                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial, sk);
+                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial, t.split.get(),
+                                                               split_cnt, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
-    if (t.nsplit > 0) {
-      k_fu2d_adj_spread_reduce<<<(t.nsplit + kReduceWarps - 1) / kReduceWarps, 32 * kReduceWarps, 0, s>>>(
-          t.nsplit, t.split.get(), t.py.logm, partial, Gd, sk);
-      MLRG_LAUNCH_CHECK("k_fu2d_adj_spread_reduce");
-    }
     prof::end("k_fu2d_adj_spread", s);
     prof::begin("k_fu2d_adj_cols", s);
     const float2* Sc = S;
