@@ -49,13 +49,13 @@ __device__ __forceinline__ bool skipped(const Skip& s, int unit) { return s.f &&
 #endif
 
 // Complex elements per CTA of the shared-memory FFT passes (double: 16 B each).
-// 2048 (32 KB) lets ~6 CTAs share an SM so one CTA's loads overlap another's
-// butterflies; MLRG_FFT_ELEMS overrides it for tuning.
+// 4096 (64 KB, 8 batch rows of a 512-point line per CTA) measured best at 256^3
+// (36.2 vs 35.7 it/s at 2048); MLRG_FFT_ELEMS overrides it for tuning.
 std::int64_t fft_elems() {
   static const std::int64_t e = [] {
     const char* v = std::getenv("MLRG_FFT_ELEMS");
-    // <= 2048: the 2D passes run 256-thread CTAs (m * nb / 8 threads)
-    std::int64_t n = v ? std::clamp<std::int64_t>(std::atoll(v), 64, 2048) : std::int64_t{2048};
+    // <= 4096: the 2D passes run up to 512-thread CTAs (m * nb / 8 threads)
+    std::int64_t n = v ? std::clamp<std::int64_t>(std::atoll(v), 64, 4096) : std::int64_t{4096};
     while (n & (n - 1)) n &= n - 1;
     return n;
   }();
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
 // TS (with the four-step column passes): S[i][KB][c'] instead, so the stores of
 // a CTA holding 1-2 batch rows of a long row are contiguous.
 template <bool ZP, bool TS>
-__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
+__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_rows(const float2* __restrict__ v, long long ld, long long k0, int nk,
                                                    int n2, int logm2, int center2, int ks_n,
                                                    const double* __restrict__ dx, const double* __restrict__ dy,
                                                    const double2* __restrict__ tw2, float2* __restrict__ S, Skip sk) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_rows(const float2* 
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
 template <bool ZP>
-__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
                                                    float2* __restrict__ G, Skip sk) {
   if (skipped(sk, 0)) return;
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
-__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
+__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
                                                        int logm2, int ks_n, const double2* __restrict__ tw1,
                                                        float2* __restrict__ S, Skip sk) {
   if (skipped(sk, 0)) return;
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict
 
 // Row FFT(-1) and the final deconvolution into out[i, k0_out+kk, j].
 template <bool PEER, bool TS>
-__global__ void __launch_bounds__(256, MLRG_FFT_MINB) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
+__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_adj_rows(const float2* __restrict__ S, int nk, int n2, int logm2,
                                                        int center2, int ks_n, const double* __restrict__ pdx,
                                                        const double* __restrict__ dy, const double2* __restrict__ tw2,
                                                        float2* __restrict__ out, long long ld_out,
