@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <numbers>
 #include <type_traits>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -970,12 +971,11 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   {  // spread patches: 8x4 cells -> targets whose W x W window touches them (targets ascending)
     const std::int64_t npr = px.m / kPatchR, npc = py.m / kPatchC;
     const int npatch = static_cast<int>(npr * npc);
-    // patches touched by a target's W x W window (dedup within the target)
-    std::vector<int> touched;
-    // the window's distinct patch rows and columns (in first-touch order), then
-    // their product in the row-major order of the full W x W scan
-    std::vector<std::int64_t> prs, pcs;
-    auto patches_of = [&](std::size_t c) {
+    // patches touched by a class's W x W window (dedup within the class): its
+    // distinct patch rows and columns (in first-touch order), then their product
+    // in the row-major order of the full W x W scan
+    auto patches_of = [&](std::size_t c, std::vector<std::int64_t>& prs, std::vector<std::int64_t>& pcs,
+                          std::vector<int>& touched) {
       const std::size_t q = static_cast<std::size_t>(rep_of[c]);
       prs.clear();
       pcs.clear();
@@ -989,22 +989,46 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
       for (const std::int64_t pr : prs)
         for (const std::int64_t pc : pcs) touched.push_back(static_cast<int>(pr * npc + pc));
     };
+    // CSR patch -> classes, classes ascending within a patch: host threads own
+    // contiguous class ranges, count per patch, then fill from per-thread offsets
+    // (thread 0's classes first), which is the sequential order
+    constexpr int kHostThreads = 8;
+    const std::size_t per = (C + kHostThreads - 1) / kHostThreads;
+    std::vector<std::vector<int>> tcnt(kHostThreads, std::vector<int>(static_cast<std::size_t>(npatch), 0));
     std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0), lst;
-    for (int pass = 0; pass < 2; ++pass) {
-      std::vector<int> pos;
-      if (pass == 1) {
-        for (std::size_t l = 1; l < cnt.size(); ++l) cnt[l] += cnt[l - 1];
-        pos.assign(cnt.begin(), cnt.end() - 1);
-        lst.resize(static_cast<std::size_t>(cnt.back()));
-      }
-      for (std::size_t c = 0; c < C; ++c) {
-        patches_of(c);
-        for (const int p : touched) {
-          if (pass == 0) cnt[static_cast<std::size_t>(p) + 1]++;
-          else lst[static_cast<std::size_t>(pos[static_cast<std::size_t>(p)]++)] = static_cast<int>(c);
-        }
+    auto run = [&](auto&& body) {
+      std::vector<std::thread> th;
+      for (int w = 0; w < kHostThreads; ++w)
+        th.emplace_back([&, w] {
+          std::vector<std::int64_t> prs, pcs;
+          std::vector<int> touched;
+          for (std::size_t c = w * per; c < std::min(C, (w + 1) * per); ++c) {
+            patches_of(c, prs, pcs, touched);
+            body(w, c, touched);
+          }
+        });
+      for (auto& x : th) x.join();
+    };
+    run([&](int w, std::size_t, const std::vector<int>& touched) {
+      for (const int p : touched) ++tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)];
+    });
+    for (int p = 0; p < npatch; ++p) {
+      int tot = 0;
+      for (int w = 0; w < kHostThreads; ++w) tot += tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)];
+      cnt[static_cast<std::size_t>(p) + 1] = cnt[static_cast<std::size_t>(p)] + tot;
+    }
+    lst.resize(static_cast<std::size_t>(cnt.back()));
+    for (int p = 0; p < npatch; ++p) {  // tcnt becomes each thread's fill position
+      int at = cnt[static_cast<std::size_t>(p)];
+      for (int w = 0; w < kHostThreads; ++w) {
+        const int n = tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)];
+        tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)] = at;
+        at += n;
       }
     }
+    run([&](int w, std::size_t c, const std::vector<int>& touched) {
+      for (const int p : touched) lst[static_cast<std::size_t>(tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)]++)] = static_cast<int>(c);
+    });
     std::vector<int> porder(static_cast<std::size_t>(npatch));
     for (int p = 0; p < npatch; ++p) porder[static_cast<std::size_t>(p)] = p;
     std::stable_sort(porder.begin(), porder.end(), [&](int a, int b) {
