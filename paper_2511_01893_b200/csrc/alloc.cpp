@@ -10,7 +10,7 @@
 namespace mlrg::alloc {
 
 namespace {
-constexpr std::size_t kMinCached = std::size_t{1} << 20;
+constexpr std::size_t kMinCached = 256;  // cudaFree of a small block can stall engine teardown for 100s of ms
 
 struct Cache {
   std::mutex mx;

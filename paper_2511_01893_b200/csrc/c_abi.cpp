@@ -449,15 +449,25 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
         for (int it = 0; it < cfg->rc.admm.n_outer; ++it)
           if (!solver->step()) break;
       }
-      mlrg::prof::HostSpan span("host:e2e_download");
-      res->report = solver->report();
-      prefault.join();
-      // the iterate is complex128 on the device: no rounding on the way out
-      MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2),
-                                cudaMemcpyDeviceToHost, sg.s));
-      MLRG_CUDA(cudaStreamSynchronize(sg.s));
+      {
+        mlrg::prof::HostSpan span("host:e2e_download");
+        res->report = solver->report();
+        prefault.join();
+        // the iterate is complex128 on the device: no rounding on the way out
+        MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2),
+                                  cudaMemcpyDeviceToHost, sg.s));
+        MLRG_CUDA(cudaStreamSynchronize(sg.s));
+      }
+      mlrg::prof::HostSpan span("host:e2e_solver_teardown");
+      solver.reset();
     }
     res->audit = eng->audit_log();
+    {
+      mlrg::prof::HostSpan span("host:e2e_engine_teardown");
+      eng.reset();
+      d = mlrg::DeviceBuffer<float2>();
+      ref = mlrg::DeviceBuffer<float2>();
+    }
     return res.release();
   });
 }
