@@ -218,6 +218,53 @@ void upload_c64(const mlrg::HostArray& a, mlrg::DeviceBuffer<float2>& dst, cudaS
   if (err) std::rethrow_exception(err);
 }
 
+/// Device -> host copy into pageable memory through a ring of pinned blocks:
+/// the copy engine fills block b + 1 while host threads move block b out.
+void d2h_staged(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
+  constexpr std::size_t kBlock = std::size_t{16} << 20;
+  constexpr int kRing = 3, kThreads = 8;
+  if (bytes < 2 * kBlock) {
+    MLRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  mlrg::PinnedBuffer<char> ring[kRing];
+  cudaEvent_t done[kRing];
+  for (int r = 0; r < kRing; ++r) {
+    ring[r].reserve(kBlock);
+    MLRG_CUDA(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+  }
+  const std::size_t nblk = (bytes + kBlock - 1) / kBlock;
+  auto issue = [&](std::size_t i) {
+    const int r = static_cast<int>(i % kRing);
+    const std::size_t off = i * kBlock, len = std::min(kBlock, bytes - off);
+    MLRG_CUDA(cudaMemcpyAsync(ring[r].get(), static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaEventRecord(done[r], s));
+  };
+  std::exception_ptr err;
+  try {
+    for (std::size_t i = 0; i < std::min<std::size_t>(kRing, nblk); ++i) issue(i);
+    for (std::size_t i = 0; i < nblk; ++i) {
+      const int r = static_cast<int>(i % kRing);
+      const std::size_t off = i * kBlock, len = std::min(kBlock, bytes - off);
+      MLRG_CUDA(cudaEventSynchronize(done[r]));
+      const std::size_t per = (len + kThreads - 1) / kThreads;
+      std::vector<std::thread> th;
+      for (int t = 0; t < kThreads; ++t) {
+        const std::size_t lo = std::min(len, t * per), hi = std::min(len, lo + per);
+        th.emplace_back([&, lo, hi] { std::memcpy(static_cast<char*>(dst) + off + lo, ring[r].get() + lo, hi - lo); });
+      }
+      for (auto& x : th) x.join();
+      if (i + kRing < nblk) issue(i + kRing);
+    }
+  } catch (...) {
+    err = std::current_exception();
+    cudaStreamSynchronize(s);
+  }
+  for (int r = 0; r < kRing; ++r) cudaEventDestroy(done[r]);
+  if (err) std::rethrow_exception(err);
+}
+
 void download_c128(const float2* src, mlrg::HostArray& a, cudaStream_t s) {
   const std::size_t n = a.data.size();
   mlrg::DeviceBuffer<double2> tmp(n);
@@ -454,9 +501,7 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
         res->report = solver->report();
         prefault.join();
         // the iterate is complex128 on the device: no rounding on the way out
-        MLRG_CUDA(cudaMemcpyAsync(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2),
-                                  cudaMemcpyDeviceToHost, sg.s));
-        MLRG_CUDA(cudaStreamSynchronize(sg.s));
+        d2h_staged(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2), sg.s);
       }
       mlrg::prof::HostSpan span("host:e2e_solver_teardown");
       solver.reset();
