@@ -136,6 +136,7 @@ class Engine {
   std::vector<std::size_t> arena_next_;
   std::unique_ptr<DeviceMemo> dmemo_;
   ops::CnnWork cnn_work_;  // encoder_variant = cnn scratch
+  bool whole_call_ = false;  // compute() runs a whole unmemoized operator call
 };
 
 }  // namespace mlrg

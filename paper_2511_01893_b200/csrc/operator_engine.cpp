@@ -162,6 +162,7 @@ std::int64_t Engine::slab0(int axis, OpId op) const {
 void Engine::compute(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,
                      std::int64_t start, std::int64_t extent) {
   const std::int64_t n0 = g_.n0, n2 = g_.n2, h = g_.h, w = g_.w, nr = shard_.nr();
+  if (op != OpId::fu2d_adj) usfft_.forget_class_sums();
   switch (op) {
     case OpId::fu1d:
       if (in_d) usfft_.fu1d(static_cast<const double2*>(in) + start * n0 * n2, static_cast<float2*>(out) + start * h * n2, extent);
@@ -180,6 +181,9 @@ void Engine::compute(OpId op, bool fused, const void* in, bool in_d, const float
         e.sub = d_hat;
         e.ld_sub = nr;
         e.k0_sub = start;
+        // the whole residual computed in one call: a following fu2d_adj of it
+        // reuses the class sums (solver.cpp: r = fu2d(v) - d, then fu2d_adj(r))
+        e.class_sums = whole_call_ && start == 0 && extent == nr;
       }
       usfft_.fu2d(static_cast<const float2*>(in), nr, start, extent, e);
       return;
@@ -202,7 +206,9 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
   const std::int64_t len = ishape.extent(axis);
   const bool use_memo = memoize && cfg_.memo_enabled;
   if (!use_memo) {
+    whole_call_ = true;
     compute(op, fused, in, in_d, d_hat, out, out_d, 0, len);
+    whole_call_ = false;
     return;
   }
   if (shard_.sharded() && (op == OpId::f2d || op == OpId::f2d_adj))

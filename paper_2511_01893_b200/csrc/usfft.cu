@@ -240,6 +240,8 @@ struct GatherOut {
   const float2* dot;
   long long ld_dot, k0_dot;
   int reduce;
+  float2* cls;           // non-null: the adjoint's class sums of the stored output ([C][KB])
+  const double2* cfac;   // the members' conjugate phases (k_fu2d_adj_prep's factors)
 };
 
 // ---- gather: one warp per target class ---------------------------------------------------
@@ -325,14 +327,18 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
     }
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    if (ph == 0 && eo.cls && kk >= nk) eo.cls[static_cast<long long>(s) * KB + kk] = make_float2(0.f, 0.f);
     if (ph == 0 && kk < nk) {
       // every detector sample of the class gets the shared sum times its own phase
+      double2 cs = make_double2(0.0, 0.0);
       for (int e = m_first[s], e1 = m_first[s + 1]; e < e1; ++e) {
         const int tq = m_tidx[e];
         const int t = tq / w, q = tq - t * w;
         double2 val = cmul(acc, m_fac[e]);
         if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
-        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = to_f(val);
+        const float2 stored = to_f(val);
+        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = stored;
+        if (eo.cls) cs = cadd(cs, cmul(to_d(stored), eo.cfac[e]));  // k_fu2d_adj_prep's sum, member order
         if (eo.reduce) {
           red[0] += val.x * val.x + val.y * val.y;
           if (eo.dot) {
@@ -341,6 +347,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
           }
         }
       }
+      if (eo.cls) eo.cls[static_cast<long long>(s) * KB + kk] = to_f(cs);
     }
   }
   if (eo.reduce) {
@@ -792,6 +799,7 @@ struct Usfft::Tables {
   DeviceBuffer<double> t_w1, t_w2;  // [C][W]
   DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint class values
+  DeviceBuffer<float2> cls;         // class sums left by a class_sums fu2d, [batch][C][KB]
   // fu2d runs its row batches on two streams (the second set of grids and
   // partial slots belongs to the side stream) so one batch's gather overlaps the
   // next batch's FFT passes
@@ -1212,6 +1220,16 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const int ggrid = (t.nclass + per_cta - 1) / per_cta;
   auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
   Tables& tm = *t_;
+  // class sums for a following fu2d_adj of this output (memo skip flags would
+  // leave batches uncomputed: not with them)
+  const bool cls = epi.class_sums && epi.out && !skip_ && nk > 0;
+  cls_src_ = cls ? epi.out : nullptr;
+  if (cls) {
+    tm.cls.resize(static_cast<std::size_t>((nk + KB - 1) / KB) * static_cast<std::size_t>(t.nclass) * KB);
+    cls_ld_ = epi.ld_out;
+    cls_k0_ = epi.k0_out;
+    cls_nk_ = nk;
+  }
   const bool pipe = nk > KB && pipelined();
   if (pipe) {
     ensure_side();
@@ -1256,7 +1274,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     }
     prof::end("k_fu2d_cols", s);
     GatherOut eo{epi.out, epi.ld_out, epi.k0_out + b, epi.sub, epi.ld_sub, epi.k0_sub + b,
-                 epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0};
+                 epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0,
+                 cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : nullptr, t.m_cfac.get()};
     prof::begin("k_fu2d_gather", s);
     // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
     gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(G, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
@@ -1279,6 +1298,9 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
   const Tables& t = *t_;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
   Tables& tm = *t_;
+  // p is exactly the output a class_sums fu2d just produced: its class sums replace the prep pass
+  const bool use_cls = cls_src_ && p == cls_src_ && ld == cls_ld_ && k0 == cls_k0_ && nk == cls_nk_ && !skip_;
+  cls_src_ = nullptr;
   const bool pipe = nk > KB && pipelined();  // row batches alternate between two streams, as in fu2d
   if (pipe) {
     ensure_side();
@@ -1298,16 +1320,18 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     cudaStream_t s = alt ? tm.side : stream_;
     float2* S = alt ? tm.S2.get() : t.S.get();
     float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
-    float2* val = alt ? tm.val2.get() : t.val.get();
+    float2* val = use_cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : alt ? tm.val2.get() : t.val.get();
     double2* partial = alt ? tm.partial2.get() : t.partial.get();
     int* split_cnt = alt ? tm.split_cnt2.get() : tm.split_cnt.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
+    if (!use_cls) {
     prof::begin("k_fu2d_adj_prep", s);
     k_fu2d_adj_prep<<<static_cast<unsigned>((t.nclass + 15) / 16), 256, 0, s>>>(
         p, ld, k0 + b, nb, t.nclass, static_cast<int>(g_.w), t.m_first.get(), t.m_tidx.get(), t.m_cfac.get(), val,
         sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_prep");
     prof::end("k_fu2d_adj_prep", s);
+    }
     prof::begin("k_fu2d_adj_spread", s);
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
     spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
@@ -1356,6 +1380,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
 }
 
 void Usfft::f2d(const float2* p, float2* out, std::int64_t count, bool adjoint) {
+  cls_src_ = nullptr;
   if (count <= 0) return;
   Tables& t = *t_;
   const std::int64_t h = g_.h, w = g_.w;

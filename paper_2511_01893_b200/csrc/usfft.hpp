@@ -32,6 +32,10 @@ struct Fu2dEpilogue {
   const float2* dot = nullptr;
   std::int64_t ld_dot = 0, k0_dot = 0;
   bool reduce = false;
+  /// Also leave the adjoint's class sums of the (rounded) output in the
+  /// operator, so a following fu2d_adj of exactly this output skips its
+  /// k_fu2d_adj_prep pass (the solver's r = fu2d(v) - d, then fu2d_adj(r)).
+  bool class_sums = false;
 };
 
 /// Sharded output of fu1d / fu2d_adj (the fused all-to-all):
@@ -84,6 +88,8 @@ class Usfft {
   /// Device-side memo: per-16-slab skip flags (a hit slab's CTAs exit at entry)
   /// for the next calls; nullptr clears.
   void set_skip(const unsigned char* flags) { skip_ = flags; }
+  /// Drops the class sums a class_sums fu2d left (the output may change next).
+  void forget_class_sums() { cls_src_ = nullptr; }
   int reduce_grid() const;  // CTAs of an elementwise reduction kernel
 
  private:
@@ -99,6 +105,9 @@ class Usfft {
   Tables* t_;
   Partials partials_;
   const unsigned char* skip_ = nullptr;
+  // class sums of the last class_sums fu2d: its output array and row range
+  const float2* cls_src_ = nullptr;
+  std::int64_t cls_ld_ = 0, cls_k0_ = 0, cls_nk_ = 0;
 };
 
 }  // namespace mlrg
