@@ -35,12 +35,12 @@ METRIC = "ADMM-FFT iterations/sec at N^3 volume"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
 # `ncu --set full` captures (profiles/), filled in per round
 TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (`ncu --set full`, one launch, cold cache)
-    "k_fu2d_gather": 42855680 + 786944, "k_fu2d_adj_spread": 10866432 + 49152,
+    "k_fu2d_gather": 43895296 + 1252352, "k_fu2d_adj_spread": 10866432 + 49152,
     "k_fu2d_cols": 16817920 + 742656, "k_fu1d": 268511488 + 109370368,
 }
 # the same captures' per-launch durations (us): ncu serialises launches, while the bench
 # overlaps fu2d row batches on two streams (live durations include the sharing)
-SERIAL_US: dict = {"k_fu2d_gather": 53.63, "k_fu2d_adj_spread": 65.54, "k_fu2d_cols": 27.04, "k_fu2d_rows": 19.46,
+SERIAL_US: dict = {"k_fu2d_gather": 56.12, "k_fu2d_adj_spread": 65.54, "k_fu2d_cols": 27.04, "k_fu2d_rows": 19.46,
                    "k_fu1d": 324.99, "k_fu1d_adj": 519.42, "k_fu2d_adj_cols": 27.17}
 
 
@@ -155,7 +155,7 @@ HBM_VOLUMES_PER_ITER = {
 # l1tex__throughput (pct of peak) of the committed ncu captures: the shared-memory FFT
 # passes work on L2-resident grids and are bound by the L1/shared pipe, not HBM
 L1TEX_PCT = {"k_fu2d_rows": 61.2, "k_fu2d_cols": 58.8, "k_fu2d_adj_cols": 54.7, "k_fu1d": 76.0, "k_fu1d_adj": 77.3,
-             "k_fu2d_adj_spread": 86.6, "k_fu2d_gather": 52.7}
+             "k_fu2d_adj_spread": 86.6, "k_fu2d_gather": 50.0}
 
 
 def local_share(n, world, rank):

@@ -1,10 +1,7 @@
-timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_all.log 2>&1; tail -2 gpurun_out/gpu_all.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench rc=$?
 P="ncu --profile-from-start off --clock-control none"
 timeout 600 $P --metrics gpu__time_duration.sum --csv --log-file gpurun_out/r1_launches_step256.csv python scripts/profile_step.py --n 256 > /dev/null 2>&1
 timeout 600 $P --metrics gpu__time_duration.sum --csv --log-file gpurun_out/r1_launches_step256_memo.csv python scripts/profile_step.py --n 256 --memo local --warmup 3 > /dev/null 2>&1
-timeout 600 $P --set full --import-source on -k regex:k_fu2d_cols -c 1 -o gpurun_out/r1_k_fu2d_cols python scripts/profile_step.py --n 256 > /dev/null 2>&1
-timeout 600 $P --set full --import-source on -k regex:k_fu2d_rows -c 1 -o gpurun_out/r1_k_fu2d_rows python scripts/profile_step.py --n 256 > /dev/null 2>&1
-timeout 600 $P --set full --import-source on -k regex:k_fu2d_adj_cols -c 1 -o gpurun_out/r1_k_fu2d_adj_cols python scripts/profile_step.py --n 256 > /dev/null 2>&1
-ls gpurun_out/r1_k_fu2d_cols.ncu-rep gpurun_out/r1_k_fu2d_rows.ncu-rep
+timeout 600 $P --set full --import-source on -k regex:k_fu2d_gather -c 1 -o gpurun_out/r1_k_fu2d_gather python scripts/profile_step.py --n 256 > /dev/null 2>&1
+ls gpurun_out/r1_k_fu2d_gather.ncu-rep
