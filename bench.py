@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--n-theta", type=int, default=None)
+    ap.add_argument("--kernel", choices=["es", "gaussian"], default="es")
     ap.add_argument("--no-memo-run", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -115,9 +116,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+KERNEL = "es"
+
+
 def config_text(n, nt, memo, n_outer=1000000, offload="off"):
     return (f"n1={n}\nn0={n}\nn2={n}\nn_theta={nt}\nh={n}\nw={n}\nn_outer={n_outer}\n"
-            f"memoization={memo}\nnudft_path=gridding\noffload={offload}\n")
+            f"memoization={memo}\nnudft_path=gridding\noffload={offload}\ngridding_kernel={KERNEL}\n")
 
 
 def algorithmic(n, nt, kernel):
@@ -215,6 +219,8 @@ def iteration_work(n, nt):
 
 def main():
     args = parse()
+    global KERNEL
+    KERNEL = args.kernel
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

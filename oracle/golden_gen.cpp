@@ -7,6 +7,8 @@
 //   golden_gen recon  <dir> N n_theta n_outer memo path [workers]
 //   golden_gen encoder <dir>                           P prefix + keys
 //   golden_gen store  <dir>                            MemoStore KATs
+//   golden_gen data   <dir> N n_theta workers random   d (+ phantom) of a large case
+//   golden_gen recon_big <dir> N n_theta n_outer memo workers random samples
 //
 // Inputs that feed a reconstruction are rounded to complex64 first so that
 // the fp32 device path and the f64 reference see bit-identical data.
@@ -18,7 +20,9 @@
 #include <random>
 #include <sstream>
 #include <string>
+#include <unordered_set>
 #include <vector>
+#include <algorithm>
 
 #include "mlr/admm.hpp"
 #include "mlr/config.hpp"
@@ -213,6 +217,141 @@ int cmd_recon(const std::string& dir, std::int64_t n, std::int64_t nt, int n_out
     save_npy(dir + "/keys.npy", keys.data(), {nk, static_cast<std::int64_t>(rc.encoder.key_dim)});
     save_npy(dir + "/key_meta.npy", key_meta.data(), {nk, 3});
     save_npy(dir + "/in_norms.npy", in_norms.data(), {nk});
+    const mlr::MemoCounterSnapshot c = client->counters();
+    std::ostringstream cs;
+    cs << "lookups=" << c.lookups << "\ncache_hits=" << c.cache_hits
+       << "\nremote_hits=" << c.remote_hits << "\nmisses=" << c.misses
+       << "\ncache_comparisons=" << c.cache_comparisons << "\ncache_probes=" << c.cache_probes
+       << "\nbatches_sent=" << c.batches_sent << "\ninserts_enqueued=" << c.inserts_enqueued
+       << "\ninserts_sent=" << c.inserts_sent << "\ninserts_dropped=" << c.inserts_dropped
+       << "\n";
+    save_text(dir + "/counters.txt", cs.str());
+  }
+  return 0;
+}
+
+// The reconstruction input of the large cases: phantom "blocks" seed 1 and
+// d = forward_L(phantom) through the reference's OperatorEngine with `workers`
+// threads (scalerun.hpp:55-60: bitwise identical to the unchunked operator),
+// both rounded to complex64 like cmd_recon. `random` replaces d by uniform
+// values in [-1, 1) from mt19937_64(seed 2511) (random_array), for sizes whose
+// dense f2d_adj projector (operators.cpp:39-74) is too slow to rerun.
+struct BigInput {
+  mlr::Volume phantom;
+  mlr::ProjectionSet d;
+};
+
+BigInput big_input(const mlr::Geometry& geom, int workers, bool random) {
+  BigInput in{round_c64(mlr::make_phantom(geom.volume_shape(), mlr::PhantomKind::blocks, 1)), {}};
+  if (random) {
+    std::mt19937_64 rng(2511);
+    in.d = random_array(geom.projection_shape(), mlr::Domain::space, rng);
+    return in;
+  }
+  mlr::EngineConfig ecfg;
+  ecfg.path = mlr::NudftPath::gridding;
+  ecfg.workers = workers;
+  mlr::OperatorEngine eng(geom, ecfg);
+  in.d = round_c64(eng.f2d_adj(eng.fu2d(eng.fu1d(in.phantom, false), false), false));
+  return in;
+}
+
+mlr::RunConfig big_config(std::int64_t n, std::int64_t nt, int n_outer, const std::string& memo, int workers) {
+  mlr::RunConfig rc;
+  for (const char* k : {"n1", "n0", "n2", "h", "w"}) rc.set(k, std::to_string(n));
+  rc.set("n_theta", std::to_string(nt));
+  rc.set("n_outer", std::to_string(n_outer));
+  rc.set("memoization", memo);
+  rc.set("nudft_path", "gridding");
+  rc.set("workers", std::to_string(workers));
+  rc.validate();
+  return rc;
+}
+
+// golden_gen data <dir> N n_theta workers random: writes data.npy (complex64)
+// and phantom.npy. The GPU parity tests run this on the box to regenerate the
+// exact d of a large fixture instead of committing hundreds of MB.
+int cmd_data(const std::string& dir, std::int64_t n, std::int64_t nt, int workers, bool random) {
+  const mlr::RunConfig rc = big_config(n, nt, 1, "off", workers);
+  const BigInput in = big_input(rc.make_geometry(), workers, random);
+  save_c64(dir + "/phantom.npy", in.phantom);
+  save_c64(dir + "/data.npy", in.d);
+  return 0;
+}
+
+// Compact reconstruction fixture for sizes whose full arrays cannot be
+// committed (configs[1] 256^3 and the configs[2] 512^3 prefix): the CSV report,
+// the audit log and counters, ||u||, a checksum of d, and u at `samples`
+// voxel indices drawn from mt19937_64(seed 4242) without replacement
+// (Floyd's algorithm, sorted), so the test's rel-L2 on the sample estimates the
+// full-volume rel-L2 with ~1/sqrt(samples) relative spread.
+int cmd_recon_big(const std::string& dir, std::int64_t n, std::int64_t nt, int n_outer,
+                  const std::string& memo, int workers, bool random, std::int64_t samples) {
+  const mlr::RunConfig rc = big_config(n, nt, n_outer, memo, workers);
+  const mlr::Geometry geom = rc.make_geometry();
+  const BigInput in = big_input(geom, workers, random);
+  mlr::EngineConfig ecfg = rc.engine;
+  ecfg.memo_enabled = rc.admm.memoization != mlr::MemoMode::off;
+  std::shared_ptr<mlr::Encoder> enc;
+  std::shared_ptr<mlr::MemoClient> client;
+  if (ecfg.memo_enabled) {
+    mlr::MemoClientConfig mcfg = rc.memo;
+    mcfg.endpoint.clear();
+    client = std::make_shared<mlr::MemoClient>(mcfg);
+    enc = std::make_shared<mlr::Encoder>(rc.encoder);
+  }
+  mlr::OperatorEngine eng(geom, ecfg, enc, client);
+  mlr::ReconResult res = mlr::reconstruct(in.d, geom, rc.admm, eng, random ? nullptr : &in.phantom);
+  const std::int64_t total = res.u.size();
+  std::vector<std::int64_t> idx;
+  {
+    std::mt19937_64 rng(4242);
+    std::vector<std::int64_t> pick;
+    std::unordered_set<std::int64_t> seen;
+    for (std::int64_t j = total - samples; j < total; ++j) {
+      const std::int64_t t = static_cast<std::int64_t>(rng() % static_cast<std::uint64_t>(j + 1));
+      if (seen.insert(t).second) pick.push_back(t);
+      else { seen.insert(j); pick.push_back(j); }
+    }
+    std::sort(pick.begin(), pick.end());
+    idx = pick;
+  }
+  std::vector<std::complex<float>> us(idx.size());
+  for (std::size_t i = 0; i < idx.size(); ++i) {
+    const cplx v = res.u.data()[idx[i]];
+    us[i] = std::complex<float>(static_cast<float>(v.real()), static_cast<float>(v.imag()));
+  }
+  save_npy(dir + "/u_idx.npy", idx.data(), {static_cast<std::int64_t>(idx.size())});
+  save_npy(dir + "/u_sample.npy", us.data(), {static_cast<std::int64_t>(us.size())});
+  const double unorm = mlr::norm2(res.u), dnorm = mlr::norm2(in.d);
+  save_npy(dir + "/u_norm.npy", &unorm, {1});
+  save_npy(dir + "/d_norm.npy", &dnorm, {1});
+  std::vector<std::complex<float>> dfirst(64);
+  const std::size_t stride = static_cast<std::size_t>(in.d.size()) / dfirst.size();
+  for (std::size_t i = 0; i < dfirst.size(); ++i)
+    dfirst[i] = std::complex<float>(static_cast<float>(in.d.data()[i * stride].real()),
+                                    static_cast<float>(in.d.data()[i * stride].imag()));
+  save_npy(dir + "/d_probe.npy", dfirst.data(), {64});
+  save_text(dir + "/report.csv", res.report.csv());
+  save_text(dir + "/config.txt", rc.str());
+  std::ostringstream ab;
+  ab << (res.report.aborted ? 1 : 0) << "\n" << res.report.abort_reason << "\n"
+     << "random_data=" << (random ? 1 : 0) << "\n";
+  save_text(dir + "/aborted.txt", ab.str());
+  if (ecfg.memo_enabled) {
+    const std::vector<mlr::ChunkAudit> audit = eng.audit_log();
+    std::vector<std::int32_t> a_int;
+    std::vector<float> a_cs;
+    for (const auto& e : audit) {
+      a_int.push_back(e.iteration);
+      a_int.push_back(static_cast<std::int32_t>(e.op));
+      a_int.push_back(static_cast<std::int32_t>(e.location.index));
+      a_int.push_back(static_cast<std::int32_t>(e.outcome));
+      a_cs.push_back(e.cs);
+    }
+    const std::int64_t na = static_cast<std::int64_t>(audit.size());
+    save_npy(dir + "/audit_int.npy", a_int.data(), {na, 4});
+    save_npy(dir + "/audit_cs.npy", a_cs.data(), {na});
     const mlr::MemoCounterSnapshot c = client->counters();
     std::ostringstream cs;
     cs << "lookups=" << c.lookups << "\ncache_hits=" << c.cache_hits
@@ -426,6 +565,11 @@ int main(int argc, char** argv) {
     if (cmd == "trace" && argc == 5) return cmd_trace(I(3), static_cast<int>(I(4)));
     if (cmd == "sens" && argc == 7) return cmd_sens(I(3), static_cast<int>(I(4)), std::stod(argv[5]), argv[6]);
     if (cmd == "store") return cmd_store(dir);
+    if (cmd == "data" && argc == 7)
+      return cmd_data(dir, I(3), I(4), static_cast<int>(I(5)), I(6) != 0);
+    if (cmd == "recon_big" && argc == 10)
+      return cmd_recon_big(dir, I(3), I(4), static_cast<int>(I(5)), argv[6], static_cast<int>(I(7)),
+                           I(8) != 0, I(9));
     std::fprintf(stderr, "bad arguments\n");
     return 2;
   } catch (const std::exception& e) {

@@ -44,6 +44,16 @@ CASES = {
     # BASELINE configs[0] exactly as-is: 64^3, 64 angles, 10 iterations, memo on,
     # default (direct) NUDFT path, 1 worker. ~5 minutes of CPU.
     "recon_cfg1_memo_direct": ["recon", "64", "64", "10", "local", "direct", "1"],
+    # BASELINE configs[1] (256^3, 256 angles) as compact fixtures (golden_gen recon_big:
+    # report, audit, counters, ||u|| and u at 2^18 seeded voxel indices; the tests
+    # regenerate d with `golden_gen data` on the box). Memo off: a 3-iteration prefix
+    # (~6 min on 8 cores); memo on: 10 iterations, which publishes > 1024 keys so the
+    # store trains its nlist-64 IVF index mid-run (~20 GB of host RAM).
+    "recon_c256_off_grid": ["recon_big", "256", "256", "3", "off", "8", "0", "262144"],
+    "recon_c256_memo_grid": ["recon_big", "256", "256", "10", "local", "8", "0", "262144"],
+    # configs[2] (512^3, 512 angles) CPU prefix of 2 iterations, memo off, on seeded
+    # random data (the reference's dense projector is O(N^4) at this size).
+    "recon_c512_off_rand": ["recon_big", "512", "512", "2", "off", "8", "1", "262144"],
 }
 
 TEXT_SUFFIXES = (".txt", ".csv")

@@ -35,6 +35,15 @@ constexpr int KB = Usfft::kRowBatch;
 
 // Device-side memo (memo_gpu.hpp): a slab whose lookup hit skips its CTAs.
 // Unit u of a launch belongs to slab (base + u) / div.
+// Grid element of the fu2d forward gather input and the adjoint spread output:
+// complex64 for the es kernel; complex128 for the reference's Gaussian plan,
+// whose deconvolution (up to e^pi = 23x per dimension, nufft.cpp:66-70) would
+// otherwise amplify the complex64 rounding of exactly these two grids into the
+// operator outputs (~4e-7 relative, 17x the output rounding, at 64^3).
+template <class TG> __device__ __forceinline__ TG to_g(double2 x);
+template <> __device__ __forceinline__ float2 to_g<float2>(double2 x) { return to_f(x); }
+template <> __device__ __forceinline__ double2 to_g<double2>(double2 x) { return x; }
+
 struct Skip {
   const unsigned char* f = nullptr;
   int base = 0, div = 1;
@@ -214,10 +223,10 @@ __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_rows(const floa
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
-template <bool ZP>
+template <bool ZP, class TG>
 __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
-                                                   float2* __restrict__ G, Skip sk) {
+                                                   TG* __restrict__ G, Skip sk) {
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_cols(const floa
     const double2 x = to_d(S[(static_cast<long long>(ok ? i : 0) * m2 + c) * KB + ks + kk]);
     return ok ? x : make_double2(0.0, 0.0);
   };
-  auto store = [&](int r, int kk, double2 x) { G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_f(x); };
+  auto store = [&](int r, int kk, double2 x) { G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_g<TG>(x); };
   fft_stockham<+1, true, true, ZP>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
@@ -270,9 +279,10 @@ int gather_per_cta() {
   return v;
 }
 
-template <int W>
-__global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_gather(
-    const float2* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
+// (the 24-tap Gaussian windows keep a whole window row of loads in flight: 2 CTAs/SM, 128 registers)
+template <int W, class TG>
+__global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? MLRG_GATHER_MINB : 2) k_fu2d_gather(
+    const TG* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
     const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
     const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
     int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
@@ -298,19 +308,19 @@ __global__ void __launch_bounds__(32 * kGatherWarps, MLRG_GATHER_MINB) k_fu2d_ga
     double2 acc = make_double2(0.0, 0.0);
     // rows are software-pipelined one ahead: the next row's W/2 loads are in
     // flight while the current row is summed
-    float2 nxt[WH];
+    TG nxt[WH];
     {
-      const float2* gr = G + (r0 & mask1) * row_stride;
+      const TG* gr = G + (r0 & mask1) * row_stride;
 #pragma unroll
       for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
     }
 #pragma unroll
     for (int a = 0; a < W; ++a) {
-      float2 v[WH];
+      TG v[WH];
 #pragma unroll
       for (int j = 0; j < WH; ++j) v[j] = nxt[j];
       if (a + 1 < W) {
-        const float2* gr = G + ((r0 + a + 1) & mask1) * row_stride;
+        const TG* gr = G + ((r0 + a + 1) & mask1) * row_stride;
 #pragma unroll
         for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
       }
@@ -447,12 +457,12 @@ __device__ __forceinline__ void stage_spread_chunk(SpreadShared& sh, int pair, i
   cp_async_commit();
 }
 
-template <int W>
+template <int W, class TG>
 __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restrict__ val, int logm1, int logm2,
                                                          int nitems, const SpreadItem* __restrict__ items,
                                                          const int* __restrict__ patch_t, const int* __restrict__ r0,
                                                          const int* __restrict__ c0, const double* __restrict__ w1,
-                                                         const double* __restrict__ w2, float2* __restrict__ G,
+                                                         const double* __restrict__ w2, TG* __restrict__ G,
                                                          double2* __restrict__ partial, const int4* __restrict__ split,
                                                          int* __restrict__ split_cnt, Skip sk) {
   if (skipped(sk, 0)) return;
@@ -523,11 +533,17 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
     }
     if (half == 0 && lane == 0) split_cnt[it.grp] = 0;  // ready for the next launch
   }
-  float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB + half * KH);
+  if constexpr (std::is_same_v<TG, double2>) {
+    double2* gp = G + (static_cast<long long>(r) * m2 + c) * KB + half * KH;
 #pragma unroll
-  for (int q = 0; q < KH / 2; ++q) {
-    const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
-    gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    for (int kk = 0; kk < KH; ++kk) gp[kk] = acc[kk];
+  } else {
+    float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB + half * KH);
+#pragma unroll
+    for (int q = 0; q < KH / 2; ++q) {
+      const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
+      gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
   }
 }
 
@@ -555,7 +571,8 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
-__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_adj_cols(const float2* __restrict__ G, int n1, int logm1, int center1,
+template <class TG>
+__global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_adj_cols(const TG* __restrict__ G, int n1, int logm1, int center1,
                                                        int logm2, int ks_n, const double2* __restrict__ tw1,
                                                        float2* __restrict__ S, Skip sk) {
   if (skipped(sk, 0)) return;
@@ -808,6 +825,7 @@ struct Usfft::Tables {
   DeviceBuffer<int> split_cnt2;
   // four-step column passes: M = A * B, A = 2^logA
   bool cols4 = false;
+  bool wide = false;  // Gd holds complex128 (the Gaussian plan's grids, see to_g)
   int logA = 0;
   DeviceBuffer<double2> a_tw, b_tw;
   cudaStream_t side = nullptr;
@@ -1075,8 +1093,9 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     t.b_tw.upload(twiddles(std::int64_t{1} << (px.logm - t.logA)), stream_);
   }
   prof::host_mark("host:usfft_patches");
+  t.wide = kernel_ == GridKernel::gaussian && !t.cols4;
   t.S.resize(static_cast<std::size_t>(px.m * py.m * KB));
-  t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB));
+  t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB) * (t.wide ? 2 : 1));
   t.val.resize(C * KB);
 
   // ---- f2d (operators.cpp:20-74) ----
@@ -1122,11 +1141,15 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     allow_big_smem(k_fu2d_rows<true, false>);
     allow_big_smem(k_fu2d_rows<false, true>);
     allow_big_smem(k_fu2d_rows<true, true>);
-    allow_big_smem(k_fu2d_adj_spread<kEsTaps>);
-    allow_big_smem(k_fu2d_adj_spread<kTaps>);
-    allow_big_smem(k_fu2d_cols<false>);
-    allow_big_smem(k_fu2d_cols<true>);
-    allow_big_smem(k_fu2d_adj_cols);
+    allow_big_smem(k_fu2d_adj_spread<kEsTaps, float2>);
+    allow_big_smem(k_fu2d_adj_spread<kTaps, float2>);
+    allow_big_smem(k_fu2d_adj_spread<kTaps, double2>);
+    allow_big_smem(k_fu2d_cols<false, float2>);
+    allow_big_smem(k_fu2d_cols<true, float2>);
+    allow_big_smem(k_fu2d_cols<false, double2>);
+    allow_big_smem(k_fu2d_cols<true, double2>);
+    allow_big_smem(k_fu2d_adj_cols<float2>);
+    allow_big_smem(k_fu2d_adj_cols<double2>);
     allow_big_smem(k_cols4_pass1<+1, true, true>);
     allow_big_smem(k_cols4_pass1<-1, false, true>);
     allow_big_smem(k_cols4_pass2<+1, false, true>);
@@ -1218,7 +1241,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
   const int per_cta = gather_per_cta();
   const int ggrid = (t.nclass + per_cta - 1) / per_cta;
-  auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps> : k_fu2d_gather<kTaps>;
+  auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps, float2> : k_fu2d_gather<kTaps, float2>;
   Tables& tm = *t_;
   // class sums for a following fu2d_adj of this output (memo skip flags would
   // leave batches uncomputed: not with them)
@@ -1266,8 +1289,14 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       G = S;
+    } else if (t.wide) {
+      (zero_padded(t.px) ? k_fu2d_cols<true, double2> : k_fu2d_cols<false, double2>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+                    static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(),
+          reinterpret_cast<double2*>(Gd), sk);
+      MLRG_LAUNCH_CHECK("k_fu2d_cols");
     } else {
-      (zero_padded(t.px) ? k_fu2d_cols<true> : k_fu2d_cols<false>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+      (zero_padded(t.px) ? k_fu2d_cols<true, float2> : k_fu2d_cols<false, float2>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                     static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_fu2d_cols");
@@ -1278,11 +1307,15 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
                  cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : nullptr, t.m_cfac.get()};
     prof::begin("k_fu2d_gather", s);
     // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
-    gather<<<ggrid, 32 * kGatherWarps, 0, s>>>(G, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
+    auto launch_gather = [&](auto kern, auto grid_ptr) {
+      kern<<<ggrid, 32 * kGatherWarps, 0, s>>>(grid_ptr, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
                                                t.t_r0.get(), t.t_c0.get(), t.t_w1.get(), t.t_w2.get(),
                                                t.m_first.get(), t.m_tidx.get(), t.m_fac.get(), eo, per_cta,
                                                partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0,
                                                sk);
+    };
+    if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G));
+    else launch_gather(gather, G);
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", s);
   }
@@ -1333,11 +1366,16 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     prof::end("k_fu2d_adj_prep", s);
     }
     prof::begin("k_fu2d_adj_spread", s);
-    auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps> : k_fu2d_adj_spread<kTaps>;
-    spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
-                                                               t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
-                                                               t.t_w1.get(), t.t_w2.get(), Gd, partial, t.split.get(),
-                                                               split_cnt, sk);
+    auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps, float2> : k_fu2d_adj_spread<kTaps, float2>;
+    if (t.wide)
+      k_fu2d_adj_spread<kTaps, double2><<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(
+          val, t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
+          t.t_w1.get(), t.t_w2.get(), reinterpret_cast<double2*>(Gd), partial, t.split.get(), split_cnt, sk);
+    else
+      spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
+                                                                 t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
+                                                                 t.t_w1.get(), t.t_w2.get(), Gd, partial, t.split.get(),
+                                                                 split_cnt, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     prof::end("k_fu2d_adj_spread", s);
     prof::begin("k_fu2d_adj_cols", s);
@@ -1353,9 +1391,15 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       Sc = Gd;
+    } else if (t.wide) {
+      k_fu2d_adj_cols<double2><<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+                                 static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+          reinterpret_cast<const double2*>(Gd), static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center),
+          t.py.logm, ks1, t.x_tw.get(), S, sk);
+      MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     } else {
-      k_fu2d_adj_cols<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
-                        static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
+      k_fu2d_adj_cols<float2><<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
+                                static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_fu2d_adj_cols");
     }

@@ -32,11 +32,12 @@ def ref_config(z):
                                               ("recon_c32_off_grid", "off", "es"),
                                               ("recon_c64_off_grid", "off", "es"),
                                               ("recon_cfg1_memo_direct", "local", "es"),
-                                              # the reference's own 24-tap kernel: its deconvolution
-                                              # amplifies the complex64 grid rounding 23x per dimension
-                                              # (es: 4.8x), so larger cases sit near the 1e-4 bound
+                                              # the reference's own 24-tap Gaussian plan (nufft.cpp:48-103)
+                                              ("recon_c16_memo_grid", "local", "gaussian"),
                                               ("recon_c32_memo_grid", "local", "gaussian"),
                                               ("recon_c32_off_grid", "off", "gaussian"),
+                                              ("recon_c64_off_grid", "off", "gaussian"),
+                                              ("recon_cfg1_memo_direct", "local", "gaussian"),
                                               # pipeline = baseline (admm.cpp:122-138): six memoizable
                                               # operators per inner step, memoized f2d / f2d_adj
                                               ("recon_c16_baseline_memo_grid", "local", "es"),
