@@ -89,6 +89,10 @@ int64_t mlrg_recon_audit(const mlrg_recon* r, int32_t* meta4, float* cs, int64_t
  * misses, cache_comparisons, cache_probes, timeouts, batches_sent,
  * inserts_enqueued, inserts_sent, inserts_dropped. */
 int mlrg_recon_counters(const mlrg_recon* r, uint64_t out[11]);
+/* Memo value tiers (cold_tier.hpp): out = {HBM ring arena bytes, values
+ * spilled to pinned host memory, bytes spilled}. B200 extension: the
+ * reference's store is one unbounded host array (memostore.cpp:112-120). */
+int mlrg_recon_tiers(const mlrg_recon* r, uint64_t out[3]);
 void mlrg_recon_free(mlrg_recon* r);
 
 /* ---- steppable device solver (the outer loop of admm.cpp:208-272) ----
@@ -101,6 +105,7 @@ int mlrg_solver_step(mlrg_solver* s, int* aborted);
 int mlrg_solver_volume(mlrg_solver* s, void* u_out);
 char* mlrg_solver_csv(const mlrg_solver* s);
 int mlrg_solver_counters(const mlrg_solver* s, uint64_t out[11]);
+int mlrg_solver_tiers(const mlrg_solver* s, uint64_t out[3]);
 int64_t mlrg_solver_audit(const mlrg_solver* s, int32_t* meta4, float* cs, int64_t cap);
 void mlrg_solver_free(mlrg_solver* s);
 

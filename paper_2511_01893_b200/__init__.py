@@ -91,12 +91,14 @@ _SIGS = {
     "mlrg_recon_abort_reason": (_P, [_P]),
     "mlrg_recon_audit": (_I64, [_P, _P, _P, _I64]),
     "mlrg_recon_counters": (C.c_int, [_P, _P]),
+    "mlrg_recon_tiers": (C.c_int, [_P, _P]),
     "mlrg_recon_free": (None, [_P]),
     "mlrg_solver_new": (_P, [C.c_char_p, _P, _P, _P]),
     "mlrg_solver_step": (C.c_int, [_P, _P]),
     "mlrg_solver_volume": (C.c_int, [_P, _P]),
     "mlrg_solver_csv": (_P, [_P]),
     "mlrg_solver_counters": (C.c_int, [_P, _P]),
+    "mlrg_solver_tiers": (C.c_int, [_P, _P]),
     "mlrg_solver_audit": (_I64, [_P, _P, _P, _I64]),
     "mlrg_solver_free": (None, [_P]),
     "mlrg_solver_new_sharded": (_P, [C.c_char_p, _P, _P, _P, _P]),
@@ -439,6 +441,12 @@ class DeviceRecon:
         _gcheck(lib().mlrg_recon_counters(self._h, out.ctypes.data))
         return dict(zip(COUNTER_NAMES, (int(x) for x in out)))
 
+    def tiers(self) -> dict:
+        """Memo value tiers: HBM ring arena bytes, values / bytes spilled to pinned host."""
+        out = np.zeros(3, np.uint64)
+        _gcheck(lib().mlrg_recon_tiers(self._h, out.ctypes.data))
+        return dict(zip(("arena_bytes", "spilled_values", "spilled_bytes"), (int(x) for x in out)))
+
     def __del__(self):
         if getattr(self, "_h", None) and _LIB is not None:
             _LIB.mlrg_recon_free(self._h)
@@ -543,6 +551,11 @@ class Solver:
         out = np.zeros(11, np.uint64)
         _gcheck(lib().mlrg_solver_counters(self._h, out.ctypes.data))
         return dict(zip(COUNTER_NAMES, (int(x) for x in out)))
+
+    def tiers(self) -> dict:
+        out = np.zeros(3, np.uint64)
+        _gcheck(lib().mlrg_solver_tiers(self._h, out.ctypes.data))
+        return dict(zip(("arena_bytes", "spilled_values", "spilled_bytes"), (int(x) for x in out)))
 
     def audit(self):
         n = lib().mlrg_solver_audit(self._h, None, None, 0)

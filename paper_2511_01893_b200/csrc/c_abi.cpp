@@ -56,6 +56,7 @@ struct mlrg_recon {
   mlrg::ReconReport report;
   std::vector<mlrg::ChunkAudit> audit;
   mlrg::MemoCounters counters;
+  uint64_t tiers[3] = {0, 0, 0};
 };
 struct mlrg_solver {
   cudaStream_t own = nullptr;
@@ -124,25 +125,35 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   if (!ec.memo_enabled) return std::make_unique<mlrg::Engine>(g, ec, s, nullptr, nullptr, std::move(comm));
 
   auto store = std::make_shared<mlrg::MemoStore>();
-  // HBM for the values the solve can insert: n_outer x the per-iteration insert
-  // cap x the largest slab value (complex64), at most 45% of free HBM
+  // HBM for the values: a ring arena (cold_tier.hpp) sized for every value the
+  // solve can insert (n_outer windows of at most `window` values each, the
+  // largest slab each, complex64), capped at 45% of free HBM; older values
+  // spill to pinned host memory when the ring would wrap onto them.
+  // MLRG_MEMO_ARENA_BYTES overrides the size (tests force spills with it).
   const std::int64_t e = ec.chunk_extent;
   const std::int64_t slab = std::max({e * g.h * g.n2, e * g.n0 * g.n2, g.n_theta * e * g.w, g.n1 * e * g.n2});
+  const double slab_bytes = static_cast<double>((slab * static_cast<std::int64_t>(sizeof(float2)) + 255) & ~std::int64_t{255});
   std::size_t free_b = 0, total_b = 0;
   MLRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  double per_iter = static_cast<double>(rc.memo.insert_queue_cap);
+  // lookups per window: every memoizable call of an outer iteration (4 per
+  // inner step, 6 with pipeline = baseline) over this rank's slabs
+  const int calls = (rc.admm.pipeline == mlrg::Pipeline::baseline ? 6 : 4) * rc.admm.n_inner;
+  std::int64_t most = std::max((g.n1 + e - 1) / e, std::max((g.h + e - 1) / e, (g.n_theta + e - 1) / e));
   if (comm && comm->world() > 1) {  // a rank stores only its own slabs' values
     const mlrg::Shard sh = mlrg::Shard::make(g, e, comm);
-    std::int64_t most = 0;
+    most = 0;
     for (int r = 0; r < sh.world; ++r) {
       const auto& pl = sh.planes[static_cast<std::size_t>(r)];
       const auto& rw = sh.rows[static_cast<std::size_t>(r)];
       most = std::max({most, (pl.second - pl.first + e - 1) / e, (rw.second - rw.first + e - 1) / e});
     }
-    per_iter = std::min(per_iter, static_cast<double>(4 * rc.admm.n_inner * most));
   }
-  const double want = static_cast<double>(rc.admm.n_outer) * per_iter * static_cast<double>(slab) * sizeof(float2);
-  const std::size_t bytes = static_cast<std::size_t>(std::min(want, 0.45 * static_cast<double>(free_b)));
+  const std::int64_t window = std::min<std::int64_t>(static_cast<std::int64_t>(rc.memo.insert_queue_cap), calls * most);
+  ec.memo_window_inserts = static_cast<int>(std::max<std::int64_t>(window, 1));
+  const double floor_b = static_cast<double>(ec.memo_window_inserts + 1) * slab_bytes;
+  const double want = static_cast<double>(rc.admm.n_outer) * static_cast<double>(window) * slab_bytes;
+  std::size_t bytes = static_cast<std::size_t>(std::max(floor_b, std::min(want, 0.45 * static_cast<double>(free_b))));
+  if (const char* ov = std::getenv("MLRG_MEMO_ARENA_BYTES")) bytes = static_cast<std::size_t>(std::atoll(ov));
   // one GPU: the lookups run on the device (memo_gpu.hpp) unless the config needs
   // the host client (global cache, baseline pipeline's memoized f2d, other slab
   // sizes) or MLRG_DEVICE_MEMO=0 asks for it
@@ -153,8 +164,7 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
       std::int64_t{1} << 20,
       static_cast<std::int64_t>(rc.admm.n_outer) * static_cast<std::int64_t>(rc.memo.insert_queue_cap) +
           static_cast<std::int64_t>(rc.memo.insert_queue_cap) + 1);
-  if ((comm && comm->world() > 1) || ec.device_memo) ec.memo_arena_bytes = bytes;
-  else store->arena().reserve(bytes);
+  ec.memo_arena_bytes = bytes;
   auto client = std::make_shared<mlrg::MemoClient>(rc.memo, store);
   std::shared_ptr<mlrg::Encoder> enc;
   if (rc.encoder.variant == mlrg::EncoderConfig::Variant::cnn)  // capi.cpp:56-65: file, else seeded init
@@ -595,6 +605,13 @@ char* mlr_bench(const mlr_config* cfg) {  // capi.cpp:437-499 on the device engi
     const double ms_compute = timed([&] { plain.fu1d(u.get(), out.get()); });
     mlrg::EngineConfig on = rc.engine;
     on.memo_enabled = true;
+    {  // one fu1d call per window: a ring of one call's slabs + one
+      const std::int64_t e = on.chunk_extent;
+      const std::int64_t slab = std::max({e * g.h * g.n2, e * g.n0 * g.n2, g.n_theta * e * g.w, g.n1 * e * g.n2});
+      on.memo_window_inserts = static_cast<int>((std::max(g.n1, g.h) + e - 1) / e);
+      on.memo_arena_bytes = static_cast<std::size_t>(on.memo_window_inserts + 1) *
+                            mlrg::ValueRing::granule(static_cast<std::size_t>(slab) * sizeof(float2));
+    }
     auto store = std::make_shared<mlrg::MemoStore>();
     auto enc = std::make_shared<mlrg::Encoder>(rc.encoder.key_dim, rc.encoder.seed);
     auto c_miss = std::make_shared<mlrg::MemoClient>(rc.memo, store);
@@ -829,6 +846,9 @@ mlrg_recon* mlrg_reconstruct(const char* config_text, const void* d, const void*
                                   static_cast<const float2*>(reference), static_cast<float2*>(u_out));
     r->audit = eng->audit_log();
     if (eng->memo()) r->counters = eng->memo()->counters();
+    r->tiers[0] = eng->memo_arena_bytes();
+    r->tiers[1] = static_cast<uint64_t>(eng->spilled_values());
+    r->tiers[2] = eng->spilled_bytes();
     return r.release();
   });
 }
@@ -854,6 +874,12 @@ int mlrg_recon_counters(const mlrg_recon* r, uint64_t out[11]) {
   return guarded([&] {
     need(r && out, "null argument");
     fill_counters(r->counters, out);
+  });
+}
+int mlrg_recon_tiers(const mlrg_recon* r, uint64_t out[3]) {
+  return guarded([&] {
+    need(r && out, "null argument");
+    std::copy(r->tiers, r->tiers + 3, out);
   });
 }
 void mlrg_recon_free(mlrg_recon* r) { delete r; }
@@ -925,6 +951,15 @@ int mlrg_solver_counters(const mlrg_solver* s, uint64_t out[11]) {
   return guarded([&] {
     need(s && out, "null argument");
     fill_counters(s->eng->memo() ? s->eng->memo()->counters() : mlrg::MemoCounters{}, out);
+  });
+}
+
+int mlrg_solver_tiers(const mlrg_solver* s, uint64_t out[3]) {
+  return guarded([&] {
+    need(s && out, "null argument");
+    out[0] = s->eng->memo_arena_bytes();
+    out[1] = static_cast<uint64_t>(s->eng->spilled_values());
+    out[2] = s->eng->spilled_bytes();
   });
 }
 

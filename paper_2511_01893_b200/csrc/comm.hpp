@@ -34,6 +34,7 @@ class HostComm {
   HostComm& operator=(const HostComm&) = delete;
 
   int rank() const { return rank_; }
+  const std::string& name() const { return name_; }
   int world() const { return world_; }
 
   void barrier();

@@ -18,6 +18,7 @@
 #include "geometry.hpp"
 #include "memo.hpp"
 #include "cnn.hpp"
+#include "cold_tier.hpp"
 #include "memo_gpu.hpp"
 #include "shard.hpp"
 #include "usfft.hpp"
@@ -33,6 +34,7 @@ struct EngineConfig {  // scalerun.hpp:27-42
   std::size_t memo_arena_bytes = 0;    // HBM reserved for memo values (sharded: per rank)
   bool device_memo = false;            // lookups on the device (memo_gpu.hpp); set by the assembler
   std::int64_t memo_max_keys = 0;      // device key index capacity
+  int memo_window_inserts = 256;       // most values one flush window inserts (per rank when sharded)
 };
 
 struct ChunkAudit {  // scalerun.hpp:45-54
@@ -73,6 +75,10 @@ class Engine {
   /// iteration). No-op otherwise.
   void drain_memo_log();
   const std::vector<ChunkAudit>& audit_log() const { return audit_; }
+  /// Memo values spilled from the HBM ring to the cold tier so far (count, bytes).
+  std::int64_t spilled_values() const;
+  std::size_t spilled_bytes() const;
+  std::size_t memo_arena_bytes() const { return dmemo_ ? dmemo_->arena_bytes() : arena_cap_; }
 
   /// Sharded mode: the exchange targets (nullptr when unsharded).
   float2* mid() const { return mid_.get(); }
@@ -113,6 +119,7 @@ class Engine {
   void register_shapes();
   void exchange_fence();  // stream sync + barrier across ranks
   float2* value_slot(int owner, std::int64_t count);
+  void spill_values();  // host-path rings: free the next window's span (cold_tier.hpp)
 
   Geometry g_;
   EngineConfig cfg_;
@@ -130,10 +137,20 @@ class Engine {
   // sharded mode
   DeviceBuffer<float2> mid_, mid2_, stage1_, stage2_;
   std::unique_ptr<PeerMemory> mid_peers_, mid2_peers_;
+  // host-path memo values (the host client on one GPU, every sharded run): one
+  // HBM ring arena per rank, bookkeeping replicated on every rank, spills to
+  // the cold tier at flush
   DeviceBuffer<char> arena_;
   std::unique_ptr<PeerMemory> arena_peers_;
-  std::size_t arena_cap_ = 0;
-  std::vector<std::size_t> arena_next_;
+  std::size_t arena_cap_ = 0, window_bytes_ = 0;
+  std::vector<ValueRing> rings_;
+  struct Pending {
+    int owner;
+    std::size_t off, bytes;
+  };
+  std::vector<Pending> pending_;  // values allocated this window, in staging (= id) order
+  std::unique_ptr<ColdTier> cold_;
+  std::int64_t spilled_ = 0;
   std::unique_ptr<DeviceMemo> dmemo_;
   ops::CnnWork cnn_work_;  // encoder_variant = cnn scratch
   bool whole_call_ = false;  // compute() runs a whole unmemoized operator call

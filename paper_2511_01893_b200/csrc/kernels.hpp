@@ -79,6 +79,8 @@ void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s
 /// Fused rsp_update + multiplier update (admm.cpp:154-181):
 /// psi_new = shrink(grad u + lam*lc, thr); lam += rho_over_lam_scale * (grad u - psi_new).
 /// Partials [|grad u - psi_new|^2, |psi_new - psi_old|^2].
+/// Partial slots one rsp_multiplier launch writes.
+int rsp_multiplier_slots();
 int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
                    double rho_over_scale, double* partials, cudaStream_t s, const Halo& halo = {});
 

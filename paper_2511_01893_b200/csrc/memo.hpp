@@ -2,8 +2,8 @@
 // semantics. Keys (60 floats) and the index live on
 // the host — they are tiny and every decision needs double-precision ranking
 // identical to the reference — while the values (operator output slabs, MBs
-// each) live in a device-resident append-only arena in HBM and never cross
-// PCIe. Replaces:
+// each) live in HBM (the engine's ring arena; cold values in mapped pinned
+// host memory, cold_tier.hpp) and never round-trip through the host. Replaces:
 //   MemoStore   memostore.hpp:12-88, memostore.cpp:17-222
 //   MemoClient  memoclient.hpp:21-164, memoclient.cpp:148-350 (local transport)
 #pragma once
@@ -32,22 +32,6 @@ struct ValueRef {
   std::size_t bytes = 0;
 };
 
-/// Device arena for values: append-only bump allocation in 1 GiB chunks.
-class ValueArena {
- public:
-  explicit ValueArena(std::size_t chunk_bytes = std::size_t{1} << 30) : chunk_(chunk_bytes) {}
-  float2* alloc(std::int64_t count);
-  /// Maps `bytes` of HBM up front (one allocation) so the solve itself never
-  /// calls cudaMalloc (which maps and clears pages at ~30 ms/GiB on B200).
-  void reserve(std::size_t bytes);
-  std::size_t bytes_used() const { return used_; }
-
- private:
-  std::size_t chunk_;
-  std::vector<DeviceBuffer<char>> chunks_;
-  std::size_t offset_ = 0, used_ = 0;
-};
-
 struct IvfConfig {  // memostore.hpp:12-20
   int nlist = 64;
   int nprobe = 8;
@@ -73,14 +57,14 @@ class MemoStore {
   std::uint64_t insert(const std::vector<float>& key, ValueRef value);
   QueryOutcome query(const std::vector<float>& key, float tau, int nprobe = 0) const;
   const ValueRef& value(std::uint64_t id) const { return values_.at(static_cast<std::size_t>(id)); }
+  /// A value moved between tiers (cold_tier.hpp): same id, key and bytes.
+  void set_value_ptr(std::uint64_t id, const float2* dev) { values_.at(static_cast<std::size_t>(id)).dev = dev; }
   std::uint64_t key_count() const;
   bool trained() const { return trained_; }
   const std::vector<std::vector<float>>& centroids() const { return centroids_; }
   /// Member ids per IVF cluster (insertion order), for the device mirror.
   std::vector<std::vector<std::uint64_t>> cluster_ids() const;
   const IvfConfig& ivf() const { return cfg_; }
-  /// Device storage of the values; lives as long as the store.
-  ValueArena& arena() { return arena_; }
 
  private:
   struct Entry {
@@ -97,7 +81,6 @@ class MemoStore {
   std::vector<std::vector<float>> centroids_;
   std::vector<std::vector<Entry>> clusters_;
   std::vector<ValueRef> values_;
-  ValueArena arena_;
 };
 
 enum class MemoOutcome : std::uint8_t { miss = 0, remote_hit = 1, cache_hit = 2 };

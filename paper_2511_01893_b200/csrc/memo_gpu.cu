@@ -232,13 +232,16 @@ __global__ void __launch_bounds__(kStageThreads) k_memo_stage(StageArgs a) {
   }
   __syncthreads();
   if (c == 0) {  // memoclient.cpp:302-325: stage up to cap per flush window, in slab order
+    // the arena is a ring (cold_tier.hpp ValueRing::alloc): a value that would
+    // cross the end starts at 0; the host freed the span this window can fill
     long long nst = st[1], off = st[2], dropped = 0;
     int overflow = 0;
     for (int k = 0; k < a.n; ++k) {
       s_staged[k] = -1;
       if (!s_miss[k]) continue;
       if (nst < a.cap) {
-        const bool fits = off + s_bytes[k] <= a.arena_bytes;
+        if (off + s_bytes[k] > a.arena_bytes) off = 0;
+        const bool fits = s_bytes[k] <= a.arena_bytes;
         s_staged[k] = 1;
         s_off[k] = fits ? off : -1;
         s_id[k] = st[0] + nst;
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(kStageThreads) k_memo_stage(StageArgs a) {
 }  // namespace
 
 DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int max_slabs, std::int64_t max_keys,
-                       std::size_t arena_bytes, cudaStream_t s)
+                       std::size_t arena_bytes, int window_inserts, cudaStream_t s)
     : client_(client),
       kd_(key_dim),
       max_slabs_(max_slabs),
@@ -296,6 +299,8 @@ DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int 
       arena_bytes_((arena_bytes + 255) & ~std::size_t{255}),
       log_cap_(std::int64_t{1} << 16) {
   if (kd_ < 1 || kd_ > kMaxKd) throw std::invalid_argument("device memo: key_dim must be in [1, 64]");
+  window_inserts_ = std::max(1, window_inserts);
+  ring_.reset(arena_bytes_);
   if (max_slabs_ > kStageThreads) throw std::invalid_argument("device memo: more than 1024 slabs per operator call");
   if (client_.config().global_cache) throw std::invalid_argument("device memo: global_cache is host-only");
   if (client_.store().ivf().nlist > kMaxProbe) throw std::invalid_argument("device memo: nlist must be <= 64");
@@ -353,6 +358,14 @@ void DeviceMemo::set_slabs(OpId op, const std::vector<std::size_t>& value_bytes,
   const int o = static_cast<int>(op);
   if (o > 3 || static_cast<int>(value_bytes.size()) > max_slabs_) throw std::logic_error("device memo: bad slab table");
   std::vector<long long> vb(value_bytes.begin(), value_bytes.end()), oc(out_counts.begin(), out_counts.end());
+  for (const std::int64_t c : out_counts)
+    max_slab_bytes_ = std::max(max_slab_bytes_, ValueRing::granule(static_cast<std::size_t>(c) * sizeof(float2)));
+  // fail at setup, not mid-solve: one window of inserts (+ the wrap of one
+  // slab) must fit the ring; everything older can spill to the cold tier
+  const std::size_t need = (static_cast<std::size_t>(window_inserts_) + 1) * max_slab_bytes_;
+  if (arena_bytes_ < need)
+    throw std::invalid_argument("device memo: value arena of " + std::to_string(arena_bytes_) +
+                                " bytes is below one insert window (" + std::to_string(need) + " bytes)");
   MLRG_CUDA(cudaMemcpyAsync(slab_vbytes_.get() + o * max_slabs_, vb.data(), vb.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, s));
   MLRG_CUDA(cudaMemcpyAsync(slab_counts_.get() + o * max_slabs_, oc.data(), oc.size() * sizeof(long long),
@@ -402,12 +415,35 @@ void DeviceMemo::upload_ivf(cudaStream_t s) {
   trained_ = true;
 }
 
+// Frees the ring span the next window can fill: the oldest values overlapping
+// it move to the cold tier (pinned host, device-mapped) and their value
+// pointers are repointed there; decisions and ids are unaffected.
+void DeviceMemo::spill(cudaStream_t s) {
+  ring_.reset_head(static_cast<std::size_t>(h_state_.get()[2]));
+  const std::vector<ValueRing::Live> out =
+      ring_.make_room(static_cast<std::size_t>(window_inserts_) * max_slab_bytes_);
+  if (out.empty()) return;
+  prof::HostSpan span("host:memo_spill");
+  std::vector<const float2*> ptrs(out.size());
+  for (std::size_t i = 0; i < out.size(); ++i) {
+    const ColdRef r = cold_.place(0, out[i].bytes);
+    cold_.copy_in(r, arena_.get() + out[i].off, out[i].bytes, s);
+    ptrs[i] = static_cast<const float2*>(cold_.device_ptr(r));
+  }
+  for (std::size_t i = 0; i < out.size(); ++i) {
+    MLRG_CUDA(cudaMemcpyAsync(vptr_.get() + out[i].id, &ptrs[i], sizeof(void*), cudaMemcpyHostToDevice, s));
+    client_.store().set_value_ptr(out[i].id, ptrs[i]);
+  }
+  MLRG_CUDA(cudaStreamSynchronize(s));
+  spilled_ += static_cast<std::int64_t>(out.size());
+}
+
 void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) {
   MLRG_CUDA(cudaMemcpyAsync(h_state_.get(), state_.get(), 6 * sizeof(long long), cudaMemcpyDeviceToHost, s));
   MLRG_CUDA(cudaStreamSynchronize(s));
   long long* st = h_state_.get();
   const long long npub = st[0], nstaged = publish ? st[1] : 0, nlog = st[3];
-  if (st[4]) throw std::runtime_error("device memo: value arena exhausted (" + std::to_string(arena_bytes_) + " bytes)");
+  if (st[4]) throw std::logic_error("device memo: a value larger than the arena (" + std::to_string(arena_bytes_) + " bytes)");
   if (nlog > log_cap_) throw std::runtime_error("device memo: decision log overflow");
   std::vector<DevLog> log(static_cast<std::size_t>(nlog));
   if (nlog) MLRG_CUDA(cudaMemcpyAsync(log.data(), log_.get(), sizeof(DevLog) * nlog, cudaMemcpyDeviceToHost, s));
@@ -446,9 +482,12 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
   // ---- publish: the host mirror gets the staged keys in order (same ids) ----
   MemoStore& store = client_.store();
   const bool was_trained = store.trained();
+  const char* arena = arena_.get();
   for (long long i = 0; i < nstaged; ++i) {
     ValueRef v;
     v.dev = vp[static_cast<std::size_t>(i)];
+    ring_.note(static_cast<std::uint64_t>(npub + i), static_cast<std::size_t>(reinterpret_cast<const char*>(v.dev) - arena),
+               static_cast<std::size_t>(vb[static_cast<std::size_t>(i)] - 8) / 2);
     v.norm = vn[static_cast<std::size_t>(i)];
     v.bytes = static_cast<std::size_t>(vb[static_cast<std::size_t>(i)]);
     v.count = static_cast<std::int64_t>((v.bytes - 8) / 16);
@@ -465,6 +504,7 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
   }
   MLRG_CUDA(cudaMemcpyAsync(state_.get(), st, 6 * sizeof(long long), cudaMemcpyHostToDevice, s));
   MLRG_CUDA(cudaStreamSynchronize(s));
+  if (publish) spill(s);
   if (store.trained() && (nstaged > 0 || !was_trained)) upload_ivf(s);
   if (st[0] > max_keys_ - static_cast<long long>(client_.config().insert_queue_cap))
     throw std::runtime_error("device memo: key index full (" + std::to_string(max_keys_) + " keys)");

@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "cold_tier.hpp"
 #include "device.hpp"
 #include "encoder.hpp"
 #include "memo.hpp"
@@ -53,8 +54,12 @@ struct DevLog {
 
 class DeviceMemo {
  public:
+  /// window_inserts: the most values one flush window can insert (the insert
+  /// cap, or fewer when the window has fewer lookups). The HBM arena is a ring
+  /// (cold_tier.hpp): it must hold one window plus one slab, older values
+  /// spill to pinned host memory at flush.
   DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int max_slabs, std::int64_t max_keys,
-             std::size_t arena_bytes, cudaStream_t s);
+             std::size_t arena_bytes, int window_inserts, cudaStream_t s);
 
   /// Per-slab value size (the reference's, scalerun.cpp:196-199) and complex64
   /// element count of `op`'s slabs, set once per operator.
@@ -78,9 +83,14 @@ class DeviceMemo {
   /// publish = false only drains the log (an aborted iteration: the reference
   /// records its decisions but never flushes its inserts).
   void flush(cudaStream_t s, std::vector<Audit>* audit, bool publish = true);
+  /// Values spilled to the cold tier so far (count, bytes).
+  std::int64_t spilled() const { return spilled_; }
+  std::size_t spilled_bytes() const { return cold_.bytes_placed(0); }
+  std::size_t arena_bytes() const { return arena_bytes_; }
 
  private:
   void upload_ivf(cudaStream_t s);
+  void spill(cudaStream_t s);
 
   MemoClient& client_;
   int kd_;
@@ -113,6 +123,11 @@ class DeviceMemo {
   int ncent_ = 0;
   bool trained_ = false;
   PinnedBuffer<long long> h_state_;
+  int window_inserts_;
+  std::size_t max_slab_bytes_ = 0;  // largest value slab (256-byte granules)
+  ValueRing ring_;
+  ColdTier cold_{"", 0};
+  std::int64_t spilled_ = 0;
 };
 
 }  // namespace mlrg

@@ -56,7 +56,8 @@ Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_
     const std::int64_t e = cfg_.chunk_extent;
     const int max_slabs = static_cast<int>(std::max((g_.n1 + e - 1) / e, (g_.h + e - 1) / e));
     dmemo_ = std::make_unique<DeviceMemo>(*memo_, enc_->key_dim(), enc_->seed(), max_slabs,
-                                          std::max<std::int64_t>(cfg_.memo_max_keys, 4096), cfg_.memo_arena_bytes, s_);
+                                          std::max<std::int64_t>(cfg_.memo_max_keys, 4096), cfg_.memo_arena_bytes,
+                                          cfg_.memo_window_inserts, s_);
     for (OpId op : {OpId::fu1d, OpId::fu2d, OpId::fu1d_adj, OpId::fu2d_adj}) {
       const int axis = chunk_axis_of(op);
       const std::vector<std::int64_t> ext = slab_extents(in_shape(op).extent(axis), e);
@@ -78,18 +79,30 @@ Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_
     stage2_.resize(static_cast<std::size_t>(g_.n1 * nr * g_.n2));
     mid_peers_ = std::make_unique<PeerMemory>(c, mid_.get());
     mid2_peers_ = std::make_unique<PeerMemory>(c, mid2_.get());
-    if (cfg_.memo_enabled) {
-      // every rank reserves the same capacity (the smallest request), so the
-      // replicated per-owner bump offsets agree everywhere
-      double cap = static_cast<double>(cfg_.memo_arena_bytes);
+  }
+  if (cfg_.memo_enabled && !dmemo_) {
+    // every rank reserves the same capacity (the smallest request), so the
+    // replicated per-owner ring offsets agree everywhere
+    double cap = static_cast<double>(cfg_.memo_arena_bytes);
+    if (shard_.sharded()) {
       std::vector<double> caps(static_cast<std::size_t>(shard_.world));
-      c.allgather(&cap, sizeof(cap), caps.data());
-      arena_cap_ = static_cast<std::size_t>(*std::min_element(caps.begin(), caps.end()));
-      arena_cap_ = std::max<std::size_t>(arena_cap_, 256);
-      arena_.resize(arena_cap_);
-      arena_peers_ = std::make_unique<PeerMemory>(c, arena_.get());
-      arena_next_.assign(static_cast<std::size_t>(shard_.world), 0);
+      shard_.comm->allgather(&cap, sizeof(cap), caps.data());
+      cap = *std::min_element(caps.begin(), caps.end());
     }
+    arena_cap_ = ValueRing::granule(static_cast<std::size_t>(cap));
+    const std::int64_t e = cfg_.chunk_extent;
+    const std::int64_t slab = std::max({e * g_.h * g_.n2, e * g_.n0 * g_.n2, g_.n_theta * e * g_.w, g_.n1 * e * g_.n2});
+    const std::size_t slab_bytes = ValueRing::granule(static_cast<std::size_t>(slab) * sizeof(float2));
+    window_bytes_ = static_cast<std::size_t>(std::max(1, cfg_.memo_window_inserts)) * slab_bytes;
+    if (arena_cap_ < window_bytes_ + slab_bytes)  // fail at setup, not mid-solve
+      throw std::invalid_argument("memo: value arena of " + std::to_string(arena_cap_) +
+                                  " bytes is below one insert window (" + std::to_string(window_bytes_ + slab_bytes) +
+                                  " bytes)");
+    arena_.resize(arena_cap_);
+    if (shard_.sharded()) arena_peers_ = std::make_unique<PeerMemory>(*shard_.comm, arena_.get());
+    rings_.assign(static_cast<std::size_t>(shard_.world), ValueRing(arena_cap_));
+    cold_ = std::make_unique<ColdTier>(shard_.sharded() ? shard_.comm->name() : std::string(),
+                                       shard_.sharded() ? shard_.comm->rank() : 0);
   }
 }
 
@@ -105,14 +118,49 @@ void Engine::exchange_fence() {
 }
 
 float2* Engine::value_slot(int owner, std::int64_t count) {
-  const std::size_t bytes = (static_cast<std::size_t>(count) * sizeof(float2) + 255) & ~std::size_t{255};
-  std::size_t& next = arena_next_[static_cast<std::size_t>(owner)];
-  if (next + bytes > arena_cap_)
-    throw std::runtime_error("memo value arena of rank " + std::to_string(owner) + " exhausted (" +
-                             std::to_string(arena_cap_) + " bytes reserved)");
-  float2* p = reinterpret_cast<float2*>(static_cast<char*>(arena_peers_->at(owner)) + next);
-  next += bytes;
-  return p;
+  const std::size_t bytes = ValueRing::granule(static_cast<std::size_t>(count) * sizeof(float2));
+  // spill_values() freed one window's span at the last flush; a window never inserts more
+  const std::size_t off = rings_[static_cast<std::size_t>(owner)].alloc(bytes);
+  pending_.push_back(Pending{owner, off, bytes});
+  char* base = arena_peers_ ? static_cast<char*>(arena_peers_->at(owner)) : arena_.get();
+  return reinterpret_cast<float2*>(base + off);
+}
+
+void Engine::spill_values() {
+  MemoStore& store = memo_->store();
+  // the window's values got ids in staging order at the flush just done
+  const std::uint64_t n = store.key_count();
+  if (n < pending_.size()) throw std::logic_error("memo: fewer published values than allocated");
+  std::uint64_t id = n - pending_.size();
+  for (const Pending& p : pending_) rings_[static_cast<std::size_t>(p.owner)].note(id++, p.off, p.bytes);
+  pending_.clear();
+  struct Moved {
+    std::uint64_t id;
+    ColdRef ref;
+  };
+  std::vector<Moved> moved;
+  const int me = shard_.sharded() ? shard_.comm->rank() : 0;
+  for (int r = 0; r < static_cast<int>(rings_.size()); ++r)
+    for (const ValueRing::Live& v : rings_[static_cast<std::size_t>(r)].make_room(window_bytes_)) {
+      const ColdRef ref = cold_->place(r, v.bytes);
+      if (r == me) cold_->copy_in(ref, arena_.get() + v.off, v.bytes, s_);
+      moved.push_back(Moved{v.id, ref});
+    }
+  if (moved.empty()) return;
+  prof::HostSpan span("host:memo_spill");
+  // the owners' copies (and segments) exist before any rank maps or reads them
+  if (shard_.sharded()) exchange_fence();
+  else MLRG_CUDA(cudaStreamSynchronize(s_));
+  for (const Moved& m : moved) store.set_value_ptr(m.id, static_cast<const float2*>(cold_->device_ptr(m.ref)));
+  spilled_ += static_cast<std::int64_t>(moved.size());
+}
+
+std::int64_t Engine::spilled_values() const { return dmemo_ ? dmemo_->spilled() : spilled_; }
+std::size_t Engine::spilled_bytes() const {
+  if (dmemo_) return dmemo_->spilled_bytes();
+  std::size_t b = 0;
+  for (int r = 0; cold_ && r < static_cast<int>(rings_.size()); ++r) b += cold_->bytes_placed(r);
+  return b;
 }
 
 void Engine::register_shapes() {  // scalerun.cpp:109-124
@@ -340,7 +388,7 @@ void Engine::apply(OpId op, bool fused, const void* in, bool in_d, const float2*
       prof::HostSpan span("host:memo_alloc");
       ValueRef v;
       v.count = out_counts[static_cast<std::size_t>(c)];
-      float2* slot = shard_.sharded() ? value_slot(owner, v.count) : memo_->store().arena().alloc(v.count);
+      float2* slot = value_slot(owner, v.count);
       if (mine) dst = slot;
       v.dev = slot;
       v.norm = nv[static_cast<std::size_t>(c)];
@@ -451,6 +499,7 @@ void Engine::flush_inserts() {
   if (shard_.sharded()) exchange_fence();
   if (dmemo_) return take_device_audit(true);
   memo_->flush_inserts();
+  spill_values();
 }
 
 void Engine::fu1d(const double2* u, float2* out, bool memoize) {

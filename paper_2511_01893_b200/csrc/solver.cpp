@@ -60,16 +60,19 @@ struct State {
   std::int64_t nchunks = 0;
   PinnedBuffer<double2> h_psi[3], h_psi_new[3], h_lam[3];
   DeviceBuffer<double2> c_psi[2][3], c_psi_new[2][3], c_lam[2][3];
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out = nullptr;
+  // offload copies: H2D on `side`, write-back D2H on `side_out`, so chunk k's
+  // compute overlaps both chunk k+1's upload and chunk k-1's write-back
+  cudaStream_t side = nullptr, side_out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_back[2] = {}, ev_out = nullptr;
 
   ~State() {
-    if (side) {
-      cudaStreamSynchronize(side);
-      cudaStreamDestroy(side);
-    }
+    for (cudaStream_t st : {side, side_out})
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
     for (int b = 0; b < 2; ++b)
-      for (cudaEvent_t e : {ev_in[b], ev_done[b]})
+      for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_back[b]})
         if (e) cudaEventDestroy(e);
     if (ev_out) cudaEventDestroy(ev_out);
   }
@@ -88,6 +91,12 @@ struct State {
     for (int c = 0; c < 3; ++c) vz(g[c], V);
     const std::int64_t np = sh.np();
     nchunks = (np + kChunk - 1) / kChunk;
+    // the fused RSP pass writes 2 partial slots per CTA per chunk into the fixed
+    // Partials table before the host sums them: refuse at setup, not by overrunning it
+    if (nchunks * ops::rsp_multiplier_slots() > Partials::kMaxSlots)
+      throw std::invalid_argument("solver: " + std::to_string(np) + " planes per rank exceed the RSP partial table (" +
+                                  std::to_string(Partials::kMaxSlots / ops::rsp_multiplier_slots() * kChunk) +
+                                  " planes); use more ranks");
     if (!offload) {
       for (int c = 0; c < 3; ++c) {
         vz(psi[c], V);
@@ -106,8 +115,10 @@ struct State {
         for (int c = 0; c < 3; ++c)
           for (auto* db : {&c_psi[b][c], &c_psi_new[b][c], &c_lam[b][c]}) db->resize(static_cast<std::size_t>(cn));
       MLRG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      MLRG_CUDA(cudaStreamCreateWithFlags(&side_out, cudaStreamNonBlocking));
       for (int b = 0; b < 2; ++b)
-        for (cudaEvent_t* e : {&ev_in[b], &ev_done[b]}) MLRG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        for (cudaEvent_t* e : {&ev_in[b], &ev_done[b], &ev_back[b]})
+          MLRG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
       MLRG_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
     }
     if (sh.sharded()) {
@@ -210,7 +221,7 @@ struct SolverState : State {
   void d2h(PinnedBuffer<double2> (&dst)[3], DeviceBuffer<double2> (&src)[3], std::int64_t k) {
     for (int c = 0; c < 3; ++c)
       MLRG_CUDA(cudaMemcpyAsync(dst[c].get() + k * kChunk * P0, src[c].get(), chunk_bytes(k), cudaMemcpyDeviceToHost,
-                                side));
+                                side_out));
   }
   static DField3 at(DeviceBuffer<double2> (&a)[3], std::int64_t off) {
     return DField3{{a[0].get() + off, a[1].get() + off, a[2].get() + off}};
@@ -249,20 +260,24 @@ struct SolverState : State {
         continue;
       }
       const int b = static_cast<int>(k & 1);
+      // buffer b: chunk k-2's compute is done with c_psi[b] and its write-back has read c_lam[b], c_psi_new[b]
       MLRG_CUDA(cudaStreamWaitEvent(side, ev_done[b], 0));
+      if (k >= 2) MLRG_CUDA(cudaStreamWaitEvent(side, ev_back[b], 0));
       h2d(c_psi[b], h_psi, k);
       h2d(c_lam[b], h_lam, k);
       MLRG_CUDA(cudaEventRecord(ev_in[b], side));
       MLRG_CUDA(cudaStreamWaitEvent(s, ev_in[b], 0));
+      if (k >= 2) MLRG_CUDA(cudaStreamWaitEvent(s, ev_back[b], 0));  // c_psi_new[b] is free again
       slots += ops::rsp_multiplier(u.get() + off, at(c_lam[b], 0), CDField3(at(c_psi[b], 0)), at(c_psi_new[b], 0), dk,
                                    lc, thr, rho_s, partials + slots, s, hk);
       MLRG_CUDA(cudaEventRecord(ev_done[b], s));
-      MLRG_CUDA(cudaStreamWaitEvent(side, ev_done[b], 0));
+      MLRG_CUDA(cudaStreamWaitEvent(side_out, ev_done[b], 0));
       d2h(h_lam, c_lam[b], k);
       d2h(h_psi_new, c_psi_new[b], k);
+      MLRG_CUDA(cudaEventRecord(ev_back[b], side_out));
     }
     if (offload) {  // the host copies are complete before anything reads them
-      MLRG_CUDA(cudaEventRecord(ev_out, side));
+      MLRG_CUDA(cudaEventRecord(ev_out, side_out));
       MLRG_CUDA(cudaStreamWaitEvent(s, ev_out, 0));
     }
     return slots;

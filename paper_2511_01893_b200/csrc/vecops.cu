@@ -366,6 +366,8 @@ void axpy(double2* y, const double2* x, double a, std::int64_t n, cudaStream_t s
   prof::end("k_axpy", s);
 }
 
+int rsp_multiplier_slots() { return 2 * grid_blocks(); }
+
 int rsp_multiplier(const double2* u, DField3 lam, CDField3 psi_old, DField3 psi_new, Dims d, double lc, double thr,
                    double rho_over_scale, double* partials, cudaStream_t s, const Halo& halo) {
   prof::begin("k_rsp_multiplier", s);

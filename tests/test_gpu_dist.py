@@ -47,8 +47,9 @@ def _worker(rank, world, port, case, memo, outdir):
     u = torch.empty((b - a, n, n), dtype=torch.complex64, device="cuda")
     solver.volume(u)
     meta, _ = solver.audit()
+    tiers = solver.tiers() if memo != "off" else {}
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), u=u.cpu().numpy(), a=a, b=b, meta=meta, csv=solver.csv,
-             aborted=aborted)
+             aborted=aborted, spilled=tiers.get("spilled_values", 0))
     del solver
     comm.barrier()
     del comm
