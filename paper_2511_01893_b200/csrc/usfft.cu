@@ -18,10 +18,12 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstring>
 #include <cstdlib>
 #include <numbers>
 #include <type_traits>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -223,10 +225,12 @@ __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_rows(const floa
 }
 
 // G[r'][c'][KB]: column FFT over the n1 non-zero wrapped rows of S.
+// The grid rows are ldg >= M2 + ghost cells long: columns [0, ghost) are
+// repeated at [M2, M2 + ghost) so the gather's windows never wrap.
 template <bool ZP, class TG>
 __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_cols(const float2* __restrict__ S, int n1, int logm1, int center1,
                                                    int logm2, int ks_n, const double2* __restrict__ tw1,
-                                                   TG* __restrict__ G, Skip sk) {
+                                                   TG* __restrict__ G, int ldg, int ghost, Skip sk) {
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int m1 = 1 << logm1, mask1 = m1 - 1, m2 = 1 << logm2;
@@ -237,7 +241,12 @@ __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_cols(const floa
     const double2 x = to_d(S[(static_cast<long long>(ok ? i : 0) * m2 + c) * KB + ks + kk]);
     return ok ? x : make_double2(0.0, 0.0);
   };
-  auto store = [&](int r, int kk, double2 x) { G[(static_cast<long long>(r) * m2 + c) * KB + ks + kk] = to_g<TG>(x); };
+  const bool dup = c < ghost;
+  auto store = [&](int r, int kk, double2 x) {
+    TG* g = G + (static_cast<long long>(r) * ldg + c) * KB + ks + kk;
+    g[0] = to_g<TG>(x);
+    if (dup) g[static_cast<long long>(m2) * KB] = to_g<TG>(x);
+  };
   fft_stockham<+1, true, true, ZP>(sd, logm1, ks_n, ks_n, tw1, load, store);
 }
 
@@ -260,16 +269,35 @@ struct GatherOut {
 // computed once and multiplied by each member's phase (Usfft::Tables).
 // Lane l owns batch row l % 16 and the window columns of parity l / 16, so a
 // half warp reads one 128 B grid cell (16 rows x complex64) per tap: every
-// load is a full coalesced line, no tap is wasted and no lane idles. The
-// window columns' grid offsets and column weights stay in registers for the
-// whole target; per window row the warp reads W/2 cells per half warp, widens
-// them, sums them against the column weights (double) and adds the row
-// weight times that sum, which is the reference's order of summation
-// (inner over columns, outer over rows, nufft.cpp:205-216). Targets are
-// processed in a spatially sorted order, gather_per_cta() per CTA, so the warps
-// of a CTA share their windows' cells in L1.
+// load is a full coalesced line, no tap is wasted and no lane idles. Per
+// window row the warp reads W/2 cells per half warp, widens them, sums them
+// against the column weights (double) and adds the row weight times that
+// sum, which is the reference's order of summation (inner over columns,
+// outer over rows, nufft.cpp:205-216). Targets are processed in a spatially
+// sorted order, a contiguous range per CTA, so the warps of a CTA share their
+// windows' cells in L1.
+//   * The CTA's class records (window origin, weights, members and phases:
+//     ClassRec, one contiguous block) arrive in shared memory through one
+//     bulk-copy (TMA engine, cp.async.bulk) on an mbarrier, so no class waits
+//     on a global load of its own parameters.
+//   * The forward grid carries `ghost` replicated columns past M2 (written by
+//     the column pass), so no window wraps horizontally: one row address per
+//     window row, the W/2 cells at immediate offsets.
+//   * Rows stream through a 2-deep register ring that runs across class
+//     boundaries: the next class's first row is in flight while the current
+//     class's last row is summed.
 constexpr int kGatherWarps = 8;
 constexpr std::size_t kClassMax = 4;
+
+template <int W>
+struct ClassRec {
+  int r0, c0, nmem, first;  // window origin (row, column), member count, first member index
+  int tq[kClassMax];        // members: packed (t << 16 | q)
+  double2 fac[kClassMax];   // members' pref x phase
+  double w1[W], w2[W];      // row and column kernel weights
+};
+static_assert(sizeof(ClassRec<10>) % 16 == 0 && sizeof(ClassRec<24>) % 16 == 0, "bulk-copy granularity");
+
 // classes per gather CTA (MLRG_GATHER_PER_CTA overrides, for tuning)
 int gather_per_cta() {
   static const int v = [] {
@@ -279,59 +307,114 @@ int gather_per_cta() {
   return v;
 }
 
-// (the 24-tap Gaussian windows keep a whole window row of loads in flight: 2 CTAs/SM, 128 registers)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+// One thread: arm `bar` for `bytes` and bulk-copy [src, src + bytes) into smem
+// (cp.async.bulk, completes on the mbarrier's transaction count).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// float -> double on the integer pipe (exact for normal numbers and zeros;
+// subnormal floats, |x| < 1.2e-38, come out as +-2^-127 (1 + m 2^-23) instead,
+// an absolute difference below 1e-38 in a sum of O(1) terms). The gather's
+// F2F conversions saturate the XU pipe (ncu: 67% of peak with every tap
+// converted there); kGatherIntCvt of each lane's W/2 window columns per row
+// are widened here instead, on the otherwise idle ALU pipe.
+__device__ __forceinline__ double widen_alu(float x) {
+  const unsigned f = __float_as_uint(x), a = f & 0x7fffffffu;
+  const unsigned hi = (a ? (a >> 3) + 0x38000000u : 0u) | (f & 0x80000000u);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(f << 29));
+}
+#ifndef MLRG_GATHER_INTCVT
+#define MLRG_GATHER_INTCVT 0
+#endif
+constexpr int kGatherIntCvt = MLRG_GATHER_INTCVT;
+template <int J, class T>
+__device__ __forceinline__ double widen_tap(T v) {
+  if constexpr (std::is_same_v<T, float> && J < kGatherIntCvt) return widen_alu(v);
+  else return static_cast<double>(v);
+}
+
+// (the 24-tap Gaussian windows: 2 CTAs/SM, 128 registers)
 template <int W, class TG>
 __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? MLRG_GATHER_MINB : 2) k_fu2d_gather(
-    const TG* __restrict__ G, int T, int w, int logm1, int logm2, int nk, const int* __restrict__ s_r0,
-    const int* __restrict__ s_c0, const double* __restrict__ s_w1, const double* __restrict__ s_w2,
-    const int* __restrict__ m_first, const int* __restrict__ m_tidx, const double2* __restrict__ m_fac, GatherOut eo,
-    int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
+    const TG* __restrict__ G, int T, int w, int logm1, int ldg, int nk, const ClassRec<W>* __restrict__ recs,
+    GatherOut eo, int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
   if (skipped(sk, 0)) return;
   constexpr int WH = W / 2;
+  // rows in flight ahead of the one summed; the ring runs across classes, so
+  // its period must divide W
+  constexpr int D = W % 2 == 0 ? 1 : 0;
+  static_assert(D == 1, "the cross-class row ring needs an even W");
+  extern __shared__ __align__(16) unsigned char gather_smem[];
+  __shared__ unsigned long long bar;
   __shared__ double red_scratch[kGatherWarps * 2];
-  __shared__ double w2s[kGatherWarps][W];  // the class's column weights (half-warp broadcast reads)
+  const ClassRec<W>* rec = reinterpret_cast<const ClassRec<W>*>(gather_smem);
+  const int s0 = blockIdx.x * per_cta, s_end = min(T, s0 + per_cta);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    bulk_load(gather_smem, recs + s0, static_cast<unsigned>((s_end - s0) * sizeof(ClassRec<W>)), &bar);
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, kk = lane & 15, ph = lane >> 4;
-  const int mask1 = (1 << logm1) - 1, mask2 = (1 << logm2) - 1;
-  const long long row_stride = static_cast<long long>(KB) << logm2;  // complex64 per grid row
+  const int mask1 = (1 << logm1) - 1;
+  const unsigned rs = static_cast<unsigned>(ldg) * KB * static_cast<unsigned>(sizeof(TG));  // bytes per grid row
+  constexpr int CB = 2 * KB * static_cast<int>(sizeof(TG));  // bytes between a lane's window columns
   double red[2] = {0.0, 0.0};
-  const int s_end = min(T, static_cast<int>(blockIdx.x + 1) * per_cta);
-  for (int s = blockIdx.x * per_cta + warp; s < s_end; s += kGatherWarps) {
-    const int r0 = s_r0[s], c0 = s_c0[s];
-    int coff[WH];
-    __syncwarp();
-    if (lane < W) w2s[warp][lane] = s_w2[static_cast<long long>(s) * W + lane];
+  mbar_wait(&bar, 0);
+  const char* gbase = reinterpret_cast<const char*>(G + ph * KB + kk);
+  auto col_base = [&](int s) { return gbase + static_cast<long long>(rec[s - s0].c0) * KB * sizeof(TG); };
+  auto row = [&](const char* cb, int r) { return cb + static_cast<unsigned>(r & mask1) * rs; };
+  TG buf[D + 1][WH];
+  int s = s0 + warp;
+  if (s < s_end) {  // prime the ring with the first class's first row
+    const char* gr = row(col_base(s), rec[s - s0].r0);
 #pragma unroll
-    for (int j = 0; j < WH; ++j) coff[j] = ((c0 + 2 * j + ph) & mask2) * KB + kk;
-    __syncwarp();
-    const double* w2r = &w2s[warp][ph];  // w2r[2 j] = weight of window column 2 j + ph
-    const double* w1p = s_w1 + static_cast<long long>(s) * W;
+    for (int j = 0; j < WH; ++j) buf[0][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
+  }
+  for (; s < s_end; s += kGatherWarps) {
+    const ClassRec<W>& R = rec[s - s0];
+    const int sn = s + kGatherWarps < s_end ? s + kGatherWarps : s;  // the next class (or a harmless reload)
+    const char* cb = col_base(s);
+    const char* cbn = col_base(sn);
+    const int r0 = R.r0, r0n = rec[sn - s0].r0;
+    double w2l[WH];  // this lane's column weights (window columns 2 j + ph)
+#pragma unroll
+    for (int j = 0; j < WH; ++j) w2l[j] = R.w2[2 * j + ph];
     double2 acc = make_double2(0.0, 0.0);
-    // rows are software-pipelined one ahead: the next row's W/2 loads are in
-    // flight while the current row is summed
-    TG nxt[WH];
-    {
-      const TG* gr = G + (r0 & mask1) * row_stride;
-#pragma unroll
-      for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
-    }
 #pragma unroll
     for (int a = 0; a < W; ++a) {
-      TG v[WH];
+      {  // row a + 1 of this class, or row 0 of the next
+        const char* gr = a + 1 < W ? row(cb, r0 + a + 1) : row(cbn, r0n);
 #pragma unroll
-      for (int j = 0; j < WH; ++j) v[j] = nxt[j];
-      if (a + 1 < W) {
-        const TG* gr = G + ((r0 + a + 1) & mask1) * row_stride;
-#pragma unroll
-        for (int j = 0; j < WH; ++j) nxt[j] = __ldg(gr + coff[j]);
+        for (int j = 0; j < WH; ++j) buf[(a + 1) % (D + 1)][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
       }
       double2 racc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int j = 0; j < WH; ++j) {
-        const double wj = w2r[2 * j];
-        racc.x = fma(wj, static_cast<double>(v[j].x), racc.x);
-        racc.y = fma(wj, static_cast<double>(v[j].y), racc.y);
-      }
-      const double wa = w1p[a];
+      auto tap = [&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        const TG v = buf[a % (D + 1)][j];
+        racc.x = fma(w2l[j], widen_tap<j>(v.x), racc.x);
+        racc.y = fma(w2l[j], widen_tap<j>(v.y), racc.y);
+      };
+      [&]<int... J>(std::integer_sequence<int, J...>) { (tap(std::integral_constant<int, J>{}), ...); }(
+          std::make_integer_sequence<int, WH>{});
+      const double wa = R.w1[a];
       acc.x = fma(wa, racc.x, acc.x);
       acc.y = fma(wa, racc.y, acc.y);
     }
@@ -341,14 +424,14 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? MLRG_GATHER_
     if (ph == 0 && kk < nk) {
       // every detector sample of the class gets the shared sum times its own phase
       double2 cs = make_double2(0.0, 0.0);
-      for (int e = m_first[s], e1 = m_first[s + 1]; e < e1; ++e) {
-        const int tq = m_tidx[e];
-        const int t = tq / w, q = tq - t * w;
-        double2 val = cmul(acc, m_fac[e]);
+      for (int e = 0; e < R.nmem; ++e) {
+        const int tq = R.tq[e];
+        const int t = tq >> 16, q = tq & 0xffff;
+        double2 val = cmul(acc, R.fac[e]);
         if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
         const float2 stored = to_f(val);
         if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = stored;
-        if (eo.cls) cs = cadd(cs, cmul(to_d(stored), eo.cfac[e]));  // k_fu2d_adj_prep's sum, member order
+        if (eo.cls) cs = cadd(cs, cmul(to_d(stored), eo.cfac[R.first + e]));  // k_fu2d_adj_prep's sum, member order
         if (eo.reduce) {
           red[0] += val.x * val.x + val.y * val.y;
           if (eo.dot) {
@@ -564,7 +647,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
   if (kk < nk)
     for (int e = m_first[c], e1 = m_first[c + 1]; e < e1; ++e) {
       const int tq = m_tidx[e];
-      const int t = tq / w, q = tq - t * w;
+      const int t = tq >> 16, q = tq & 0xffff;  // packed (Usfft::Tables)
       acc = cadd(acc, cmul(to_d(p[(t * ld + k0 + kk) * w + q]), m_cfac[e]));
     }
   val[static_cast<long long>(c) * KB + kk] = to_f(acc);
@@ -640,10 +723,12 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict
 
 // TO_S: keep the n1 output slots that map to modes, at their S rows (adjoint);
 // otherwise all M rows in natural order (forward). TS: S in the transposed layout.
+// (forward: `out` is the gather's grid, rows ldo cells long with `ghost`
+// repeated columns, as k_fu2d_cols writes it)
 template <int SIGN, bool TO_S, bool TS>
 __global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict__ Y, int n1, int logm1, int center1,
                                                         int logA, int logm2, const double2* __restrict__ twB,
-                                                        float2* __restrict__ out, Skip sk) {
+                                                        float2* __restrict__ out, int ldo, int ghost, Skip sk) {
   if (skipped(sk, 0)) return;
   extern __shared__ double2 sd[];
   const int mask1 = (1 << logm1) - 1, m2 = 1 << logm2, logB = logm1 - logA;
@@ -658,7 +743,13 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass2(const float2* __restrict
       r = (r + center1) & mask1;
       if (r >= n1) return;
     }
-    out[T ? cols4_ts(r, c0, l, m2) : (static_cast<long long>(r) * m2 + c0) * KB + l] = to_f(x);
+    if constexpr (T) {
+      out[cols4_ts(r, c0, l, m2)] = to_f(x);
+    } else {
+      float2* o = out + (static_cast<long long>(r) * ldo + c0) * KB + l;
+      o[0] = to_f(x);
+      if (c0 + l / KB < ghost) o[static_cast<long long>(m2) * KB] = to_f(x);
+    }
   };
   fft_stockham<SIGN, true, true>(sd, logB, kCols4Lanes, kCols4Lanes, twB, load, store);
 }
@@ -812,6 +903,9 @@ struct Usfft::Tables {
   // target classes (coincident frequencies), spatially sorted: window origin
   // and weights per class, member lists with each member's phase factors
   int nclass = 0;
+  int gather_per = 16;  // classes per gather CTA (whole waves of resident CTAs)
+  int ghost = 0, ldg = 0;  // forward grid: repeated columns and row length (cells)
+  DeviceBuffer<unsigned char> recs;  // ClassRec<W>[C]
   DeviceBuffer<int> t_r0, t_c0, m_first, m_tidx;
   DeviceBuffer<double> t_w1, t_w2;  // [C][W]
   DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
@@ -848,6 +942,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   prof::HostSpan span("host:usfft_tables");
   Tables& t = *t_;
   const FrequencyGrids fg = frequency_grids(g_);
+  if (g_.w > 0xffff || g_.n_theta > 0x7fff)  // packed (t, q) member indices of the fu2d classes
+    throw std::invalid_argument("fu2d: w must be < 65536 and n_theta < 32768");
   // ---- fu1d plan (nufft.cpp:109-110) ----
   t.pz = DimPlan::make(g_.n0, fg.nu_z, kernel_);
   const int W = t.pz.taps;
@@ -978,7 +1074,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
       std::copy_n(py.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
                   w2.begin() + static_cast<std::ptrdiff_t>(c * WS));
       for (const int e : members[c]) {
-        mtidx.push_back(e);
+        mtidx.push_back(static_cast<int>((e / g_.w) << 16 | (e % g_.w)));  // packed (t, q)
         mfac.push_back(tf[static_cast<std::size_t>(e)]);
         mcfac.push_back(tcf[static_cast<std::size_t>(e)]);
       }
@@ -992,6 +1088,30 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     t.m_tidx.upload(mtidx, stream_);
     t.m_fac.upload(mfac, stream_);
     t.m_cfac.upload(mcfac, stream_);
+    // the gather's per-class records (bulk-copied into shared memory per CTA)
+    auto build = [&](auto tag) {
+      using Rec = decltype(tag);
+      constexpr int RW = sizeof(Rec::w1) / sizeof(double);
+      std::vector<Rec> rv(C);
+      for (std::size_t c = 0; c < C; ++c) {
+        Rec& r = rv[c];
+        std::memset(&r, 0, sizeof(Rec));
+        r.r0 = r0[c];
+        r.c0 = c0[c];
+        r.first = mfirst[c];
+        r.nmem = mfirst[c + 1] - mfirst[c];
+        for (int e = 0; e < r.nmem; ++e) {
+          r.tq[e] = mtidx[static_cast<std::size_t>(mfirst[c] + e)];
+          r.fac[e] = mfac[static_cast<std::size_t>(mfirst[c] + e)];
+        }
+        std::copy_n(w1.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w1);
+        std::copy_n(w2.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w2);
+      }
+      t.recs.upload(reinterpret_cast<const unsigned char*>(rv.data()), rv.size() * sizeof(Rec), stream_);
+      MLRG_CUDA(cudaStreamSynchronize(stream_));
+    };
+    if (W == kEsTaps) build(ClassRec<kEsTaps>{});
+    else build(ClassRec<kTaps>{});
   }
   prof::host_mark("host:usfft_classes");
   {  // spread patches: 8x4 cells -> targets whose W x W window touches them (targets ascending)
@@ -1094,9 +1214,24 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   prof::host_mark("host:usfft_patches");
   t.wide = kernel_ == GridKernel::gaussian && !t.cols4;
-  t.S.resize(static_cast<std::size_t>(px.m * py.m * KB));
-  t.Gd.resize(static_cast<std::size_t>(px.m * py.m * KB) * (t.wide ? 2 : 1));
+  t.ghost = (W - 1 + 7) & ~7;
+  t.ldg = static_cast<int>(py.m) + t.ghost;
+  t.S.resize(static_cast<std::size_t>(px.m * t.ldg * KB));
+  t.Gd.resize(static_cast<std::size_t>(px.m * t.ldg * KB) * (t.wide ? 2 : 1));
   t.val.resize(C * KB);
+  {  // classes per gather CTA: ~gather_per_cta(), rounded so the grid is whole waves
+    int nb = 0;
+    const std::size_t rb = static_cast<std::size_t>(gather_per_cta()) *
+                           (W == kEsTaps ? sizeof(ClassRec<kEsTaps>) : sizeof(ClassRec<kTaps>));
+    if (t.wide) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kTaps, double2>, 32 * kGatherWarps, rb);
+    else if (W == kEsTaps) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kEsTaps, float2>, 32 * kGatherWarps, rb);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kTaps, float2>, 32 * kGatherWarps, rb);
+    const std::int64_t slots = std::max(1, nb) * static_cast<std::int64_t>(sm_count());
+    const std::int64_t per = gather_per_cta();
+    const std::int64_t waves = std::max<std::int64_t>(1, (static_cast<std::int64_t>(C) + per * slots - 1) / (per * slots));
+    t.gather_per = static_cast<int>(std::max<std::int64_t>(1, (static_cast<std::int64_t>(C) + waves * slots - 1) / (waves * slots)));
+    if (std::getenv("MLRG_GATHER_PER_CTA")) t.gather_per = static_cast<int>(per);
+  }
 
   // ---- f2d (operators.cpp:20-74) ----
   t.f2d_fft = is_pow2(g_.h) && is_pow2(g_.w) && g_.h >= 8 && g_.w >= 8;
@@ -1239,9 +1374,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   const Tables& t = *t_;
   const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
-  const int per_cta = gather_per_cta();
+  const int per_cta = t.gather_per;
   const int ggrid = (t.nclass + per_cta - 1) / per_cta;
-  auto gather = t.px.taps == kEsTaps ? k_fu2d_gather<kEsTaps, float2> : k_fu2d_gather<kTaps, float2>;
   Tables& tm = *t_;
   // class sums for a following fu2d_adj of this output (memo skip flags would
   // leave batches uncomputed: not with them)
@@ -1286,19 +1420,21 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
           t.x_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
       k_cols4_pass2<+1, false, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
-          Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S, sk);
+          Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S,
+          t.ldg, t.ghost, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       G = S;
     } else if (t.wide) {
       (zero_padded(t.px) ? k_fu2d_cols<true, double2> : k_fu2d_cols<false, double2>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                     static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(),
-          reinterpret_cast<double2*>(Gd), sk);
+          reinterpret_cast<double2*>(Gd), t.ldg, t.ghost, sk);
       MLRG_LAUNCH_CHECK("k_fu2d_cols");
     } else {
       (zero_padded(t.px) ? k_fu2d_cols<true, float2> : k_fu2d_cols<false, float2>)<<<dim3(KB / ks1, static_cast<unsigned>(t.py.m)), static_cast<unsigned>(ks1 * t.px.m / 8),
                     static_cast<std::size_t>(t.px.m * ks1) * sizeof(double2), s>>>(
-          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd, sk);
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.py.logm, ks1, t.x_tw.get(), Gd,
+          t.ldg, t.ghost, sk);
       MLRG_LAUNCH_CHECK("k_fu2d_cols");
     }
     prof::end("k_fu2d_cols", s);
@@ -1307,15 +1443,15 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
                  cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : nullptr, t.m_cfac.get()};
     prof::begin("k_fu2d_gather", s);
     // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
-    auto launch_gather = [&](auto kern, auto grid_ptr) {
-      kern<<<ggrid, 32 * kGatherWarps, 0, s>>>(grid_ptr, t.nclass, static_cast<int>(g_.w), t.px.logm, t.py.logm, nb,
-                                               t.t_r0.get(), t.t_c0.get(), t.t_w1.get(), t.t_w2.get(),
-                                               t.m_first.get(), t.m_tidx.get(), t.m_fac.get(), eo, per_cta,
-                                               partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0,
-                                               sk);
+    auto launch_gather = [&](auto kern, auto grid_ptr, auto rec_tag) {
+      using Rec = decltype(rec_tag);
+      kern<<<ggrid, 32 * kGatherWarps, static_cast<std::size_t>(per_cta) * sizeof(Rec), s>>>(
+          grid_ptr, t.nclass, static_cast<int>(g_.w), t.px.logm, t.ldg, nb, reinterpret_cast<const Rec*>(t.recs.get()),
+          eo, per_cta, partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0, sk);
     };
-    if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G));
-    else launch_gather(gather, G);
+    if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kTaps>{});
+    else if (t.px.taps == kEsTaps) launch_gather(k_fu2d_gather<kEsTaps, float2>, G, ClassRec<kEsTaps>{});
+    else launch_gather(k_fu2d_gather<kTaps, float2>, G, ClassRec<kTaps>{});
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", s);
   }
@@ -1388,7 +1524,8 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
           t.x_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
       k_cols4_pass2<-1, true, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
-          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd, sk);
+          S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd,
+          static_cast<int>(t.py.m), 0, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
       Sc = Gd;
     } else if (t.wide) {

@@ -1,3 +1,10 @@
-nproc
-timeout 1500 python -m pytest tests/test_gpu_parity_large.py tests/test_gpu_cold_tier.py -q -x 2>&1 | tail -25
-timeout 1500 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_parity_large.py --deselect tests/test_gpu_cold_tier.py 2>&1 | tail -5
+for v in default ic1 ic2 ic3; do
+  if [ $v = default ]; then unset MLRG_LIB; else export MLRG_LIB=$PWD/paper_2511_01893_b200/libv/$v/libmlr.so; fi
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-memo-run --no-offload-run > gpurun_out/b_$v.json 2> gpurun_out/b_$v.err
+  python -c "
+import json,sys
+d=json.load(open('gpurun_out/b_$v.json')); k=d['roofline']['kernels_ms_per_step']
+print('$v', 'it/s %.2f'%d['value'], ' '.join('%s=%.2f'%(n.replace('k_fu2d_',''),v) for n,v in k.items()))"
+done
+export MLRG_LIB=$PWD/paper_2511_01893_b200/libv/ic2/libmlr.so
+timeout 600 python -m pytest tests/test_gpu_ops.py tests/test_gpu_recon.py -q -x 2>&1 | tail -1
