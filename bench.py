@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-offload-run", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the gaussian line and the configs[0]/[2] runs")
     ap.add_argument("--same-gpu", action="store_true",
                     help="testing: every rank on cuda:0 with a gloo group (exercises the sharded path on one GPU)")
     return ap.parse_args()
@@ -256,23 +257,34 @@ def main():
     m.lib()
     stream = torch.cuda.current_stream()
 
-    # synthetic data of the configured shape: the "blocks" phantom (seed 1) projected on the device
-    ph_host = m.make_phantom("blocks", n, n, n, 1).numpy().astype(np.complex64)
-    phantom = torch.from_numpy(ph_host).cuda()
-    ctx = m.Context(n, n, n, nt, n, n, stream=stream.cuda_stream)
-    d = torch.empty((nt, n, n), dtype=torch.complex64, device="cuda")
-    ctx.forward_L(phantom, d)
-    ctx.sync()
-    del ctx
+    def make_data(n, nt):
+        """Synthetic data of the configured shape: the "blocks" phantom (seed 1) projected on the device."""
+        ph_host = m.make_phantom("blocks", n, n, n, 1).numpy().astype(np.complex64)
+        phantom = torch.from_numpy(ph_host).cuda()
+        ctx = m.Context(n, n, n, nt, n, n, stream=stream.cuda_stream)
+        d = torch.empty((nt, n, n), dtype=torch.complex64, device="cuda")
+        ctx.forward_L(phantom, d)
+        ctx.sync()
+        del ctx
+        return d, phantom
 
-    def timed_run(memo: str, profile_steps: int, offload: str = "off", steps: int = 0):
+    d, phantom = make_data(n, nt)
+
+    def timed_run(memo: str, profile_steps: int, offload: str = "off", steps: int = 0, kernel: str = "",
+                  data=None, size=None, warmup=None):
         """W warm-up steps, K timed steps (CUDA events on the solver's stream, no
         profiling hooks), then `profile_steps` more with per-kernel event timers."""
+        global KERNEL
+        kernel_prev, KERNEL = KERNEL, kernel or KERNEL
+        dd, ph = data if data is not None else (d, phantom)
+        nn, nnt = size if size is not None else (n, nt)
+        warm = args.warmup if warmup is None else warmup
         # n_outer = the iterations this run makes (sizes the memo value arena, reserved at setup)
         steps = steps or args.steps
-        solver = m.Solver(config_text(n, nt, memo, args.warmup + steps + profile_steps, offload), d,
-                          reference=phantom, stream=stream.cuda_stream, comm=comm)
-        for _ in range(args.warmup):
+        solver = m.Solver(config_text(nn, nnt, memo, warm + steps + profile_steps, offload), dd,
+                          reference=ph, stream=stream.cuda_stream, comm=comm)
+        KERNEL = kernel_prev
+        for _ in range(warm):
             solver.step()
         m.lib().mlrg_prof_enable(0)
         c0 = solver.counters()
@@ -309,7 +321,8 @@ def main():
             torch.cuda.synchronize()
             m.lib().mlrg_prof_enable(0)
             for k in ("k_fu2d_gather", "k_fu2d_adj_spread", "k_fu2d_rows", "k_fu2d_cols", "k_fu2d_adj_cols",
-                      "k_fu2d_adj_rows", "k_fu2d_adj_prep", "k_fu1d", "k_fu1d_adj") + HBM_KERNELS:
+                      "k_fu2d_adj_rows", "k_fu2d_adj_prep", "k_fu1d", "k_fu1d_adj", "k_encode", "k_memo_lookup",
+                      "k_memo_stage", "k_dev_materialize", "k_dev_store") + HBM_KERNELS:
                 tot, cnt = m.prof_query(k)
                 if cnt:
                     prof[k] = {"ms_total": tot, "launches": cnt}
@@ -335,6 +348,54 @@ def main():
                    "remote_hits": c["remote_hits"], "cache_hits": c["cache_hits"],
                    "hit_rate": hits / c["lookups"] if c["lookups"] else None,
                    "aborted": on["steps_done"] < args.steps, "step_ms": on["step_ms"]}
+
+    def summarize(r, n_, nt_):
+        c = r["counters"]
+        hits = c["remote_hits"] + c["cache_hits"]
+        ms_ = allmax(r["ms"]) / max(r["steps_done"], 1)
+        out_ = {"value": 1000.0 / ms_ if r["steps_done"] else None, "unit": "it/s", "ms_per_step": ms_,
+                "steps": r["steps_done"], "step_ms": r["step_ms"]}
+        if c["lookups"]:
+            out_.update(lookups=c["lookups"], misses=c["misses"], remote_hits=c["remote_hits"],
+                        cache_hits=c["cache_hits"], hit_rate=hits / c["lookups"])
+        if r["prof"]:
+            ps = max(r["prof_steps"], 1)
+            out_["kernels_ms_per_step"] = {k: v["ms_total"] / ps for k, v in r["prof"].items()}
+            g = r["prof"].get("k_fu2d_gather")
+            if g:
+                avg = g["ms_total"] / g["launches"]
+                out_["gather_avg_launch_ms"] = avg
+                out_["gather_tflops_576tap"] = algorithmic(n_, nt_, "k_fu2d_gather")["flops"] / (avg * 1e-3) / 1e12
+        return out_
+
+    # the reference's own 24-tap Gaussian plan (gridding_kernel = gaussian, nufft.cpp:48-103):
+    # the operator the CPU arm runs, reported beside the 10-tap es default
+    gaussian = None
+    if not args.no_extra:
+        gaussian = summarize(timed_run("off", profile_steps=2, kernel="gaussian", steps=min(args.steps, 10)), n, nt)
+        gaussian["nudft"] = "gridding, the reference's 24-tap Gaussian plan (nufft.cpp:48-103), complex128 grids"
+
+    # the other BASELINE configurations that fit one GPU
+    extra = None
+    if not args.no_extra and world == 1:
+        extra = {}
+        d0, p0 = make_data(64, 64)
+        timed_run("local", 0, steps=10, warmup=0, data=(d0, p0), size=(64, 64))  # process warm-up (module loads)
+        c0 = summarize(timed_run("local", 0, steps=10, warmup=0, data=(d0, p0), size=(64, 64)), 64, 64)
+        c0.update(workload="configs[0]: 64^3 phantom, 64 angles, 10 ADMM iterations, memo on (a whole fresh solve)",
+                  job_s=c0["ms_per_step"] * c0["steps"] / 1e3,
+                  reference_as_is_s=286.6,
+                  reference_as_is_note="SURVEY.md §6: the reference as-is (direct NUDFT, 1 worker) on the survey "
+                                       "container's 8-core Xeon; its gridding path took 54.0 s")
+        extra["configs[0]"] = c0
+        del d0, p0
+        d2, p2 = make_data(512, 512)
+        c2 = summarize(timed_run("off", 2, steps=5, warmup=2, data=(d2, p2), size=(512, 512)), 512, 512)
+        c2_on = summarize(timed_run("local", 0, steps=5, warmup=2, data=(d2, p2), size=(512, 512)), 512, 512)
+        c2.update(workload="configs[2]: 512^3 phantom, 512 angles, memo off, 1 B200", memo_on=c2_on)
+        extra["configs[2]"] = c2
+        del d2, p2
+        torch.cuda.empty_cache()
 
     offload = None
     if not args.no_offload_run:
@@ -448,13 +509,14 @@ def main():
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c64 (fp32)", "data": "synthetic (blocks phantom seed 1, d = forward_L on GPU)",
-        "config": {"workload": f"configs[1]: {n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)",
+        "config": {"workload": (f"configs[1]: {n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)"
+                                if (n, nt) == (256, 256) else f"{n}^3 volume, {nt} angles, memo off (memo-on run in memo_on)"),
                    "n": n, "n_theta": nt, "n_inner": 4, "memo": "off",
                    "nudft": "gridding, 10-tap ES kernel (NUDFT to 2e-9; reference: 24-tap Gaussian, 3e-12)",
                    "parallelism": f"z-slab sharded x{world} (16-slab assign(), P2P all-to-all)" if world > 1
                    else "1 GPU",
                    "l2": "no flush: every per-iteration array (134 MB) exceeds the 126 MB L2"},
-        "memo_on": memo_on, "offload": offload, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
+        "memo_on": memo_on, "gaussian": gaussian, "configs_extra": extra, "offload": offload, "roofline": roof, "iteration_hbm": iter_hbm, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": off["launches"], "clocks": off["clocks"],
     }
     if rank == 0:

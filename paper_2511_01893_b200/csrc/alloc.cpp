@@ -40,6 +40,16 @@ void release_cache() {
   c.dev_dirty = false;
 }
 
+std::size_t cached_device_bytes() {
+  Cache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mx);
+  const int d = current_device();
+  std::size_t b = 0;
+  for (const auto& [k, p] : c.dev)
+    if (k.first == d) b += k.second;
+  return b;
+}
+
 void* device(std::size_t bytes) {
   if (bytes >= kMinCached) {
     Cache& c = cache();

@@ -135,6 +135,7 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   const double slab_bytes = static_cast<double>((slab * static_cast<std::int64_t>(sizeof(float2)) + 255) & ~std::int64_t{255});
   std::size_t free_b = 0, total_b = 0;
   MLRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  free_b += mlrg::alloc::cached_device_bytes();  // blocks a previous engine returned to the cache
   // lookups per window: every memoizable call of an outer iteration (4 per
   // inner step, 6 with pipeline = baseline) over this rank's slabs
   const int calls = (rc.admm.pipeline == mlrg::Pipeline::baseline ? 6 : 4) * rc.admm.n_inner;
@@ -152,7 +153,19 @@ std::unique_ptr<mlrg::Engine> build_engine(const mlrg::RunConfig& rc, const mlrg
   ec.memo_window_inserts = static_cast<int>(std::max<std::int64_t>(window, 1));
   const double floor_b = static_cast<double>(ec.memo_window_inserts + 1) * slab_bytes;
   const double want = static_cast<double>(rc.admm.n_outer) * static_cast<double>(window) * slab_bytes;
-  std::size_t bytes = static_cast<std::size_t>(std::max(floor_b, std::min(want, 0.45 * static_cast<double>(free_b))));
+  // what the solve still allocates besides the arena: the complex128 state (17
+  // local volumes incl. the reference), the complex64 detector-side and exchange
+  // arrays (8 local projection / mid arrays), two 16-row grid sets, the encoder
+  // matrices (2 distinct slab shapes x key_dim x 2 x slab floats), 2 GiB of tables
+  double local = 1.0;
+  if (comm && comm->world() > 1) local = 1.0 / comm->world() + 1.0 / (g.n1 / e > 0 ? g.n1 / e : 1);
+  const double V = static_cast<double>(g.n1 * g.n0 * g.n2) * local;
+  const double P = static_cast<double>(std::max(g.n_theta * g.h * g.w, g.n1 * g.h * g.n2)) * local;
+  const double grids = 4.0 * static_cast<double>(4 * g.n1 * g.n2 * 16 * 16);
+  const double enc_bytes = 2.0 * rc.encoder.key_dim * 2.0 * static_cast<double>(slab) * sizeof(float);
+  const double after = 17.0 * 16.0 * V + 8.0 * 8.0 * P + grids + enc_bytes + 2.0 * (1u << 30);
+  const double budget = std::max(0.0, static_cast<double>(free_b) - after) * 0.9;
+  std::size_t bytes = static_cast<std::size_t>(std::max(floor_b, std::min(want, budget)));
   if (const char* ov = std::getenv("MLRG_MEMO_ARENA_BYTES")) bytes = static_cast<std::size_t>(std::atoll(ov));
   // one GPU: the lookups run on the device (memo_gpu.hpp) unless the config needs
   // the host client (global cache, baseline pipeline's memoized f2d, other slab

@@ -20,6 +20,8 @@ ColdTier::ColdTier(std::string name, int rank, std::size_t chunk_bytes)
 }
 
 ColdTier::~ColdTier() {
+  if (pool_thread_.joinable()) pool_thread_.join();
+  for (void* p : pool_) cudaFreeHost(p);
   for (auto& [key, c] : chunks_) {
     if (!c.host) continue;
     if (c.shm) {
@@ -61,6 +63,15 @@ ColdTier::Chunk& ColdTier::chunk(int owner, int c, std::size_t bytes) {
   ch.bytes = bytes;
   if (name_.empty()) {
     if (owner != rank_) throw std::logic_error("cold tier: a private tier holds this rank's values only");
+    if (bytes == chunk_bytes_) {
+      if (pool_thread_.joinable()) pool_thread_.join();
+      std::lock_guard<std::mutex> lk(pool_mu_);
+      if (!pool_.empty()) {
+        ch.host = pool_.back();
+        pool_.pop_back();
+        return ch;
+      }
+    }
     MLRG_CUDA(cudaHostAlloc(&ch.host, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
     return ch;
   }
@@ -92,6 +103,33 @@ ColdTier::Chunk& ColdTier::chunk(int owner, int c, std::size_t bytes) {
   ch.shm = true;
   ch.owned = own;
   return ch;
+}
+
+void ColdTier::prefetch(std::size_t bytes) {
+  if (!name_.empty() || pool_thread_.joinable()) return;
+  std::size_t have = 0;
+  {
+    std::lock_guard<std::mutex> lk(pool_mu_);
+    have = pool_.size() * chunk_bytes_;
+  }
+  const auto it = cur_.find(rank_);
+  if (it != cur_.end()) have += it->second.last - it->second.used;  // room left in the open chunk
+  if (have >= bytes) return;
+  const std::size_t n = (bytes - have + chunk_bytes_ - 1) / chunk_bytes_;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  pool_thread_ = std::thread([this, n, dev] {
+    cudaSetDevice(dev);
+    for (std::size_t i = 0; i < n; ++i) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, chunk_bytes_, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return;  // place() allocates synchronously (and reports) instead
+      }
+      std::lock_guard<std::mutex> lk(pool_mu_);
+      pool_.push_back(p);
+    }
+  });
 }
 
 void* ColdTier::device_ptr(const ColdRef& r) {
@@ -151,6 +189,70 @@ std::size_t ValueRing::live_bytes() const {
   std::size_t s = 0;
   for (const Live& v : live_) s += v.bytes;
   return s;
+}
+
+// ---- ColdSpiller ---------------------------------------------------------------------------
+
+ColdSpiller::ColdSpiller(char* arena, std::size_t capacity, std::size_t window, SetPtr set_ptr)
+    : arena_(arena), window_(window), ring_(capacity), set_ptr_(std::move(set_ptr)) {
+  MLRG_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  MLRG_CUDA(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming));
+  MLRG_CUDA(cudaEventCreateWithFlags(&ev_copied_, cudaEventDisableTiming));
+}
+
+ColdSpiller::~ColdSpiller() {
+  if (side_) {
+    cudaStreamSynchronize(side_);
+    cudaStreamDestroy(side_);
+  }
+  if (ev_ready_) cudaEventDestroy(ev_ready_);
+  if (ev_copied_) cudaEventDestroy(ev_copied_);
+}
+
+std::vector<ColdSpiller::Moved> ColdSpiller::copy_out(const std::vector<ValueRing::Live>& v, cudaStream_t s) {
+  std::vector<Moved> out;
+  out.reserve(v.size());
+  for (const ValueRing::Live& x : v) {
+    const ColdRef r = cold_.place(0, x.bytes);
+    cold_.copy_in(r, arena_ + x.off, x.bytes, s);
+    out.push_back(Moved{x.id, cold_.device_ptr(r)});
+  }
+  spilled_ += static_cast<std::int64_t>(v.size());
+  return out;
+}
+
+void ColdSpiller::apply(const std::vector<Moved>& m, cudaStream_t s) {
+  if (m.empty()) return;
+  std::vector<std::uint64_t> ids;
+  std::vector<const void*> ptrs;
+  for (const Moved& x : m) {
+    ids.push_back(x.id);
+    ptrs.push_back(x.ptr);
+  }
+  set_ptr_(ids, ptrs, s);
+}
+
+void ColdSpiller::flush(cudaStream_t s) {
+  // 1. last flush's copies are done before window k+1 can overwrite their span
+  if (!pending_.empty()) {
+    MLRG_CUDA(cudaStreamWaitEvent(s, ev_copied_, 0));
+    apply(pending_, s);
+    pending_.clear();
+  }
+  // 2. anything left in window k+1's span goes now, in stream order
+  apply(copy_out(ring_.make_room(window_), s), s);
+  // 3. the span after it starts moving out in the background
+  if (ring_.capacity() >= 2 * window_ + window_ / 2 && !ring_.empty()) {
+    ValueRing probe = ring_;
+    const std::vector<ValueRing::Live> later = probe.make_room(2 * window_);
+    if (!later.empty()) {
+      ring_ = probe;  // those values leave the live list now; their HBM copies stay valid until step 1
+      MLRG_CUDA(cudaEventRecord(ev_ready_, s));
+      MLRG_CUDA(cudaStreamWaitEvent(side_, ev_ready_, 0));
+      pending_ = copy_out(later, side_);
+      MLRG_CUDA(cudaEventRecord(ev_copied_, side_));
+    }
+  }
 }
 
 }  // namespace mlrg

@@ -23,7 +23,10 @@
 #include <cstddef>
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -54,6 +57,10 @@ class ColdTier {
   /// Enqueues the spill copy of this rank's value (call on the owner only).
   void copy_in(const ColdRef& r, const void* dev_src, std::size_t bytes, cudaStream_t s);
   std::size_t bytes_placed(int owner) const;
+  /// Private tier: keep at least `bytes` of pinned chunks allocated ahead of
+  /// place(), on a host thread (page pinning costs ~0.1-0.3 s/GB and would
+  /// otherwise sit on the flush's critical path).
+  void prefetch(std::size_t bytes);
 
  private:
   struct Chunk {
@@ -76,6 +83,10 @@ class ColdTier {
   std::map<int, Cursor> cur_;
   std::map<std::pair<int, int>, Chunk> chunks_;
   std::map<std::pair<int, int>, std::size_t> sizes_;  // chunk sizes (replicated)
+  // pre-allocated pinned chunks of chunk_bytes_ (private tier)
+  std::mutex pool_mu_;
+  std::vector<void*> pool_;
+  std::thread pool_thread_;
 };
 
 /// Bookkeeping of one HBM ring arena (capacity bytes, 256-byte granules).
@@ -105,10 +116,53 @@ class ValueRing {
   /// [head, head + window), or [head, cap) and [0, window) when that wraps.
   std::vector<Live> make_room(std::size_t window);
   std::size_t live_bytes() const;
+  bool empty() const { return live_.empty(); }
 
  private:
   std::size_t cap_ = 0, head_ = 0;
   std::deque<Live> live_;  // allocation order
+};
+
+/// The spill policy of one process-private ring (the device memo and the
+/// host client on one GPU), asynchronous: at the flush that ends window k it
+///   1. makes the main stream wait for the copies started at flush k-1 and
+///      repoints those values to their cold copies,
+///   2. spills (synchronously, on the main stream) whatever still overlaps
+///      the span window k+1 can fill,
+///   3. starts copying out, on a side stream, the values in the span after
+///      it (window k+2's), whose HBM copies stay readable until step 1 of the
+///      next flush, so those transfers overlap window k+1's compute.
+/// (Pinned cold chunks are allocated when first needed: pinning on a host
+/// thread ahead of need stalled the launching thread in the driver.)
+class ColdSpiller {
+ public:
+  /// set_ptr(id, ptr): repoint value `id` (the caller updates its tables, ordered on `s`).
+  using SetPtr = std::function<void(const std::vector<std::uint64_t>&, const std::vector<const void*>&, cudaStream_t)>;
+  ColdSpiller(char* arena, std::size_t capacity, std::size_t window, SetPtr set_ptr);
+  ~ColdSpiller();
+  ValueRing& ring() { return ring_; }
+  /// At each flush, after the window's values were noted in ring().
+  void flush(cudaStream_t s);
+  std::int64_t spilled() const { return spilled_; }
+  std::size_t spilled_bytes() const { return cold_.bytes_placed(0); }
+
+ private:
+  struct Moved {
+    std::uint64_t id;
+    const void* ptr;
+  };
+  std::vector<Moved> copy_out(const std::vector<ValueRing::Live>& v, cudaStream_t s);
+  void apply(const std::vector<Moved>& m, cudaStream_t s);
+
+  char* arena_;
+  std::size_t window_;
+  ValueRing ring_;
+  ColdTier cold_{"", 0};
+  SetPtr set_ptr_;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_ready_ = nullptr, ev_copied_ = nullptr;
+  std::vector<Moved> pending_;  // copies in flight on side_
+  std::int64_t spilled_ = 0;
 };
 
 }  // namespace mlrg

@@ -60,6 +60,8 @@ void device_free(void* p, std::size_t bytes);
 void* pinned(std::size_t bytes);
 void pinned_free(void* p, std::size_t bytes);
 void release_cache();
+/// Device bytes held by the cache (free for this process's next allocations).
+std::size_t cached_device_bytes();
 }  // namespace alloc
 #define MLRG_LAUNCH_CHECK(name) (::mlrg::prof::count_launch(), ::mlrg::cuda_check(cudaGetLastError(), name))
 

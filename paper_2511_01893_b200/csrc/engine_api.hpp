@@ -149,7 +149,8 @@ class Engine {
     std::size_t off, bytes;
   };
   std::vector<Pending> pending_;  // values allocated this window, in staging (= id) order
-  std::unique_ptr<ColdTier> cold_;
+  std::unique_ptr<ColdTier> cold_;        // sharded: shared segments, synchronous spills
+  std::unique_ptr<ColdSpiller> spiller_;  // one rank: asynchronous spills
   std::int64_t spilled_ = 0;
   std::unique_ptr<DeviceMemo> dmemo_;
   ops::CnnWork cnn_work_;  // encoder_variant = cnn scratch

@@ -300,7 +300,6 @@ DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int 
       log_cap_(std::int64_t{1} << 16) {
   if (kd_ < 1 || kd_ > kMaxKd) throw std::invalid_argument("device memo: key_dim must be in [1, 64]");
   window_inserts_ = std::max(1, window_inserts);
-  ring_.reset(arena_bytes_);
   if (max_slabs_ > kStageThreads) throw std::invalid_argument("device memo: more than 1024 slabs per operator call");
   if (client_.config().global_cache) throw std::invalid_argument("device memo: global_cache is host-only");
   if (client_.store().ivf().nlist > kMaxProbe) throw std::invalid_argument("device memo: nlist must be <= 64");
@@ -366,6 +365,14 @@ void DeviceMemo::set_slabs(OpId op, const std::vector<std::size_t>& value_bytes,
   if (arena_bytes_ < need)
     throw std::invalid_argument("device memo: value arena of " + std::to_string(arena_bytes_) +
                                 " bytes is below one insert window (" + std::to_string(need) + " bytes)");
+  spiller_ = std::make_unique<ColdSpiller>(
+      arena_.get(), arena_bytes_, static_cast<std::size_t>(window_inserts_) * max_slab_bytes_,
+      [this](const std::vector<std::uint64_t>& ids, const std::vector<const void*>& ptrs, cudaStream_t st) {
+        for (std::size_t i = 0; i < ids.size(); ++i) {  // pageable source: staged before the call returns
+          MLRG_CUDA(cudaMemcpyAsync(vptr_.get() + ids[i], &ptrs[i], sizeof(void*), cudaMemcpyHostToDevice, st));
+          client_.store().set_value_ptr(ids[i], static_cast<const float2*>(ptrs[i]));
+        }
+      });
   MLRG_CUDA(cudaMemcpyAsync(slab_vbytes_.get() + o * max_slabs_, vb.data(), vb.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, s));
   MLRG_CUDA(cudaMemcpyAsync(slab_counts_.get() + o * max_slabs_, oc.data(), oc.size() * sizeof(long long),
@@ -415,27 +422,13 @@ void DeviceMemo::upload_ivf(cudaStream_t s) {
   trained_ = true;
 }
 
-// Frees the ring span the next window can fill: the oldest values overlapping
-// it move to the cold tier (pinned host, device-mapped) and their value
-// pointers are repointed there; decisions and ids are unaffected.
+// Frees the ring span the next window can fill (ColdSpiller: the oldest
+// values overlapping it move to pinned host memory and their value pointers
+// are repointed there, partly in the background); decisions and ids are unaffected.
 void DeviceMemo::spill(cudaStream_t s) {
-  ring_.reset_head(static_cast<std::size_t>(h_state_.get()[2]));
-  const std::vector<ValueRing::Live> out =
-      ring_.make_room(static_cast<std::size_t>(window_inserts_) * max_slab_bytes_);
-  if (out.empty()) return;
   prof::HostSpan span("host:memo_spill");
-  std::vector<const float2*> ptrs(out.size());
-  for (std::size_t i = 0; i < out.size(); ++i) {
-    const ColdRef r = cold_.place(0, out[i].bytes);
-    cold_.copy_in(r, arena_.get() + out[i].off, out[i].bytes, s);
-    ptrs[i] = static_cast<const float2*>(cold_.device_ptr(r));
-  }
-  for (std::size_t i = 0; i < out.size(); ++i) {
-    MLRG_CUDA(cudaMemcpyAsync(vptr_.get() + out[i].id, &ptrs[i], sizeof(void*), cudaMemcpyHostToDevice, s));
-    client_.store().set_value_ptr(out[i].id, ptrs[i]);
-  }
-  MLRG_CUDA(cudaStreamSynchronize(s));
-  spilled_ += static_cast<std::int64_t>(out.size());
+  spiller_->ring().reset_head(static_cast<std::size_t>(h_state_.get()[2]));
+  spiller_->flush(s);
 }
 
 void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) {
@@ -486,8 +479,9 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
   for (long long i = 0; i < nstaged; ++i) {
     ValueRef v;
     v.dev = vp[static_cast<std::size_t>(i)];
-    ring_.note(static_cast<std::uint64_t>(npub + i), static_cast<std::size_t>(reinterpret_cast<const char*>(v.dev) - arena),
-               static_cast<std::size_t>(vb[static_cast<std::size_t>(i)] - 8) / 2);
+    spiller_->ring().note(static_cast<std::uint64_t>(npub + i),
+                          static_cast<std::size_t>(reinterpret_cast<const char*>(v.dev) - arena),
+                          static_cast<std::size_t>(vb[static_cast<std::size_t>(i)] - 8) / 2);
     v.norm = vn[static_cast<std::size_t>(i)];
     v.bytes = static_cast<std::size_t>(vb[static_cast<std::size_t>(i)]);
     v.count = static_cast<std::int64_t>((v.bytes - 8) / 16);

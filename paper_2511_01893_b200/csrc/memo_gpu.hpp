@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "cold_tier.hpp"
@@ -84,8 +85,8 @@ class DeviceMemo {
   /// records its decisions but never flushes its inserts).
   void flush(cudaStream_t s, std::vector<Audit>* audit, bool publish = true);
   /// Values spilled to the cold tier so far (count, bytes).
-  std::int64_t spilled() const { return spilled_; }
-  std::size_t spilled_bytes() const { return cold_.bytes_placed(0); }
+  std::int64_t spilled() const { return spiller_ ? spiller_->spilled() : 0; }
+  std::size_t spilled_bytes() const { return spiller_ ? spiller_->spilled_bytes() : 0; }
   std::size_t arena_bytes() const { return arena_bytes_; }
 
  private:
@@ -125,9 +126,7 @@ class DeviceMemo {
   PinnedBuffer<long long> h_state_;
   int window_inserts_;
   std::size_t max_slab_bytes_ = 0;  // largest value slab (256-byte granules)
-  ValueRing ring_;
-  ColdTier cold_{"", 0};
-  std::int64_t spilled_ = 0;
+  std::unique_ptr<ColdSpiller> spiller_;  // created with the first slab table
 };
 
 }  // namespace mlrg

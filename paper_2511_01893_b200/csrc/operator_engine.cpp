@@ -100,9 +100,17 @@ Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_
                                   " bytes)");
     arena_.resize(arena_cap_);
     if (shard_.sharded()) arena_peers_ = std::make_unique<PeerMemory>(*shard_.comm, arena_.get());
-    rings_.assign(static_cast<std::size_t>(shard_.world), ValueRing(arena_cap_));
-    cold_ = std::make_unique<ColdTier>(shard_.sharded() ? shard_.comm->name() : std::string(),
-                                       shard_.sharded() ? shard_.comm->rank() : 0);
+    if (shard_.sharded()) {
+      rings_.assign(static_cast<std::size_t>(shard_.world), ValueRing(arena_cap_));
+      cold_ = std::make_unique<ColdTier>(shard_.comm->name(), shard_.comm->rank());
+    } else {
+      spiller_ = std::make_unique<ColdSpiller>(
+          arena_.get(), arena_cap_, window_bytes_,
+          [this](const std::vector<std::uint64_t>& ids, const std::vector<const void*>& ptrs, cudaStream_t) {
+            for (std::size_t i = 0; i < ids.size(); ++i)
+              memo_->store().set_value_ptr(ids[i], static_cast<const float2*>(ptrs[i]));
+          });
+    }
   }
 }
 
@@ -120,7 +128,8 @@ void Engine::exchange_fence() {
 float2* Engine::value_slot(int owner, std::int64_t count) {
   const std::size_t bytes = ValueRing::granule(static_cast<std::size_t>(count) * sizeof(float2));
   // spill_values() freed one window's span at the last flush; a window never inserts more
-  const std::size_t off = rings_[static_cast<std::size_t>(owner)].alloc(bytes);
+  ValueRing& ring = spiller_ ? spiller_->ring() : rings_[static_cast<std::size_t>(owner)];
+  const std::size_t off = ring.alloc(bytes);
   pending_.push_back(Pending{owner, off, bytes});
   char* base = arena_peers_ ? static_cast<char*>(arena_peers_->at(owner)) : arena_.get();
   return reinterpret_cast<float2*>(base + off);
@@ -132,8 +141,13 @@ void Engine::spill_values() {
   const std::uint64_t n = store.key_count();
   if (n < pending_.size()) throw std::logic_error("memo: fewer published values than allocated");
   std::uint64_t id = n - pending_.size();
-  for (const Pending& p : pending_) rings_[static_cast<std::size_t>(p.owner)].note(id++, p.off, p.bytes);
+  for (const Pending& p : pending_)
+    (spiller_ ? spiller_->ring() : rings_[static_cast<std::size_t>(p.owner)]).note(id++, p.off, p.bytes);
   pending_.clear();
+  if (spiller_) {  // one rank: host-side pointers only, the copies are ordered on the engine stream
+    spiller_->flush(s_);
+    return;
+  }
   struct Moved {
     std::uint64_t id;
     ColdRef ref;
@@ -155,9 +169,12 @@ void Engine::spill_values() {
   spilled_ += static_cast<std::int64_t>(moved.size());
 }
 
-std::int64_t Engine::spilled_values() const { return dmemo_ ? dmemo_->spilled() : spilled_; }
+std::int64_t Engine::spilled_values() const {
+  return dmemo_ ? dmemo_->spilled() : spiller_ ? spiller_->spilled() : spilled_;
+}
 std::size_t Engine::spilled_bytes() const {
   if (dmemo_) return dmemo_->spilled_bytes();
+  if (spiller_) return spiller_->spilled_bytes();
   std::size_t b = 0;
   for (int r = 0; cold_ && r < static_cast<int>(rings_.size()); ++r) b += cold_->bytes_placed(r);
   return b;

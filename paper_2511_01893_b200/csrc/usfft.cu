@@ -482,8 +482,11 @@ constexpr int kPatchR = 8, kPatchC = 4;
 constexpr int KH = KB / 2;
 
 struct SpreadShared {
-  double wr[2][2][32][kPatchR];  // [pair][buf][target][patch row]
-  double wc[2][2][32][kPatchC];  // [pair][buf][target][patch column]
+  // [pair][buf][patch row / column][target], rows padded to 33 doubles: the
+  // staging writes (lane = target) and the per-target reads (lane = cell:
+  // 8 rows / 4 columns, one target) are both bank-conflict free
+  double wr[2][2][kPatchR][33];
+  double wc[2][2][kPatchC][33];
   float4 vstage[4][2][32][KH / 2];  // per warp, double-buffered half values
   double2 vald[4][32][KH];          // per warp, widened chunk values
   int last[2];                      // per pair: this item completes its split patch
@@ -522,7 +525,7 @@ __device__ __forceinline__ void stage_spread_chunk(SpreadShared& sh, int pair, i
 #pragma unroll
       for (int i = 0; i < kPatchR; ++i) {
         const int a = (a0 + i) & mask1;
-        sh.wr[pair][buf][lane][i] = a < W ? wt[a] : 0.0;
+        sh.wr[pair][buf][i][lane] = a < W ? wt[a] : 0.0;
       }
     } else {
       const int b0 = pc0 - c0[t];
@@ -530,7 +533,7 @@ __device__ __forceinline__ void stage_spread_chunk(SpreadShared& sh, int pair, i
 #pragma unroll
       for (int j = 0; j < kPatchC; ++j) {
         const int b = (b0 + j) & mask2;
-        sh.wc[pair][buf][lane][j] = b < W ? wt[b] : 0.0;
+        sh.wc[pair][buf][j][lane] = b < W ? wt[b] : 0.0;
       }
     }
     const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB + half * KH);
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
     __syncwarp();
 #pragma unroll 2
     for (int j = 0; j < n; ++j) {
-      const double wgt = sh.wr[pair][buf][j][ri] * sh.wc[pair][buf][j][cj];
+      const double wgt = sh.wr[pair][buf][ri][j] * sh.wc[pair][buf][cj][j];
       const double2* vp = sh.vald[warp][j];
 #pragma unroll
       for (int kk = 0; kk < KH; ++kk) {

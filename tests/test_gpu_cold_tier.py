@@ -15,12 +15,14 @@ import test_gpu_dist as dist_t
 pytestmark = pytest.mark.gpu
 
 
-def min_arena(n, n_inner=4, world=1):
-    """One insert window + one slab (c_abi.cpp build_engine): the smallest legal ring."""
+def min_arena(n, n_inner=4, world=1, windows=1):
+    """`windows` insert windows + one slab (c_abi.cpp build_engine); 1: the smallest
+    legal ring (every spill synchronous at the flush), >= 2.5: ColdSpiller also
+    copies the following window's span out in the background."""
     slabs = -(-n // 16)
     most = -(-slabs // world)
     window = min(256, 4 * n_inner * most)
-    return (window + 1) * ((16 * n * n * 8 + 255) // 256 * 256)
+    return (windows * window + 1) * ((16 * n * n * 8 + 255) // 256 * 256)
 
 
 def config_text(n, nt, memo):
@@ -30,17 +32,18 @@ def config_text(n, nt, memo):
 
 @pytest.mark.parametrize("case", ["recon_c32_memo_grid", "recon_cfg1_memo_direct"])
 @pytest.mark.parametrize("device_memo", ["1", "0"])
-def test_tiny_arena_spills_and_matches_reference(mlrg, torch_cuda, monkeypatch, case, device_memo):
+@pytest.mark.parametrize("windows", [1, 3])
+def test_tiny_arena_spills_and_matches_reference(mlrg, torch_cuda, monkeypatch, case, device_memo, windows):
     torch = torch_cuda
     z = golden(case)
     n, nt = z["phantom"].shape[0], z["data"].shape[0]
     monkeypatch.setenv("MLRG_DEVICE_MEMO", device_memo)
-    monkeypatch.setenv("MLRG_MEMO_ARENA_BYTES", str(min_arena(n)))
+    monkeypatch.setenv("MLRG_MEMO_ARENA_BYTES", str(min_arena(n, windows=windows)))
     u = torch.empty((n, n, n), dtype=torch.complex64, device="cuda")
     r = mlrg.reconstruct_device(config_text(n, nt, "local"), torch.from_numpy(z["data"]).cuda(), u,
                                 reference=torch.from_numpy(z["phantom"]).cuda())
     t = r.tiers()
-    assert t["arena_bytes"] == min_arena(n)
+    assert t["arena_bytes"] == min_arena(n, windows=windows)
     assert t["spilled_values"] > 0 and t["spilled_bytes"] > 0, t
     meta, _ = r.audit()
     assert np.array_equal(meta, z["audit_int"]), "decisions differ with a spilling arena"
