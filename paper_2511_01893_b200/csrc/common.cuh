@@ -205,9 +205,9 @@ struct NoStore {
 // first pass reads load(row, b) for row < m (natural input order); with GOUT
 // the last pass hands X[row] of column b to store(row, b, X) and the tile is
 // left as scratch; otherwise the tile holds the input / output.
-template <int SIGN, bool GIN = false, bool GOUT = false, bool ZP = false, class Load = NoLoad, class Store = NoStore>
-__device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw,
-                                             const Load& load = Load(), const Store& store = Store()) {
+template <int SIGN, bool GIN, bool GOUT, bool ZP, class Load, class Store>
+__device__ __forceinline__ void fft_stockham_impl(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw,
+                                                  const Load& load, const Store& store) {
   const int b = threadIdx.x % nb, g = threadIdx.x / nb;
   const int npass = (logm + 2) / 3;
   int logns = 0, p = 0;
@@ -229,6 +229,28 @@ __device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int l
     else if (last) stockham_pass<8, 3, SIGN, false, GOUT, false>(s, ld, b, g, logm, logns, tw, load, store);
     else stockham_pass<8, 3, SIGN, false, false, false>(s, ld, b, g, logm, logns, tw, load, store);
   }
+}
+
+// The transform with the common shapes' (logm, nb, ld) as literals, so the
+// inlined passes' index arithmetic (strides, masks, the column / butterfly
+// split of threadIdx) folds into immediates: 256^3 and 512^3 run 512- and
+// 1024-point transforms over 4 or 8 columns per CTA. Other shapes take the
+// general path.
+template <int SIGN, bool GIN = false, bool GOUT = false, bool ZP = false, class Load = NoLoad, class Store = NoStore>
+__device__ __forceinline__ void fft_stockham(double2* s, int logm, int nb, int ld, const double2* __restrict__ tw,
+                                             const Load& load = Load(), const Store& store = Store()) {
+#ifndef MLRG_FFT_GENERIC_ONLY
+#define MLRG_FFT_CASE(L, N)                                                                      \
+  if (logm == L && nb == N) {                                                                    \
+    if (ld == N) return fft_stockham_impl<SIGN, GIN, GOUT, ZP>(s, L, N, N, tw, load, store);     \
+    if (ld == N + 1) return fft_stockham_impl<SIGN, GIN, GOUT, ZP>(s, L, N, N + 1, tw, load, store); \
+  }
+  MLRG_FFT_CASE(9, 8)
+  MLRG_FFT_CASE(10, 4)
+  MLRG_FFT_CASE(10, 8)
+#undef MLRG_FFT_CASE
+#endif
+  fft_stockham_impl<SIGN, GIN, GOUT, ZP>(s, logm, nb, ld, tw, load, store);
 }
 
 }  // namespace mlrg

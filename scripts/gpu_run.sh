@@ -1,9 +1,9 @@
-timeout 1200 python -m pytest tests/test_gpu_cold_tier.py -q -x > gpurun_out/cold.txt 2>&1; tail -1 gpurun_out/cold.txt
-timeout 1200 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-offload-run > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; tail -2 gpurun_out/bench_full.err
-python - <<'PY'
-import json
-d=json.load(open('gpurun_out/bench_full.json'))
-print('value', d['value'], 'memo_on', json.dumps(d['memo_on']))
-for k,v in (d['configs_extra'] or {}).items(): print(k, v['value'], json.dumps(v.get('memo_on'))[:500])
-PY
-nvidia-smi --query-gpu=memory.total --format=csv; free -g | head -2
+timeout 600 python -m pytest tests/test_gpu_ops.py tests/test_gpu_cols4.py -q -x 2>&1 | tail -1
+for v in default gen; do
+  if [ $v = default ]; then unset MLRG_LIB; else export MLRG_LIB=$PWD/paper_2511_01893_b200/libv/$v/libmlr.so; fi
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-memo-run --no-offload-run --no-extra > gpurun_out/b_$v.json 2> gpurun_out/b_$v.err
+  python -c "
+import json,sys
+d=json.load(open('gpurun_out/b_$v.json')); k=d['roofline']['kernels_ms_per_step']
+print('$v', 'it/s %.2f'%d['value'], ' '.join('%s=%.2f'%(n.replace('k_fu2d_',''),v) for n,v in k.items()))"
+done
