@@ -123,6 +123,16 @@ void encode(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns,
 void encode(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
             double* work, float* keys, double* norms2, cudaStream_t s);
 std::size_t encode_work_doubles(int ns, int kd);
+/// The same GEMM on the tcgen05 tensor cores (encode_tc.cu): one launch of at
+/// most 16 slabs writing encode_tc_grid() CTA partial tiles [slab][kd + 1] into
+/// `work` (summed by the k_encode_reduce pass). Supported when kd <= 60, 2n is
+/// a multiple of 4 and K = 2n spans at least two 128-column stages per SM.
+bool encode_tc_supported(SlabGeom shape, const float* P, int kd, int ns);
+int encode_tc_grid();
+void encode_tc(const float2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+               double* work, cudaStream_t s);
+void encode_tc(const double2* x, SlabGeom shape, const std::int64_t* starts, int ns, const float* P, int kd,
+               double* work, cudaStream_t s);
 
 /// A list of slabs of one SlabGeom (start/extent per entry) for the batched
 /// copies: hits read `value[q]` scaled by `scale[q]`, stores write `dst[q]`.

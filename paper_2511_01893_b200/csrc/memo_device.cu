@@ -4,6 +4,7 @@
 // materialise hits and capture miss values (scalerun.cpp:86-105, 250-283).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "device.hpp"
@@ -506,14 +507,24 @@ void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns
     const int nb = std::min(kEncSlabs, ns - b);
     SlabList sl{};
     for (int q = 0; q < nb; ++q) sl.start[q] = starts[b + q];
-    const int blocks = enc_blocks();
+    int blocks = enc_blocks();
     prof::begin("k_encode", s);
-    static const bool tc = [] {  // MLRG_ENCODE_TC=0: the FFMA path
+    // MLRG_ENCODE_TC: unset / "tcgen05" = the tcgen05 kernel where supported, "mma" = the
+    // mma.sync TF32 kernel, "0" = the FFMA path
+    static const int mode = [] {
       const char* e = std::getenv("MLRG_ENCODE_TC");
-      return !(e && *e == '0');
+      if (e && *e == '0') return 0;
+      if (e && std::string(e) == "mma") return 1;
+      return 2;
     }();
-    if (tc) k_encode<TX, true><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
-    else k_encode<TX, false><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
+    if (mode == 2 && encode_tc_supported(shape, P, kd, nb)) {
+      blocks = encode_tc_grid();
+      encode_tc(x, shape, starts + b, nb, P, kd, work, s);
+    } else if (mode >= 1) {
+      k_encode<TX, true><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
+    } else {
+      k_encode<TX, false><<<blocks, kEncWarps * 32, smem, s>>>(x, shape, sl, nb, P, n, kd, p_vec, work);
+    }
     MLRG_LAUNCH_CHECK("k_encode");
     prof::end("k_encode", s);
     const int per = nb * (kd + 1);

@@ -298,6 +298,15 @@ struct ClassRec {
 };
 static_assert(sizeof(ClassRec<10>) % 16 == 0 && sizeof(ClassRec<24>) % 16 == 0, "bulk-copy granularity");
 
+// MLRG_WIDE_GRID=1: complex128 grids for the ES kernel too (experiment)
+bool wide_grids_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("MLRG_WIDE_GRID");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // classes per gather CTA (MLRG_GATHER_PER_CTA overrides, for tuning)
 int gather_per_cta() {
   static const int v = [] {
@@ -353,7 +362,7 @@ __device__ __forceinline__ double widen_tap(T v) {
 
 // (the 24-tap Gaussian windows: 2 CTAs/SM, 128 registers)
 template <int W, class TG>
-__global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? MLRG_GATHER_MINB : 2) k_fu2d_gather(
+__global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) == 8 ? MLRG_GATHER_MINB : 3) : 2) k_fu2d_gather(
     const TG* __restrict__ G, int T, int w, int logm1, int ldg, int nk, const ClassRec<W>* __restrict__ recs,
     GatherOut eo, int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
   if (skipped(sk, 0)) return;
@@ -1216,7 +1225,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     t.b_tw.upload(twiddles(std::int64_t{1} << (px.logm - t.logA)), stream_);
   }
   prof::host_mark("host:usfft_patches");
-  t.wide = kernel_ == GridKernel::gaussian && !t.cols4;
+  t.wide = (kernel_ == GridKernel::gaussian || wide_grids_env()) && !t.cols4;
   t.ghost = (W - 1 + 7) & ~7;
   t.ldg = static_cast<int>(py.m) + t.ghost;
   t.S.resize(static_cast<std::size_t>(px.m * t.ldg * KB));
@@ -1226,7 +1235,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     int nb = 0;
     const std::size_t rb = static_cast<std::size_t>(gather_per_cta()) *
                            (W == kEsTaps ? sizeof(ClassRec<kEsTaps>) : sizeof(ClassRec<kTaps>));
-    if (t.wide) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kTaps, double2>, 32 * kGatherWarps, rb);
+    if (t.wide && W == kEsTaps) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kEsTaps, double2>, 32 * kGatherWarps, rb);
+    else if (t.wide) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kTaps, double2>, 32 * kGatherWarps, rb);
     else if (W == kEsTaps) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kEsTaps, float2>, 32 * kGatherWarps, rb);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fu2d_gather<kTaps, float2>, 32 * kGatherWarps, rb);
     const std::int64_t slots = std::max(1, nb) * static_cast<std::int64_t>(sm_count());
@@ -1452,7 +1462,8 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
           grid_ptr, t.nclass, static_cast<int>(g_.w), t.px.logm, t.ldg, nb, reinterpret_cast<const Rec*>(t.recs.get()),
           eo, per_cta, partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0, sk);
     };
-    if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kTaps>{});
+    if (t.wide && t.px.taps == kEsTaps) launch_gather(k_fu2d_gather<kEsTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kEsTaps>{});
+    else if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kTaps>{});
     else if (t.px.taps == kEsTaps) launch_gather(k_fu2d_gather<kEsTaps, float2>, G, ClassRec<kEsTaps>{});
     else launch_gather(k_fu2d_gather<kTaps, float2>, G, ClassRec<kTaps>{});
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
@@ -1507,7 +1518,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     prof::begin("k_fu2d_adj_spread", s);
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps, float2> : k_fu2d_adj_spread<kTaps, float2>;
     if (t.wide)
-      k_fu2d_adj_spread<kTaps, double2><<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(
+      (t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps, double2> : k_fu2d_adj_spread<kTaps, double2>)<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(
           val, t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
           t.t_w1.get(), t.t_w2.get(), reinterpret_cast<double2*>(Gd), partial, t.split.get(), split_cnt, sk);
     else

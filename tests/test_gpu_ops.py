@@ -129,6 +129,30 @@ def test_encode_keys_match_reference(mlrg, torch_cuda):
             assert abs(norms[s] - np.linalg.norm(chunk)) < 1e-6 * norms[s]
 
 
+@pytest.mark.parametrize("shape", [(64, 64, 64), (40, 48, 72)])
+def test_encode_tcgen05_keys_match_reference(mlrg, torch_cuda, shape):
+    """Slab shapes large enough for the tcgen05 encoder (encode_tc.cu: K = 2n spans
+    >= 2 stages of 128 columns per SM): keys of both slab axes against the
+    reference's double-accumulated projection (encoder.cpp:405-422), including a
+    ragged last slab (40 planes / 48 rows = 2.5 / 3 slabs)."""
+    torch = torch_cuda
+    d0, d1, d2 = shape
+    ctx = mlrg.Context(d0, d1, d2, d0, d1, d2)
+    x = (np.random.default_rng(5).standard_normal(shape) + 1j * np.random.default_rng(6).standard_normal(shape)
+         + 0.25).astype(np.complex64)
+    for op in ("fu1d", "fu2d"):
+        keys, norms = ctx.encode(op, dev(torch, x))
+        ax = 1 if op == "fu2d" else 0
+        mats = {}
+        for s in range(keys.shape[0]):
+            chunk = np.take(x.astype(np.complex128), range(16 * s, min(16 * s + 16, shape[ax])), axis=ax)
+            if chunk.shape not in mats:
+                mats[chunk.shape] = O.projection_matrix(chunk.shape)
+            want = O.slot_mix(O.encode_projection(chunk, mats[chunk.shape]), 1337, s, mlrg.OPS[op])
+            assert np.allclose(keys[s], want, rtol=1e-5, atol=1e-5 * np.abs(want).max()), (op, s)
+            assert abs(norms[s] - np.linalg.norm(chunk)) < 1e-6 * norms[s]
+
+
 @pytest.mark.parametrize("idx,shape", [(0, (16, 16, 16)), (1, (4, 16, 16)), (2, (16, 8, 12))])
 def test_cnn_encoder_matches_reference_keys(mlrg, torch_cuda, idx, shape):
     """Device CNN keys (cnn.cu) against the reference's (encoder.cpp:95-197) for
