@@ -165,6 +165,9 @@ uint64_t mlrg_launch_count(void);
 void mlrg_prof_enable(int on);
 void mlrg_prof_reset(void);
 int mlrg_prof_query(const char* name, double* total_ms, int64_t* count);
+/** Writes every profiled span since the last reset as "name stream start_ms end_ms"
+ *  (times relative to the earliest span start). */
+int mlrg_prof_dump(const char* path);
 
 /* ---- the drop-in result's memo audit (extension of mlr.h) ---- */
 struct mlr_result;

@@ -123,6 +123,7 @@ _SIGS = {
     "mlrg_prof_enable": (None, [C.c_int]),
     "mlrg_prof_reset": (None, []),
     "mlrg_prof_query": (C.c_int, [C.c_char_p, _P, _P]),
+    "mlrg_prof_dump": (C.c_int, [C.c_char_p]),
 }
 EXPORTS = tuple(_SIGS)
 

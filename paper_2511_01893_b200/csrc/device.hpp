@@ -154,7 +154,7 @@ class PinnedBuffer {
 /// CTA order, so every reduction is deterministic (no float atomics).
 class Partials {
  public:
-  static constexpr int kMaxSlots = 1 << 17;
+  static constexpr int kMaxSlots = 1 << 20;  // 8 MB: the RSP pass of ~14K planes per rank
   Partials() {
     dev_.resize(static_cast<std::size_t>(kMaxSlots));
     host_.reserve(static_cast<std::size_t>(kMaxSlots));

@@ -528,7 +528,9 @@ void encode_impl(const TX* x, SlabGeom shape, const std::int64_t* starts, int ns
     MLRG_LAUNCH_CHECK("k_encode");
     prof::end("k_encode", s);
     const int per = nb * (kd + 1);
+    prof::begin("k_encode_reduce", s);
     k_encode_reduce<<<(per * 32 + 255) / 256, 256, 0, s>>>(work, blocks, nb, kd, keys + b * kd, norms2 + b);
+    prof::end("k_encode_reduce", s);
     MLRG_LAUNCH_CHECK("k_encode_reduce");
   }
 }
@@ -567,23 +569,31 @@ void store_impl(TO* out, SlabGeom g, const SlabBatch& b, int nb, const float2* s
 void dev_materialize(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
                      cudaStream_t s) {
   if (n <= 0) return;
+  prof::begin("k_dev_materialize", s);
   k_dev_materialize<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
+  prof::end("k_dev_materialize", s);
   MLRG_LAUNCH_CHECK("k_dev_materialize");
 }
 void dev_materialize(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
   if (n <= 0) return;
+  prof::begin("k_dev_materialize", s);
   k_dev_materialize<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
+  prof::end("k_dev_materialize", s);
   MLRG_LAUNCH_CHECK("k_dev_materialize");
 }
 void dev_store(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
                cudaStream_t s) {
   if (n <= 0) return;
+  prof::begin("k_dev_store", s);
   k_dev_store<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
+  prof::end("k_dev_store", s);
   MLRG_LAUNCH_CHECK("k_dev_store");
 }
 void dev_store(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
   if (n <= 0) return;
+  prof::begin("k_dev_store", s);
   k_dev_store<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
+  prof::end("k_dev_store", s);
   MLRG_LAUNCH_CHECK("k_dev_store");
 }
 

@@ -390,13 +390,17 @@ void DeviceMemo::lookup(OpId op, int n, const float* keys, const double* norms2,
                 client_.config().tau, keys, mix_perm_.get(), mix_sign_.get(), qkeys_.get(), cache_key_.get(),
                 cache_vid_.get(), keys_.get(), vbytes_.get(), svb, centroids_.get(), cl_ptr_.get(),
                 cl_ids_.get(), state_.get(), slabs_.get(), flags_.get(), flags_.get() + max_slabs_};
+  prof::begin("k_memo_lookup", s);
   k_memo_lookup<<<n, kLookupThreads, 0, s>>>(la);
+  prof::end("k_memo_lookup", s);
   MLRG_LAUNCH_CHECK("k_memo_lookup");
   StageArgs sa{n, kd_, o, iteration, static_cast<int>(client_.config().insert_queue_cap),
                static_cast<long long>(arena_bytes_), log_cap_, qkeys_.get(), norms2, svb, scn, keys_.get(),
                vbytes_.get(), vnorm_.get(), vptr_.get(), arena_.get(), state_.get(), slabs_.get(), skip_.get(),
                la.probed, la.queried, log_.get()};
+  prof::begin("k_memo_stage", s);
   k_memo_stage<<<1, static_cast<unsigned>((n + 31) / 32 * 32), 0, s>>>(sa);
+  prof::end("k_memo_stage", s);
   MLRG_LAUNCH_CHECK("k_memo_stage");
 }
 

@@ -2,6 +2,7 @@
 // are recorded on the launching stream, so a timer measures exactly the
 // kernel's device time span even when the host runs ahead.
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <map>
 #include <mutex>
@@ -21,6 +22,7 @@ std::atomic<bool> g_enabled{false};
 std::mutex g_mx;
 struct Span {
   cudaEvent_t a, b;
+  cudaStream_t s;
 };
 std::map<std::string, std::vector<Span>>& spans() {
   static std::map<std::string, std::vector<Span>> m;
@@ -86,7 +88,7 @@ void end(const char* name, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_mx);
   auto it = open_events().find(std::string(name) + "@" + std::to_string(reinterpret_cast<std::uintptr_t>(s)));
   if (it == open_events().end()) return;
-  spans()[name].push_back({it->second, e});
+  spans()[name].push_back({it->second, e, s});
   open_events().erase(it);
 }
 
@@ -107,6 +109,36 @@ void mlrg_prof_reset(void) {
     }
   mlrg::prof::spans().clear();
   mlrg::prof::host_spans().clear();
+}
+
+int mlrg_prof_dump(const char* path) {
+  std::lock_guard<std::mutex> lk(mlrg::prof::g_mx);
+  struct Row {
+    std::string name;
+    const mlrg::prof::Span* sp;
+  };
+  std::vector<Row> rows;
+  for (auto& [k, v] : mlrg::prof::spans())
+    for (auto& s : v) rows.push_back({k, &s});
+  if (rows.empty()) return 0;
+  // reference: the span whose start is earliest
+  cudaEvent_t ref = rows[0].sp->a;
+  for (auto& r : rows) {
+    if (cudaEventSynchronize(r.sp->b) != cudaSuccess) return MLR_ERR_RUNTIME;
+    float d = 0.f;
+    if (cudaEventElapsedTime(&d, ref, r.sp->a) != cudaSuccess) return MLR_ERR_RUNTIME;
+    if (d < 0.f) ref = r.sp->a;
+  }
+  std::FILE* f = std::fopen(path, "w");
+  if (!f) return MLR_ERR_IO;
+  for (auto& r : rows) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ref, r.sp->a);
+    cudaEventElapsedTime(&b, ref, r.sp->b);
+    std::fprintf(f, "%s %llu %.4f %.4f\n", r.name.c_str(), static_cast<unsigned long long>(reinterpret_cast<std::uintptr_t>(r.sp->s)), a, b);
+  }
+  std::fclose(f);
+  return 0;
 }
 
 int mlrg_prof_query(const char* name, double* total_ms, int64_t* count) {

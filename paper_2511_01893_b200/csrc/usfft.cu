@@ -1009,9 +1009,11 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   // ---- fu2d plans (nufft.cpp:185-187) ----
   t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
   t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
-  // the 2D grid passes run 256-thread CTAs (launch bounds 256 x 4): m * nb / 8 <= 256
-  if (t.px.m > 2048 || t.py.m > 2048)
-    throw std::invalid_argument("fu2d: n1 and n2 up to 1024 are supported on one device");
+  // the 2D grid passes hold one M-point double column per CTA (M x 16 B of shared memory,
+  // M / 8 threads) and the four-step column passes split M = A B up to 4096: n1, n2 <= 2048
+  // (configs[4]'s 2048^3)
+  if (t.px.m > 4096 || t.py.m > 4096)
+    throw std::invalid_argument("fu2d: n1 and n2 up to 2048 are supported");
   const std::size_t WS = static_cast<std::size_t>(W);
   const DimPlan &px = t.px, &py = t.py;
   const std::size_t T = fg.nu_x.size();
@@ -1292,6 +1294,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     allow_big_smem(k_fu2d_adj_spread<kEsTaps, float2>);
     allow_big_smem(k_fu2d_adj_spread<kTaps, float2>);
     allow_big_smem(k_fu2d_adj_spread<kTaps, double2>);
+    allow_big_smem(k_fu2d_adj_spread<kEsTaps, double2>);
     allow_big_smem(k_fu2d_cols<false, float2>);
     allow_big_smem(k_fu2d_cols<true, float2>);
     allow_big_smem(k_fu2d_cols<false, double2>);
