@@ -307,6 +307,12 @@ bool wide_grids_env() {
   return v;
 }
 
+// gather prefetch depth: rows in flight ahead of the row being summed
+#ifndef MLRG_GATHER_D
+#define MLRG_GATHER_D 1
+#endif
+constexpr int gather_depth(int W) { return W == 10 ? MLRG_GATHER_D : 1; }
+
 // classes per gather CTA (MLRG_GATHER_PER_CTA overrides, for tuning)
 int gather_per_cta() {
   static const int v = [] {
@@ -368,9 +374,9 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
   if (skipped(sk, 0)) return;
   constexpr int WH = W / 2;
   // rows in flight ahead of the one summed; the ring runs across classes, so
-  // its period must divide W
-  constexpr int D = W % 2 == 0 ? 1 : 0;
-  static_assert(D == 1, "the cross-class row ring needs an even W");
+  // its period D + 1 must divide W
+  constexpr int D = gather_depth(W);
+  static_assert(W % (D + 1) == 0, "the cross-class row ring period must divide W");
   extern __shared__ __align__(16) unsigned char gather_smem[];
   __shared__ unsigned long long bar;
   __shared__ double red_scratch[kGatherWarps * 2];
@@ -392,10 +398,14 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
   auto row = [&](const char* cb, int r) { return cb + static_cast<unsigned>(r & mask1) * rs; };
   TG buf[D + 1][WH];
   int s = s0 + warp;
-  if (s < s_end) {  // prime the ring with the first class's first row
-    const char* gr = row(col_base(s), rec[s - s0].r0);
+  if (s < s_end) {  // prime the ring with the first class's first D rows
+    const char* cb0 = col_base(s);
 #pragma unroll
-    for (int j = 0; j < WH; ++j) buf[0][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
+    for (int a = 0; a < D; ++a) {
+      const char* gr = row(cb0, rec[s - s0].r0 + a);
+#pragma unroll
+      for (int j = 0; j < WH; ++j) buf[a][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
+    }
   }
   for (; s < s_end; s += kGatherWarps) {
     const ClassRec<W>& R = rec[s - s0];
@@ -409,10 +419,10 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
     for (int a = 0; a < W; ++a) {
-      {  // row a + 1 of this class, or row 0 of the next
-        const char* gr = a + 1 < W ? row(cb, r0 + a + 1) : row(cbn, r0n);
+      {  // row a + D of this class, or row a + D - W of the next
+        const char* gr = a + D < W ? row(cb, r0 + a + D) : row(cbn, r0n + a + D - W);
 #pragma unroll
-        for (int j = 0; j < WH; ++j) buf[(a + 1) % (D + 1)][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
+        for (int j = 0; j < WH; ++j) buf[(a + D) % (D + 1)][j] = __ldg(reinterpret_cast<const TG*>(gr + j * CB));
       }
       double2 racc = make_double2(0.0, 0.0);
       auto tap = [&](auto jc) {
