@@ -150,6 +150,12 @@ int mlrg_memo_lookup(mlrg_memo* m, int64_t n, int key_dim, const float* keys, co
 int mlrg_memo_insert(mlrg_memo* m, int key_dim, const float* key, uint64_t value_bytes);
 int mlrg_memo_flush(mlrg_memo* m);
 int mlrg_memo_counters(const mlrg_memo* m, uint64_t out[11]);
+/* The store's IVF training (memostore.cpp:40-108): k-means++ seeding + Lloyd over
+ * nk keys of dim floats, then each key's nearest centroid; on_device selects the
+ * GPU trainer (memo_gpu.cu), which must equal the host's bit for bit. Writes
+ * min(k, nk) x dim centroids and nk indices. */
+int mlrg_kmeans(const float* keys, int64_t nk, int dim, int k, uint64_t seed, int iters, int on_device,
+                float* centroids, int64_t* nearest);
 
 /* ---- encoder matrix and slot mix (encoder.cpp:16-86, 369-379), host ---- */
 int mlrg_projection_matrix(int64_t d0, int64_t d1, int64_t d2, int key_dim, uint64_t seed, float* out,

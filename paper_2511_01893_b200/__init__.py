@@ -116,6 +116,7 @@ _SIGS = {
     "mlrg_memo_insert": (C.c_int, [_P, C.c_int, _P, _U64]),
     "mlrg_memo_flush": (C.c_int, [_P]),
     "mlrg_memo_counters": (C.c_int, [_P, _P]),
+    "mlrg_kmeans": (C.c_int, [_P, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, _P, _P]),
     "mlrg_projection_matrix": (C.c_int, [_I64, _I64, _I64, C.c_int, _U64, _P, _I64]),
     "mlrg_slot_mix": (C.c_int, [_P, C.c_int, _U64, _I64, C.c_int]),
     "mlrg_result_audit": (_I64, [_P, _P, _P, _I64]),

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <exception>
 #include <memory>
 #include <sstream>
@@ -1060,6 +1061,38 @@ int mlrg_memo_counters(const mlrg_memo* m, uint64_t out[11]) {
   return guarded([&] {
     need(m && out, "null argument");
     fill_counters(m->client->counters(), out);
+  });
+}
+
+int mlrg_kmeans(const float* keys, int64_t nk, int dim, int k, uint64_t seed, int iters, int on_device,
+                float* centroids, int64_t* nearest) {
+  return guarded([&] {
+    need(keys && centroids && nearest && nk > 0 && dim > 0 && k > 0, "null or empty argument");
+    std::vector<std::vector<float>> kv(static_cast<std::size_t>(nk));
+    for (int64_t i = 0; i < nk; ++i) kv[static_cast<std::size_t>(i)].assign(keys + i * dim, keys + (i + 1) * dim);
+    std::vector<std::vector<float>> cent;
+    std::vector<std::size_t> near(static_cast<std::size_t>(nk));
+    if (on_device) {
+      int dev = 0;
+      MLRG_CUDA(cudaGetDevice(&dev));
+      need(mlrg::gpu_kmeans_fits(static_cast<int>(nk), k, dim), "kmeans: too many keys for the device trainer");
+      mlrg::gpu_kmeans(kv, k, seed, iters, cent, near, dev);
+    } else {
+      cent = mlrg::kmeans_train(kv, k, seed, iters);
+      for (std::size_t i = 0; i < kv.size(); ++i) {
+        double best = std::numeric_limits<double>::max();
+        for (std::size_t c = 0; c < cent.size(); ++c) {
+          const double d = mlrg::l2_sq(kv[i].data(), cent[c].data(), dim);
+          if (d < best) {
+            best = d;
+            near[i] = c;
+          }
+        }
+      }
+    }
+    for (std::size_t c = 0; c < cent.size(); ++c)
+      std::memcpy(centroids + c * static_cast<std::size_t>(dim), cent[c].data(), sizeof(float) * static_cast<std::size_t>(dim));
+    for (std::size_t i = 0; i < near.size(); ++i) nearest[i] = static_cast<int64_t>(near[i]);
   });
 }
 

@@ -53,7 +53,13 @@ struct QueryOutcome {
 
 class MemoStore {
  public:
+  /// Trains the IVF index: centroids for `keys` (kmeans_train's exact result)
+  /// and each key's nearest final centroid (nearest_centroid's).
+  using Trainer = std::function<void(const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
+                                     std::vector<std::vector<float>>& centroids, std::vector<std::size_t>& nearest)>;
   explicit MemoStore(IvfConfig cfg = {});
+  /// Replaces the host k-means (the device memo trains on the GPU, memo_gpu.cu).
+  void set_trainer(Trainer t) { trainer_ = std::move(t); }
   std::uint64_t insert(const std::vector<float>& key, ValueRef value);
   QueryOutcome query(const std::vector<float>& key, float tau, int nprobe = 0) const;
   const ValueRef& value(std::uint64_t id) const { return values_.at(static_cast<std::size_t>(id)); }
@@ -75,6 +81,7 @@ class MemoStore {
   void train();
 
   IvfConfig cfg_;
+  Trainer trainer_;
   int key_dim_ = 0;
   bool trained_ = false;
   std::vector<Entry> flat_;

@@ -1,6 +1,8 @@
 #include "memo_gpu.hpp"
 
 #include <algorithm>
+#include <limits>
+#include <random>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -290,6 +292,177 @@ __global__ void __launch_bounds__(kStageThreads) k_memo_stage(StageArgs a) {
 
 }  // namespace
 
+namespace {
+
+// ---- IVF training on the GPU (memostore.cpp:40-108, kmeans_train in memo.cpp) ----
+// One CTA: k-means++ seeding with the reference's draws (pre-drawn on the host
+// from the same mt19937_64, one per centroid), then the Lloyd iterations and
+// the final nearest-centroid assignment. Every distance is the sequential
+// double sum over the key's dimensions with explicit _rn arithmetic (no FMA
+// contraction), every centroid sum runs over the keys in key order, ties
+// resolve to the lower index: the host's results bit for bit.
+constexpr int kKmThreads = 1024;
+
+__device__ __forceinline__ double km_l2(const float* __restrict__ a, const float* __restrict__ b, int d) {
+  double acc = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double x = __dsub_rn(static_cast<double>(a[i]), static_cast<double>(b[i]));
+    acc = __dadd_rn(acc, __dmul_rn(x, x));
+  }
+  return acc;
+}
+
+// Seeding (memostore.cpp:50-84) in one CTA: the distance updates run in
+// parallel, the total and the cumulative scan on one thread in key order.
+__global__ void __launch_bounds__(kKmThreads) k_km_seed(const float* __restrict__ keys, int nk, int dim, int k,
+                                                        const unsigned long long* __restrict__ draws,
+                                                        float* __restrict__ cent) {
+  extern __shared__ double km_smem[];
+  double* dist2 = km_smem;  // [nk]
+  __shared__ int pick;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  if (tid == 0) pick = static_cast<int>(draws[0] % static_cast<unsigned long long>(nk));
+  for (int i = tid; i < nk; i += bd) dist2[i] = 1.7976931348623157e308;
+  __syncthreads();
+  for (int c = 0;; ++c) {
+    const int p = pick;
+    for (int d = tid; d < dim; d += bd) cent[c * dim + d] = keys[static_cast<long long>(p) * dim + d];
+    __syncthreads();
+    if (c + 1 == k) break;
+    for (int i = tid; i < nk; i += bd) {
+      const double d = km_l2(keys + static_cast<long long>(i) * dim, cent + c * dim, dim);
+      if (d < dist2[i]) dist2[i] = d;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double total = 0.0;
+#pragma unroll 8
+      for (int i = 0; i < nk; ++i) total = __dadd_rn(total, dist2[i]);
+      int q = 0;
+      if (total > 0.0) {
+        const double target = __dmul_rn(static_cast<double>(draws[c + 1] >> 11) * 0x1.0p-53, total);
+        double run = 0.0;
+        q = nk - 1;
+        for (int i = 0; i < nk; ++i) {
+          run = __dadd_rn(run, dist2[i]);
+          if (run >= target) {
+            q = i;
+            break;
+          }
+        }
+      } else {
+        q = static_cast<int>(draws[c + 1] % static_cast<unsigned long long>(nk));
+      }
+      pick = q;
+    }
+    __syncthreads();
+  }
+}
+
+// Lloyd step 1: every (key, centroid) distance, one thread each.
+__global__ void k_km_dist(const float* __restrict__ keys, int nk, int dim, int k, const float* __restrict__ cent,
+                          double* __restrict__ dist) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(nk) * k) return;
+  const int i = static_cast<int>(t / k), c = static_cast<int>(t - static_cast<long long>(i) * k);
+  dist[t] = km_l2(keys + static_cast<long long>(i) * dim, cent + c * dim, dim);
+}
+// Lloyd step 2: each key's nearest centroid in centroid order (lower index wins ties).
+__global__ void k_km_assign(const double* __restrict__ dist, int nk, int k, int* __restrict__ owner) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nk) return;
+  double best = 1.7976931348623157e308;
+  int arg = 0;
+  for (int c = 0; c < k; ++c) {
+    const double d = dist[static_cast<long long>(i) * k + c];
+    if (d < best) {
+      best = d;
+      arg = c;
+    }
+  }
+  owner[i] = arg;
+}
+// Lloyd step 3: centroid (c, d) = mean of its keys' coordinate d, summed in key order.
+__global__ void k_km_update(const float* __restrict__ keys, int nk, int dim, int k, const int* __restrict__ owner,
+                            float* __restrict__ cent) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= k * dim) return;
+  const int c = o / dim, d = o - c * dim;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int i = 0; i < nk; ++i)
+    if (__ldg(owner + i) == c) {
+      ++cnt;
+      sum = __dadd_rn(sum, static_cast<double>(__ldg(keys + static_cast<long long>(i) * dim + d)));
+    }
+  if (cnt) cent[o] = __double2float_rn(__ddiv_rn(sum, static_cast<double>(cnt)));  // empty: keep
+}
+
+}  // namespace
+
+struct KmeansScratch {
+  cudaStream_t s = nullptr;
+  DeviceBuffer<float> keys, cent;
+  DeviceBuffer<double> dist;
+  DeviceBuffer<int> owner;
+  DeviceBuffer<unsigned long long> draws;
+  ~KmeansScratch() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+void gpu_kmeans(const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
+                std::vector<std::vector<float>>& cent, std::vector<std::size_t>& nearest, int device,
+                KmeansScratch* scratch) {
+  if (keys.empty()) throw std::invalid_argument("kmeans: no keys");
+  MLRG_CUDA(cudaSetDevice(device));  // may run on a host worker thread
+  KmeansScratch local;
+  KmeansScratch& w = scratch ? *scratch : local;
+  if (!w.s) MLRG_CUDA(cudaStreamCreateWithFlags(&w.s, cudaStreamNonBlocking));
+  const int nk = static_cast<int>(keys.size()), dim = static_cast<int>(keys.front().size());
+  k = std::min(k, nk);
+  std::mt19937_64 rng(seed);  // kmeans_train's draws: one for the first centroid, one per further centroid
+  std::vector<unsigned long long> draws(static_cast<std::size_t>(k));
+  for (auto& d : draws) d = rng();
+  std::vector<float> flat(static_cast<std::size_t>(nk) * dim);
+  for (int i = 0; i < nk; ++i) std::copy(keys[i].begin(), keys[i].end(), flat.begin() + static_cast<std::ptrdiff_t>(i) * dim);
+  static bool attr = false;
+  if (!attr) {
+    MLRG_CUDA(cudaFuncSetAttribute(k_km_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  w.keys.upload(flat, w.s);
+  w.draws.upload(draws, w.s);
+  w.cent.resize(static_cast<std::size_t>(k) * dim);
+  w.dist.resize(static_cast<std::size_t>(nk) * k);
+  w.owner.resize(static_cast<std::size_t>(nk));
+  k_km_seed<<<1, kKmThreads, sizeof(double) * static_cast<std::size_t>(nk), w.s>>>(w.keys.get(), nk, dim, k, w.draws.get(),
+                                                                                 w.cent.get());
+  MLRG_LAUNCH_CHECK("k_km_seed");
+  const long long pairs = static_cast<long long>(nk) * k;
+  const unsigned gd = static_cast<unsigned>((pairs + 255) / 256), ga = static_cast<unsigned>((nk + 255) / 256),
+                 gu = static_cast<unsigned>((k * dim + 127) / 128);
+  for (int it = 0; it <= iters; ++it) {  // iters Lloyd steps, then the final assignment
+    k_km_dist<<<gd, 256, 0, w.s>>>(w.keys.get(), nk, dim, k, w.cent.get(), w.dist.get());
+    k_km_assign<<<ga, 256, 0, w.s>>>(w.dist.get(), nk, k, w.owner.get());
+    if (it < iters) k_km_update<<<gu, 128, 0, w.s>>>(w.keys.get(), nk, dim, k, w.owner.get(), w.cent.get());
+  }
+  MLRG_LAUNCH_CHECK("k_km_lloyd");
+  std::vector<float> hc(static_cast<std::size_t>(k) * dim);
+  std::vector<int> hn(static_cast<std::size_t>(nk));
+  MLRG_CUDA(cudaMemcpyAsync(hc.data(), w.cent.get(), hc.size() * sizeof(float), cudaMemcpyDeviceToHost, w.s));
+  MLRG_CUDA(cudaMemcpyAsync(hn.data(), w.owner.get(), hn.size() * sizeof(int), cudaMemcpyDeviceToHost, w.s));
+  MLRG_CUDA(cudaStreamSynchronize(w.s));
+  cent.assign(static_cast<std::size_t>(k), std::vector<float>(static_cast<std::size_t>(dim)));
+  for (int c = 0; c < k; ++c) std::copy(hc.begin() + static_cast<std::ptrdiff_t>(c) * dim, hc.begin() + static_cast<std::ptrdiff_t>(c + 1) * dim, cent[c].begin());
+  nearest.assign(hn.begin(), hn.end());
+}
+
+bool gpu_kmeans_fits(int nk, int k, int dim) {
+  return static_cast<std::size_t>(nk) * sizeof(double) <= 200 * 1024 && static_cast<long long>(nk) * k < (1LL << 31) &&
+         k * dim > 0;
+}
+
 DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int max_slabs, std::int64_t max_keys,
                        std::size_t arena_bytes, int window_inserts, cudaStream_t s)
     : client_(client),
@@ -303,6 +476,31 @@ DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int 
   if (max_slabs_ > kStageThreads) throw std::invalid_argument("device memo: more than 1024 slabs per operator call");
   if (client_.config().global_cache) throw std::invalid_argument("device memo: global_cache is host-only");
   if (client_.store().ivf().nlist > kMaxProbe) throw std::invalid_argument("device memo: nlist must be <= 64");
+  {  // the IVF training runs on the GPU (bit-identical to the host k-means)
+    int dev = 0;
+    MLRG_CUDA(cudaGetDevice(&dev));
+    km_ = std::make_unique<KmeansScratch>();
+    client_.store().set_trainer([dev, this](const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
+                                      std::vector<std::vector<float>>& cent, std::vector<std::size_t>& nearest) {
+      const int dim = keys.empty() ? 0 : static_cast<int>(keys.front().size());
+      if (!gpu_kmeans_fits(static_cast<int>(keys.size()), k, dim)) {
+        cent = kmeans_train(keys, k, seed, iters);
+        nearest.resize(keys.size());
+        for (std::size_t i = 0; i < keys.size(); ++i) {
+          double best = std::numeric_limits<double>::max();
+          for (std::size_t c = 0; c < cent.size(); ++c) {
+            const double d = l2_sq(keys[i].data(), cent[c].data(), dim);
+            if (d < best) {
+              best = d;
+              nearest[i] = c;
+            }
+          }
+        }
+        return;
+      }
+      gpu_kmeans(keys, k, seed, iters, cent, nearest, dev, km_.get());
+    });
+  }
   const std::size_t per_key = 8 + 4 * static_cast<std::size_t>(kd_);
   batch_keys_ = static_cast<int>((client_.config().coalesce_bytes + per_key - 1) / per_key);
   keys_.resize(static_cast<std::size_t>(max_keys_ * kd_));
@@ -380,7 +578,20 @@ void DeviceMemo::set_slabs(OpId op, const std::vector<std::size_t>& value_bytes,
   MLRG_CUDA(cudaStreamSynchronize(s));
 }
 
+DeviceMemo::~DeviceMemo() {
+  if (pending_.valid()) pending_.wait();
+}
+
+void DeviceMemo::join(cudaStream_t s) {
+  if (!pending_.valid()) return;
+  pending_.get();  // rethrows a failure of the store update
+  if (pending_spill_) spill(s);
+  pending_spill_ = false;
+  upload_ivf(s);
+}
+
 void DeviceMemo::lookup(OpId op, int n, const float* keys, const double* norms2, int iteration, cudaStream_t s) {
+  join(s);
   const int o = static_cast<int>(op);
   if (n > max_slabs_) throw std::logic_error("device memo: too many slabs");
   if (o > 3) throw std::logic_error("device memo: operator not memoizable on the device");
@@ -436,6 +647,7 @@ void DeviceMemo::spill(cudaStream_t s) {
 }
 
 void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) {
+  join(s);
   MLRG_CUDA(cudaMemcpyAsync(h_state_.get(), state_.get(), 6 * sizeof(long long), cudaMemcpyDeviceToHost, s));
   MLRG_CUDA(cudaStreamSynchronize(s));
   long long* st = h_state_.get();
@@ -480,8 +692,9 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
   MemoStore& store = client_.store();
   const bool was_trained = store.trained();
   const char* arena = arena_.get();
+  std::vector<ValueRef> vals(static_cast<std::size_t>(nstaged));
   for (long long i = 0; i < nstaged; ++i) {
-    ValueRef v;
+    ValueRef& v = vals[static_cast<std::size_t>(i)];
     v.dev = vp[static_cast<std::size_t>(i)];
     spiller_->ring().note(static_cast<std::uint64_t>(npub + i),
                           static_cast<std::size_t>(reinterpret_cast<const char*>(v.dev) - arena),
@@ -489,11 +702,15 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
     v.norm = vn[static_cast<std::size_t>(i)];
     v.bytes = static_cast<std::size_t>(vb[static_cast<std::size_t>(i)]);
     v.count = static_cast<std::int64_t>((v.bytes - 8) / 16);
-    const std::vector<float> k(keys.begin() + i * kd_, keys.begin() + (i + 1) * kd_);
-    const std::uint64_t id = store.insert(k, v);
-    if (static_cast<long long>(id) != npub + i) throw std::logic_error("device memo: id mismatch with the host mirror");
-    ++ctr.inserts_sent;
   }
+  ctr.inserts_sent += static_cast<std::uint64_t>(nstaged);
+  auto insert_all = [this, &store, npub, nstaged, keys = std::move(keys), vals = std::move(vals)]() {
+    for (long long i = 0; i < nstaged; ++i) {
+      const std::vector<float> k(keys.begin() + i * kd_, keys.begin() + (i + 1) * kd_);
+      const std::uint64_t id = store.insert(k, vals[static_cast<std::size_t>(i)]);
+      if (static_cast<long long>(id) != npub + i) throw std::logic_error("device memo: id mismatch with the host mirror");
+    }
+  };
   st[3] = 0;  // the log is drained either way
   if (publish) {
     st[0] = npub + nstaged;
@@ -502,10 +719,19 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
   }
   MLRG_CUDA(cudaMemcpyAsync(state_.get(), st, 6 * sizeof(long long), cudaMemcpyHostToDevice, s));
   MLRG_CUDA(cudaStreamSynchronize(s));
-  if (publish) spill(s);
-  if (store.trained() && (nstaged > 0 || !was_trained)) upload_ivf(s);
   if (st[0] > max_keys_ - static_cast<long long>(client_.config().insert_queue_cap))
     throw std::runtime_error("device memo: key index full (" + std::to_string(max_keys_) + " keys)");
+  const bool trains = !was_trained && static_cast<long long>(store.key_count()) + nstaged >= store.ivf().train_size;
+  if (trains) {
+    // the k-means training runs on a host thread while the GPU continues; the
+    // spill (it repoints stored values by id) and the IVF upload wait for it (join)
+    pending_ = std::async(std::launch::async, std::move(insert_all));
+    pending_spill_ = publish;
+    return;
+  }
+  insert_all();
+  if (publish) spill(s);
+  if (store.trained() && (nstaged > 0 || !was_trained)) upload_ivf(s);
 }
 
 }  // namespace mlrg

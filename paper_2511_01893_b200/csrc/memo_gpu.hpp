@@ -27,6 +27,8 @@
 #include <memory>
 #include <vector>
 
+#include <future>
+
 #include "cold_tier.hpp"
 #include "device.hpp"
 #include "encoder.hpp"
@@ -52,6 +54,15 @@ struct DevLog {
   int queried; // went to the store
   int staged;  // 1 accepted, 0 dropped, -1 not a miss
 };
+
+/// The IVF k-means (kmeans_train + nearest_centroid, memo.cpp) in one GPU CTA on
+/// its own stream of `device`; bit-identical to the host. gpu_kmeans_fits: the
+/// per-key state and the centroids fit in shared memory.
+struct KmeansScratch;  // device buffers and stream, reused across trainings
+void gpu_kmeans(const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
+                std::vector<std::vector<float>>& cent, std::vector<std::size_t>& nearest, int device,
+                KmeansScratch* scratch = nullptr);
+bool gpu_kmeans_fits(int nk, int k, int dim);
 
 class DeviceMemo {
  public:
@@ -89,9 +100,16 @@ class DeviceMemo {
   std::size_t spilled_bytes() const { return spiller_ ? spiller_->spilled_bytes() : 0; }
   std::size_t arena_bytes() const { return arena_bytes_; }
 
+ ~DeviceMemo();
+
  private:
   void upload_ivf(cudaStream_t s);
   void spill(cudaStream_t s);
+  /// Completes a flush whose store update runs on a host thread (the flush
+  /// that trains the IVF index: k-means over train_size keys takes ~10 ms of
+  /// host time, overlapped with the objective and the next iteration's first
+  /// encode); called before anything reads the store or the device IVF state.
+  void join(cudaStream_t s);
 
   MemoClient& client_;
   int kd_;
@@ -127,6 +145,9 @@ class DeviceMemo {
   int window_inserts_;
   std::size_t max_slab_bytes_ = 0;  // largest value slab (256-byte granules)
   std::unique_ptr<ColdSpiller> spiller_;  // created with the first slab table
+  std::future<void> pending_;             // asynchronous store update (join())
+  std::unique_ptr<KmeansScratch> km_;     // the GPU IVF trainer's buffers
+  bool pending_spill_ = false;
 };
 
 }  // namespace mlrg

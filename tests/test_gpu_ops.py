@@ -168,3 +168,26 @@ def test_cnn_encoder_matches_reference_keys(mlrg, torch_cuda, idx, shape):
         want = z[f"raw{idx}"][op]
         assert np.allclose(keys[0], want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
         assert abs(norms[0] - np.linalg.norm(z[f"x{idx}_op{op}"])) <= 1e-6 * norms[0]
+
+
+@pytest.mark.parametrize("nk,k,dup", [(1024, 64, False), (1100, 64, True), (40, 64, False)])
+def test_gpu_kmeans_bit_identical_to_host(mlrg, torch_cuda, nk, k, dup):
+    """The device IVF trainer (memo_gpu.cu k_kmeans) against the host k-means
+    (memo.cpp kmeans_train, pinned to the reference's store KATs): identical
+    centroids and nearest-centroid assignment, bit for bit, including duplicate
+    keys (ties) and fewer keys than centroids."""
+    import ctypes as C
+    rng = np.random.default_rng(nk)
+    keys = rng.standard_normal((nk, 60)).astype(np.float32)
+    if dup:
+        keys[1::7] = keys[0::7][: len(keys[1::7])]
+    out = {}
+    for dev_flag in (0, 1):
+        kk = min(k, nk)
+        cent = np.zeros((kk, 60), np.float32)
+        near = np.zeros(nk, np.int64)
+        rc = mlrg.lib().mlrg_kmeans(keys.ctypes.data, nk, 60, k, 7, 20, dev_flag, cent.ctypes.data, near.ctypes.data)
+        assert rc == 0, mlrg.lib().mlrg_last_error()
+        out[dev_flag] = (cent, near)
+    assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
+    assert np.array_equal(out[0][1], out[1][1])
