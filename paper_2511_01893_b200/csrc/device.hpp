@@ -160,6 +160,32 @@ class Partials {
     host_.reserve(static_cast<std::size_t>(kMaxSlots));
   }
   double* dev() const { return dev_.get(); }
+  /// A [count / nv][nv] table of CTA partials at slot offset `off`.
+  struct Range {
+    int off, count, nv;
+  };
+  /// Slot offset for reductions that stay pending across other reducing
+  /// kernels (they write from slot 0) until a batched sum() reads them.
+  static constexpr int kParked = kMaxSlots / 2;
+  /// Column sums of several tables read back with one stream synchronisation
+  /// (each table summed in CTA order, as sum() does).
+  std::vector<std::vector<double>> sum(const std::vector<Range>& ranges, cudaStream_t s) {
+    for (const Range& r : ranges) {
+      if (r.off < 0 || r.count < 0 || r.off + r.count > kMaxSlots) throw std::logic_error("Partials: range out of bounds");
+      if (r.nv <= 0 || r.count % r.nv) throw std::logic_error("Partials: count is not a multiple of nv");
+      if (r.count)
+        MLRG_CUDA(cudaMemcpyAsync(host_.get() + r.off, dev_.get() + r.off, static_cast<std::size_t>(r.count) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    MLRG_CUDA(cudaStreamSynchronize(s));
+    std::vector<std::vector<double>> out;
+    for (const Range& r : ranges) {
+      std::vector<double> v(static_cast<std::size_t>(r.nv), 0.0);
+      for (int i = 0; i < r.count; ++i) v[static_cast<std::size_t>(i % r.nv)] += host_.get()[r.off + i];
+      out.push_back(std::move(v));
+    }
+    return out;
+  }
   /// Copies `count` doubles back (synchronising `s`) and returns the column sums
   /// of a [count / nv][nv] table.
   std::vector<double> sum(int count, int nv, cudaStream_t s) {

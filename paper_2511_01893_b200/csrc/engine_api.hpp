@@ -102,7 +102,11 @@ class Engine {
   /// Non-memoized fu2d whose output is only reduced: {sum |fu2d(v) - sub|^2,
   /// Re<dot, fu2d(v) - sub>} (line search terms admm.cpp:95-102 and the data
   /// term of objective(), admm.cpp:190-195); summed over ranks.
-  std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot);
+  /// `extra`: partial tables of kernels already enqueued (at Partials::kParked
+  /// and up) summed with the same readback, into `extra_out` (summed over ranks).
+  std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot,
+                                    const std::vector<Partials::Range>& extra = {},
+                                    std::vector<std::vector<double>>* extra_out = nullptr);
 
  private:
   void apply(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,

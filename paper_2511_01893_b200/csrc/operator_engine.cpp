@@ -601,7 +601,9 @@ void Engine::f2d_adj(const float2* p, float2* out, bool memoize) {
   apply(OpId::f2d_adj, false, p, false, nullptr, out, false, memoize);
 }
 
-std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot) {
+std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot,
+                                          const std::vector<Partials::Range>& extra,
+                                          std::vector<std::vector<double>>* extra_out) {
   const std::int64_t nr = shard_.nr();
   Fu2dEpilogue e;
   e.sub = sub;
@@ -610,9 +612,12 @@ std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, co
   e.ld_dot = nr;
   e.reduce = true;
   const int slots = usfft_.fu2d(v, nr, 0, nr, e);
-  std::vector<double> r = usfft_.partials().sum(slots, 2, s_);
-  allreduce(r.data(), 2);
-  return {r[0], r[1]};
+  std::vector<Partials::Range> ranges{{0, slots, 2}};
+  ranges.insert(ranges.end(), extra.begin(), extra.end());
+  std::vector<std::vector<double>> all = usfft_.partials().sum(ranges, s_);
+  for (auto& x : all) allreduce(x.data(), static_cast<int>(x.size()));
+  if (extra_out) extra_out->assign(all.begin() + 1, all.end());
+  return {all[0][0], all[0][1]};
 }
 
 }  // namespace mlrg

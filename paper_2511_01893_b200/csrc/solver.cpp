@@ -363,6 +363,7 @@ bool Solver::step() {
       for (int inner = 0; inner < cfg.n_inner; ++inner) {
         // gradient(u): r_hat, loss terms, G
         double rr = 0.0;
+        Partials::Range rr_range{Partials::kParked, 0, 2};  // |r_hat|^2, read back with the gradient's terms
         st.push_u();  // published by fu1d's exchange fences
         eng.fu1d(st.u.get(), st.mid);
         if (baseline) {
@@ -372,7 +373,7 @@ bool Solver::step() {
           eng.f2d(st.dpred.get(), st.rhat.get());
         } else {
           eng.fu2d_fused(st.mid, st.dhat.get(), st.rhat.get());
-          rr = sum(ops::norm2_diff(st.rhat.get(), nullptr, st.P, part.dev(), s), 2)[1];
+          rr_range.count = ops::norm2_diff(st.rhat.get(), nullptr, st.P, part.dev() + Partials::kParked, s);
         }
         eng.fu2d_adj(st.rhat.get(), st.mid2);
         eng.fu1d_adj(st.mid2, st.G.get());
@@ -381,7 +382,10 @@ bool Solver::step() {
             ops::grad_update(st.u.get(), CDField3(st.f(st.g)), st.G.get(), hd ? st.p_prev.get() : nullptr,
                              hd ? st.G_prev.get() : nullptr, dims, st.rho, part.dev(), s, st.halo());
         st.push_G_pp();  // published by the allreduce below
-        const std::vector<double> gu = sum(gu_slots, 3);
+        std::vector<std::vector<double>> sums = part.sum({{0, gu_slots, 3}, rr_range}, s);
+        for (auto& x : sums) eng.allreduce(x.data(), static_cast<int>(x.size()));
+        const std::vector<double>& gu = sums[0];
+        if (!baseline) rr = sums[1][1];
         const double loss = 0.5 * rr + 0.5 * st.rho * gu[0];
         st.inner_losses.push_back(loss);
         const std::size_t n = st.inner_losses.size();
@@ -395,12 +399,14 @@ bool Solver::step() {
         double beta = 0.0;
         if (hd && gu[2] > 0.0) beta = normG2 / gu[2];
         auto step_terms = [&](double bt, double& a, double& b) {
-          const std::vector<double> dr =
-              sum(ops::direction(st.G.get(), st.p_prev.get(), bt, st.u.get(), CDField3(st.f(st.g)), st.p.get(), dims,
-                                 part.dev(), s, st.halo()),
-                  2);
+          // the direction's terms are read back with fu2d_reduce's (one synchronisation)
+          const int dr_slots = ops::direction(st.G.get(), st.p_prev.get(), bt, st.u.get(), CDField3(st.f(st.g)),
+                                              st.p.get(), dims, part.dev() + Partials::kParked, s, st.halo());
           eng.fu1d(st.p.get(), st.mid, false);
-          const std::array<double, 2> q = eng.fu2d_reduce(st.mid, nullptr, st.rhat.get());
+          std::vector<std::vector<double>> drv;
+          const std::array<double, 2> q =
+              eng.fu2d_reduce(st.mid, nullptr, st.rhat.get(), {{Partials::kParked, dr_slots, 2}}, &drv);
+          const std::vector<double>& dr = drv[0];
           a = q[0] + st.rho * dr[0];
           b = q[1] + st.rho * dr[1];
         };
@@ -451,12 +457,19 @@ bool Solver::step() {
     }
     eng.flush_inserts();  // admm.cpp:251-254
     // objective (admm.cpp:190-195), not memoized
+    // TV term and accuracy enqueued first, all three read back with one synchronisation
+    const int tv_slots = ops::tv_norm(st.u.get(), dims, part.dev() + Partials::kParked, s, st.halo());
+    std::vector<Partials::Range> extra{{Partials::kParked, tv_slots, 1}};
+    if (st.has_reference)
+      extra.push_back({Partials::kParked + tv_slots,
+                       ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev() + Partials::kParked + tv_slots, s), 2});
     eng.fu1d(st.u.get(), st.mid, false);
-    const std::array<double, 2> data = eng.fu2d_reduce(st.mid, st.dhat.get(), nullptr);
-    const double tv = sum(ops::tv_norm(st.u.get(), dims, part.dev(), s, st.halo()), 1)[0];
+    std::vector<std::vector<double>> ex;
+    const std::array<double, 2> data = eng.fu2d_reduce(st.mid, st.dhat.get(), nullptr, extra, &ex);
+    const double tv = ex[0][0];
     row.loss = 0.5 * data[0] + cfg.alpha * tv;
     if (st.has_reference) {  // accuracy(reference, u), admm.cpp:183-188
-      const std::vector<double> nd = sum(ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev(), s), 2);
+      const std::vector<double>& nd = ex[1];
       if (nd[1] == 0.0) throw std::invalid_argument("accuracy: reference volume has zero norm");
       row.e = std::sqrt(nd[0]) / std::sqrt(nd[1]);
       row.accuracy = 1.0 - row.e;
