@@ -34,14 +34,17 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max 
 METRIC = "ADMM-FFT iterations/sec at N^3 volume"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
 # `ncu --set full` captures (profiles/), filled in per round
-TRAFFIC: dict = {  # round 1: profiles/r1_ncu_*.txt (`ncu --set full`, one launch, cold cache)
-    "k_fu2d_gather": 43895296 + 1252352, "k_fu2d_adj_spread": 10866432 + 49152,
-    "k_fu2d_cols": 16817920 + 742656, "k_fu1d": 268511488 + 109370368,
+TRAFFIC: dict = {  # round 2: profiles/r2/ncu_baseline_*.txt (`ncu --set full`, one launch, cold cache)
+    "k_fu2d_gather": 45798656 + 1252864, "k_fu2d_adj_spread": 10870016 + 452864,
+    "k_fu2d_cols": 16846848 + 578816, "k_fu2d_rows": 8462592, "k_fu1d": 268778240 + 108069888,
 }
 # the same captures' per-launch durations (us): ncu serialises launches, while the bench
 # overlaps fu2d row batches on two streams (live durations include the sharing)
-SERIAL_US: dict = {"k_fu2d_gather": 56.12, "k_fu2d_adj_spread": 65.54, "k_fu2d_cols": 27.04, "k_fu2d_rows": 19.46,
-                   "k_fu1d": 324.99, "k_fu1d_adj": 519.42, "k_fu2d_adj_cols": 27.17}
+SERIAL_US: dict = {"k_fu2d_gather": 46.40, "k_fu2d_adj_spread": 66.18, "k_fu2d_cols": 25.38, "k_fu2d_rows": 17.66,
+                   "k_fu1d": 312.74}
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # DFMA peak at max clock (computed)
+F2F_PER_CLK_SM = 16  # F2F.F64.F32 per clock per SM (scripts/microbench.cu)
+PLAN: dict = {}  # fu2d plan figures of the benchmarked geometry (mlrg_ctx_stats)
 
 
 def parse():
@@ -159,8 +162,8 @@ HBM_VOLUMES_PER_ITER = {
 
 # l1tex__throughput (pct of peak) of the committed ncu captures: the shared-memory FFT
 # passes work on L2-resident grids and are bound by the L1/shared pipe, not HBM
-L1TEX_PCT = {"k_fu2d_rows": 61.2, "k_fu2d_cols": 58.8, "k_fu2d_adj_cols": 54.7, "k_fu1d": 76.0, "k_fu1d_adj": 77.3,
-             "k_fu2d_adj_spread": 86.6, "k_fu2d_gather": 50.0}
+L1TEX_PCT = {"k_fu2d_rows": 63.9, "k_fu2d_cols": 65.0, "k_fu2d_adj_cols": 58.2, "k_fu1d": 78.9,
+             "k_fu2d_adj_spread": 84.2, "k_fu2d_gather": 63.9}  # round 2: profiles/r2/ncu_baseline_*.txt
 
 
 def local_share(n, world, rank):
@@ -265,6 +268,7 @@ def main():
         d = torch.empty((nt, n, n), dtype=torch.complex64, device="cuda")
         ctx.forward_L(phantom, d)
         ctx.sync()
+        PLAN.setdefault((n, nt), ctx.stats())
         del ctx
         return d, phantom
 
@@ -426,6 +430,22 @@ def main():
                     "avg_launch_ms": avg_ms, "traffic": TRAFFIC.get(name),
                     "hbm_view": {"bytes_per_launch": work["bytes"],
                                  "achieved_gbs": work["bytes"] / (avg_ms * 1e-3) / 1e9, "peak_gbs": P["hbm_gbs"]}}
+            st_ = PLAN.get((n, nt))
+            if st_ and name == "k_fu2d_gather":
+                # what the kernel executes: one W x W window per target class (not per target),
+                # 16 rows, fp64 taps (2 DFMA per complex tap and per window row) on values
+                # widened by F2F (2 per tap): the conversion rate is its tightest compute roof
+                C, W = st_["nclass"], st_["taps"]
+                fl = C * 16 * (4 * W * W + 4 * W)
+                f2f = C * 16 * 2 * W * W
+                f2f_us = f2f / (148 * F2F_PER_CLK_SM * 1.965e9) * 1e6
+                roof["executed"] = {
+                    "classes_per_launch": C, "taps": W, "fp64_flop_per_launch": fl,
+                    "achieved_fp64_tflops": fl / (avg_ms * 1e-3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                    "fp64_frac": fl / (avg_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                    "f2f_per_launch": f2f, "f2f_roof_us": f2f_us, "f2f_frac": f2f_us / (avg_ms * 1e3),
+                    "f2f_frac_serialized": f2f_us / SERIAL_US["k_fu2d_gather"],
+                    "note": "live launch duration includes sharing the SMs with the other stream's FFT passes"}
         else:
             ach = work["bytes"] / (avg_ms * 1e-3) / 1e9
             roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"], "unit": "GB/s",
@@ -436,7 +456,7 @@ def main():
             v = (work["flops"] if roof["unit"] == "TFLOP/s" else work["bytes"]) / (SERIAL_US[name] * 1e-6)
             v = v / 1e12 if roof["unit"] == "TFLOP/s" else v / 1e9
             roof["serialized_ncu"] = {"avg_launch_us": SERIAL_US[name], "achieved": v, "frac": v / roof["peak"],
-                                      "source": f"profiles/r1_ncu_{name}.txt"}
+                                      "source": f"profiles/r2/ncu_baseline_{name}.txt"}
         roof["share_of_step"] = rec["ms_total"] / ps / ms_step
         roof["kernels_ms_per_step"] = {k: v["ms_total"] / ps for k, v in off["prof"].items()}
         roof["kernels"] = kernel_table(off["prof"], n, nt, ps, P["hbm_gbs"], local_share(n, world, rank))

@@ -40,6 +40,10 @@ mlrg_ctx* mlrg_ctx_create_kernel(int64_t n1, int64_t n0, int64_t n2, int64_t n_t
                                  double phi, void* stream, int kernel);
 void mlrg_ctx_destroy(mlrg_ctx* ctx);
 int mlrg_sync(mlrg_ctx* ctx);
+/* Plan figures for measurement (bench.py): {fu2d target classes per detector row,
+ * kernel taps per dimension, oversampled grid extents M1, M2, gather CTAs and
+ * classes per CTA per 16-row batch}. */
+int mlrg_ctx_stats(mlrg_ctx* ctx, int64_t out[6]);
 
 /* nufft::fu1d_gridding (nufft.cpp:107-134): dev u (d0, n0, n2) -> dev out (d0, h, n2). */
 int mlrg_fu1d(mlrg_ctx* ctx, const void* u, void* out, int64_t d0);

@@ -116,6 +116,7 @@ _SIGS = {
     "mlrg_memo_insert": (C.c_int, [_P, C.c_int, _P, _U64]),
     "mlrg_memo_flush": (C.c_int, [_P]),
     "mlrg_memo_counters": (C.c_int, [_P, _P]),
+    "mlrg_ctx_stats": (C.c_int, [_P, _P]),
     "mlrg_kmeans": (C.c_int, [_P, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, _P, _P]),
     "mlrg_projection_matrix": (C.c_int, [_I64, _I64, _I64, C.c_int, _U64, _P, _I64]),
     "mlrg_slot_mix": (C.c_int, [_P, C.c_int, _U64, _I64, C.c_int]),
@@ -399,6 +400,11 @@ class Context:
         _gcheck(lib().mlrg_encode_cnn(self._h, OPS[op], _dp(x), chunk_extent, key_dim, seed,
                                       keys.ctypes.data, norms.ctypes.data, ns))
         return keys, norms
+
+    def stats(self) -> dict:
+        out = np.zeros(6, np.int64)
+        _gcheck(lib().mlrg_ctx_stats(self._h, out.ctypes.data))
+        return dict(zip(("nclass", "taps", "m1", "m2", "gather_ctas", "classes_per_cta"), (int(x) for x in out)))
 
     def sync(self):
         _gcheck(lib().mlrg_sync(self._h))

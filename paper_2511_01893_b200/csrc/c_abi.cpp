@@ -678,6 +678,15 @@ mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, i
 
 void mlrg_ctx_destroy(mlrg_ctx* ctx) { delete ctx; }
 
+int mlrg_ctx_stats(mlrg_ctx* ctx, int64_t out[6]) {
+  return guarded([&] {
+    need(ctx && out, "null argument");
+    const mlrg::Usfft::Stats st = ctx->usfft->stats();
+    const int64_t v[6] = {st.nclass, st.taps, st.m1, st.m2, st.gather_ctas, st.classes_per_cta};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
 int mlrg_sync(mlrg_ctx* ctx) {
   return guarded([&] {
     need(ctx != nullptr, "null context");

@@ -1489,6 +1489,12 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   return epi.reduce && nk > 0 ? (pipe ? 4 : 2) * ggrid : 0;
 }
 
+Usfft::Stats Usfft::stats() const {
+  const Tables& t = *t_;
+  const std::int64_t per = t.gather_per;
+  return {t.nclass, t.px.taps, t.px.m, t.py.m, (t.nclass + per - 1) / per, per};
+}
+
 void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
                      std::int64_t ld_out, std::int64_t k0_out, const PeerOut* peer) {
   const Tables& t = *t_;

@@ -76,6 +76,12 @@ class Usfft {
   /// array via the epilogue. Returns the number of partial doubles written
   /// (2 per gather CTA) when epi.reduce is set, else 0.
   int fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t nk, const Fu2dEpilogue& epi);
+  /// Plan figures for measurement: fu2d target classes per detector row, kernel
+  /// taps per dimension, oversampled grid extents, gather CTAs per row batch.
+  struct Stats {
+    std::int64_t nclass, taps, m1, m2, gather_ctas, classes_per_cta;
+  };
+  Stats stats() const;
   /// Rows [k0, k0+nk) of an (n_theta, ld, w) array -> rows [k0_out, k0_out+nk)
   /// of an (n1, ld_out, n2) array.
   void fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int64_t nk, float2* out,
