@@ -85,6 +85,9 @@ class Engine {
   float2* mid2() const { return mid2_.get(); }
   /// Sums `v` over the ranks in rank order (no-op unsharded).
   void allreduce(double* v, int n) const;
+  /// Sharded: stream-ordered fence across the ranks (PeerEvents; MLRG_FENCE=sync
+  /// restores the stream synchronisation + host barrier). No-op unsharded.
+  void fence();
 
   // Full-array applications (scalerun.hpp:77-92).
   // The volume side (fu1d input, fu1d_adj output) is the solver's complex128
@@ -121,7 +124,8 @@ class Engine {
   Shape3 out_shape(OpId op) const;  // this rank's output array
   std::int64_t slab0(int axis, OpId op) const;  // global index of this rank's first slab
   void register_shapes();
-  void exchange_fence();  // stream sync + barrier across ranks
+  void exchange_fence() { fence(); }
+  void host_fence();  // stream sync + barrier across ranks (the host reads the results)
   float2* value_slot(int owner, std::int64_t count);
   void spill_values();  // host-path rings: free the next window's span (cold_tier.hpp)
 
@@ -157,6 +161,7 @@ class Engine {
   std::unique_ptr<ColdSpiller> spiller_;  // one rank: asynchronous spills
   std::int64_t spilled_ = 0;
   std::unique_ptr<DeviceMemo> dmemo_;
+  std::unique_ptr<PeerEvents> pev_;  // sharded: the stream-ordered fence
   ops::CnnWork cnn_work_;  // encoder_variant = cnn scratch
   bool whole_call_ = false;  // compute() runs a whole unmemoized operator call
 };

@@ -50,6 +50,13 @@ Engine::Engine(const Geometry& g, EngineConfig cfg, cudaStream_t s, std::shared_
   if (cfg_.memo_enabled && (!enc_ || !memo_))
     throw std::invalid_argument("OperatorEngine: memoization needs an encoder and a client");
   if (cfg_.memo_enabled) register_shapes();
+  if (shard_.sharded()) {
+    try {
+      pev_ = std::make_unique<PeerEvents>(*shard_.comm);
+    } catch (const std::exception&) {
+      pev_.reset();  // no interprocess events: host fences (same semantics)
+    }
+  }
   if (cfg_.memo_enabled && cfg_.device_memo && !shard_.sharded()) {
     // the device-side lookup needs one memo slab per 16-row fu2d batch
     if (cfg_.chunk_extent != Usfft::kRowBatch) throw std::invalid_argument("device memo needs chunk_extent = 16");
@@ -120,9 +127,24 @@ void Engine::allreduce(double* v, int n) const {
   if (shard_.sharded()) shard_.comm->allreduce_sum(v, n);
 }
 
-void Engine::exchange_fence() {
+void Engine::host_fence() {
   MLRG_CUDA(cudaStreamSynchronize(s_));
   shard_.comm->barrier();
+}
+
+void Engine::fence() {
+  if (!shard_.sharded()) return;
+  // MLRG_FENCE=sync / =event force either; by default the event fence runs when every
+  // rank has its own GPU (PeerEvents::distinct_devices)
+  static const int mode = [] {
+    const char* e = std::getenv("MLRG_FENCE");
+    if (e && std::string(e) == "sync") return 0;
+    if (e && std::string(e) == "event") return 1;
+    return -1;
+  }();
+  const bool ev = pev_ && (mode == 1 || (mode == -1 && pev_->distinct_devices()));
+  if (!ev) return host_fence();
+  pev_->fence(s_);
 }
 
 float2* Engine::value_slot(int owner, std::int64_t count) {
@@ -163,7 +185,7 @@ void Engine::spill_values() {
   if (moved.empty()) return;
   prof::HostSpan span("host:memo_spill");
   // the owners' copies (and segments) exist before any rank maps or reads them
-  if (shard_.sharded()) exchange_fence();
+  if (shard_.sharded()) host_fence();
   else MLRG_CUDA(cudaStreamSynchronize(s_));
   for (const Moved& m : moved) store.set_value_ptr(m.id, static_cast<const float2*>(cold_->device_ptr(m.ref)));
   spilled_ += static_cast<std::int64_t>(moved.size());
@@ -513,7 +535,7 @@ void Engine::flush_inserts() {
   if (!memo_) return;
   // sharded: a value is read by its first hit only after this flush; the owner's
   // copy must be complete on its stream before any rank publishes the key
-  if (shard_.sharded()) exchange_fence();
+  if (shard_.sharded()) host_fence();
   if (dmemo_) return take_device_audit(true);
   memo_->flush_inserts();
   spill_values();

@@ -80,6 +80,44 @@ PeerMemory::~PeerMemory() {
     if (static_cast<int>(r) != rank_ && ptrs_[r]) cudaIpcCloseMemHandle(ptrs_[r]);
 }
 
+PeerEvents::PeerEvents(HostComm& comm) : comm_(comm) {
+  const int world = comm.world();
+  peers_.assign(static_cast<std::size_t>(world), nullptr);
+  MLRG_CUDA(cudaEventCreateWithFlags(&mine_, cudaEventDisableTiming | cudaEventInterprocess));
+  if (world == 1) return;
+  {
+    int dev = 0;
+    MLRG_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop{};
+    MLRG_CUDA(cudaGetDeviceProperties(&prop, dev));
+    std::vector<cudaUUID_t> ids(static_cast<std::size_t>(world));
+    comm.allgather(&prop.uuid, sizeof(cudaUUID_t), ids.data());
+    for (int a = 0; a < world; ++a)
+      for (int b = a + 1; b < world; ++b)
+        if (std::memcmp(&ids[static_cast<std::size_t>(a)], &ids[static_cast<std::size_t>(b)], sizeof(cudaUUID_t)) == 0)
+          distinct_ = false;
+  }
+  cudaIpcEventHandle_t h{};
+  MLRG_CUDA(cudaIpcGetEventHandle(&h, mine_));
+  std::vector<cudaIpcEventHandle_t> all(static_cast<std::size_t>(world));
+  comm.allgather(&h, sizeof(h), all.data());
+  for (int r = 0; r < world; ++r)
+    if (r != comm.rank()) MLRG_CUDA(cudaIpcOpenEventHandle(&peers_[static_cast<std::size_t>(r)], all[static_cast<std::size_t>(r)]));
+}
+
+PeerEvents::~PeerEvents() {
+  for (cudaEvent_t e : peers_)
+    if (e) cudaEventDestroy(e);
+  if (mine_) cudaEventDestroy(mine_);
+}
+
+void PeerEvents::fence(cudaStream_t s) {
+  MLRG_CUDA(cudaEventRecord(mine_, s));
+  comm_.barrier();  // every rank's record is enqueued before anyone waits on it
+  for (cudaEvent_t e : peers_)
+    if (e) MLRG_CUDA(cudaStreamWaitEvent(s, e, 0));
+}
+
 namespace ops {
 
 namespace {

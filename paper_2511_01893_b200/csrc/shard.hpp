@@ -65,6 +65,32 @@ class PeerMemory {
   std::vector<void*> ptrs_;
 };
 
+/// Stream-ordered cross-rank fence: every rank records its interprocess event
+/// on its stream, the host barrier only orders the records (no stream
+/// synchronisation), then every rank's stream waits on all peers' events. All
+/// work enqueued before the fence on any rank happens before all work enqueued
+/// after it on every rank (the P2P stores of the producing kernels are visible,
+/// and no rank overwrites a buffer a peer is still reading).
+class PeerEvents {
+ public:
+  explicit PeerEvents(HostComm& comm);
+  ~PeerEvents();
+  PeerEvents(const PeerEvents&) = delete;
+  PeerEvents& operator=(const PeerEvents&) = delete;
+  void fence(cudaStream_t s);
+  /// Every rank drives its own GPU (device UUIDs all distinct). Ranks sharing a
+  /// device time-slice: a stream waiting on another process's event then waits
+  /// for a context switch (measured 2x slower than a host fence at 256^3, two
+  /// ranks on one B200), so the engine uses the event fence only here.
+  bool distinct_devices() const { return distinct_; }
+
+ private:
+  HostComm& comm_;
+  bool distinct_ = true;
+  cudaEvent_t mine_ = nullptr;
+  std::vector<cudaEvent_t> peers_;
+};
+
 namespace ops {
 
 constexpr int kMaxRanks = 64;

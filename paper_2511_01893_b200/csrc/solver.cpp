@@ -425,10 +425,7 @@ bool Solver::step() {
       const auto t1 = clock::now();
       // ---- RSP + multiplier/penalty, one fused pass (admm.cpp:154-181) ----
       st.push_u();
-      if (eng.shard().sharded()) {  // publish the u halos
-        MLRG_CUDA(cudaStreamSynchronize(s));
-        eng.shard().comm->barrier();
-      }
+      eng.fence();  // sharded: publish the u halos
       const std::vector<double> rs = sum(
           st.rsp_chunks(st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s, geo), 2);
       st.swap_psi();

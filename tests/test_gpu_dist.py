@@ -62,10 +62,18 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("case,memo", [("recon_c32_memo_grid", "local"), ("recon_c64_off_grid", "off"),
-                                       ("recon_cfg1_memo_direct", "local")])
-def test_sharded_solver_matches_reference(mlrg, torch_cuda, tmp_path, case, memo):
+@pytest.mark.parametrize("case,memo,fence", [("recon_c32_memo_grid", "local", "default"),
+                                             ("recon_c64_off_grid", "off", "default"),
+                                             ("recon_cfg1_memo_direct", "local", "default"),
+                                             ("recon_c32_memo_grid", "local", "event")])
+def test_sharded_solver_matches_reference(mlrg, torch_cuda, tmp_path, case, memo, fence, monkeypatch):
+    """fence=event forces the stream-ordered interprocess-event fence (shard.hpp
+    PeerEvents), which the engine otherwise uses only when every rank has its own
+    GPU: the ranks here share cuda:0."""
     import torch.multiprocessing as mp
+
+    if fence != "default":
+        monkeypatch.setenv("MLRG_FENCE", fence)
 
     z = golden(case)
     n = z["phantom"].shape[0]
