@@ -335,19 +335,42 @@ __global__ void __launch_bounds__(kKmThreads) k_km_seed(const float* __restrict_
     }
     __syncthreads();
     if (tid == 0) {
+      // the sequential sums in key order (bit-identical), 8 values per chunk so the
+      // shared-memory loads run ahead of the dependent adds
       double total = 0.0;
-#pragma unroll 8
-      for (int i = 0; i < nk; ++i) total = __dadd_rn(total, dist2[i]);
+      int i = 0;
+      for (; i + 8 <= nk; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = dist2[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) total = __dadd_rn(total, x[u]);
+      }
+      for (; i < nk; ++i) total = __dadd_rn(total, dist2[i]);
       int q = 0;
       if (total > 0.0) {
         const double target = __dmul_rn(static_cast<double>(draws[c + 1] >> 11) * 0x1.0p-53, total);
         double run = 0.0;
         q = nk - 1;
-        for (int i = 0; i < nk; ++i) {
+        bool found = false;
+        for (i = 0; i + 8 <= nk && !found; i += 8) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = dist2[i + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            run = __dadd_rn(run, x[u]);
+            if (!found && run >= target) {
+              q = i + u;
+              found = true;
+            }
+          }
+        }
+        for (; i < nk && !found; ++i) {
           run = __dadd_rn(run, dist2[i]);
           if (run >= target) {
             q = i;
-            break;
+            found = true;
           }
         }
       } else {
