@@ -959,8 +959,43 @@ struct Usfft::Tables {
   DeviceBuffer<float2> f2d_tmp;
 };
 
+namespace {
+// Table uploads of the constructor through pinned staging blocks (the caching
+// allocator's): the host never waits on a pageable copy queued behind the
+// drop-in's concurrent input upload; one synchronisation when the tables are done.
+class Stager {
+ public:
+  explicit Stager(cudaStream_t s) : s_(s) {}
+  ~Stager() {
+    cudaStreamSynchronize(s_);
+    for (auto& b : blocks_) alloc::pinned_free(b.first, b.second);
+  }
+  Stager(const Stager&) = delete;
+  Stager& operator=(const Stager&) = delete;
+  template <class T>
+  void up(DeviceBuffer<T>& d, const T* src, std::size_t n) {
+    d.resize(n);
+    if (!n) return;
+    const std::size_t bytes = n * sizeof(T);
+    void* h = alloc::pinned(bytes);
+    blocks_.emplace_back(h, bytes);
+    std::memcpy(h, src, bytes);
+    MLRG_CUDA(cudaMemcpyAsync(d.get(), h, bytes, cudaMemcpyHostToDevice, s_));
+  }
+  template <class T>
+  void up(DeviceBuffer<T>& d, const std::vector<T>& v) {
+    up(d, v.data(), v.size());
+  }
+
+ private:
+  cudaStream_t s_;
+  std::vector<std::pair<void*, std::size_t>> blocks_;
+};
+}  // namespace
+
 Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     : g_(g), stream_(stream), kernel_(kernel), t_(new Tables) {
+  Stager stg(stream_);
   prof::HostSpan span("host:usfft_tables");
   Tables& t = *t_;
   const FrequencyGrids fg = frequency_grids(g_);
@@ -983,19 +1018,19 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   if (const char* e = std::getenv("MLRG_FU1D_ADJ_NCOL"))  // tuning override (threads = ncol * m / 8 <= 512)
     t.z_ncol_adj = static_cast<int>(std::clamp<std::int64_t>(std::atoll(e), 1, std::max<std::int64_t>(1, 4096 / pz.m)));
   t.z_ncol_adj = static_cast<int>(std::min<std::int64_t>(t.z_ncol_adj, g_.n2));
-  t.z_deconv.upload(pz.deconv, stream_);
+  stg.up(t.z_deconv, pz.deconv);
   std::vector<double> pdec(pz.deconv.size());
   for (std::size_t i = 0; i < pdec.size(); ++i) pdec[i] = pz.pref * pz.deconv[i];
-  t.z_pdeconv.upload(pdec, stream_);
-  t.z_start.upload(std::vector<int>(pz.start.begin(), pz.start.end()), stream_);
-  t.z_w.upload(pz.weights, stream_);
+  stg.up(t.z_pdeconv, pdec);
+  stg.up(t.z_start, std::vector<int>(pz.start.begin(), pz.start.end()));
+  stg.up(t.z_w, pz.weights);
   std::vector<double2> fac(static_cast<std::size_t>(g_.h)), cph(static_cast<std::size_t>(g_.h));
   for (std::size_t k = 0; k < fac.size(); ++k) {
     fac[k] = make_double2(pz.pref * pz.phase_re[k], pz.pref * pz.phase_im[k]);
     cph[k] = make_double2(pz.phase_re[k], -pz.phase_im[k]);
   }
-  t.z_fac.upload(fac, stream_);
-  t.z_cphase.upload(cph, stream_);
+  stg.up(t.z_fac, fac);
+  stg.up(t.z_cphase, cph);
   {  // cell -> (target, weight) CSR for the scatter-free adjoint, targets ascending
     std::vector<int> cnt(static_cast<std::size_t>(pz.m + 1), 0);
     for (std::int64_t k = 0; k < g_.h; ++k)
@@ -1009,16 +1044,17 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
         ck[static_cast<std::size_t>(pos[l])] = static_cast<int>(k);
         cw[static_cast<std::size_t>(pos[l]++)] = pz.weights[static_cast<std::size_t>(k * W + a)];
       }
-    t.z_cell_ptr.upload(cnt, stream_);
-    t.z_cell_k.upload(ck, stream_);
-    t.z_cell_w.upload(cw, stream_);
+    stg.up(t.z_cell_ptr, cnt);
+    stg.up(t.z_cell_k, ck);
+    stg.up(t.z_cell_w, cw);
   }
-  t.z_tw.upload(twiddles(pz.m), stream_);
+  stg.up(t.z_tw, twiddles(pz.m));
 
   prof::host_mark("host:usfft_fu1d_plan");
   // ---- fu2d plans (nufft.cpp:185-187) ----
   t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
   t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
+  prof::host_mark("host:usfft_fu2d_dimplans");
   // the 2D grid passes hold one M-point double column per CTA (M x 16 B of shared memory,
   // M / 8 threads) and the four-step column passes split M = A B up to 4096: n1, n2 <= 2048
   // (configs[4]'s 2048^3)
@@ -1027,11 +1063,11 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   const std::size_t WS = static_cast<std::size_t>(W);
   const DimPlan &px = t.px, &py = t.py;
   const std::size_t T = fg.nu_x.size();
-  t.x_deconv.upload(px.deconv, stream_);
-  t.y_deconv.upload(py.deconv, stream_);
+  stg.up(t.x_deconv, px.deconv);
+  stg.up(t.y_deconv, py.deconv);
   std::vector<double> pdx(px.deconv.size());
   for (std::size_t i = 0; i < pdx.size(); ++i) pdx[i] = px.pref * py.pref * px.deconv[i];
-  t.x_pdeconv.upload(pdx, stream_);
+  stg.up(t.x_pdeconv, pdx);
   std::vector<double2> tf(T), tcf(T);
   for (std::size_t q = 0; q < T; ++q) {
     const std::complex<double> ph = std::complex<double>(px.phase_re[q], px.phase_im[q]) *
@@ -1055,6 +1091,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return key[static_cast<std::size_t>(a)] < key[static_cast<std::size_t>(b)]; });
+  prof::host_mark("host:usfft_class_sort");
   auto same_weights = [&](std::size_t a, std::size_t b) {
     for (std::size_t k = 0; k < WS; ++k)
       if (std::abs(px.weights[a * WS + k] - px.weights[b * WS + k]) > 1e-13 ||
@@ -1085,6 +1122,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   }
   const std::size_t C = members.size();
   t.nclass = static_cast<int>(C);
+  prof::host_mark("host:usfft_class_group");
   {
     std::vector<int> r0(C), c0(C), mfirst(C + 1, 0), mtidx;
     std::vector<double> w1(C * WS), w2(C * WS);
@@ -1104,14 +1142,14 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
       }
       mfirst[c + 1] = static_cast<int>(mtidx.size());
     }
-    t.t_r0.upload(r0, stream_);
-    t.t_c0.upload(c0, stream_);
-    t.t_w1.upload(w1, stream_);
-    t.t_w2.upload(w2, stream_);
-    t.m_first.upload(mfirst, stream_);
-    t.m_tidx.upload(mtidx, stream_);
-    t.m_fac.upload(mfac, stream_);
-    t.m_cfac.upload(mcfac, stream_);
+    stg.up(t.t_r0, r0);
+    stg.up(t.t_c0, c0);
+    stg.up(t.t_w1, w1);
+    stg.up(t.t_w2, w2);
+    stg.up(t.m_first, mfirst);
+    stg.up(t.m_tidx, mtidx);
+    stg.up(t.m_fac, mfac);
+    stg.up(t.m_cfac, mcfac);
     // the gather's per-class records (bulk-copied into shared memory per CTA)
     auto build = [&](auto tag) {
       using Rec = decltype(tag);
@@ -1131,8 +1169,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
         std::copy_n(w1.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w1);
         std::copy_n(w2.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w2);
       }
-      t.recs.upload(reinterpret_cast<const unsigned char*>(rv.data()), rv.size() * sizeof(Rec), stream_);
-      MLRG_CUDA(cudaStreamSynchronize(stream_));
+      stg.up(t.recs, reinterpret_cast<const unsigned char*>(rv.data()), rv.size() * sizeof(Rec));
     };
     if (W == kEsTaps) build(ClassRec<kEsTaps>{});
     else build(ClassRec<kTaps>{});
@@ -1221,20 +1258,20 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     }
     t.nitems = static_cast<int>(items.size());
     t.nsplit = static_cast<int>(split.size());
-    t.items.upload(items, stream_);
-    t.split.upload(split, stream_);
+    stg.up(t.items, items);
+    stg.up(t.split, split);
     t.partial.resize(static_cast<std::size_t>(std::max(slots, 1)) * 32 * KB);
     t.split_cnt.resize(static_cast<std::size_t>(std::max(t.nsplit, 1)));
     t.split_cnt.zero(stream_);
-    t.patch_t.upload(lst, stream_);
+    stg.up(t.patch_t, lst);
   }
-  t.x_tw.upload(twiddles(px.m), stream_);
-  t.y_tw.upload(twiddles(py.m), stream_);
+  stg.up(t.x_tw, twiddles(px.m));
+  stg.up(t.y_tw, twiddles(py.m));
   t.cols4 = use_cols4(px.m);
   if (t.cols4) {
     t.logA = px.logm / 2;
-    t.a_tw.upload(twiddles(std::int64_t{1} << t.logA), stream_);
-    t.b_tw.upload(twiddles(std::int64_t{1} << (px.logm - t.logA)), stream_);
+    stg.up(t.a_tw, twiddles(std::int64_t{1} << t.logA));
+    stg.up(t.b_tw, twiddles(std::int64_t{1} << (px.logm - t.logA)));
   }
   prof::host_mark("host:usfft_patches");
   t.wide = (kernel_ == GridKernel::gaussian || wide_grids_env()) && !t.cols4;
@@ -1261,8 +1298,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   // ---- f2d (operators.cpp:20-74) ----
   t.f2d_fft = is_pow2(g_.h) && is_pow2(g_.w) && g_.h >= 8 && g_.w >= 8;
   if (t.f2d_fft) {
-    t.h_tw.upload(twiddles(g_.h), stream_);
-    t.w_tw.upload(twiddles(g_.w), stream_);
+    stg.up(t.h_tw, twiddles(g_.h));
+    stg.up(t.w_tw, twiddles(g_.w));
   } else {
     auto mat = [](std::int64_t n, bool conj) {
       std::vector<double2> W(static_cast<std::size_t>(n * n));
@@ -1276,10 +1313,10 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
         }
       return W;
     };
-    t.Wh.upload(mat(g_.h, false), stream_);
-    t.Ww.upload(mat(g_.w, false), stream_);
-    t.Whc.upload(mat(g_.h, true), stream_);
-    t.Wwc.upload(mat(g_.w, true), stream_);
+    stg.up(t.Wh, mat(g_.h, false));
+    stg.up(t.Ww, mat(g_.w, false));
+    stg.up(t.Whc, mat(g_.h, true));
+    stg.up(t.Wwc, mat(g_.w, true));
   }
   MLRG_CUDA(cudaStreamSynchronize(stream_));
   static bool smem_set = [] {
