@@ -703,7 +703,10 @@ __global__ void __launch_bounds__(512, MLRG_FFT_MINB / 2) k_fu2d_adj_cols(const 
 // A CTA of either pass holds kCols4 grid columns x all 16 batch rows, a
 // contiguous 512 B block of every grid row it touches, so all traffic is in
 // whole lines at the cost of one more trip through the grid.
-constexpr int kCols4 = 4;
+#ifndef MLRG_COLS4_W
+#define MLRG_COLS4_W 4
+#endif
+constexpr int kCols4 = MLRG_COLS4_W;
 constexpr int kCols4Lanes = kCols4 * KB;
 
 // The block of a grid row a CTA owns: lane l is (column c0 + l / KB, batch row
@@ -1478,11 +1481,11 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     if (t.cols4) {  // S -> Gd (intermediate) -> S (the grid, all M1 rows)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<+1, true, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<+1, true, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
-      k_cols4_pass2<+1, false, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass2<+1, false, true><<<dim3(A, nc), kCols4Lanes * B / 8, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), S,
           t.ldg, t.ghost, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
@@ -1589,11 +1592,11 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     if (t.cols4) {  // Gd -> S (intermediate) -> Gd (rows of the n1 mode slots)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<-1, false, true><<<dim3(B, nc), 8 * A, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<-1, false, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
-      k_cols4_pass2<-1, true, true><<<dim3(A, nc), 8 * B, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass2<-1, true, true><<<dim3(A, nc), kCols4Lanes * B / 8, static_cast<std::size_t>(B * kCols4Lanes) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.b_tw.get(), Gd,
           static_cast<int>(t.py.m), 0, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass2");
