@@ -461,8 +461,11 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
     auto res = std::make_unique<mlr_result>();
     // the result volume is allocated and its pages faulted in by host threads
     // while the device iterates (first-touch faults of hundreds of MB otherwise
-    // land inside the final device-to-host copy)
-    std::thread prefault([&res, shape = g.volume_shape()] {
+    // land inside the final device-to-host copy); started once the operator
+    // tables are built, so its threads do not compete with the table build
+    std::thread prefault;
+    auto start_prefault = [&] {
+      prefault = std::thread([&res, shape = g.volume_shape()] {
       res->u.a = mlrg::HostArray(shape, 0, /*zero=*/false);
       auto& v = res->u.a.data;
       const std::size_t n = v.size(), nt = 8, per = (n + nt - 1) / nt;
@@ -472,7 +475,8 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
           for (std::size_t i = lo; i < std::min(n, lo + per); i += 256) v[i] = {0.0, 0.0};
         });
       for (auto& x : th) x.join();
-    });
+      });
+    };
     struct Joiner {
       std::thread& t;
       ~Joiner() {
@@ -508,6 +512,7 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
       }
       uploader.join();
       if (up_err) std::rethrow_exception(up_err);
+      start_prefault();
     }
     {
       std::unique_ptr<mlrg::Solver> solver;
@@ -523,7 +528,7 @@ mlr_result* mlr_reconstruct(const mlr_config* cfg, const mlr_array* data, const 
       {
         mlrg::prof::HostSpan span("host:e2e_download");
         res->report = solver->report();
-        prefault.join();
+        if (prefault.joinable()) prefault.join();
         // the iterate is complex128 on the device: no rounding on the way out
         d2h_staged(res->u.a.data.data(), solver->u(), res->u.a.data.size() * sizeof(double2), sg.s);
       }

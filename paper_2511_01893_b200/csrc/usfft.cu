@@ -19,6 +19,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <future>
 #include <cstdlib>
 #include <numbers>
 #include <type_traits>
@@ -1005,6 +1006,10 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   if (g_.w > 0xffff || g_.n_theta > 0x7fff)  // packed (t, q) member indices of the fu2d classes
     throw std::invalid_argument("fu2d: w must be < 65536 and n_theta < 32768");
   // ---- fu1d plan (nufft.cpp:109-110) ----
+  // the two fu2d plans (the largest host tables) build on worker threads while the
+  // fu1d plan and its tables are made here
+  auto fx = std::async(std::launch::async, [&] { return DimPlan::make(g_.n1, fg.nu_x, kernel_); });
+  auto fy = std::async(std::launch::async, [&] { return DimPlan::make(g_.n2, fg.nu_y, kernel_); });
   t.pz = DimPlan::make(g_.n0, fg.nu_z, kernel_);
   const int W = t.pz.taps;
   const DimPlan& pz = t.pz;
@@ -1055,8 +1060,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
 
   prof::host_mark("host:usfft_fu1d_plan");
   // ---- fu2d plans (nufft.cpp:185-187) ----
-  t.px = DimPlan::make(g_.n1, fg.nu_x, kernel_);
-  t.py = DimPlan::make(g_.n2, fg.nu_y, kernel_);
+  t.px = fx.get();
+  t.py = fy.get();
   prof::host_mark("host:usfft_fu2d_dimplans");
   // the 2D grid passes hold one M-point double column per CTA (M x 16 B of shared memory,
   // M / 8 threads) and the four-step column passes split M = A B up to 4096: n1, n2 <= 2048
@@ -1104,33 +1109,73 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   };
   std::vector<int> rep_of;                   // class representative (lowest target index)
   std::vector<std::vector<int>> members;
-  for (std::size_t i = 0; i < T;) {
-    std::size_t j = i;
-    while (j < T && key[static_cast<std::size_t>(order[j])] == key[static_cast<std::size_t>(order[i])]) ++j;
-    std::vector<int> run(order.begin() + static_cast<std::ptrdiff_t>(i), order.begin() + static_cast<std::ptrdiff_t>(j));
-    std::sort(run.begin(), run.end());
-    const std::size_t first_class = members.size();
-    for (const int q : run) {
-      std::size_t c = first_class;
-      while (c < members.size() && (members[c].size() >= kClassMax ||
-                                    !same_weights(static_cast<std::size_t>(rep_of[c]), static_cast<std::size_t>(q))))
-        ++c;
-      if (c == members.size()) {
-        rep_of.push_back(q);
-        members.emplace_back();
-      }
-      members[c].push_back(q);
+  {
+    // runs of equal keys are independent (a class never spans two runs): host
+    // threads group contiguous ranges of runs, concatenated in order (the
+    // sequential scan's class order)
+    const int nth = static_cast<int>(std::min<std::size_t>(T / 4096 + 1, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+    std::vector<std::size_t> cut(static_cast<std::size_t>(nth) + 1, T);
+    cut[0] = 0;
+    for (int w = 1; w < nth; ++w) {
+      std::size_t j = std::max(cut[static_cast<std::size_t>(w) - 1], T * static_cast<std::size_t>(w) / static_cast<std::size_t>(nth));
+      while (j > 0 && j < T && key[static_cast<std::size_t>(order[j])] == key[static_cast<std::size_t>(order[j - 1])]) ++j;
+      cut[static_cast<std::size_t>(w)] = j;
     }
-    i = j;
+    std::vector<std::vector<int>> reps(static_cast<std::size_t>(nth));
+    std::vector<std::vector<std::vector<int>>> mems(static_cast<std::size_t>(nth));
+    auto group = [&](int w) {
+      std::vector<int>& rp = reps[static_cast<std::size_t>(w)];
+      std::vector<std::vector<int>>& mb = mems[static_cast<std::size_t>(w)];
+      for (std::size_t i = cut[static_cast<std::size_t>(w)]; i < cut[static_cast<std::size_t>(w) + 1];) {
+        std::size_t j = i;
+        while (j < T && key[static_cast<std::size_t>(order[j])] == key[static_cast<std::size_t>(order[i])]) ++j;
+        std::vector<int> run(order.begin() + static_cast<std::ptrdiff_t>(i), order.begin() + static_cast<std::ptrdiff_t>(j));
+        std::sort(run.begin(), run.end());
+        const std::size_t first_class = mb.size();
+        for (const int q : run) {
+          std::size_t c = first_class;
+          while (c < mb.size() && (mb[c].size() >= kClassMax ||
+                                   !same_weights(static_cast<std::size_t>(rp[c]), static_cast<std::size_t>(q))))
+            ++c;
+          if (c == mb.size()) {
+            rp.push_back(q);
+            mb.emplace_back();
+          }
+          mb[c].push_back(q);
+        }
+        i = j;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int w = 1; w < nth; ++w) th.emplace_back(group, w);
+    group(0);
+    for (auto& x : th) x.join();
+    for (int w = 0; w < nth; ++w) {
+      rep_of.insert(rep_of.end(), reps[static_cast<std::size_t>(w)].begin(), reps[static_cast<std::size_t>(w)].end());
+      for (auto& m : mems[static_cast<std::size_t>(w)]) members.push_back(std::move(m));
+    }
   }
   const std::size_t C = members.size();
   t.nclass = static_cast<int>(C);
   prof::host_mark("host:usfft_class_group");
   {
-    std::vector<int> r0(C), c0(C), mfirst(C + 1, 0), mtidx;
+    std::vector<int> r0(C), c0(C), mfirst(C + 1, 0);
     std::vector<double> w1(C * WS), w2(C * WS);
-    std::vector<double2> mfac, mcfac;
-    for (std::size_t c = 0; c < C; ++c) {
+    for (std::size_t c = 0; c < C; ++c) mfirst[c + 1] = mfirst[c] + static_cast<int>(members[c].size());
+    std::vector<int> mtidx(static_cast<std::size_t>(mfirst[C]));
+    std::vector<double2> mfac(mtidx.size()), mcfac(mtidx.size());
+    const int nthc = static_cast<int>(std::min<std::size_t>(C / 2048 + 1, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+    auto par_classes = [&](auto&& fn) {  // contiguous class ranges on host threads
+      std::vector<std::thread> th;
+      const std::size_t per = (C + static_cast<std::size_t>(nthc) - 1) / static_cast<std::size_t>(nthc);
+      for (int w = 1; w < nthc; ++w)
+        th.emplace_back([&, w] {
+          for (std::size_t c = w * per; c < std::min(C, (w + 1) * per); ++c) fn(c);
+        });
+      for (std::size_t c = 0; c < std::min(C, per); ++c) fn(c);
+      for (auto& x : th) x.join();
+    };
+    par_classes([&](std::size_t c) {
       const std::size_t q = static_cast<std::size_t>(rep_of[c]);
       r0[c] = px.start[q];
       c0[c] = py.start[q];
@@ -1138,13 +1183,15 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
                   w1.begin() + static_cast<std::ptrdiff_t>(c * WS));
       std::copy_n(py.weights.begin() + static_cast<std::ptrdiff_t>(q * WS), WS,
                   w2.begin() + static_cast<std::ptrdiff_t>(c * WS));
+      std::size_t k = static_cast<std::size_t>(mfirst[c]);
       for (const int e : members[c]) {
-        mtidx.push_back(static_cast<int>((e / g_.w) << 16 | (e % g_.w)));  // packed (t, q)
-        mfac.push_back(tf[static_cast<std::size_t>(e)]);
-        mcfac.push_back(tcf[static_cast<std::size_t>(e)]);
+        mtidx[k] = static_cast<int>((e / g_.w) << 16 | (e % g_.w));  // packed (t, q)
+        mfac[k] = tf[static_cast<std::size_t>(e)];
+        mcfac[k] = tcf[static_cast<std::size_t>(e)];
+        ++k;
       }
-      mfirst[c + 1] = static_cast<int>(mtidx.size());
-    }
+    });
+    prof::host_mark("host:usfft_class_tables");
     stg.up(t.t_r0, r0);
     stg.up(t.t_c0, c0);
     stg.up(t.t_w1, w1);
@@ -1153,12 +1200,13 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     stg.up(t.m_tidx, mtidx);
     stg.up(t.m_fac, mfac);
     stg.up(t.m_cfac, mcfac);
+    prof::host_mark("host:usfft_class_uploads");
     // the gather's per-class records (bulk-copied into shared memory per CTA)
     auto build = [&](auto tag) {
       using Rec = decltype(tag);
       constexpr int RW = sizeof(Rec::w1) / sizeof(double);
       std::vector<Rec> rv(C);
-      for (std::size_t c = 0; c < C; ++c) {
+      par_classes([&](std::size_t c) {
         Rec& r = rv[c];
         std::memset(&r, 0, sizeof(Rec));
         r.r0 = r0[c];
@@ -1171,7 +1219,7 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
         }
         std::copy_n(w1.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w1);
         std::copy_n(w2.begin() + static_cast<std::ptrdiff_t>(c * RW), RW, r.w2);
-      }
+      });
       stg.up(t.recs, reinterpret_cast<const unsigned char*>(rv.data()), rv.size() * sizeof(Rec));
     };
     if (W == kEsTaps) build(ClassRec<kEsTaps>{});

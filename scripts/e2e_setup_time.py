@@ -14,7 +14,7 @@ cfg = m.Config(n1=n, n0=n, n2=n, n_theta=n, h=n, w=n, n_outer=1, memoization="of
 ph = m.make_phantom("blocks", n, n, n, 1)
 data = m.project(cfg, ph)
 m.reconstruct(cfg, data, ph)  # warm-up: module loading
-PHASES = ("host:e2e_total", "host:e2e_teardown_and_rest", "host:e2e_solver_teardown", "host:e2e_engine_teardown", "host:usfft_fu1d_plan", "host:usfft_fu2d_dimplans", "host:usfft_fu2d_plans", "host:usfft_class_sort", "host:usfft_class_group", "host:usfft_classes", "host:usfft_patches", "host:e2e_engine", "host:usfft_tables", "host:e2e_upload", "host:e2e_solver_setup", "host:e2e_iterations",
+PHASES = ("host:e2e_total", "host:e2e_teardown_and_rest", "host:e2e_solver_teardown", "host:e2e_engine_teardown", "host:usfft_fu1d_plan", "host:usfft_fu2d_dimplans", "host:usfft_fu2d_plans", "host:usfft_class_sort", "host:usfft_class_group", "host:usfft_class_tables", "host:usfft_class_uploads", "host:usfft_classes", "host:usfft_patches", "host:e2e_engine", "host:usfft_tables", "host:e2e_upload", "host:e2e_solver_setup", "host:e2e_iterations",
           "host:e2e_download")
 for k in (1, 2, 4, 8):
     m.lib().mlrg_prof_reset()
