@@ -940,16 +940,21 @@ struct Usfft::Tables {
   // fu2d runs its row batches on two streams (the second set of grids and
   // partial slots belongs to the side stream) so one batch's gather overlaps the
   // next batch's FFT passes
-  DeviceBuffer<float2> S2, Gd2, val2;
-  DeviceBuffer<double2> partial2;
-  DeviceBuffer<int> split_cnt2;
+  // stream j > 0 of the K-stream pipeline owns sides[j - 1] and these buffers
+  struct Lane {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev_join = nullptr;
+    DeviceBuffer<float2> S, Gd, val;
+    DeviceBuffer<double2> partial;
+    DeviceBuffer<int> split_cnt;
+  };
+  std::vector<std::unique_ptr<Lane>> sides;
   // four-step column passes: M = A * B, A = 2^logA
   bool cols4 = false;
   bool wide = false;  // Gd holds complex128 (the Gaussian plan's grids, see to_g)
   int logA = 0;
   DeviceBuffer<double2> a_tw, b_tw;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr;
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
   int nitems = 0, nsplit = 0;
   DeviceBuffer<int> patch_t;
@@ -1416,23 +1421,37 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
   (void)smem_set;
 }
 
+// streams of the fu2d / fu2d_adj row-batch pipeline (MLRG_FU2D_STREAMS, default 2;
+// MLRG_FU2D_PIPE=0: one)
+int pipe_streams() {
+  static const int k = [] {
+    if (!pipelined()) return 1;
+    const char* e = std::getenv("MLRG_FU2D_STREAMS");
+    return e ? std::clamp(std::atoi(e), 1, 8) : 2;
+  }();
+  return k;
+}
+
 void Usfft::ensure_side() {
   Tables& t = *t_;
-  if (t.side) return;
-  MLRG_CUDA(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
-  MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
-  MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_join, cudaEventDisableTiming));
-  t.S2.resize(t.S.size());
-  t.Gd2.resize(t.Gd.size());
+  if (!t.ev_fork) MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
+  while (static_cast<int>(t.sides.size()) + 1 < pipe_streams()) {
+    auto l = std::make_unique<Tables::Lane>();
+    MLRG_CUDA(cudaStreamCreateWithFlags(&l->s, cudaStreamNonBlocking));
+    MLRG_CUDA(cudaEventCreateWithFlags(&l->ev_join, cudaEventDisableTiming));
+    l->S.resize(t.S.size());
+    l->Gd.resize(t.Gd.size());
+    t.sides.push_back(std::move(l));
+  }
 }
 
 Usfft::~Usfft() {
-  if (t_->side) {
-    cudaStreamSynchronize(t_->side);
-    cudaStreamDestroy(t_->side);
+  for (auto& l : t_->sides) {
+    cudaStreamSynchronize(l->s);
+    cudaStreamDestroy(l->s);
+    cudaEventDestroy(l->ev_join);
   }
   if (t_->ev_fork) cudaEventDestroy(t_->ev_fork);
-  if (t_->ev_join) cudaEventDestroy(t_->ev_join);
   delete t_;
 }
 
@@ -1501,19 +1520,22 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     cls_k0_ = epi.k0_out;
     cls_nk_ = nk;
   }
-  const bool pipe = nk > KB && pipelined();
+  // K streams take the row batches round robin (stream j: batches j, j + K, ...)
+  const int K = static_cast<int>(std::min<std::int64_t>(pipe_streams(), (nk + KB - 1) / KB));
+  const bool pipe = K > 1;
   if (pipe) {
     ensure_side();
     MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));  // inputs and partial slots ready
-    MLRG_CUDA(cudaStreamWaitEvent(tm.side, tm.ev_fork, 0));
+    for (int j = 1; j < K; ++j) MLRG_CUDA(cudaStreamWaitEvent(tm.sides[static_cast<std::size_t>(j - 1)]->s, tm.ev_fork, 0));
   }
   int bi = 0;
   for (std::int64_t b = 0; b < nk; b += KB, ++bi) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
-    const bool alt = pipe && (bi & 1);
-    cudaStream_t s = alt ? tm.side : stream_;
-    float2* S = alt ? tm.S2.get() : t.S.get();
-    float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
+    const int lane = pipe ? bi % K : 0;
+    Tables::Lane* L = lane ? tm.sides[static_cast<std::size_t>(lane - 1)].get() : nullptr;
+    cudaStream_t s = L ? L->s : stream_;
+    float2* S = L ? L->S.get() : t.S.get();
+    float2* Gd = L ? L->Gd.get() : t.Gd.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     prof::begin("k_fu2d_rows", s);
     auto rows = zero_padded(t.py) ? (t.cols4 ? k_fu2d_rows<true, true> : k_fu2d_rows<true, false>)
@@ -1556,12 +1578,12 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
                  epi.dot, epi.ld_dot, epi.k0_dot + b, epi.reduce ? 1 : 0,
                  cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : nullptr, t.m_cfac.get()};
     prof::begin("k_fu2d_gather", s);
-    // each stream accumulates into its own partial slots (stream 0: [0, 2 ggrid), side: the next 2 ggrid)
+    // each stream accumulates into its own partial slots (stream j: [2 j ggrid, 2 (j + 1) ggrid))
     auto launch_gather = [&](auto kern, auto grid_ptr, auto rec_tag) {
       using Rec = decltype(rec_tag);
       kern<<<ggrid, 32 * kGatherWarps, static_cast<std::size_t>(per_cta) * sizeof(Rec), s>>>(
           grid_ptr, t.nclass, static_cast<int>(g_.w), t.px.logm, t.ldg, nb, reinterpret_cast<const Rec*>(t.recs.get()),
-          eo, per_cta, partials_.dev() + (alt ? 2 * ggrid : 0), bi >= (pipe ? 2 : 1) ? 1 : 0, sk);
+          eo, per_cta, partials_.dev() + 2 * lane * ggrid, bi >= K ? 1 : 0, sk);
     };
     if (t.wide && t.px.taps == kEsTaps) launch_gather(k_fu2d_gather<kEsTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kEsTaps>{});
     else if (t.wide) launch_gather(k_fu2d_gather<kTaps, double2>, reinterpret_cast<const double2*>(G), ClassRec<kTaps>{});
@@ -1570,11 +1592,13 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     MLRG_LAUNCH_CHECK("k_fu2d_gather");
     prof::end("k_fu2d_gather", s);
   }
-  if (pipe) {
-    MLRG_CUDA(cudaEventRecord(tm.ev_join, tm.side));
-    MLRG_CUDA(cudaStreamWaitEvent(stream_, tm.ev_join, 0));
-  }
-  return epi.reduce && nk > 0 ? (pipe ? 4 : 2) * ggrid : 0;
+  if (pipe)
+    for (int j = 1; j < K; ++j) {
+      Tables::Lane& l = *tm.sides[static_cast<std::size_t>(j - 1)];
+      MLRG_CUDA(cudaEventRecord(l.ev_join, l.s));
+      MLRG_CUDA(cudaStreamWaitEvent(stream_, l.ev_join, 0));
+    }
+  return epi.reduce && nk > 0 ? 2 * K * ggrid : 0;
 }
 
 Usfft::Stats Usfft::stats() const {
@@ -1591,28 +1615,32 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
   // p is exactly the output a class_sums fu2d just produced: its class sums replace the prep pass
   const bool use_cls = cls_src_ && p == cls_src_ && ld == cls_ld_ && k0 == cls_k0_ && nk == cls_nk_ && !skip_;
   cls_src_ = nullptr;
-  const bool pipe = nk > KB && pipelined();  // row batches alternate between two streams, as in fu2d
+  // row batches round robin over K streams, as in fu2d
+  const int K = static_cast<int>(std::min<std::int64_t>(pipe_streams(), (nk + KB - 1) / KB));
+  const bool pipe = K > 1;
   if (pipe) {
     ensure_side();
-    if (tm.val2.size() != tm.val.size()) {
-      tm.val2.resize(tm.val.size());
-      tm.partial2.resize(tm.partial.size());
-      tm.split_cnt2.resize(tm.split_cnt.size());
-      tm.split_cnt2.zero(stream_);
-    }
+    for (auto& l : tm.sides)
+      if (l->val.size() != tm.val.size()) {
+        l->val.resize(tm.val.size());
+        l->partial.resize(tm.partial.size());
+        l->split_cnt.resize(tm.split_cnt.size());
+        l->split_cnt.zero(stream_);
+      }
     MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));
-    MLRG_CUDA(cudaStreamWaitEvent(tm.side, tm.ev_fork, 0));
+    for (int j = 1; j < K; ++j) MLRG_CUDA(cudaStreamWaitEvent(tm.sides[static_cast<std::size_t>(j - 1)]->s, tm.ev_fork, 0));
   }
   int bi = 0;
   for (std::int64_t b = 0; b < nk; b += KB, ++bi) {
     const int nb = static_cast<int>(std::min<std::int64_t>(KB, nk - b));
-    const bool alt = pipe && (bi & 1);
-    cudaStream_t s = alt ? tm.side : stream_;
-    float2* S = alt ? tm.S2.get() : t.S.get();
-    float2* Gd = alt ? tm.Gd2.get() : t.Gd.get();
-    float2* val = use_cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : alt ? tm.val2.get() : t.val.get();
-    double2* partial = alt ? tm.partial2.get() : t.partial.get();
-    int* split_cnt = alt ? tm.split_cnt2.get() : tm.split_cnt.get();
+    const int lane = pipe ? bi % K : 0;
+    Tables::Lane* L = lane ? tm.sides[static_cast<std::size_t>(lane - 1)].get() : nullptr;
+    cudaStream_t s = L ? L->s : stream_;
+    float2* S = L ? L->S.get() : t.S.get();
+    float2* Gd = L ? L->Gd.get() : t.Gd.get();
+    float2* val = use_cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : L ? L->val.get() : t.val.get();
+    double2* partial = L ? L->partial.get() : t.partial.get();
+    int* split_cnt = L ? L->split_cnt.get() : tm.split_cnt.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
     if (!use_cls) {
     prof::begin("k_fu2d_adj_prep", s);
@@ -1675,10 +1703,12 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     MLRG_LAUNCH_CHECK("k_fu2d_adj_rows");
     prof::end("k_fu2d_adj_rows", s);
   }
-  if (pipe) {
-    MLRG_CUDA(cudaEventRecord(tm.ev_join, tm.side));
-    MLRG_CUDA(cudaStreamWaitEvent(stream_, tm.ev_join, 0));
-  }
+  if (pipe)
+    for (int j = 1; j < K; ++j) {
+      Tables::Lane& l = *tm.sides[static_cast<std::size_t>(j - 1)];
+      MLRG_CUDA(cudaEventRecord(l.ev_join, l.s));
+      MLRG_CUDA(cudaStreamWaitEvent(stream_, l.ev_join, 0));
+    }
 }
 
 void Usfft::f2d(const float2* p, float2* out, std::int64_t count, bool adjoint) {
