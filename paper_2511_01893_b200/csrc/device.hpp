@@ -22,6 +22,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
 /// both through mlrg_prof_* / mlrg_launch_count).
 namespace prof {
 void count_launch();
+/// Adds n launches (a CUDA graph replay of n captured kernels).
+void count_launches(std::uint64_t n);
+/// Launches counted so far.
+std::uint64_t launches();
 bool enabled();
 /// Brackets one launch of `name` on `s` with events when profiling is on.
 void begin(const char* name, cudaStream_t s);

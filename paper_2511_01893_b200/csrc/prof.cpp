@@ -69,6 +69,8 @@ HostSpan::~HostSpan() {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(std::uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+std::uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
 bool enabled() { return g_enabled.load(std::memory_order_relaxed); }
 
 void begin(const char* name, cudaStream_t s) {

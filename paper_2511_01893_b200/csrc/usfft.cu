@@ -20,6 +20,8 @@
 #include <complex>
 #include <cstring>
 #include <future>
+#include <unordered_set>
+#include <unordered_map>
 #include <cstdlib>
 #include <numbers>
 #include <type_traits>
@@ -1432,6 +1434,86 @@ int pipe_streams() {
   return k;
 }
 
+// CUDA graphs of the fu2d / fu2d_adj kernel sequences (one per distinct call):
+// 3 kernels per 16-row batch on K streams make a call 48+ launches at 256^3,
+// launch-bound at the small configs[0] volume.
+bool graphs_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("MLRG_GRAPHS");
+    return !(e && *e == '0');
+  }();
+  return v;
+}
+
+struct GraphKey {
+  std::string s;
+  template <class T>
+  GraphKey& add(const T& x) {
+    static_assert(std::is_trivially_copyable_v<T>);
+    s.append(reinterpret_cast<const char*>(&x), sizeof(T));
+    return *this;
+  }
+  GraphKey& add(const char* tag) {
+    s.append(tag);
+    s.push_back('\0');
+    return *this;
+  }
+};
+
+struct Usfft::Graphs {
+  struct Entry {
+    cudaGraphExec_t exec = nullptr;
+    std::uint64_t launches = 0;
+  };
+  std::unordered_map<std::string, Entry> exec;
+  std::unordered_set<std::string> seen;
+  cudaStream_t capture = nullptr;  // the engine stream may be the legacy default stream (not capturable)
+  ~Graphs() {
+    for (auto& [k, e] : exec)
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (capture) cudaStreamDestroy(capture);
+  }
+};
+
+template <class F>
+void Usfft::graph_run(const std::string& key, F&& enqueue) {
+  if (!graphs_enabled() || prof::enabled()) return enqueue();
+  if (!graphs_) graphs_ = new Graphs;
+  auto it = graphs_->exec.find(key);
+  if (it != graphs_->exec.end()) {
+    MLRG_CUDA(cudaGraphLaunch(it->second.exec, stream_));
+    prof::count_launches(it->second.launches);
+    return;
+  }
+  if (graphs_->seen.insert(key).second) return enqueue();  // first call: buffers and side streams get made
+  if (!graphs_->capture) MLRG_CUDA(cudaStreamCreateWithFlags(&graphs_->capture, cudaStreamNonBlocking));
+  const std::uint64_t n0 = prof::launches();
+  cudaGraph_t g = nullptr;
+  // capture on a private stream standing in for the engine stream (the kernels'
+  // order and the side streams' fork/join are the same), replay on the engine stream
+  const cudaStream_t engine = stream_;
+  stream_ = graphs_->capture;
+  MLRG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue();
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &g);
+    stream_ = engine;
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  const cudaError_t ce = cudaStreamEndCapture(stream_, &g);
+  stream_ = engine;
+  MLRG_CUDA(ce);
+  Graphs::Entry e;
+  e.launches = prof::launches() - n0;
+  prof::count_launches(0);
+  MLRG_CUDA(cudaGraphInstantiate(&e.exec, g, 0));
+  MLRG_CUDA(cudaGraphDestroy(g));
+  MLRG_CUDA(cudaGraphLaunch(e.exec, stream_));
+  graphs_->exec.emplace(key, e);
+}
+
 void Usfft::ensure_side() {
   Tables& t = *t_;
   if (!t.ev_fork) MLRG_CUDA(cudaEventCreateWithFlags(&t.ev_fork, cudaEventDisableTiming));
@@ -1446,6 +1528,7 @@ void Usfft::ensure_side() {
 }
 
 Usfft::~Usfft() {
+  delete graphs_;
   for (auto& l : t_->sides) {
     cudaStreamSynchronize(l->s);
     cudaStreamDestroy(l->s);
@@ -1523,6 +1606,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
   // K streams take the row batches round robin (stream j: batches j, j + K, ...)
   const int K = static_cast<int>(std::min<std::int64_t>(pipe_streams(), (nk + KB - 1) / KB));
   const bool pipe = K > 1;
+  auto enqueue = [&] {
   if (pipe) {
     ensure_side();
     MLRG_CUDA(cudaEventRecord(tm.ev_fork, stream_));  // inputs and partial slots ready
@@ -1598,6 +1682,12 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
       MLRG_CUDA(cudaEventRecord(l.ev_join, l.s));
       MLRG_CUDA(cudaStreamWaitEvent(stream_, l.ev_join, 0));
     }
+  };
+  GraphKey key;
+  key.add("fu2d").add(v).add(ld).add(k0).add(nk).add(epi.out).add(epi.ld_out).add(epi.k0_out).add(epi.sub)
+      .add(epi.ld_sub).add(epi.k0_sub).add(epi.dot).add(epi.ld_dot).add(epi.k0_dot).add(epi.reduce).add(cls)
+      .add(skip_).add(K).add(tm.cls.get());
+  graph_run(key.s, enqueue);
   return epi.reduce && nk > 0 ? 2 * K * ggrid : 0;
 }
 
@@ -1618,6 +1708,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
   // row batches round robin over K streams, as in fu2d
   const int K = static_cast<int>(std::min<std::int64_t>(pipe_streams(), (nk + KB - 1) / KB));
   const bool pipe = K > 1;
+  auto enqueue = [&] {
   if (pipe) {
     ensure_side();
     for (auto& l : tm.sides)
@@ -1709,6 +1800,12 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
       MLRG_CUDA(cudaEventRecord(l.ev_join, l.s));
       MLRG_CUDA(cudaStreamWaitEvent(stream_, l.ev_join, 0));
     }
+  };
+  if (peer) return enqueue();  // sharded: fenced exchanges, plain launches
+  GraphKey key;
+  key.add("fu2d_adj").add(p).add(ld).add(k0).add(nk).add(out).add(ld_out).add(k0_out).add(use_cls).add(skip_).add(K)
+      .add(tm.cls.get());
+  graph_run(key.s, enqueue);
 }
 
 void Usfft::f2d(const float2* p, float2* out, std::int64_t count, bool adjoint) {

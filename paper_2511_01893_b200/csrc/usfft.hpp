@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "device.hpp"
 #include "geometry.hpp"
@@ -104,6 +105,13 @@ class Usfft {
   template <class TOut>
   void fu1d_adj_t(const float2* v, TOut* out, std::int64_t d0);
   void ensure_side();  // second stream + grids for the pipelined row batches
+  /// Runs `enqueue` (the kernels of one fu2d / fu2d_adj call) through a CUDA graph
+  /// captured for its exact arguments `key` on the call's second occurrence and
+  /// replayed from then on (MLRG_GRAPHS=0: plain launches; never while profiling).
+  template <class F>
+  void graph_run(const std::string& key, F&& enqueue);
+  struct Graphs;
+  Graphs* graphs_ = nullptr;
   struct Tables;
   Geometry g_;
   cudaStream_t stream_;
