@@ -1485,7 +1485,10 @@ void Usfft::graph_run(const std::string& key, F&& enqueue) {
     prof::count_launches(it->second.launches);
     return;
   }
-  if (graphs_->seen.insert(key).second) return enqueue();  // first call: buffers and side streams get made
+  // first call: buffers and side streams get made; a bounded cache (the solver makes
+  // a handful of distinct calls; callers cycling through many arrays launch plainly)
+  constexpr std::size_t kMaxGraphs = 64;
+  if (graphs_->exec.size() >= kMaxGraphs || graphs_->seen.insert(key).second) return enqueue();
   if (!graphs_->capture) MLRG_CUDA(cudaStreamCreateWithFlags(&graphs_->capture, cudaStreamNonBlocking));
   const std::uint64_t n0 = prof::launches();
   cudaGraph_t g = nullptr;
