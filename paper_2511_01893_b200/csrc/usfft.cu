@@ -1488,6 +1488,7 @@ void Usfft::graph_run(const std::string& key, F&& enqueue) {
   // first call: buffers and side streams get made; a bounded cache (the solver makes
   // a handful of distinct calls; callers cycling through many arrays launch plainly)
   constexpr std::size_t kMaxGraphs = 64;
+  if (graphs_->seen.size() > 4096) graphs_->seen.clear();
   if (graphs_->exec.size() >= kMaxGraphs || graphs_->seen.insert(key).second) return enqueue();
   if (!graphs_->capture) MLRG_CUDA(cudaStreamCreateWithFlags(&graphs_->capture, cudaStreamNonBlocking));
   const std::uint64_t n0 = prof::launches();
