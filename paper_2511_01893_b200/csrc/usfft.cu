@@ -491,27 +491,29 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---- warp-cooperative spread (adjoint) -----------------------------------------------------
-// One warp pair owns an 8x4 patch of grid cells (lane = cell), each warp 8 of
-// the 16 batch rows, and walks the host-built list of targets whose window
-// touches the patch, 32 targets per chunk, one chunk ahead: per target the
-// pair stages only the 8 row and 4 column weights this patch needs (zero
-// outside the window) and each warp cp.asyncs its half of the 16 values; the
-// warp widens them to double once, then every lane adds weight x value for its
-// cell. The 2D weight is the double product w1 * w2 as in nufft.cpp:250-256,
-// and all sums run in double (cells near nu = 0 receive thousands of terms).
-// Patches are processed heaviest first.
+// One warp pair owns an 8x4 patch of grid cells and the 16 batch rows (warp
+// half h: rows 8h..8h+7) and walks the host-built list of targets whose window
+// touches the patch, kSpreadChunk targets per chunk, one chunk ahead. Per
+// target the pair stages the 32 cell weights w1[row] * w2[col] of this patch
+// (zero outside the window; the double product of nufft.cpp:250-256) and each
+// warp cp.asyncs its half of the 16 values, then widens them to double once.
+// A lane owns 4 cells x 2 batch rows (register blocking): per target it reads
+// two 16-byte weight pairs and two double2 values (4 shared wavefronts per
+// warp) for 16 DFMA, where a lane-per-cell layout needs 10 wavefronts (8 value
+// broadcasts + 2 weights) and a DMUL for the same 16 DFMA. Every (cell, row)
+// sum runs in target order in double exactly as before (cells near nu = 0
+// receive thousands of terms). Patches are processed heaviest first.
 constexpr int kPatchR = 8, kPatchC = 4;
 constexpr int KH = KB / 2;
+constexpr int kSpreadChunk = 16;
+
+constexpr int kWgtStride = 34;  // doubles per target row: 16-byte aligned, conflict-free STS.128 / LDS.128
 
 struct SpreadShared {
-  // [pair][buf][patch row / column][target], rows padded to 33 doubles: the
-  // staging writes (lane = target) and the per-target reads (lane = cell:
-  // 8 rows / 4 columns, one target) are both bank-conflict free
-  double wr[2][2][kPatchR][33];
-  double wc[2][2][kPatchC][33];
-  float4 vstage[4][2][32][KH / 2];  // per warp, double-buffered half values
-  double2 vald[4][32][KH];          // per warp, widened chunk values
-  int last[2];                      // per pair: this item completes its split patch
+  double wgt[2][2][kSpreadChunk][kWgtStride];    // [pair][buf][target][cell]
+  float4 vstage[4][2][kSpreadChunk][KH / 2];     // per warp, double-buffered half values
+  double2 vald[4][kSpreadChunk][KH];             // per warp, widened chunk values
+  int last[2];                                   // per pair: this item completes its split patch
 };
 
 __device__ __forceinline__ void pair_sync(int pair) {
@@ -529,47 +531,75 @@ struct SpreadItem {
 };
 constexpr int kSplit = 256;
 
-// Stages targets [e, min(e+32, e1)) into buffer `buf`: warp half 0 writes the
-// 8 row weights, half 1 the 4 column weights (both zero outside the window);
-// each warp cp.asyncs its half of the values.
+// Chunk staging, software-pipelined so that no global load latency sits in
+// front of the arithmetic: a chunk's list entries are loaded two chunks ahead,
+// its weights one chunk ahead (in registers, turned into products after the
+// current chunk's arithmetic), its values by cp.async one chunk ahead. Pair
+// lane pl = part * 16 + j owns target j of a chunk: the weights of patch rows
+// 2*part, 2*part+1 (cells 8*part .. 8*part+7, four 16-byte stores); each warp
+// cp.asyncs its half of the values (two 16-byte pieces per lane).
+// A list entry is (target, a0 | b0 << 16): the target's window offsets of the
+// patch origin, (pr0 - r0[t]) mod m1 and (pc0 - c0[t]) mod m2, host-computed.
+// (Measured and not kept: 8 lanes per target loading one weight row each and
+// exchanging column weights by shuffle -- fewer cache lines per load, but the
+// shuffles cost as many L1 data-pipe wavefronts as they save.)
+struct SpreadW {
+  double r[2], c[kPatchC];
+  bool ok;
+};
+
+__device__ __forceinline__ int2 spread_entry(const int2* __restrict__ lst, int e, int e1, int lane) {
+  const int j = lane & (kSpreadChunk - 1);
+  return e + j < e1 ? lst[e + j] : make_int2(-1, 0);
+}
+
 template <int W>
-__device__ __forceinline__ void stage_spread_chunk(SpreadShared& sh, int pair, int half, int warp, int buf, int e,
-                                                   int e1, int pr0, int pc0, int mask1, int mask2,
-                                                   const int* __restrict__ patch_t, const int* __restrict__ r0,
-                                                   const int* __restrict__ c0, const double* __restrict__ w1,
-                                                   const double* __restrict__ w2, const float2* __restrict__ val,
-                                                   int lane) {
-  if (e + lane < e1) {
-    const int t = patch_t[e + lane];
-    if (half == 0) {
-      const int a0 = pr0 - r0[t];
-      const double* wt = w1 + static_cast<long long>(t) * W;
+__device__ __forceinline__ SpreadW spread_weights(int2 en, int part, int mask1, int mask2,
+                                                  const double* __restrict__ w1, const double* __restrict__ w2) {
+  SpreadW w;
+  w.ok = en.x >= 0;
+  const int a0 = (en.y & 0xffff) + 2 * part, b0 = en.y >> 16;
+  const double* wr = w1 + static_cast<long long>(en.x) * W;
+  const double* wc = w2 + static_cast<long long>(en.x) * W;
 #pragma unroll
-      for (int i = 0; i < kPatchR; ++i) {
-        const int a = (a0 + i) & mask1;
-        sh.wr[pair][buf][i][lane] = a < W ? wt[a] : 0.0;
-      }
-    } else {
-      const int b0 = pc0 - c0[t];
-      const double* wt = w2 + static_cast<long long>(t) * W;
+  for (int i = 0; i < 2; ++i) {
+    const int a = (a0 + i) & mask1;
+    w.r[i] = w.ok && a < W ? wr[a] : 0.0;
+  }
 #pragma unroll
-      for (int j = 0; j < kPatchC; ++j) {
-        const int b = (b0 + j) & mask2;
-        sh.wc[pair][buf][j][lane] = b < W ? wt[b] : 0.0;
-      }
-    }
-    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(t) * KB + half * KH);
-#pragma unroll
-    for (int q = 0; q < KH / 2; ++q) cp_async16(&sh.vstage[warp][buf][lane][q], v + q);
+  for (int q = 0; q < kPatchC; ++q) {
+    const int b = (b0 + q) & mask2;
+    w.c[q] = w.ok && b < W ? wc[b] : 0.0;
+  }
+  return w;
+}
+
+__device__ __forceinline__ void spread_values(SpreadShared& sh, int2 en, int half, int warp, int buf,
+                                              const float2* __restrict__ val, int lane) {
+  if (en.x >= 0) {
+    const int j = lane & (kSpreadChunk - 1), q0 = (lane >> 4) * 2;
+    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(en.x) * KB + half * KH);
+    cp_async16(&sh.vstage[warp][buf][j][q0], v + q0);
+    cp_async16(&sh.vstage[warp][buf][j][q0 + 1], v + q0 + 1);
   }
   cp_async_commit();
 }
 
+__device__ __forceinline__ void spread_store_weights(SpreadShared& sh, const SpreadW& w, int pair, int buf, int part,
+                                                     int lane) {
+  if (!w.ok) return;
+  double2* dst = reinterpret_cast<double2*>(&sh.wgt[pair][buf][lane & (kSpreadChunk - 1)][8 * part]);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {  // the double product w1 * w2 (nufft.cpp:250-256)
+    dst[2 * i] = make_double2(w.r[i] * w.c[0], w.r[i] * w.c[1]);
+    dst[2 * i + 1] = make_double2(w.r[i] * w.c[2], w.r[i] * w.c[3]);
+  }
+}
+
 template <int W, class TG>
-__global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restrict__ val, int logm1, int logm2,
+__global__ void __launch_bounds__(128, 4) k_fu2d_adj_spread(const float2* __restrict__ val, int logm1, int logm2,
                                                          int nitems, const SpreadItem* __restrict__ items,
-                                                         const int* __restrict__ patch_t, const int* __restrict__ r0,
-                                                         const int* __restrict__ c0, const double* __restrict__ w1,
+                                                         const int2* __restrict__ lst, const double* __restrict__ w1,
                                                          const double* __restrict__ w2, TG* __restrict__ G,
                                                          double2* __restrict__ partial, const int4* __restrict__ split,
                                                          int* __restrict__ split_cnt, Skip sk) {
@@ -583,48 +613,60 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
   const SpreadItem it = items[pi];
   const int npc = m2 / kPatchC;
   const int pr0 = (it.patch / npc) * kPatchR, pc0 = (it.patch % npc) * kPatchC;
-  const int ri = lane / kPatchC, cj = lane % kPatchC;
-  double2 acc[KH];
+  // this lane: cells 2g, 2g+1, 16+2g, 17+2g (cell = row * 4 + col) and batch rows kb, kb+1
+  const int g = lane & 7, kb = half * KH + 2 * (lane >> 3);
+  double2 acc[4][2];
 #pragma unroll
-  for (int kk = 0; kk < KH; ++kk) acc[kk] = make_double2(0.0, 0.0);
+  for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = make_double2(0.0, 0.0);
+  const int part = half * 2 + (lane >> 4);  // staging role
   const int e0 = it.e0, e1 = it.e1;
-  stage_spread_chunk<W>(sh, pair, half, warp, 0, e0, e1, pr0, pc0, mask1, mask2, patch_t, r0, c0, w1, w2, val, lane);
-  for (int e = e0, chunk = 0; e < e1; e += 32, ++chunk) {
+  {
+    const int2 en0 = spread_entry(lst, e0, e1, lane);
+    spread_values(sh, en0, half, warp, 0, val, lane);
+    spread_store_weights(sh, spread_weights<W>(en0, part, mask1, mask2, w1, w2), pair, 0, part, lane);
+  }
+  int2 en = spread_entry(lst, e0 + kSpreadChunk, e1, lane);  // the next chunk's entries
+  for (int e = e0, chunk = 0; e < e1; e += kSpreadChunk, ++chunk) {
     const int buf = chunk & 1;
     pair_sync(pair);  // weights of this chunk visible; the other buffer is free
-    if (e + 32 < e1) {
-      stage_spread_chunk<W>(sh, pair, half, warp, buf ^ 1, e + 32, e1, pr0, pc0, mask1, mask2, patch_t, r0, c0, w1,
-                            w2, val, lane);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const SpreadW wn = spread_weights<W>(en, part, mask1, mask2, w1, w2);  // lands during the arithmetic
+    spread_values(sh, en, half, warp, buf ^ 1, val, lane);
+    en = spread_entry(lst, e + 2 * kSpreadChunk, e1, lane);
+    cp_async_wait<1>();  // this chunk's values (the next chunk's group may be pending)
     __syncwarp();
-    const int n = min(32, e1 - e);
+    const int n = min(kSpreadChunk, e1 - e);
     for (int idx = lane; idx < n * (KH / 2); idx += 32) {  // widen once per warp
-      const int j = idx / (KH / 2), part = idx - j * (KH / 2);
-      const float4 x = sh.vstage[warp][buf][j][part];
-      sh.vald[warp][j][2 * part] = make_double2(x.x, x.y);
-      sh.vald[warp][j][2 * part + 1] = make_double2(x.z, x.w);
+      const int j = idx / (KH / 2), q = idx - j * (KH / 2);
+      const float4 x = sh.vstage[warp][buf][j][q];
+      sh.vald[warp][j][2 * q] = make_double2(x.x, x.y);
+      sh.vald[warp][j][2 * q + 1] = make_double2(x.z, x.w);
     }
     __syncwarp();
+    const double* wrow = &sh.wgt[pair][buf][0][0];
 #pragma unroll 2
     for (int j = 0; j < n; ++j) {
-      const double wgt = sh.wr[pair][buf][ri][j] * sh.wc[pair][buf][cj][j];
-      const double2* vp = sh.vald[warp][j];
+      const double2 wa = *reinterpret_cast<const double2*>(wrow + j * kWgtStride + 2 * g);
+      const double2 wb = *reinterpret_cast<const double2*>(wrow + j * kWgtStride + 16 + 2 * g);
+      const double2 x0 = sh.vald[warp][j][kb - half * KH], x1 = sh.vald[warp][j][kb - half * KH + 1];
+      const double w[4] = {wa.x, wa.y, wb.x, wb.y};
 #pragma unroll
-      for (int kk = 0; kk < KH; ++kk) {
-        const double2 x = vp[kk];
-        acc[kk].x = fma(wgt, x.x, acc[kk].x);
-        acc[kk].y = fma(wgt, x.y, acc[kk].y);
+      for (int c = 0; c < 4; ++c) {
+        acc[c][0].x = fma(w[c], x0.x, acc[c][0].x);
+        acc[c][0].y = fma(w[c], x0.y, acc[c][0].y);
+        acc[c][1].x = fma(w[c], x1.x, acc[c][1].x);
+        acc[c][1].y = fma(w[c], x1.y, acc[c][1].y);
       }
     }
+    spread_store_weights(sh, wn, pair, buf ^ 1, part, lane);
   }
-  const int r = pr0 + ri, c = pc0 + cj;
+  const int cells[4] = {2 * g, 2 * g + 1, 16 + 2 * g, 17 + 2 * g};
   if (it.slot >= 0) {
-    double2* pp = partial + (static_cast<long long>(it.slot) * 32 + lane) * KB + half * KH;
 #pragma unroll
-    for (int kk = 0; kk < KH; ++kk) pp[kk] = acc[kk];
+    for (int c = 0; c < 4; ++c) {
+      double2* pp = partial + (static_cast<long long>(it.slot) * 32 + cells[c]) * KB + kb;
+      pp[0] = acc[c][0];
+      pp[1] = acc[c][1];
+    }
     __threadfence();  // this pair's partials are visible before its arrival is counted
     pair_sync(pair);
     const int4 sp = split[it.grp];  // (patch, first slot, slots, -)
@@ -633,24 +675,27 @@ __global__ void __launch_bounds__(128) k_fu2d_adj_spread(const float2* __restric
     if (!sh.last[pair]) return;
     __threadfence();
 #pragma unroll
-    for (int kk = 0; kk < KH; ++kk) acc[kk] = make_double2(0.0, 0.0);
+    for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = make_double2(0.0, 0.0);
     for (int q = 0; q < sp.z; ++q) {  // slot order
-      const double2* src = partial + (static_cast<long long>(sp.y + q) * 32 + lane) * KB + half * KH;
 #pragma unroll
-      for (int kk = 0; kk < KH; ++kk) acc[kk] = cadd(acc[kk], __ldcg(src + kk));
+      for (int c = 0; c < 4; ++c) {
+        const double2* src = partial + (static_cast<long long>(sp.y + q) * 32 + cells[c]) * KB + kb;
+        acc[c][0] = cadd(acc[c][0], __ldcg(src));
+        acc[c][1] = cadd(acc[c][1], __ldcg(src + 1));
+      }
     }
     if (half == 0 && lane == 0) split_cnt[it.grp] = 0;  // ready for the next launch
   }
-  if constexpr (std::is_same_v<TG, double2>) {
-    double2* gp = G + (static_cast<long long>(r) * m2 + c) * KB + half * KH;
 #pragma unroll
-    for (int kk = 0; kk < KH; ++kk) gp[kk] = acc[kk];
-  } else {
-    float4* gp = reinterpret_cast<float4*>(G + (static_cast<long long>(r) * m2 + c) * KB + half * KH);
-#pragma unroll
-    for (int q = 0; q < KH / 2; ++q) {
-      const float2 lo = to_f(acc[2 * q]), hi = to_f(acc[2 * q + 1]);
-      gp[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  for (int c = 0; c < 4; ++c) {
+    const int r = pr0 + cells[c] / kPatchC, col = pc0 + cells[c] % kPatchC;
+    const long long o = (static_cast<long long>(r) * m2 + col) * KB + kb;
+    if constexpr (std::is_same_v<TG, double2>) {
+      G[o] = acc[c][0];
+      G[o + 1] = acc[c][1];
+    } else {
+      const float2 lo = to_f(acc[c][0]), hi = to_f(acc[c][1]);
+      *reinterpret_cast<float4*>(G + o) = make_float4(lo.x, lo.y, hi.x, hi.y);
     }
   }
 }
@@ -934,7 +979,7 @@ struct Usfft::Tables {
   int gather_per = 16;  // classes per gather CTA (whole waves of resident CTAs)
   int ghost = 0, ldg = 0;  // forward grid: repeated columns and row length (cells)
   DeviceBuffer<unsigned char> recs;  // ClassRec<W>[C]
-  DeviceBuffer<int> t_r0, t_c0, m_first, m_tidx;
+  DeviceBuffer<int> m_first, m_tidx;
   DeviceBuffer<double> t_w1, t_w2;  // [C][W]
   DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
   DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint class values
@@ -959,7 +1004,7 @@ struct Usfft::Tables {
   cudaEvent_t ev_fork = nullptr;
   // warp-cooperative spread: 8x4 cell patches -> targets, heaviest patch first
   int nitems = 0, nsplit = 0;
-  DeviceBuffer<int> patch_t;
+  DeviceBuffer<int2> patch_t;  // (class, a0 | b0 << 16) per patch list entry
   DeviceBuffer<SpreadItem> items;
   DeviceBuffer<int4> split;
   DeviceBuffer<double2> partial;
@@ -1199,8 +1244,6 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
       }
     });
     prof::host_mark("host:usfft_class_tables");
-    stg.up(t.t_r0, r0);
-    stg.up(t.t_c0, c0);
     stg.up(t.t_w1, w1);
     stg.up(t.t_w2, w2);
     stg.up(t.m_first, mfirst);
@@ -1260,7 +1303,8 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
     constexpr int kHostThreads = 8;
     const std::size_t per = (C + kHostThreads - 1) / kHostThreads;
     std::vector<std::vector<int>> tcnt(kHostThreads, std::vector<int>(static_cast<std::size_t>(npatch), 0));
-    std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0), lst;
+    std::vector<int> cnt(static_cast<std::size_t>(npatch + 1), 0);
+    std::vector<int2> lst;
     auto run = [&](auto&& body) {
       std::vector<std::thread> th;
       for (int w = 0; w < kHostThreads; ++w)
@@ -1292,7 +1336,13 @@ Usfft::Usfft(const Geometry& g, cudaStream_t stream, GridKernel kernel)
       }
     }
     run([&](int w, std::size_t c, const std::vector<int>& touched) {
-      for (const int p : touched) lst[static_cast<std::size_t>(tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)]++)] = static_cast<int>(c);
+      const std::size_t q = static_cast<std::size_t>(rep_of[c]);
+      for (const int p : touched) {  // the window offsets of the patch origin (the kernel's a0, b0)
+        const std::int64_t a0 = ((p / npc * kPatchR - px.start[q]) % px.m + px.m) % px.m;
+        const std::int64_t b0 = ((p % npc * kPatchC - py.start[q]) % py.m + py.m) % py.m;
+        lst[static_cast<std::size_t>(tcnt[static_cast<std::size_t>(w)][static_cast<std::size_t>(p)]++)] =
+            make_int2(static_cast<int>(c), static_cast<int>(a0 | b0 << 16));
+      }
     });
     std::vector<int> porder(static_cast<std::size_t>(npatch));
     for (int p = 0; p < npatch; ++p) porder[static_cast<std::size_t>(p)] = p;
@@ -1749,12 +1799,11 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     auto spread = t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps, float2> : k_fu2d_adj_spread<kTaps, float2>;
     if (t.wide)
       (t.px.taps == kEsTaps ? k_fu2d_adj_spread<kEsTaps, double2> : k_fu2d_adj_spread<kTaps, double2>)<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(
-          val, t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
+          val, t.px.logm, t.py.logm, t.nitems, t.items.get(), t.patch_t.get(),
           t.t_w1.get(), t.t_w2.get(), reinterpret_cast<double2*>(Gd), partial, t.split.get(), split_cnt, sk);
     else
       spread<<<(t.nitems + 1) / 2, 128, sizeof(SpreadShared), s>>>(val, t.px.logm, t.py.logm, t.nitems, t.items.get(),
-                                                                 t.patch_t.get(), t.t_r0.get(), t.t_c0.get(),
-                                                                 t.t_w1.get(), t.t_w2.get(), Gd, partial, t.split.get(),
+                                                                 t.patch_t.get(), t.t_w1.get(), t.t_w2.get(), Gd, partial, t.split.get(),
                                                                  split_cnt, sk);
     MLRG_LAUNCH_CHECK("k_fu2d_adj_spread");
     prof::end("k_fu2d_adj_spread", s);

@@ -29,6 +29,14 @@ def summarize(rep):
         for k in KEYS:
             if k in d:
                 lines.append(f"  {k:<66} {d[k][1]:>16} {d[k][0]}")
+        br = []  # which L1 / L2 sub-unit sets the throughput figure (the breakdown section)
+        for h, (u, v) in d.items():
+            if h.startswith(("l1tex__", "lts__")) and "pct_of_peak" in h:
+                try:
+                    br.append((float(v.replace(",", "")), h))
+                except ValueError:
+                    pass
+        lines.append("  l1/l2 breakdown: " + ", ".join(f"{h}={v:.1f}" for v, h in sorted(br, reverse=True)[:6]))
         st = sorted(((float(v[1]), h) for h, v in d.items()
                      if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")),
                     reverse=True)
