@@ -7,7 +7,7 @@ for k in $ks; do
   memo=off; case $k in k_encode*) memo=local;; esac
   timeout 300 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"^${k}$" --launch-skip 3 -c 1 -o gpurun_out/ncu_${tag}_${k} -f \
-    python scripts/profile_step.py --n 256 --memo $memo > gpurun_out/ncu_${tag}_${k}.log 2>&1
+    python scripts/profile_step.py --n ${N:-256} --memo $memo > gpurun_out/ncu_${tag}_${k}.log 2>&1
   echo "$k rc $?"
 done
 # summaries here (reports with source are too big to bring back all at once)
