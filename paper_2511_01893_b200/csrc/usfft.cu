@@ -776,6 +776,15 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict
   extern __shared__ double2 sd[];
   const int mask1 = (1 << logm1) - 1, m2 = 1 << logm2, logB = logm1 - logA;
   const int b = blockIdx.x, c0 = blockIdx.y * kCols4;
+  // this CTA's inter-pass twiddles W_M^(b ka), ka < A, staged behind the tile
+  // before the first pass (its closing barrier publishes them), so the last
+  // pass's products do not wait on global loads
+  double2* twb = sd + (kCols4Lanes << logA);
+  for (int ka = threadIdx.x; ka < (1 << logA); ka += blockDim.x) {
+    double2 w = twM[b * ka];  // b * ka < M
+    if (SIGN < 0) w.y = -w.y;
+    twb[ka] = w;
+  }
   auto load = [&](int a, int l) {
     const int r = (a << logB) + b;  // one row per warp: the branch is uniform
     int i = r;
@@ -787,8 +796,7 @@ __global__ void __launch_bounds__(512, 2) k_cols4_pass1(const float2* __restrict
     return to_d(in[(static_cast<long long>(i) * m2 + c0) * KB + l]);
   };
   auto store = [&](int ka, int l, double2 x) {
-    double2 w = twM[b * ka];  // b * ka < M
-    if (SIGN < 0) w.y = -w.y;
+    const double2 w = twb[ka];
     Y[(static_cast<long long>((b << logA) + ka) * m2 + c0) * KB + cols4_off(l, FROM_S && TS)] = to_f(cmul(x, w));
   };
   fft_stockham<SIGN, true, true>(sd, logA, kCols4Lanes, kCols4Lanes, twA, load, store);
@@ -1689,7 +1697,7 @@ int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t 
     if (t.cols4) {  // S -> Gd (intermediate) -> S (the grid, all M1 rows)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<+1, true, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<+1, true, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * (kCols4Lanes + 1)) * sizeof(double2), s>>>(
           S, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), Gd, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
@@ -1812,7 +1820,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     if (t.cols4) {  // Gd -> S (intermediate) -> Gd (rows of the n1 mode slots)
       const int A = 1 << t.logA, B = t.px.m >> t.logA;
       const unsigned nc = static_cast<unsigned>(t.py.m / kCols4);
-      k_cols4_pass1<-1, false, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * kCols4Lanes) * sizeof(double2), s>>>(
+      k_cols4_pass1<-1, false, true><<<dim3(B, nc), kCols4Lanes * A / 8, static_cast<std::size_t>(A * (kCols4Lanes + 1)) * sizeof(double2), s>>>(
           Gd, static_cast<int>(g_.n1), t.px.logm, static_cast<int>(t.px.center), t.logA, t.py.logm, t.a_tw.get(),
           t.x_tw.get(), S, sk);
       MLRG_LAUNCH_CHECK("k_cols4_pass1");
