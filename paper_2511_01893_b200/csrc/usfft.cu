@@ -261,7 +261,7 @@ struct GatherOut {
   const float2* dot;
   long long ld_dot, k0_dot;
   int reduce;
-  float2* cls;           // non-null: the adjoint's class sums of the stored output ([C][KB])
+  double2* cls;          // non-null: the adjoint's class sums of the stored output ([C][KB], complex64 values widened)
   const double2* cfac;   // the members' conjugate phases (k_fu2d_adj_prep's factors)
 };
 
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
     }
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
-    if (ph == 0 && eo.cls && kk >= nk) eo.cls[static_cast<long long>(s) * KB + kk] = make_float2(0.f, 0.f);
+    if (ph == 0 && eo.cls && kk >= nk) eo.cls[static_cast<long long>(s) * KB + kk] = make_double2(0.0, 0.0);
     if (ph == 0 && kk < nk) {
       // every detector sample of the class gets the shared sum times its own phase
       double2 cs = make_double2(0.0, 0.0);
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
           }
         }
       }
-      if (eo.cls) eo.cls[static_cast<long long>(s) * KB + kk] = to_f(cs);
+      if (eo.cls) eo.cls[static_cast<long long>(s) * KB + kk] = to_d(to_f(cs));
     }
   }
   if (eo.reduce) {
@@ -496,7 +496,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // touches the patch, kSpreadChunk targets per chunk, one chunk ahead. Per
 // target the pair stages the 32 cell weights w1[row] * w2[col] of this patch
 // (zero outside the window; the double product of nufft.cpp:250-256) and each
-// warp cp.asyncs its half of the 16 values, then widens them to double once.
+// warp cp.asyncs its half of the 16 values (complex64 values the producers
+// store widened to double, so no conversion pass sits in the chunk loop).
 // A lane owns 4 cells x 2 batch rows (register blocking): per target it reads
 // two 16-byte weight pairs and two double2 values (4 shared wavefronts per
 // warp) for 16 DFMA, where a lane-per-cell layout needs 10 wavefronts (8 value
@@ -511,8 +512,7 @@ constexpr int kWgtStride = 34;  // doubles per target row: 16-byte aligned, conf
 
 struct SpreadShared {
   double wgt[2][2][kSpreadChunk][kWgtStride];    // [pair][buf][target][cell]
-  float4 vstage[4][2][kSpreadChunk][KH / 2];     // per warp, double-buffered half values
-  double2 vald[4][kSpreadChunk][KH];             // per warp, widened chunk values
+  double2 vals[4][2][kSpreadChunk][KH];          // per warp, double-buffered half values
   int last[2];                                   // per pair: this item completes its split patch
 };
 
@@ -537,7 +537,7 @@ constexpr int kSplit = 256;
 // current chunk's arithmetic), its values by cp.async one chunk ahead. Pair
 // lane pl = part * 16 + j owns target j of a chunk: the weights of patch rows
 // 2*part, 2*part+1 (cells 8*part .. 8*part+7, four 16-byte stores); each warp
-// cp.asyncs its half of the values (two 16-byte pieces per lane).
+// cp.asyncs its half of the values (four 16-byte pieces per lane).
 // A list entry is (target, a0 | b0 << 16): the target's window offsets of the
 // patch origin, (pr0 - r0[t]) mod m1 and (pc0 - c0[t]) mod m2, host-computed.
 // (Measured and not kept: 8 lanes per target loading one weight row each and
@@ -575,12 +575,12 @@ __device__ __forceinline__ SpreadW spread_weights(int2 en, int part, int mask1, 
 }
 
 __device__ __forceinline__ void spread_values(SpreadShared& sh, int2 en, int half, int warp, int buf,
-                                              const float2* __restrict__ val, int lane) {
+                                              const double2* __restrict__ val, int lane) {
   if (en.x >= 0) {
-    const int j = lane & (kSpreadChunk - 1), q0 = (lane >> 4) * 2;
-    const float4* v = reinterpret_cast<const float4*>(val + static_cast<long long>(en.x) * KB + half * KH);
-    cp_async16(&sh.vstage[warp][buf][j][q0], v + q0);
-    cp_async16(&sh.vstage[warp][buf][j][q0 + 1], v + q0 + 1);
+    const int j = lane & (kSpreadChunk - 1), q0 = (lane >> 4) * (KH / 2);
+    const double2* v = val + static_cast<long long>(en.x) * KB + half * KH;
+#pragma unroll
+    for (int q = q0; q < q0 + KH / 2; ++q) cp_async16(&sh.vals[warp][buf][j][q], v + q);
   }
   cp_async_commit();
 }
@@ -597,7 +597,7 @@ __device__ __forceinline__ void spread_store_weights(SpreadShared& sh, const Spr
 }
 
 template <int W, class TG>
-__global__ void __launch_bounds__(128, 4) k_fu2d_adj_spread(const float2* __restrict__ val, int logm1, int logm2,
+__global__ void __launch_bounds__(128, 4) k_fu2d_adj_spread(const double2* __restrict__ val, int logm1, int logm2,
                                                          int nitems, const SpreadItem* __restrict__ items,
                                                          const int2* __restrict__ lst, const double* __restrict__ w1,
                                                          const double* __restrict__ w2, TG* __restrict__ G,
@@ -635,19 +635,12 @@ __global__ void __launch_bounds__(128, 4) k_fu2d_adj_spread(const float2* __rest
     cp_async_wait<1>();  // this chunk's values (the next chunk's group may be pending)
     __syncwarp();
     const int n = min(kSpreadChunk, e1 - e);
-    for (int idx = lane; idx < n * (KH / 2); idx += 32) {  // widen once per warp
-      const int j = idx / (KH / 2), q = idx - j * (KH / 2);
-      const float4 x = sh.vstage[warp][buf][j][q];
-      sh.vald[warp][j][2 * q] = make_double2(x.x, x.y);
-      sh.vald[warp][j][2 * q + 1] = make_double2(x.z, x.w);
-    }
-    __syncwarp();
     const double* wrow = &sh.wgt[pair][buf][0][0];
 #pragma unroll 2
     for (int j = 0; j < n; ++j) {
       const double2 wa = *reinterpret_cast<const double2*>(wrow + j * kWgtStride + 2 * g);
       const double2 wb = *reinterpret_cast<const double2*>(wrow + j * kWgtStride + 16 + 2 * g);
-      const double2 x0 = sh.vald[warp][j][kb - half * KH], x1 = sh.vald[warp][j][kb - half * KH + 1];
+      const double2 x0 = sh.vals[warp][buf][j][kb - half * KH], x1 = sh.vals[warp][buf][j][kb - half * KH + 1];
       const double w[4] = {wa.x, wa.y, wb.x, wb.y};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -708,7 +701,7 @@ __global__ void __launch_bounds__(128, 4) k_fu2d_adj_spread(const float2* __rest
 __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict__ p, long long ld, long long k0,
                                                        int nk, int C, int w, const int* __restrict__ m_first,
                                                        const int* __restrict__ m_tidx,
-                                                       const double2* __restrict__ m_cfac, float2* __restrict__ val, Skip sk) {
+                                                       const double2* __restrict__ m_cfac, double2* __restrict__ val, Skip sk) {
   if (skipped(sk, 0)) return;
   const int kk = threadIdx.x & (KB - 1);
   const int c = blockIdx.x * (blockDim.x / KB) + threadIdx.x / KB;
@@ -720,7 +713,7 @@ __global__ void __launch_bounds__(256) k_fu2d_adj_prep(const float2* __restrict_
       const int t = tq >> 16, q = tq & 0xffff;  // packed (Usfft::Tables)
       acc = cadd(acc, cmul(to_d(p[(t * ld + k0 + kk) * w + q]), m_cfac[e]));
     }
-  val[static_cast<long long>(c) * KB + kk] = to_f(acc);
+  val[static_cast<long long>(c) * KB + kk] = to_d(to_f(acc));  // complex64 values, stored widened for the spread
 }
 
 // Column FFT(-1) over natural rows; keep only the n1 rows that map to modes.
@@ -990,8 +983,9 @@ struct Usfft::Tables {
   DeviceBuffer<int> m_first, m_tidx;
   DeviceBuffer<double> t_w1, t_w2;  // [C][W]
   DeviceBuffer<double2> m_fac, m_cfac, x_tw, y_tw;
-  DeviceBuffer<float2> S, Gd, val;  // scratch: row pass, grid, adjoint class values
-  DeviceBuffer<float2> cls;         // class sums left by a class_sums fu2d, [batch][C][KB]
+  DeviceBuffer<float2> S, Gd;  // scratch: row pass, grid
+  DeviceBuffer<double2> val;   // adjoint class values (complex64 values, widened)
+  DeviceBuffer<double2> cls;        // class sums left by a class_sums fu2d, [batch][C][KB]
   // fu2d runs its row batches on two streams (the second set of grids and
   // partial slots belongs to the side stream) so one batch's gather overlaps the
   // next batch's FFT passes
@@ -999,7 +993,8 @@ struct Usfft::Tables {
   struct Lane {
     cudaStream_t s = nullptr;
     cudaEvent_t ev_join = nullptr;
-    DeviceBuffer<float2> S, Gd, val;
+    DeviceBuffer<float2> S, Gd;
+    DeviceBuffer<double2> val;
     DeviceBuffer<double2> partial;
     DeviceBuffer<int> split_cnt;
   };
@@ -1791,7 +1786,7 @@ void Usfft::fu2d_adj(const float2* p, std::int64_t ld, std::int64_t k0, std::int
     cudaStream_t s = L ? L->s : stream_;
     float2* S = L ? L->S.get() : t.S.get();
     float2* Gd = L ? L->Gd.get() : t.Gd.get();
-    float2* val = use_cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : L ? L->val.get() : t.val.get();
+    double2* val = use_cls ? tm.cls.get() + static_cast<long long>(bi) * t.nclass * KB : L ? L->val.get() : t.val.get();
     double2* partial = L ? L->partial.get() : t.partial.get();
     int* split_cnt = L ? L->split_cnt.get() : tm.split_cnt.get();
     const Skip sk{skip_, static_cast<int>((k0 + b) / KB), 1};
