@@ -1,6 +1,7 @@
 #include "memo_gpu.hpp"
 
 #include <algorithm>
+#include <mutex>
 #include <limits>
 #include <random>
 #include <cmath>
@@ -434,6 +435,13 @@ struct KmeansScratch {
   }
 };
 
+void kmeans_seed_attr() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    MLRG_CUDA(cudaFuncSetAttribute(k_km_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  });
+}
+
 void gpu_kmeans(const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
                 std::vector<std::vector<float>>& cent, std::vector<std::size_t>& nearest, int device,
                 KmeansScratch* scratch) {
@@ -449,11 +457,7 @@ void gpu_kmeans(const std::vector<std::vector<float>>& keys, int k, std::uint64_
   for (auto& d : draws) d = rng();
   std::vector<float> flat(static_cast<std::size_t>(nk) * dim);
   for (int i = 0; i < nk; ++i) std::copy(keys[i].begin(), keys[i].end(), flat.begin() + static_cast<std::ptrdiff_t>(i) * dim);
-  static bool attr = false;
-  if (!attr) {
-    MLRG_CUDA(cudaFuncSetAttribute(k_km_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  kmeans_seed_attr();
   w.keys.upload(flat, w.s);
   w.draws.upload(draws, w.s);
   w.cent.resize(static_cast<std::size_t>(k) * dim);
@@ -481,6 +485,27 @@ void gpu_kmeans(const std::vector<std::vector<float>>& keys, int k, std::uint64_
   nearest.assign(hn.begin(), hn.end());
 }
 
+// Setup-time preparation of the trainer (the solve's DeviceMemo constructor):
+// its stream, scratch for up to `nk` keys, the seed kernel's shared-memory
+// opt-in, and the k-means kernels' modules loaded (lazy loading would load
+// them at the first training, inside an iteration), so the training
+// iteration makes no driver calls beyond its launches and copies.
+void gpu_kmeans_prepare(KmeansScratch* w, int nk, int k, int dim) {
+  if (!w->s) MLRG_CUDA(cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking));
+  k = std::min(k, nk);
+  w->keys.resize(static_cast<std::size_t>(nk) * dim);
+  w->draws.resize(static_cast<std::size_t>(k));
+  w->cent.resize(static_cast<std::size_t>(k) * dim);
+  w->dist.resize(static_cast<std::size_t>(nk) * k);
+  w->owner.resize(static_cast<std::size_t>(nk));
+  cudaFuncAttributes fa{};
+  MLRG_CUDA(cudaFuncGetAttributes(&fa, k_km_seed));
+  MLRG_CUDA(cudaFuncGetAttributes(&fa, k_km_dist));
+  MLRG_CUDA(cudaFuncGetAttributes(&fa, k_km_assign));
+  MLRG_CUDA(cudaFuncGetAttributes(&fa, k_km_update));
+  kmeans_seed_attr();
+}
+
 bool gpu_kmeans_fits(int nk, int k, int dim) {
   return static_cast<std::size_t>(nk) * sizeof(double) <= 200 * 1024 && static_cast<long long>(nk) * k < (1LL << 31) &&
          k * dim > 0;
@@ -503,6 +528,9 @@ DeviceMemo::DeviceMemo(MemoClient& client, int key_dim, std::uint64_t seed, int 
     int dev = 0;
     MLRG_CUDA(cudaGetDevice(&dev));
     km_ = std::make_unique<KmeansScratch>();
+    const IvfConfig& ivf = client_.store().ivf();
+    const int nk_max = 2 * ivf.train_size;  // a flush can carry the store past train_size
+    if (gpu_kmeans_fits(nk_max, ivf.nlist, kd_)) gpu_kmeans_prepare(km_.get(), nk_max, ivf.nlist, kd_);
     client_.store().set_trainer([dev, this](const std::vector<std::vector<float>>& keys, int k, std::uint64_t seed, int iters,
                                       std::vector<std::vector<float>>& cent, std::vector<std::size_t>& nearest) {
       const int dim = keys.empty() ? 0 : static_cast<int>(keys.front().size());
