@@ -34,14 +34,14 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # CUDA-core FFMA peak at max 
 METRIC = "ADMM-FFT iterations/sec at N^3 volume"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
 # `ncu --set full` captures (profiles/), filled in per round
-TRAFFIC: dict = {  # round 2: profiles/r2/ncu_baseline_*.txt (`ncu --set full`, one launch, cold cache)
-    "k_fu2d_gather": 45798656 + 1252864, "k_fu2d_adj_spread": 10870016 + 452864,
-    "k_fu2d_cols": 16846848 + 578816, "k_fu2d_rows": 8462592, "k_fu1d": 268778240 + 108069888,
+TRAFFIC: dict = {  # round 2 final: profiles/r2/ncu_final_*.txt (`ncu --set full`, one launch, cold cache)
+    "k_fu2d_gather": 45841664 + 2166016, "k_fu2d_adj_spread": 15731456 + 297472,
+    "k_fu2d_cols": 16847104 + 506368, "k_fu2d_rows": 8462336, "k_fu1d": 268567808 + 107938560,
 }
 # the same captures' per-launch durations (us): ncu serialises launches, while the bench
 # overlaps fu2d row batches on two streams (live durations include the sharing)
-SERIAL_US: dict = {"k_fu2d_gather": 46.40, "k_fu2d_adj_spread": 66.18, "k_fu2d_cols": 25.38, "k_fu2d_rows": 17.66,
-                   "k_fu1d": 312.74}
+SERIAL_US: dict = {"k_fu2d_gather": 47.49, "k_fu2d_adj_spread": 48.77, "k_fu2d_cols": 25.31, "k_fu2d_rows": 17.50,
+                   "k_fu1d": 312.58}
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # DFMA peak at max clock (computed)
 F2F_PER_CLK_SM = 16  # F2F.F64.F32 per clock per SM (scripts/microbench.cu)
 PLAN: dict = {}  # fu2d plan figures of the benchmarked geometry (mlrg_ctx_stats)
@@ -170,8 +170,8 @@ HBM_VOLUMES_PER_ITER = {
 
 # l1tex__throughput (pct of peak) of the committed ncu captures: the shared-memory FFT
 # passes work on L2-resident grids and are bound by the L1/shared pipe, not HBM
-L1TEX_PCT = {"k_fu2d_rows": 63.9, "k_fu2d_cols": 65.0, "k_fu2d_adj_cols": 58.2, "k_fu1d": 78.9,
-             "k_fu2d_adj_spread": 84.2, "k_fu2d_gather": 63.9}  # round 2: profiles/r2/ncu_baseline_*.txt
+L1TEX_PCT = {"k_fu2d_rows": 63.2, "k_fu2d_cols": 65.6, "k_fu2d_adj_cols": 58.1, "k_fu1d": 79.1,
+             "k_fu2d_adj_spread": 83.8, "k_fu2d_gather": 63.0}  # round 2 final: profiles/r2/ncu_final_*.txt
 
 
 def local_share(n, world, rank):
@@ -464,7 +464,7 @@ def main():
             v = (work["flops"] if roof["unit"] == "TFLOP/s" else work["bytes"]) / (SERIAL_US[name] * 1e-6)
             v = v / 1e12 if roof["unit"] == "TFLOP/s" else v / 1e9
             roof["serialized_ncu"] = {"avg_launch_us": SERIAL_US[name], "achieved": v, "frac": v / roof["peak"],
-                                      "source": f"profiles/r2/ncu_baseline_{name}.txt"}
+                                      "source": f"profiles/r2/ncu_final_{name}.txt"}
         roof["share_of_step"] = rec["ms_total"] / ps / ms_step
         roof["kernels_ms_per_step"] = {k: v["ms_total"] / ps for k, v in off["prof"].items()}
         roof["kernels"] = kernel_table(off["prof"], n, nt, ps, P["hbm_gbs"], local_share(n, world, rank))
