@@ -1,3 +1,6 @@
+"""Per-iteration CSV of a device reconstruction of the c64 golden case (n, n_outer from argv),
+with the reference volume for the accuracy column:  python scripts/trace_recon.py 64 10
+"""
 import os, sys
 import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
