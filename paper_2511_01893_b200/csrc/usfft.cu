@@ -369,6 +369,56 @@ __device__ __forceinline__ double widen_tap(T v) {
   else return static_cast<double>(v);
 }
 
+// The class's window sum, shared by its members: each member's sample is the
+// sum times its own phase (minus its d_hat value when fused), stored as
+// complex64; optional class sums for the adjoint and the residual's
+// reductions (operators.cpp:285-299).
+template <int W>
+__device__ __forceinline__ void gather_epilogue(double2 acc, const ClassRec<W>& R, int s, const GatherOut& eo, int w,
+                                                int nk, int kk, int ph, double (&red)[2]) {
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+  if (ph == 0 && eo.cls && kk >= nk) eo.cls[static_cast<long long>(s) * KB + kk] = make_double2(0.0, 0.0);
+  if (ph == 0 && kk < nk) {
+    // every detector sample of the class gets the shared sum times its own phase
+    double2 cs = make_double2(0.0, 0.0);
+    for (int e = 0; e < R.nmem; ++e) {
+      const int tq = R.tq[e];
+      const int t = tq >> 16, q = tq & 0xffff;
+      double2 val = cmul(acc, R.fac[e]);
+      if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
+      const float2 stored = to_f(val);
+      if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = stored;
+      if (eo.cls) cs = cadd(cs, cmul(to_d(stored), eo.cfac[R.first + e]));  // k_fu2d_adj_prep's sum, member order
+      if (eo.reduce) {
+        red[0] += val.x * val.x + val.y * val.y;
+        if (eo.dot) {
+          const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
+          red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
+        }
+      }
+    }
+    if (eo.cls) eo.cls[static_cast<long long>(s) * KB + kk] = to_d(to_f(cs));
+  }
+}
+
+__device__ __forceinline__ void gather_finish(double (&red)[2], double* red_scratch, const GatherOut& eo,
+                                              double* __restrict__ partials, int accumulate) {
+  if (eo.reduce) {
+    block_sum<2>(red, red_scratch);
+    if (threadIdx.x == 0) {
+      double* p = partials + 2 * blockIdx.x;
+      if (accumulate) {
+        p[0] += red[0];
+        p[1] += red[1];
+      } else {
+        p[0] = red[0];
+        p[1] = red[1];
+      }
+    }
+  }
+}
+
 // (the 24-tap Gaussian windows: 2 CTAs/SM, 128 registers)
 template <int W, class TG>
 __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) == 8 ? MLRG_GATHER_MINB : 3) : 2) k_fu2d_gather(
@@ -440,44 +490,9 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
       acc.x = fma(wa, racc.x, acc.x);
       acc.y = fma(wa, racc.y, acc.y);
     }
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
-    if (ph == 0 && eo.cls && kk >= nk) eo.cls[static_cast<long long>(s) * KB + kk] = make_double2(0.0, 0.0);
-    if (ph == 0 && kk < nk) {
-      // every detector sample of the class gets the shared sum times its own phase
-      double2 cs = make_double2(0.0, 0.0);
-      for (int e = 0; e < R.nmem; ++e) {
-        const int tq = R.tq[e];
-        const int t = tq >> 16, q = tq & 0xffff;
-        double2 val = cmul(acc, R.fac[e]);
-        if (eo.sub) val = csub(val, to_d(eo.sub[(t * eo.ld_sub + eo.k0_sub + kk) * w + q]));
-        const float2 stored = to_f(val);
-        if (eo.out) eo.out[(t * eo.ld_out + eo.k0_out + kk) * w + q] = stored;
-        if (eo.cls) cs = cadd(cs, cmul(to_d(stored), eo.cfac[R.first + e]));  // k_fu2d_adj_prep's sum, member order
-        if (eo.reduce) {
-          red[0] += val.x * val.x + val.y * val.y;
-          if (eo.dot) {
-            const float2 d = eo.dot[(t * eo.ld_dot + eo.k0_dot + kk) * w + q];
-            red[1] += static_cast<double>(d.x) * val.x + static_cast<double>(d.y) * val.y;
-          }
-        }
-      }
-      if (eo.cls) eo.cls[static_cast<long long>(s) * KB + kk] = to_d(to_f(cs));
-    }
+    gather_epilogue(acc, R, s, eo, w, nk, kk, ph, red);
   }
-  if (eo.reduce) {
-    block_sum<2>(red, red_scratch);
-    if (threadIdx.x == 0) {
-      double* p = partials + 2 * blockIdx.x;
-      if (accumulate) {
-        p[0] += red[0];
-        p[1] += red[1];
-      } else {
-        p[0] = red[0];
-        p[1] = red[1];
-      }
-    }
-  }
+  gather_finish(red, red_scratch, eo, partials, accumulate);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
