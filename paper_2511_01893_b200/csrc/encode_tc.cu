@@ -172,14 +172,6 @@ struct TcSlabs {
   long long start[kSlabs];
 };
 
-// element offset of complex element ce of the slab starting at `start`
-__device__ __forceinline__ long long slab_elem(const SlabGeom& g, long long start, long long ce) {
-  if (g.axis == 0) return start * g.d1 * g.d2 + ce;
-  const long long per = g.extent * g.d2;
-  const long long i = ce / per, rem = ce - i * per, kl = rem / g.d2;
-  return (i * g.d1 + start + kl) * g.d2 + (rem - kl * g.d2);
-}
-
 // Launch requirement (encode_tc_supported): every slab's 64-element stage
 // chunk is one contiguous run of the input (axis-0 slabs always; axis-1 slabs
 // when extent * d2 is a multiple of 64 and d2 is even) and n is a multiple of 64.

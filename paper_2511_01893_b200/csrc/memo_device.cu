@@ -22,15 +22,6 @@ struct SlabList {
   long long start[kMaxSlabs];
 };
 
-__device__ __forceinline__ long long slab_offset(const SlabGeom& g, long long start, long long ce) {
-  if (g.axis == 0) return start * g.d1 * g.d2 + ce;
-  const long long per = g.extent * g.d2;
-  const long long i = ce / per;
-  const long long rem = ce - i * per;
-  const long long kl = rem / g.d2;
-  return (i * g.d1 + start + kl) * g.d2 + (rem - kl * g.d2);
-}
-
 // Split-K skinny GEMM keys[s][r] = sum_k P[r][k] X[s][k] over K = 2n for up
 // to 16 slabs per launch, with P in the reference's row layout but interleaved
 // columns (column 2i weights Re x_i, 2i+1 weights Im x_i; the reference's row

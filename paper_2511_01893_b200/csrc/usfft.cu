@@ -348,27 +348,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       : "memory");
 }
 
-// float -> double on the integer pipe (exact for normal numbers and zeros;
-// subnormal floats, |x| < 1.2e-38, come out as +-2^-127 (1 + m 2^-23) instead,
-// an absolute difference below 1e-38 in a sum of O(1) terms). The gather's
-// F2F conversions saturate the XU pipe (ncu: 67% of peak with every tap
-// converted there); kGatherIntCvt of each lane's W/2 window columns per row
-// are widened here instead, on the otherwise idle ALU pipe.
-__device__ __forceinline__ double widen_alu(float x) {
-  const unsigned f = __float_as_uint(x), a = f & 0x7fffffffu;
-  const unsigned hi = (a ? (a >> 3) + 0x38000000u : 0u) | (f & 0x80000000u);
-  return __hiloint2double(static_cast<int>(hi), static_cast<int>(f << 29));
-}
-#ifndef MLRG_GATHER_INTCVT
-#define MLRG_GATHER_INTCVT 0
-#endif
-constexpr int kGatherIntCvt = MLRG_GATHER_INTCVT;
-template <int J, class T>
-__device__ __forceinline__ double widen_tap(T v) {
-  if constexpr (std::is_same_v<T, float> && J < kGatherIntCvt) return widen_alu(v);
-  else return static_cast<double>(v);
-}
-
 // The class's window sum, shared by its members: each member's sample is the
 // sum times its own phase (minus its d_hat value when fused), stored as
 // complex64; optional class sums for the adjoint and the residual's
@@ -481,8 +460,8 @@ __global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) 
       auto tap = [&](auto jc) {
         constexpr int j = decltype(jc)::value;
         const TG v = buf[a % (D + 1)][j];
-        racc.x = fma(w2l[j], widen_tap<j>(v.x), racc.x);
-        racc.y = fma(w2l[j], widen_tap<j>(v.y), racc.y);
+        racc.x = fma(w2l[j], static_cast<double>(v.x), racc.x);
+        racc.y = fma(w2l[j], static_cast<double>(v.y), racc.y);
       };
       [&]<int... J>(std::integer_sequence<int, J...>) { (tap(std::integral_constant<int, J>{}), ...); }(
           std::make_integer_sequence<int, WH>{});
@@ -1660,7 +1639,6 @@ void Usfft::fu1d_adj(const float2* v, double2* out, std::int64_t d0) { fu1d_adj_
 
 int Usfft::fu2d(const float2* v, std::int64_t ld, std::int64_t k0, std::int64_t nk, const Fu2dEpilogue& epi) {
   const Tables& t = *t_;
-  const std::int64_t T = g_.n_theta * g_.w;
   const int ks1 = pass_cols(t.px.m), ks2 = pass_cols(t.py.m);
   const int per_cta = t.gather_per;
   const int ggrid = (t.nclass + per_cta - 1) / per_cta;
