@@ -59,6 +59,9 @@ __device__ __forceinline__ bool skipped(const Skip& s, int unit) { return s.f &&
 #ifndef MLRG_FFT_MINB
 #define MLRG_FFT_MINB 4
 #endif
+#ifndef MLRG_GATHER_MINB_G
+#define MLRG_GATHER_MINB_G 2  // the 24-tap Gaussian windows
+#endif
 #ifndef MLRG_GATHER_MINB
 #define MLRG_GATHER_MINB 4
 #endif
@@ -175,8 +178,20 @@ __global__ void __launch_bounds__(512, 2) k_fu1d_adj(const float2* __restrict__ 
   for (int idx = threadIdx.x; idx < m * ncol; idx += blockDim.x) {
     const int l = idx / ncol, c = idx - l * ncol;
     double2 acc = make_double2(0.0, 0.0);
-    const int e1 = cell_ptr[l + 1];
-    for (int e = cell_ptr[l]; e < e1; ++e) {
+    const int e0 = cell_ptr[l], e1 = cell_ptr[l + 1];
+    // the first kSpread1 entries unrolled (their list loads issue together), the rest in order
+    constexpr int kSpread1 = 8;
+#pragma unroll
+    for (int i = 0; i < kSpread1; ++i) {
+      const int e = e0 + i;
+      if (e < e1) {
+        const double2 x = vt[cell_k[e] * ncol + c];
+        const double wv = __ldg(cell_w + e);
+        acc.x = fma(x.x, wv, acc.x);
+        acc.y = fma(x.y, wv, acc.y);
+      }
+    }
+    for (int e = e0 + kSpread1; e < e1; ++e) {
       const double2 x = vt[cell_k[e] * ncol + c];
       const double wv = __ldg(cell_w + e);
       acc.x = fma(x.x, wv, acc.x);
@@ -400,7 +415,7 @@ __device__ __forceinline__ void gather_finish(double (&red)[2], double* red_scra
 
 // (the 24-tap Gaussian windows: 2 CTAs/SM, 128 registers)
 template <int W, class TG>
-__global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) == 8 ? MLRG_GATHER_MINB : 3) : 2) k_fu2d_gather(
+__global__ void __launch_bounds__(32 * kGatherWarps, W == kEsTaps ? (sizeof(TG) == 8 ? MLRG_GATHER_MINB : 3) : MLRG_GATHER_MINB_G) k_fu2d_gather(
     const TG* __restrict__ G, int T, int w, int logm1, int ldg, int nk, const ClassRec<W>* __restrict__ recs,
     GatherOut eo, int per_cta, double* __restrict__ partials, int accumulate, Skip sk) {
   if (skipped(sk, 0)) return;

@@ -58,6 +58,10 @@ def run(n, memo, steps, warm, kernel, prof):
                     if not k.startswith("host"):
                         ks += ms
             line.append(f"kern {ks:6.2f}")
+            for k in HOST + ["k_encode"]:
+                ms, cnt = m.prof_query(k)
+                if cnt:
+                    line.append(f"{k.replace('host:', '')} {ms:.2f}")
         print(" ".join(line), flush=True)
     if prof:
         for k, v in tot.items():
