@@ -33,7 +33,7 @@ int mlrg_version(void);
  * orders the calls with work a host framework issued on its default stream. */
 mlrg_ctx* mlrg_ctx_create(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w,
                           double phi, void* stream);
-/* Same with an explicit spreading kernel: 0 = es (12 taps, the default of
+/* Same with an explicit spreading kernel: 0 = es (10 taps, the default of
  * mlrg_ctx_create), 1 = gaussian (the reference's 24-tap plan, nufft.cpp:48-103).
  * Both evaluate the NUDFT of operators.cpp:87-200; see geometry.hpp. */
 mlrg_ctx* mlrg_ctx_create_kernel(int64_t n1, int64_t n0, int64_t n2, int64_t n_theta, int64_t h, int64_t w,

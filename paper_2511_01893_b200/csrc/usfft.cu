@@ -1,20 +1,27 @@
 // USFFT operator kernels for sm_100a (see usfft.hpp for the reference map).
 //
-// Data flow per operator (M = oversampled grid = next_pow2(2n)):
-//   fu1d      one CTA per (volume row i, tile of C columns j): wrapped +
-//             deconvolved placement -> in-smem DIF FFT (bit-reversed output)
-//             -> W-tap gather read straight from the bit-reversed positions.
+// Data flow per operator (M = oversampled grid = next_pow2(2n)); every FFT is
+// the self-sorting radix-8 Stockham transform of common.cuh, in place in
+// shared memory, natural order in and out (no bit reversal):
+//   fu1d      one CTA per (volume plane i, 8 columns j): wrapped + deconvolved
+//             placement fused into the first pass's loads -> M-point FFT
+//             (+1) -> W-tap gather per detector row from the tile -> x pref x
+//             phase, stored (or sent to the owning rank's mid array, PeerOut).
 //   fu1d_adj  mirror: conj-phase load -> W-tap spread in gather form over a
-//             host-built cell->target CSR (no atomics) -> DIF FFT(-1) -> read.
-//   fu2d      per batch of 16 detector rows, grid layout [M1][M2][16] (row
-//             batch innermost, 128 B per grid cell): row FFT pass, column FFT
-//             pass (both DIF, indices stay bit-reversed), then a W x W-tap
-//             gather per target, one warp per target (lane = batch row).
-// W = 12 (es kernel) or 24 (the reference's Gaussian), geometry.hpp.
-//   fu2d_adj  mirror: targets listed per 8x4 cell patch (host CSR) -> each cell
-//             gathers its targets (no atomics) -> column DIF(-1) -> row DIT(-1).
+//             host-built cell -> detector-row CSR (no atomics) -> FFT(-1) ->
+//             wrapped read x pref x deconv.
+//   fu2d      per batch of 16 detector rows, grid layout [M1][M2 + ghost][16]
+//             (row batch innermost, 128 B per grid cell): row FFT pass, column
+//             FFT pass (four-step passes for M >= 1024), then the W x W-tap
+//             gather, one warp per target class (coincident frequencies share
+//             one window sum; class records bulk-copied into shared memory).
+//   fu2d_adj  mirror: class values -> spread onto 8x4 cell patches from
+//             host-built patch lists (warp pairs, no atomics, split lists
+//             summed in slot order) -> column FFT(-1) -> row FFT(-1).
+// W = 10 (the default es kernel) or 24 (the reference's Gaussian), geometry.hpp.
 // FFT butterflies, twiddles, deconvolution and accumulations run in double;
-// the oversampled grids between passes are stored in complex64 (common.cuh).
+// the oversampled grids between passes are stored in complex64 (complex128
+// for the Gaussian plan's gather/spread grids, see to_g).
 #include <algorithm>
 #include <cmath>
 #include <complex>
