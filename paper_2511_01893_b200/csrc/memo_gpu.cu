@@ -17,7 +17,6 @@ constexpr int kLookupThreads = 256;
 constexpr int kMaxKd = 64;
 constexpr int kMaxProbe = 64;
 constexpr int kStageThreads = 1024;  // one thread per slab (max_slabs <= 1024)
-constexpr int kIlp = 4;              // keys per thread in flight in the distance loop
 
 // memostore.cpp:30-38, in the reference's operation order (no contraction).
 __device__ __forceinline__ double l2_sq_d(const float* a, const float* b, int d) {
@@ -72,43 +71,66 @@ struct LookupArgs {
 };
 
 // Candidate j of the store query: flat, key j; trained, entry j of the
-// concatenated lists of the probed clusters (pre = their prefix sizes).
-__device__ __forceinline__ long long candidate(const LookupArgs& a, long long j, int np, const int* probe,
+// concatenated lists of the probed clusters (base = their starts in cl_ids,
+// pre = their prefix sizes).
+__device__ __forceinline__ long long candidate(const LookupArgs& a, long long j, int np, const int* base,
                                                const int* pre) {
   if (!a.trained) return j;
   int p = 0;
   while (p + 1 < np && j >= pre[p + 1]) ++p;
-  return a.cl_ids[a.cl_ptr[probe[p]] + (j - pre[p])];
+  return a.cl_ids[base[p] + (j - pre[p])];
 }
 
 // One CTA per slab: cache probe, then (on a cache miss) the store query. The
 // query's distances are independent per candidate key, so the CTA spreads the
-// candidates over its threads, kIlp interleaved per thread; each distance is
-// still the reference's sequential sum, and the (l2, lower id) minimum does not
-// depend on the visiting order.
+// candidates over its threads; each distance is still the reference's
+// sequential sum, and the (l2, lower id) minimum does not depend on the
+// visiting order. The keys the single-thread and per-centroid sums read (the
+// cached key, the centroids, the best key) are first staged in shared memory
+// by all threads, so no 60-long chain of dependent global loads sits on one
+// thread; the candidate scan reads its keys directly, kIlp per thread.
+// 4-byte cp.async into shared memory: a thread's staging loads all in flight at once
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+constexpr int kChunk = kMaxProbe;   // staged rows (the centroids)
+constexpr int kRow = kMaxKd + 1;    // staged row stride (odd: conflict-free column reads)
+constexpr int kIlp = 4;             // candidate keys per thread in flight in the distance loop
+
 __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
   __shared__ float q[kMaxKd];
+  __shared__ float kb[kChunk * kRow];  // staged key rows
   __shared__ Best red[kLookupThreads / 32];
   __shared__ double cd[kMaxProbe];
   __shared__ int probe[kMaxProbe];
   __shared__ int pre[kMaxProbe + 1];
+  __shared__ int cbase[kMaxProbe], csize[kMaxProbe];
   __shared__ int done;
+  __shared__ long long best_id;
   const int c = blockIdx.x, t = threadIdx.x, kd = a.kd;
   const long long slot = static_cast<long long>(a.op) * a.max_slabs + c;
   const int mix = static_cast<int>(slot) * kd;
+  const long long vid = a.cache_vid[slot];
   if (t < kd) {  // slot_mix (encoder.cpp:66-86): tables from the host
     q[t] = a.sign[mix + t] * a.raw[static_cast<long long>(c) * kd + a.perm[mix + t]];
     a.qkeys[static_cast<long long>(c) * kd + t] = q[t];
+    if (vid >= 0) kb[t] = a.cache_key[slot * kd + t];
   }
   __syncthreads();
   DevSlab& out = a.slabs[c];
   if (t == 0) {
     done = 0;
-    const long long vid = a.cache_vid[slot];
     a.probed[c] = vid >= 0;
     a.queried[c] = 0;
     if (vid >= 0) {
-      const float cs = static_cast<float>(cosine_d(q, a.cache_key + slot * kd, kd));
+      const float cs = static_cast<float>(cosine_d(q, kb, kd));
       if (cs > a.tau && a.vbytes[vid] == a.slab_vbytes[c]) {
         out.outcome = 2;
         out.cs = cs;
@@ -125,7 +147,11 @@ __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
   if (a.trained) {
     // the nprobe clusters with the smallest (l2, index), ascending: the rank of
     // centroid t is the number of centroids ordered before it
-    if (t < a.ncent) cd[t] = l2_sq_d(q, a.cent + static_cast<long long>(t) * kd, kd);
+    for (int r = t >> 5; r < a.ncent; r += kLookupThreads / 32)  // a warp per centroid row
+      for (int i = t & 31; i < kd; i += 32) cp_async4(&kb[r * kRow + i], a.cent + static_cast<long long>(r) * kd + i);
+    cp_async_all();
+    __syncthreads();
+    if (t < a.ncent) cd[t] = l2_sq_d(q, kb + t * kRow, kd);
     __syncthreads();
     np = min(a.nprobe, a.ncent);
     if (t < a.ncent) {
@@ -134,13 +160,20 @@ __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
       if (rank < np) probe[rank] = t;
     }
     __syncthreads();
+    if (t < np) {  // each probed list's start and size (one thread per list)
+      cbase[t] = a.cl_ptr[probe[t]];
+      csize[t] = a.cl_ptr[probe[t] + 1] - cbase[t];
+    }
+    __syncthreads();
     if (t == 0) {
       pre[0] = 0;
-      for (int p = 0; p < np; ++p) pre[p + 1] = pre[p] + (a.cl_ptr[probe[p] + 1] - a.cl_ptr[probe[p]]);
+      for (int p = 0; p < np; ++p) pre[p + 1] = pre[p] + csize[p];
     }
     __syncthreads();
     total = pre[np];
   }
+  // candidates straight from global memory, kIlp interleaved per thread (all 256
+  // threads busy: at a thousand candidates this beats staging them in rounds)
   Best b{0.0, -1};
   for (long long j0 = t; j0 < total; j0 += static_cast<long long>(kIlp) * kLookupThreads) {
     const float* row[kIlp];
@@ -149,11 +182,12 @@ __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
 #pragma unroll
     for (int k = 0; k < kIlp; ++k) {
       const long long j = j0 + static_cast<long long>(k) * kLookupThreads;
-      id[k] = j < total ? candidate(a, j, np, probe, pre) : -1;
+      id[k] = j < total ? candidate(a, j, np, cbase, pre) : -1;
       row[k] = a.keys + (id[k] < 0 ? 0 : id[k]) * kd;
       acc[k] = 0.0;
     }
-    for (int i = 0; i < kd; ++i) {
+#pragma unroll 8
+    for (int i = 0; i < kd; ++i) {  // unrolled: 8 dims x kIlp keys of loads in flight
       const double qi = static_cast<double>(q[i]);
 #pragma unroll
       for (int k = 0; k < kIlp; ++k) {
@@ -175,21 +209,28 @@ __global__ void __launch_bounds__(kLookupThreads) k_memo_lookup(LookupArgs a) {
   }
   if ((t & 31) == 0) red[t >> 5] = b;
   __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < kLookupThreads / 32; ++w)
+      if (better(red[w], b)) b = red[w];
+    best_id = b.id;
+  }
+  __syncthreads();
+  const long long bid = best_id;
+  if (bid >= 0 && t < kd) kb[t] = a.keys[bid * kd + t];
+  __syncthreads();
   if (t != 0) return;
-  for (int w = 1; w < kLookupThreads / 32; ++w)
-    if (better(red[w], b)) b = red[w];
   a.queried[c] = 1;
   out.outcome = 0;
   out.cs = 0.0f;
   out.vid = -1;
-  if (b.id < 0) return;  // empty store: a miss with cs 0
-  const float cs = static_cast<float>(cosine_d(q, a.keys + b.id * kd, kd));
+  if (bid < 0) return;  // empty store: a miss with cs 0
+  const float cs = static_cast<float>(cosine_d(q, kb, kd));
   out.cs = cs;
-  if (cs > a.tau && a.vbytes[b.id] == a.slab_vbytes[c]) {  // memoclient.cpp:284-292
+  if (cs > a.tau && a.vbytes[bid] == a.slab_vbytes[c]) {  // memoclient.cpp:284-292
     out.outcome = 1;
-    out.vid = b.id;
+    out.vid = bid;
     for (int i = 0; i < kd; ++i) a.cache_key[slot * kd + i] = q[i];  // the QUERY key
-    a.cache_vid[slot] = b.id;
+    a.cache_vid[slot] = bid;
   }
 }
 

@@ -4,10 +4,10 @@ tag=$1; shift
 ks=${@:-"k_fu2d_gather k_fu2d_adj_spread k_fu2d_cols k_fu2d_rows k_fu2d_adj_cols k_fu2d_adj_rows k_fu1d k_fu1d_adj"}
 mkdir -p gpurun_out
 for k in $ks; do
-  memo=off; case $k in k_encode*) memo=local;; esac
+  memo=off; case $k in k_encode*|k_memo*|k_dev*|k_fu2d_adj_prep) memo=local;; esac
   timeout 300 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"^${k}$" --launch-skip 3 -c 1 -o gpurun_out/ncu_${tag}_${k} -f \
-    python scripts/profile_step.py --n ${N:-256} --memo $memo > gpurun_out/ncu_${tag}_${k}.log 2>&1
+    python scripts/profile_step.py --n ${N:-256} --memo $memo --warmup ${WARMUP:-2} > gpurun_out/ncu_${tag}_${k}.log 2>&1
   echo "$k rc $?"
 done
 # summaries here (reports with source are too big to bring back all at once)
