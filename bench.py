@@ -334,7 +334,7 @@ def main():
             m.lib().mlrg_prof_enable(0)
             for k in ("k_fu2d_gather", "k_fu2d_adj_spread", "k_fu2d_rows", "k_fu2d_cols", "k_fu2d_adj_cols",
                       "k_fu2d_adj_rows", "k_fu2d_adj_prep", "k_fu1d", "k_fu1d_adj", "k_encode", "k_memo_lookup",
-                      "k_memo_stage", "k_dev_materialize", "k_dev_store") + HBM_KERNELS:
+                      "k_memo_stage", "k_dev_finish") + HBM_KERNELS:
                 tot, cnt = m.prof_query(k)
                 if cnt:
                     prof[k] = {"ms_total": tot, "launches": cnt}

@@ -157,12 +157,10 @@ void slab_store(double2* out, SlabGeom g, const SlabBatch& b, int nb, cudaStream
 /// Device-side memo: the same copies driven by the per-slab decisions in HBM
 /// (slab c = [c * chunk, ...) along g.axis): hits get value * scale (- sub),
 /// misses are copied to their arena slot (when accepted) and then get out -= sub.
-void dev_materialize(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
-                     cudaStream_t s);
-void dev_materialize(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s);
-void dev_store(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
-               cudaStream_t s);
-void dev_store(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s);
+/// One launch (k_dev_finish) per call.
+void dev_finish(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+                cudaStream_t s);
+void dev_finish(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s);
 
 }  // namespace ops
 }  // namespace mlrg

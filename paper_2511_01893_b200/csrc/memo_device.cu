@@ -392,12 +392,10 @@ constexpr int kCopyThreads = 256;
 constexpr int kPer = static_cast<int>(kSeg) / kCopyThreads;
 constexpr int kInFlight = 4;
 
+// hit slab: its value (x scale, - sub) into the output
 template <class TO>
-__global__ void __launch_bounds__(kCopyThreads, 4) k_dev_materialize(TO* __restrict__ out, SlabGeom g,
-                                                                     const DevSlab* __restrict__ slabs,
-                                                                     long long chunk, const float2* __restrict__ sub) {
-  const DevSlab d = slabs[blockIdx.y];
-  if (d.outcome == 0) return;
+__device__ __forceinline__ void dev_materialize_slab(TO* __restrict__ out, SlabGeom g, const DevSlab& d,
+                                                     long long chunk, const float2* __restrict__ sub) {
   const long long start = blockIdx.y * chunk;
   const SlabRuns sr = slab_runs(g, start, min(chunk, slab_len(g) - start));
   const float2* __restrict__ value = d.src;
@@ -432,12 +430,10 @@ __global__ void __launch_bounds__(kCopyThreads, 4) k_dev_materialize(TO* __restr
   }
 }
 
+// miss slab: the computed output into its arena slot (complex64), then - sub
 template <class TO>
-__global__ void __launch_bounds__(kCopyThreads, 4) k_dev_store(TO* __restrict__ out, SlabGeom g,
-                                                               const DevSlab* __restrict__ slabs, long long chunk,
-                                                               const float2* __restrict__ sub) {
-  const DevSlab d = slabs[blockIdx.y];
-  if (d.outcome != 0) return;
+__device__ __forceinline__ void dev_store_slab(TO* __restrict__ out, SlabGeom g, const DevSlab& d, long long chunk,
+                                               const float2* __restrict__ sub) {
   const long long start = blockIdx.y * chunk;
   const SlabRuns sr = slab_runs(g, start, min(chunk, slab_len(g) - start));
   float2* __restrict__ value = d.dst;
@@ -465,6 +461,18 @@ __global__ void __launch_bounds__(kCopyThreads, 4) k_dev_store(TO* __restrict__ 
       }
     }
   }
+}
+
+// One launch per memoized call finishes every slab: hits are materialized,
+// accepted misses stored into the value arena (one grid, so the hit and miss
+// slabs' copies share the waves instead of running as two launches).
+template <class TO>
+__global__ void __launch_bounds__(kCopyThreads, 4) k_dev_finish(TO* __restrict__ out, SlabGeom g,
+                                                                const DevSlab* __restrict__ slabs, long long chunk,
+                                                                const float2* __restrict__ sub) {
+  const DevSlab d = slabs[blockIdx.y];
+  if (d.outcome != 0) dev_materialize_slab(out, g, d, chunk, sub);
+  else dev_store_slab(out, g, d, chunk, sub);
 }
 
 int enc_blocks() { return 2 * sm_count(); }
@@ -557,35 +565,20 @@ void store_impl(TO* out, SlabGeom g, const SlabBatch& b, int nb, const float2* s
 }
 }  // namespace
 
-void dev_materialize(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
-                     cudaStream_t s) {
+void dev_finish(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
+                cudaStream_t s) {
   if (n <= 0) return;
-  prof::begin("k_dev_materialize", s);
-  k_dev_materialize<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
-  prof::end("k_dev_materialize", s);
-  MLRG_LAUNCH_CHECK("k_dev_materialize");
+  prof::begin("k_dev_finish", s);
+  k_dev_finish<float2><<<batch_grid(n), kCopyThreads, 0, s>>>(out, g, slabs, chunk, sub);
+  prof::end("k_dev_finish", s);
+  MLRG_LAUNCH_CHECK("k_dev_finish");
 }
-void dev_materialize(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
+void dev_finish(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
   if (n <= 0) return;
-  prof::begin("k_dev_materialize", s);
-  k_dev_materialize<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
-  prof::end("k_dev_materialize", s);
-  MLRG_LAUNCH_CHECK("k_dev_materialize");
-}
-void dev_store(float2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, const float2* sub,
-               cudaStream_t s) {
-  if (n <= 0) return;
-  prof::begin("k_dev_store", s);
-  k_dev_store<float2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, sub);
-  prof::end("k_dev_store", s);
-  MLRG_LAUNCH_CHECK("k_dev_store");
-}
-void dev_store(double2* out, SlabGeom g, const DevSlab* slabs, int n, std::int64_t chunk, cudaStream_t s) {
-  if (n <= 0) return;
-  prof::begin("k_dev_store", s);
-  k_dev_store<double2><<<batch_grid(n), 256, 0, s>>>(out, g, slabs, chunk, nullptr);
-  prof::end("k_dev_store", s);
-  MLRG_LAUNCH_CHECK("k_dev_store");
+  prof::begin("k_dev_finish", s);
+  k_dev_finish<double2><<<batch_grid(n), kCopyThreads, 0, s>>>(out, g, slabs, chunk, nullptr);
+  prof::end("k_dev_finish", s);
+  MLRG_LAUNCH_CHECK("k_dev_finish");
 }
 
 void slab_materialize(float2* out, SlabGeom g, const SlabBatch& b, int nb, const float2* sub, cudaStream_t s) {

@@ -504,13 +504,8 @@ void Engine::apply_device_memo(OpId op, bool fused, const void* in, bool in_d, c
   }
   usfft_.set_skip(nullptr);
   const ops::SlabGeom og{oshape.d0, oshape.d1, oshape.d2, axis, 0, 0};
-  if (out_d) {
-    ops::dev_materialize(static_cast<double2*>(out), og, dmemo_->slabs(), n, e, s_);
-    ops::dev_store(static_cast<double2*>(out), og, dmemo_->slabs(), n, e, s_);
-  } else {
-    ops::dev_materialize(static_cast<float2*>(out), og, dmemo_->slabs(), n, e, fused ? d_hat : nullptr, s_);
-    ops::dev_store(static_cast<float2*>(out), og, dmemo_->slabs(), n, e, fused ? d_hat : nullptr, s_);
-  }
+  if (out_d) ops::dev_finish(static_cast<double2*>(out), og, dmemo_->slabs(), n, e, s_);
+  else ops::dev_finish(static_cast<float2*>(out), og, dmemo_->slabs(), n, e, fused ? d_hat : nullptr, s_);
   if (cfg_.flush_after_apply) flush_inserts();
 }
 
