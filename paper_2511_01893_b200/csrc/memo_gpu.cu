@@ -317,7 +317,17 @@ __global__ void __launch_bounds__(kStageThreads) k_memo_stage(StageArgs a) {
     if (staged == 1) {
       const long long id = s_id[c];
       float2* dst = s_off[c] >= 0 ? reinterpret_cast<float2*>(a.arena + s_off[c]) : nullptr;
-      for (int i = 0; i < a.kd; ++i) a.keys[id * a.kd + i] = a.qkeys[static_cast<long long>(c) * a.kd + i];
+      const float* __restrict__ src = a.qkeys + static_cast<long long>(c) * a.kd;
+      float* __restrict__ kdst = a.keys + id * a.kd;
+      for (int i0 = 0; i0 < a.kd; i0 += 16) {  // 16 loads issued before their stores (the arrays never alias)
+        float buf[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i0 + i < a.kd) buf[i] = src[i0 + i];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i0 + i < a.kd) kdst[i0 + i] = buf[i];
+      }
       a.vbytes[id] = a.slab_vbytes[c];
       a.vnorm[id] = live;
       a.vptr[id] = dst;
