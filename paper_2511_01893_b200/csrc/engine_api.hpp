@@ -70,6 +70,10 @@ class Engine {
 
   void set_iteration(int it) { iteration_ = it; }
   void flush_inserts();
+  /// No memoized call runs from here to the next flush_inserts(): the device
+  /// memo reads its log back behind this point, overlapping what is enqueued
+  /// in between (the objective). No-op without the device memo.
+  void mark_flush_point();
   /// Device-side memo: moves the decisions made so far into audit_log() and the
   /// client's counters without publishing the staged inserts (an aborted
   /// iteration). No-op otherwise.
@@ -110,6 +114,11 @@ class Engine {
   std::array<double, 2> fu2d_reduce(const float2* v, const float2* sub, const float2* dot,
                                     const std::vector<Partials::Range>& extra = {},
                                     std::vector<std::vector<double>>* extra_out = nullptr);
+  /// fu2d_reduce in two halves: enqueue (returns the partial-slot count), then
+  /// read back (with `extra`, as fu2d_reduce) after other host work.
+  int fu2d_reduce_begin(const float2* v, const float2* sub, const float2* dot);
+  std::array<double, 2> fu2d_reduce_end(int slots, const std::vector<Partials::Range>& extra = {},
+                                        std::vector<std::vector<double>>* extra_out = nullptr);
 
  private:
   void apply(OpId op, bool fused, const void* in, bool in_d, const float2* d_hat, void* out, bool out_d,

@@ -682,6 +682,22 @@ void DeviceMemo::set_slabs(OpId op, const std::vector<std::size_t>& value_bytes,
 
 DeviceMemo::~DeviceMemo() {
   if (pending_.valid()) pending_.wait();
+  if (rb_) {
+    cudaStreamSynchronize(rb_);
+    cudaStreamDestroy(rb_);
+  }
+  if (fp_) cudaEventDestroy(fp_);
+  if (rb_done_) cudaEventDestroy(rb_done_);
+}
+
+void DeviceMemo::mark(cudaStream_t s) {
+  if (!rb_) {
+    MLRG_CUDA(cudaStreamCreateWithFlags(&rb_, cudaStreamNonBlocking));
+    MLRG_CUDA(cudaEventCreateWithFlags(&fp_, cudaEventDisableTiming));
+    MLRG_CUDA(cudaEventCreateWithFlags(&rb_done_, cudaEventDisableTiming));
+  }
+  MLRG_CUDA(cudaEventRecord(fp_, s));
+  marked_ = true;
 }
 
 void DeviceMemo::join(cudaStream_t s) {
@@ -749,26 +765,35 @@ void DeviceMemo::spill(cudaStream_t s) {
 }
 
 void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) {
+  const bool joined = pending_.valid();
   join(s);
-  MLRG_CUDA(cudaMemcpyAsync(h_state_.get(), state_.get(), 6 * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  MLRG_CUDA(cudaStreamSynchronize(s));
+  // after a mark (and no join work just enqueued on s), the readback and the
+  // state update run on the readback stream behind the mark
+  cudaStream_t rs = s;
+  if (marked_ && !joined) {
+    rs = rb_;
+    MLRG_CUDA(cudaStreamWaitEvent(rb_, fp_, 0));
+  }
+  marked_ = false;
+  MLRG_CUDA(cudaMemcpyAsync(h_state_.get(), state_.get(), 6 * sizeof(long long), cudaMemcpyDeviceToHost, rs));
+  MLRG_CUDA(cudaStreamSynchronize(rs));
   long long* st = h_state_.get();
   const long long npub = st[0], nstaged = publish ? st[1] : 0, nlog = st[3];
   if (st[4]) throw std::logic_error("device memo: a value larger than the arena (" + std::to_string(arena_bytes_) + " bytes)");
   if (nlog > log_cap_) throw std::runtime_error("device memo: decision log overflow");
   std::vector<DevLog> log(static_cast<std::size_t>(nlog));
-  if (nlog) MLRG_CUDA(cudaMemcpyAsync(log.data(), log_.get(), sizeof(DevLog) * nlog, cudaMemcpyDeviceToHost, s));
+  if (nlog) MLRG_CUDA(cudaMemcpyAsync(log.data(), log_.get(), sizeof(DevLog) * nlog, cudaMemcpyDeviceToHost, rs));
   std::vector<float> keys(static_cast<std::size_t>(nstaged) * kd_);
   std::vector<long long> vb(static_cast<std::size_t>(nstaged));
   std::vector<double> vn(static_cast<std::size_t>(nstaged));
   std::vector<const float2*> vp(static_cast<std::size_t>(nstaged));
   if (nstaged) {
-    MLRG_CUDA(cudaMemcpyAsync(keys.data(), keys_.get() + npub * kd_, keys.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
-    MLRG_CUDA(cudaMemcpyAsync(vb.data(), vbytes_.get() + npub, vb.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
-    MLRG_CUDA(cudaMemcpyAsync(vn.data(), vnorm_.get() + npub, vn.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    MLRG_CUDA(cudaMemcpyAsync(vp.data(), vptr_.get() + npub, vp.size() * sizeof(void*), cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaMemcpyAsync(keys.data(), keys_.get() + npub * kd_, keys.size() * sizeof(float), cudaMemcpyDeviceToHost, rs));
+    MLRG_CUDA(cudaMemcpyAsync(vb.data(), vbytes_.get() + npub, vb.size() * sizeof(long long), cudaMemcpyDeviceToHost, rs));
+    MLRG_CUDA(cudaMemcpyAsync(vn.data(), vnorm_.get() + npub, vn.size() * sizeof(double), cudaMemcpyDeviceToHost, rs));
+    MLRG_CUDA(cudaMemcpyAsync(vp.data(), vptr_.get() + npub, vp.size() * sizeof(void*), cudaMemcpyDeviceToHost, rs));
   }
-  MLRG_CUDA(cudaStreamSynchronize(s));
+  MLRG_CUDA(cudaStreamSynchronize(rs));
   // ---- replay the decisions into the client's counters and the audit ----
   MemoCounters& ctr = client_.counters_mut();
   long long queried_in_call = 0;
@@ -819,8 +844,12 @@ void DeviceMemo::flush(cudaStream_t s, std::vector<Audit>* audit, bool publish) 
     st[1] = 0;
     st[5] = 0;
   }
-  MLRG_CUDA(cudaMemcpyAsync(state_.get(), st, 6 * sizeof(long long), cudaMemcpyHostToDevice, s));
-  MLRG_CUDA(cudaStreamSynchronize(s));
+  MLRG_CUDA(cudaMemcpyAsync(state_.get(), st, 6 * sizeof(long long), cudaMemcpyHostToDevice, rs));
+  if (rs != s) {  // the next lookups on s come after the state update
+    MLRG_CUDA(cudaEventRecord(rb_done_, rs));
+    MLRG_CUDA(cudaStreamWaitEvent(s, rb_done_, 0));
+  }
+  MLRG_CUDA(cudaStreamSynchronize(rs));
   if (st[0] > max_keys_ - static_cast<long long>(client_.config().insert_queue_cap))
     throw std::runtime_error("device memo: key index full (" + std::to_string(max_keys_) + " keys)");
   const bool trains = !was_trained && static_cast<long long>(store.key_count()) + nstaged >= store.ivf().train_size;

@@ -95,6 +95,11 @@ class DeviceMemo {
   /// publish = false only drains the log (an aborted iteration: the reference
   /// records its decisions but never flushes its inserts).
   void flush(cudaStream_t s, std::vector<Audit>* audit, bool publish = true);
+  /// Marks the point of `s` after which no memoized call runs before the next
+  /// flush (the objective's unmemoized operators): that flush then reads the
+  /// decision log back on its own stream ordered after the mark, so the host's
+  /// drain overlaps the work enqueued on `s` after it.
+  void mark(cudaStream_t s);
   /// Values spilled to the cold tier so far (count, bytes).
   std::int64_t spilled() const { return spiller_ ? spiller_->spilled() : 0; }
   std::size_t spilled_bytes() const { return spiller_ ? spiller_->spilled_bytes() : 0; }
@@ -111,6 +116,9 @@ class DeviceMemo {
   /// encode); called before anything reads the store or the device IVF state.
   void join(cudaStream_t s);
 
+  cudaStream_t rb_ = nullptr;  // flush readback stream (after a mark)
+  cudaEvent_t fp_ = nullptr, rb_done_ = nullptr;
+  bool marked_ = false;
   MemoClient& client_;
   int kd_;
   int max_slabs_;

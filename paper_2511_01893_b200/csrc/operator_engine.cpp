@@ -618,9 +618,7 @@ void Engine::f2d_adj(const float2* p, float2* out, bool memoize) {
   apply(OpId::f2d_adj, false, p, false, nullptr, out, false, memoize);
 }
 
-std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot,
-                                          const std::vector<Partials::Range>& extra,
-                                          std::vector<std::vector<double>>* extra_out) {
+int Engine::fu2d_reduce_begin(const float2* v, const float2* sub, const float2* dot) {
   const std::int64_t nr = shard_.nr();
   Fu2dEpilogue e;
   e.sub = sub;
@@ -628,13 +626,27 @@ std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, co
   e.dot = dot;
   e.ld_dot = nr;
   e.reduce = true;
-  const int slots = usfft_.fu2d(v, nr, 0, nr, e);
+  return usfft_.fu2d(v, nr, 0, nr, e);
+}
+
+std::array<double, 2> Engine::fu2d_reduce_end(int slots, const std::vector<Partials::Range>& extra,
+                                              std::vector<std::vector<double>>* extra_out) {
   std::vector<Partials::Range> ranges{{0, slots, 2}};
   ranges.insert(ranges.end(), extra.begin(), extra.end());
   std::vector<std::vector<double>> all = usfft_.partials().sum(ranges, s_);
   for (auto& x : all) allreduce(x.data(), static_cast<int>(x.size()));
   if (extra_out) extra_out->assign(all.begin() + 1, all.end());
   return {all[0][0], all[0][1]};
+}
+
+std::array<double, 2> Engine::fu2d_reduce(const float2* v, const float2* sub, const float2* dot,
+                                          const std::vector<Partials::Range>& extra,
+                                          std::vector<std::vector<double>>* extra_out) {
+  return fu2d_reduce_end(fu2d_reduce_begin(v, sub, dot), extra, extra_out);
+}
+
+void Engine::mark_flush_point() {
+  if (dmemo_) dmemo_->mark(s_);
 }
 
 }  // namespace mlrg

@@ -452,17 +452,21 @@ bool Solver::step() {
       st.rep.abort_reason = ex.what();
       return false;
     }
-    eng.flush_inserts();  // admm.cpp:251-254
-    // objective (admm.cpp:190-195), not memoized
-    // TV term and accuracy enqueued first, all three read back with one synchronisation
+    // objective (admm.cpp:190-195), not memoized: enqueued first, then the memo
+    // flush (admm.cpp:251-254; no lookup runs in between, so the order does not
+    // change a decision) drains the decision log behind the mark while the GPU
+    // runs the objective; TV term and accuracy are read back with the data term
+    eng.mark_flush_point();
     const int tv_slots = ops::tv_norm(st.u.get(), dims, part.dev() + Partials::kParked, s, st.halo());
     std::vector<Partials::Range> extra{{Partials::kParked, tv_slots, 1}};
     if (st.has_reference)
       extra.push_back({Partials::kParked + tv_slots,
                        ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev() + Partials::kParked + tv_slots, s), 2});
     eng.fu1d(st.u.get(), st.mid, false);
+    const int obj_slots = eng.fu2d_reduce_begin(st.mid, st.dhat.get(), nullptr);
+    eng.flush_inserts();
     std::vector<std::vector<double>> ex;
-    const std::array<double, 2> data = eng.fu2d_reduce(st.mid, st.dhat.get(), nullptr, extra, &ex);
+    const std::array<double, 2> data = eng.fu2d_reduce_end(obj_slots, extra, &ex);
     const double tv = ex[0][0];
     row.loss = 0.5 * data[0] + cfg.alpha * tv;
     if (st.has_reference) {  // accuracy(reference, u), admm.cpp:183-188
