@@ -190,6 +190,28 @@ class Partials {
     }
     return out;
   }
+  /// sum(count, nv, s) in two halves: enqueue the copy of the table (stream
+  /// order puts it before any later kernel that reuses the slots), then wait for
+  /// that copy alone and sum. Nothing may read host slots [0, count) in between.
+  void sum_begin(int count, cudaStream_t s) {
+    if (count > kMaxSlots) throw std::logic_error("Partials: too many slots");
+    if (!ev_) MLRG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
+    MLRG_CUDA(cudaMemcpyAsync(host_.get(), dev_.get(), static_cast<std::size_t>(count) * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+    MLRG_CUDA(cudaEventRecord(ev_, s));
+  }
+  std::vector<double> sum_end(int count, int nv) {
+    if (count % nv) throw std::logic_error("Partials: count is not a multiple of nv");
+    MLRG_CUDA(cudaEventSynchronize(ev_));
+    std::vector<double> out(static_cast<std::size_t>(nv), 0.0);
+    for (int i = 0; i < count; ++i) out[static_cast<std::size_t>(i % nv)] += host_.get()[i];
+    return out;
+  }
+  ~Partials() {
+    if (ev_) cudaEventDestroy(ev_);
+  }
+  Partials(const Partials&) = delete;
+  Partials& operator=(const Partials&) = delete;
   /// Copies `count` doubles back (synchronising `s`) and returns the column sums
   /// of a [count / nv][nv] table.
   std::vector<double> sum(int count, int nv, cudaStream_t s) {
@@ -206,6 +228,7 @@ class Partials {
  private:
   DeviceBuffer<double> dev_;
   PinnedBuffer<double> host_;
+  cudaEvent_t ev_ = nullptr;
 };
 
 /// Number of SMs of the current device (grids are sized in multiples of it).

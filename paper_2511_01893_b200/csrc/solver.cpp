@@ -353,6 +353,7 @@ bool Solver::step() {
     eng.set_iteration(outer);
     IterationRow row;
     row.iteration = outer;
+    int obj_tv_slots = 0, obj_nd_slots = 0, obj_slots = 0;  // the objective's partial tables (enqueued after RSP)
     try {
       const auto t0 = clock::now();
       // ---- LSP (admm.cpp:59-118, 122-152) ----
@@ -426,9 +427,21 @@ bool Solver::step() {
       // ---- RSP + multiplier/penalty, one fused pass (admm.cpp:154-181) ----
       st.push_u();
       eng.fence();  // sharded: publish the u halos
-      const std::vector<double> rs = sum(
-          st.rsp_chunks(st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s, geo), 2);
+      // the RSP partials' copy is enqueued now and read after the objective is
+      // enqueued behind it (the objective reuses the slots after the copy, in
+      // stream order), so the host's readback overlaps the objective's kernels
+      const int rsp_slots =
+          st.rsp_chunks(st.lam_scale / st.rho, cfg.alpha / st.rho, st.rho / st.lam_scale, part.dev(), s, geo);
+      part.sum_begin(rsp_slots, s);
       st.swap_psi();
+      eng.mark_flush_point();  // no memoized call from here to the flush
+      obj_tv_slots = ops::tv_norm(st.u.get(), dims, part.dev() + Partials::kParked, s, st.halo());
+      if (st.has_reference)
+        obj_nd_slots = ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev() + Partials::kParked + obj_tv_slots, s);
+      eng.fu1d(st.u.get(), st.mid, false);
+      obj_slots = eng.fu2d_reduce_begin(st.mid, st.dhat.get(), nullptr);
+      std::vector<double> rs = part.sum_end(rsp_slots, 2);
+      eng.allreduce(rs.data(), 2);
       const auto t2 = clock::now();
       const double r = std::sqrt(rs[0]);
       const double sres = st.rho * std::sqrt(rs[1]);
@@ -452,18 +465,13 @@ bool Solver::step() {
       st.rep.abort_reason = ex.what();
       return false;
     }
-    // objective (admm.cpp:190-195), not memoized: enqueued first, then the memo
-    // flush (admm.cpp:251-254; no lookup runs in between, so the order does not
-    // change a decision) drains the decision log behind the mark while the GPU
-    // runs the objective; TV term and accuracy are read back with the data term
-    eng.mark_flush_point();
-    const int tv_slots = ops::tv_norm(st.u.get(), dims, part.dev() + Partials::kParked, s, st.halo());
-    std::vector<Partials::Range> extra{{Partials::kParked, tv_slots, 1}};
-    if (st.has_reference)
-      extra.push_back({Partials::kParked + tv_slots,
-                       ops::norm2_diff(st.ref.get(), st.u.get(), st.V, part.dev() + Partials::kParked + tv_slots, s), 2});
-    eng.fu1d(st.u.get(), st.mid, false);
-    const int obj_slots = eng.fu2d_reduce_begin(st.mid, st.dhat.get(), nullptr);
+    // objective (admm.cpp:190-195), not memoized, enqueued above behind the
+    // RSP pass; the memo flush (admm.cpp:251-254; no lookup runs in between, so
+    // the order does not change a decision) drains the decision log behind the
+    // mark while the GPU runs it; TV term and accuracy are read back with the
+    // data term
+    std::vector<Partials::Range> extra{{Partials::kParked, obj_tv_slots, 1}};
+    if (st.has_reference) extra.push_back({Partials::kParked + obj_tv_slots, obj_nd_slots, 2});
     eng.flush_inserts();
     std::vector<std::vector<double>> ex;
     const std::array<double, 2> data = eng.fu2d_reduce_end(obj_slots, extra, &ex);
